@@ -1,0 +1,206 @@
+/*
+ * hb.h -- C ABI of the B200-native short-range particle-particle engine.
+ *
+ * Plain pointers and sizes only (no torch or CUDA types): every array argument
+ * is a DEVICE pointer unless marked "host"; `stream` is a cudaStream_t passed
+ * as void* (NULL = legacy default stream).  Every entry point returns an
+ * HbStatus and fills HbError.  Caller owns all memory; work buffers come from a
+ * caller-provided arena whose size the matching *_workspace() query returns.
+ *
+ * Each entry point replaces one reference function of the hydrobox hot path
+ * (hb/ = /root/reference/pkg/src/hydrobox/); the python binding a maintainer
+ * would add is shown in INTEGRATION.md.
+ */
+#ifndef HB_H_
+#define HB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_ABI_VERSION 1
+
+/* status codes; map onto hb/errors.py */
+enum HbStatus {
+  HB_OK = 0,
+  HB_NONFINITE = 1, /* KernelEvalError "non-finite partial in leaf pair (a, b)" hb/lane.py:106-107 */
+  HB_OVERFLOW = 2,  /* KernelEvalError "accumulator overflow ..."            hb/lane.py:108,197-198 */
+  HB_CONTRACT = 3,  /* HydroboxError: argument contract violated            hb/lane.py:137-144 */
+  HB_CUDA = 4       /* CUDA runtime failure                                            */
+};
+
+typedef struct HbError {
+  int32_t status;
+  int32_t cuda_err;
+  int64_t leaf_a; /* first failing leaf pair, as the reference's counters[6..7] */
+  int64_t leaf_b;
+  char msg[224];
+} HbError;
+
+int hb_abi_version(void);
+/* SM count and compute capability of the current device (host outputs). */
+int hb_device_query(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---------------------------------------------------------------------------
+ * Chaining-mesh bins + k-d leaves.  Replaces build_mesh_and_leaves
+ * (hb/cmtree.py:125-196): flat bin key of binning_pos = pos + shift*L
+ * (hb/particles.py:131-133), stable bin sort, per-bin recursive median split
+ * along the longest axis with stable tie-break (hb/cmtree.py:110-122), tight
+ * leaf AABBs, ghost-only flags.  Output `perm` is the reorder the caller
+ * applies to its particle set (row k of the new order = old row perm[k]).
+ * Leaves are numbered bin-ascending then depth-first, so bin_ptr is the CSR
+ * bin -> leaves and the leaf ids of a bin are contiguous (bin_ids = arange).
+ * ------------------------------------------------------------------------- */
+typedef struct HbMeshArgs {
+  int64_t n;
+  const double* pos;         /* (n,3) canonical wrapped positions               */
+  const int8_t* image_shift; /* (n,3) periodic image of ghost copies            */
+  const uint8_t* ghost;      /* (n)                                             */
+  double side_length;        /* L                                               */
+  double lo[3];              /* host: mesh bounds_lo                            */
+  double width[3];           /* host: realised bin widths extent/nb             */
+  int64_t nb[3];             /* host: bins per axis                             */
+  int64_t max_leaf_size;
+  int64_t leaf_cap;          /* capacity of the leaf arrays below               */
+  /* outputs */
+  int64_t* perm;             /* (n)                                             */
+  int64_t* leaf_start;       /* (leaf_cap)                                      */
+  int64_t* leaf_end;         /* (leaf_cap)                                      */
+  double* leaf_lo;           /* (leaf_cap,3)                                    */
+  double* leaf_hi;           /* (leaf_cap,3)                                    */
+  uint8_t* leaf_ghost_only;  /* (leaf_cap)                                      */
+  int64_t* leaf_bin;         /* (leaf_cap)                                      */
+  int64_t* bin_ptr;          /* (nbins+1)                                       */
+  int64_t* n_leaves_dev;     /* device scalar                                   */
+  int64_t* n_leaves_host;    /* host scalar or NULL (NULL: no host sync)        */
+  int64_t* max_bin_leaves_host; /* host scalar or NULL                          */
+} HbMeshArgs;
+
+size_t hb_build_mesh_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size);
+/* upper bound of the leaf count for n particles in nbins bins */
+int64_t hb_leaf_capacity(int64_t n, int64_t nbins, int64_t max_leaf_size);
+int hb_build_mesh(const HbMeshArgs* args, void* ws, size_t ws_bytes, void* stream, HbError* err);
+
+/* Gather rows by perm for a column block of `width` bytes per row (used to
+ * apply the build permutation to particle fields on device;
+ * hb/particles.py:115-127).  inv_remap: optional int64 column remapped through
+ * the inverse permutation (ghost_src), -1 preserved. */
+int hb_permute_rows(int64_t n, const int64_t* perm, const void* src, void* dst,
+                    int64_t row_bytes, void* stream, HbError* err);
+int hb_remap_through_inverse(int64_t n, const int64_t* perm, int64_t* values,
+                             int64_t* scratch, void* stream, HbError* err);
+
+/* Grow leaf AABBs to cover current member positions (hb/cmtree.py:199-207). */
+int hb_grow_aabbs(int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
+                  const double* pos, const int8_t* image_shift, double side_length,
+                  double* leaf_lo, double* leaf_hi, void* stream, HbError* err);
+
+/* ---------------------------------------------------------------------------
+ * Leaf-pair interaction lists.  Replaces assemble_interaction_lists +
+ * _assemble_core (hb/cmtree.py:210-337): 27-stencil sweep per active leaf
+ * (level >= active_depth and not ghost-only), periodic wrap on full-box axes
+ * with image shift, duplicate (bin, shift) suppression, per-axis AABB gap
+ * <= reach in exact float64, output lexsorted by (a, b, sx, sy, sz).
+ * Call with out_* == NULL to count; then again with capacity >= count.
+ * ------------------------------------------------------------------------- */
+typedef struct HbListArgs {
+  int64_t n_leaves;
+  const int64_t* leaf_bin;
+  const double* leaf_lo;           /* (n_leaves,3) */
+  const double* leaf_hi;
+  const int64_t* leaf_level;       /* may be NULL: all level 0 */
+  const uint8_t* leaf_ghost_only;
+  const int64_t* bin_ptr;          /* (nbins+1) CSR bin -> positions in bin_ids */
+  const int64_t* bin_ids;          /* leaf ids; NULL = identity                 */
+  int64_t nb[3];                   /* host */
+  uint8_t periodic[3];             /* host */
+  double side_length;
+  double reach;
+  int64_t active_depth;
+  int64_t capacity;
+  int64_t* out_a;                  /* (capacity) or NULL to count */
+  int64_t* out_b;
+  int8_t* out_shift;               /* (capacity,3) */
+  int64_t* count_host;             /* host: number of entries */
+} HbListArgs;
+
+size_t hb_assemble_lists_workspace(int64_t n_leaves, int64_t capacity);
+int hb_assemble_lists(const HbListArgs* args, void* ws, size_t ws_bytes, void* stream,
+                      HbError* err);
+
+/* ---------------------------------------------------------------------------
+ * Pair evaluation over a leaf-pair list.  Replaces eval_pairs_core
+ * (hb/kernels.py:281-392) with the same argument meaning: kernel id,
+ * float64 state matrix (n,12) in the column layout of hb/particles.py:46-54,
+ * per-particle image shift, aux columns, list (a, b, shift), leaf ranges,
+ * params, L, lane half-width W2 (accepted; affects only the FLOP-proxy
+ * counters), reach, include_self, mirror, channel signs, mirror map, scales,
+ * deterministic flag.  Outputs are ACCUMULATED into caller-zeroed out_flt
+ * (relaxed) or out_int (deterministic, int64 quanta of the per-pair FP32
+ * contribution); counters[8] (host) as hb/kernels.py:46-58.
+ * Execution: list entries grouped by receiver leaf (CSR, stable), each
+ * receiver leaf cut into <=32-particle tiles, one warp per target tile,
+ * FP32 leaf-relative coordinates, gather accumulation (no atomics).
+ * ------------------------------------------------------------------------- */
+typedef struct HbEvalArgs {
+  int32_t kid;
+  int32_t nchan;
+  int64_t n;
+  const double* state;        /* (n,12)                                  */
+  const int8_t* pshift;       /* (n,3) or NULL (zeros)                   */
+  const double* aux;          /* (n,naux) or NULL                        */
+  int32_t naux;
+  int32_t W2;
+  int64_t n_pairs;
+  const int64_t* pair_a;
+  const int64_t* pair_b;
+  const int8_t* pair_shift;   /* (n_pairs,3)                             */
+  int64_t n_leaves;
+  const int64_t* leaf_start;
+  const int64_t* leaf_end;
+  double params[4];           /* host                                    */
+  double side_length;
+  double reach;
+  int32_t include_self;
+  int32_t mirror;
+  int64_t chan_sign[10];      /* host                                    */
+  int64_t mirror_map[10];     /* host                                    */
+  double scales[10];          /* host                                    */
+  int32_t deterministic;
+  int32_t exact_counters;     /* 1: pairs_in_reach over all species, as the
+                                 reference counts it (an extra counting pass
+                                 for the gas-only SPH kernels)            */
+  int64_t* out_int;           /* (n,nchan) device                        */
+  double* out_flt;            /* (n,nchan) device                        */
+  int64_t counters[8];        /* host out                                */
+} HbEvalArgs;
+
+size_t hb_eval_pairs_workspace(const HbEvalArgs* args);
+int hb_eval_pairs(HbEvalArgs* args, void* ws, size_t ws_bytes, void* stream, HbError* err);
+
+/* ---------------------------------------------------------------------------
+ * CRK linear correction coefficients from the 10 accumulated moments
+ * (hb/hydro.py:115-150): per gas row with m0 > 0, 2-norm condition number of
+ * m2 (symmetric: |lambda|max/|lambda|min) < cond_limit, B = m2^-1 m1 by
+ * partially pivoted elimination, A = 1/(m0 - B.m1) with the |d| > 1e-300
+ * guard, fallback A = 1/m0, B = 0.  Float64.
+ * ------------------------------------------------------------------------- */
+int hb_crk_solve(int64_t n, const double* moments, int64_t stride, const uint8_t* species,
+                 double cond_limit, double* A, double* B, uint8_t* fallback, void* stream,
+                 HbError* err);
+
+/* ---------------------------------------------------------------------------
+ * Resident force evaluation (the s = 0 boundary of subcycle_pm_step,
+ * hb/stepper.py:113-179, with the reference's ordered, single-count
+ * semantics -- SURVEY.md 8c): mesh build, lists, neighbour count,
+ * density (+ EOS), CRK moments + solve, short-range gravity, hydro force.
+ * All buffers stay on device; see HbStepArgs in hb_step.h.
+ * ------------------------------------------------------------------------- */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HB_H_ */

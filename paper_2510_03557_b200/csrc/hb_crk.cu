@@ -1,0 +1,115 @@
+// hb_crk.cu -- CRK linear-correction solve and small C-ABI utilities.
+//
+// hb_crk_solve restates compute_crk_coefficients' epilogue (hb/hydro.py:115-150)
+// per particle in float64: cond_2(m2) via symmetric Jacobi eigenvalues
+// (np.linalg.cond = sigma_max / sigma_min; sigma = |lambda| for symmetric m2),
+// B = m2^-1 m1 by Gaussian elimination with partial pivoting (LAPACK gesv),
+// A = 1/(m0 - B.m1) with the |d| > 1e-300 guard, fallback A = 1/m0, B = 0.
+#include "hb_common.cuh"
+
+namespace hb {
+
+__device__ void jacobi_eig3(double a[3][3], double ev[3]) {
+  for (int sweep = 0; sweep < 32; ++sweep) {
+    double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+    if (off == 0.0) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (a[p][q] == 0.0) continue;
+        double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        if (!isfinite(theta)) t = 0.5 / theta;  // huge theta: t ~ 1/(2 theta)
+        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 3; ++k) {  // A <- J^T A J
+          double akp = a[k][p], akq = a[k][q];
+          a[k][p] = c * akp - s * akq;
+          a[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {
+          double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = c * apk - s * aqk;
+          a[q][k] = s * apk + c * aqk;
+        }
+        a[p][q] = a[q][p] = 0.0;
+      }
+  }
+  ev[0] = a[0][0]; ev[1] = a[1][1]; ev[2] = a[2][2];
+}
+
+__global__ void k_crk_solve(int64_t n, const double* mom, int64_t stride, const uint8_t* species,
+                            double cond_limit, double* A, double* B, uint8_t* fallback) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* v = mom + i * stride;
+  double m0 = v[0];
+  double m1[3] = {v[1], v[2], v[3]};
+  double Ai = 1.0, Bi[3] = {0.0, 0.0, 0.0};
+  bool fb = false;
+  if (species[i] == 1 && m0 > 0.0) {
+    double m2[3][3] = {{v[4], v[5], v[6]}, {v[5], v[7], v[8]}, {v[6], v[8], v[9]}};
+    double e[3][3];
+    for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) e[r][c] = m2[r][c];
+    double ev[3];
+    jacobi_eig3(e, ev);
+    double smax = fmax(fabs(ev[0]), fmax(fabs(ev[1]), fabs(ev[2])));
+    double smin = fmin(fabs(ev[0]), fmin(fabs(ev[1]), fabs(ev[2])));
+    double cond = smax / smin;  // inf (or nan) when singular
+    bool good = isfinite(cond) && cond < cond_limit;
+    if (good) {
+      double m[3][4];
+      for (int r = 0; r < 3; ++r) { for (int c = 0; c < 3; ++c) m[r][c] = m2[r][c]; m[r][3] = m1[r]; }
+      for (int c = 0; c < 3; ++c) {  // partial pivoting
+        int piv = c;
+        for (int r = c + 1; r < 3; ++r) if (fabs(m[r][c]) > fabs(m[piv][c])) piv = r;
+        if (piv != c) for (int k = 0; k < 4; ++k) { double t = m[c][k]; m[c][k] = m[piv][k]; m[piv][k] = t; }
+        for (int r = c + 1; r < 3; ++r) {
+          double f = m[r][c] / m[c][c];
+          for (int k = c; k < 4; ++k) m[r][k] -= f * m[c][k];
+        }
+      }
+      for (int r = 2; r >= 0; --r) {
+        double s = m[r][3];
+        for (int k = r + 1; k < 3; ++k) s -= m[r][k] * Bi[k];
+        Bi[r] = s / m[r][r];
+      }
+    } else {
+      fb = true;
+    }
+    double denom = m0 - (Bi[0] * m1[0] + Bi[1] * m1[1] + Bi[2] * m1[2]);
+    bool bad = !(isfinite(denom) && fabs(denom) > 1e-300);
+    if (bad) { fb = true; denom = m0; }
+    Ai = 1.0 / denom;
+    if (fb) { Ai = 1.0 / m0; Bi[0] = Bi[1] = Bi[2] = 0.0; }
+  }
+  A[i] = Ai;
+  B[3 * i] = Bi[0]; B[3 * i + 1] = Bi[1]; B[3 * i + 2] = Bi[2];
+  fallback[i] = fb;
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" int hb_abi_version(void) { return HB_ABI_VERSION; }
+
+extern "C" int hb_device_query(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HB_CUDA;
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return HB_CUDA;
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return HB_OK;
+}
+
+extern "C" int hb_crk_solve(int64_t n, const double* moments, int64_t stride,
+                            const uint8_t* species, double cond_limit, double* A, double* B,
+                            uint8_t* fallback, void* stream, HbError* err) {
+  if (err) *err = HbError{};
+  if (n <= 0) return HB_OK;
+  k_crk_solve<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(n, moments, stride, species,
+                                                                   cond_limit, A, B, fallback);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}

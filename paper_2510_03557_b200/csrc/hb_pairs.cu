@@ -1,0 +1,825 @@
+// hb_pairs.cu -- the leaf-pair evaluation engine (replaces eval_pairs_core,
+// hb/kernels.py:281-392, behind hb_eval_pairs in include/hb.h).
+//
+// Layout (all device-resident, built per call from the reference-order state):
+//   * the list is expanded (mirror mode: + reversed entries, so every ordered
+//     pair is gathered on its receiving side -- no scatter, no atomics) and
+//     grouped by receiver leaf with a stable radix sort (deterministic order);
+//   * every leaf's selected particles (all, or gas only for the SPH kernels
+//     whose phi vanishes off gas-gas pairs, hb/kernels.py:171,188,194,223,260)
+//     are cut into spatially compact tiles of <= 32 by proportional median
+//     splits: the receiving tile maps onto one warp, lane = target;
+//   * coordinates are FP32 relative to a per-leaf float64 origin; the
+//     separation of a listed image is dx = x_i - (x_j - D) with
+//     D = f32(o_A - o_B - s L)  ==  (pos_i - pos_j) + tau L  of hb/kernels.py:346-355;
+//   * per entry, source tiles are culled against the target tile box, then
+//     per source; survivors are staged in shared memory and broadcast;
+//   * integer outputs (counting, neighbour counts, pairs_in_reach) decide the
+//     reach / 4h^2 predicates in float64 with the reference's exact expression
+//     whenever the FP32 r^2 falls within 2^-12 of the threshold.
+#include "hb_pairs.cuh"
+
+namespace hb {
+
+constexpr int kTileMax = 32;
+constexpr int kTileBuildBlock = 256;
+constexpr int kTileBuildCap = 2048;  // selected members per leaf held in shared memory
+constexpr int kEvalWarps = 4;
+constexpr int kStage = 64;           // staged sources per warp
+
+struct Tiling {
+  int64_t n_leaves, n_tiles_cap;
+  int64_t* sel_cnt;     // (n_leaves+1)
+  int64_t* sel_off;     // (n_leaves+1)
+  int64_t* tile_cnt;    // (n_leaves+1)
+  int64_t* tile_ptr;    // (n_leaves+1)  CSR leaf -> tiles
+  int32_t* tperm;       // (n) internal -> state row
+  int32_t* tile_start;  // (cap) internal index
+  int32_t* tile_n;
+  int32_t* tile_leaf;
+  float4* tile_lo;      // w = hmax
+  float4* tile_hi;
+  double* origin;       // (n_leaves,3)
+  int* overflow;        // device flag: a leaf exceeded kTileBuildCap
+};
+
+// ---------------------------------------------------------------- tiling
+__global__ void k_tile_count(int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
+                             const double* state, int sel, int64_t* sel_cnt, int64_t* tile_cnt) {
+  int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (leaf >= n_leaves) return;
+  int64_t s = leaf_start[leaf], e = leaf_end[leaf];
+  int c = 0;
+  for (int64_t r = s + lane; r < e; r += 32) c += (sel == 0 || state[r * NCOL + C_SP] == 1.0);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) {
+    sel_cnt[leaf] = c;
+    tile_cnt[leaf] = (c + kTileMax - 1) / kTileMax;
+  }
+}
+
+__device__ __forceinline__ double bin_coord(double p, int8_t s, double L) {
+  return __dadd_rn(p, __dmul_rn((double)s, L));
+}
+
+__global__ void __launch_bounds__(kTileBuildBlock)
+k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const double* state,
+             const int8_t* pshift, double L, int sel) {
+  __shared__ int32_t s_row[kTileBuildCap];
+  __shared__ int32_t s_tmp[kTileBuildCap];
+  __shared__ float s_c[3][kTileBuildCap];
+  __shared__ int32_t s_flag_scan[kTileBuildBlock];
+  __shared__ double red[2][3][kTileBuildBlock / 32];
+  __shared__ double org[3];
+  __shared__ int stk_a[64], stk_m[64], stk_k[64];
+  __shared__ int sp_sh, tile_j;
+  __shared__ float seg_ext[3][2][kTileBuildBlock / 32];
+  int64_t leaf = blockIdx.x;
+  int64_t s = leaf_start[leaf], e = leaf_end[leaf];
+  int m_sel = (int)T.sel_cnt[leaf];
+  if (m_sel == 0) {
+    if (threadIdx.x < 3) T.origin[3 * leaf + threadIdx.x] = 0.0;
+    return;
+  }
+  if (m_sel > kTileBuildCap) {
+    if (threadIdx.x == 0) atomicExch(T.overflow, 1);
+    return;
+  }
+  // 1. compact selected rows in row order
+  int base = 0;
+  for (int64_t r0 = s; r0 < e; r0 += blockDim.x) {
+    int64_t r = r0 + threadIdx.x;
+    int f = r < e && (sel == 0 || state[r * NCOL + C_SP] == 1.0);
+    // block exclusive scan of f
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned b = __ballot_sync(0xffffffffu, f);
+    int wpre = __popc(b & lanemask_lt());
+    if (lane == 0) s_flag_scan[wid] = __popc(b);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      int c = s_flag_scan[w];
+      if (w < wid) before += c;
+      total += c;
+    }
+    if (f) s_row[base + before + wpre] = (int32_t)r;
+    base += total;
+    __syncthreads();
+  }
+  // 2. origin = midpoint of the selected binning positions (float64)
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int k = threadIdx.x; k < m_sel; k += blockDim.x) {
+    int64_t r = s_row[k];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double v = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+      mn[d] = fmin(mn[d], v); mx[d] = fmax(mx[d], v);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mn[d] = fmin(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
+      mx[d] = fmax(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
+    }
+  {
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0)
+      for (int d = 0; d < 3; ++d) { red[0][d][wid] = mn[d]; red[1][d][wid] = mx[d]; }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      int d = threadIdx.x;
+      double a = red[0][d][0], b = red[1][d][0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { a = fmin(a, red[0][d][w]); b = fmax(b, red[1][d][w]); }
+      org[d] = 0.5 * (a + b);
+      T.origin[3 * leaf + d] = org[d];
+    }
+    __syncthreads();
+  }
+  for (int k = threadIdx.x; k < m_sel; k += blockDim.x) {
+    int64_t r = s_row[k];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double v = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+      s_c[d][k] = (float)(v - org[d]);
+    }
+  }
+  int ntiles = (m_sel + kTileMax - 1) / kTileMax;
+  if (threadIdx.x == 0) { sp_sh = 1; stk_a[0] = 0; stk_m[0] = m_sel; stk_k[0] = ntiles; tile_j = 0; }
+  __syncthreads();
+  // 3. proportional median splits into ntiles tiles of <= 32 (DFS left-first)
+  while (true) {
+    int sp = sp_sh;
+    if (sp == 0) break;
+    int a0 = stk_a[sp - 1], m = stk_m[sp - 1], kk = stk_k[sp - 1];
+    __syncthreads();
+    if (kk == 1) {
+      if (threadIdx.x == 0) {
+        int64_t t = T.tile_ptr[leaf] + tile_j;
+        T.tile_start[t] = (int32_t)(T.sel_off[leaf] + a0);
+        T.tile_n[t] = m;
+        T.tile_leaf[t] = (int32_t)leaf;
+        tile_j += 1;
+        sp_sh = sp - 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    // longest axis of this segment (FP32)
+    float lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int k = threadIdx.x; k < m; k += blockDim.x)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        float v = s_c[d][a0 + k];
+        lo3[d] = fminf(lo3[d], v); hi3[d] = fmaxf(hi3[d], v);
+      }
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        lo3[d] = fminf(lo3[d], __shfl_xor_sync(0xffffffffu, lo3[d], o));
+        hi3[d] = fmaxf(hi3[d], __shfl_xor_sync(0xffffffffu, hi3[d], o));
+      }
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0)
+      for (int d = 0; d < 3; ++d) { seg_ext[d][0][wid] = lo3[d]; seg_ext[d][1][wid] = hi3[d]; }
+    __syncthreads();
+    float ex[3];
+    for (int d = 0; d < 3; ++d) {
+      float a = seg_ext[d][0][0], b = seg_ext[d][1][0];
+      for (int w = 1; w < nw; ++w) { a = fminf(a, seg_ext[d][0][w]); b = fmaxf(b, seg_ext[d][1][w]); }
+      ex[d] = b - a;
+    }
+    int axis = ex[1] > ex[0] ? 1 : 0;
+    if (ex[2] > ex[axis]) axis = 2;
+    // rank sort of the segment by (coord, position): deterministic
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+      float v = s_c[axis][a0 + k];
+      int rank = 0;
+      for (int q = 0; q < m; ++q) {
+        float w = s_c[axis][a0 + q];
+        rank += (w < v) || (w == v && q < k);
+      }
+      s_tmp[a0 + rank] = a0 + k;  // source slot
+    }
+    __syncthreads();
+    // apply the permutation to rows and coords (via registers)
+    int32_t rr[kTileBuildCap / kTileBuildBlock];
+    float cc[3][kTileBuildCap / kTileBuildBlock];
+    int nloc = 0;
+    for (int k = threadIdx.x; k < m; k += blockDim.x, ++nloc) {
+      int src = s_tmp[a0 + k];
+      rr[nloc] = s_row[src];
+      for (int d = 0; d < 3; ++d) cc[d][nloc] = s_c[d][src];
+    }
+    __syncthreads();
+    nloc = 0;
+    for (int k = threadIdx.x; k < m; k += blockDim.x, ++nloc) {
+      s_row[a0 + k] = rr[nloc];
+      for (int d = 0; d < 3; ++d) s_c[d][a0 + k] = cc[d][nloc];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int k1 = (kk + 1) / 2, k2 = kk - k1;
+      int left = (int)(((int64_t)m * k1 + kk - 1) / kk);
+      stk_a[sp - 1] = a0 + left; stk_m[sp - 1] = m - left; stk_k[sp - 1] = k2;
+      stk_a[sp] = a0; stk_m[sp] = left; stk_k[sp] = k1;
+      sp_sh = sp + 1;
+    }
+    __syncthreads();
+  }
+  // 4. internal order -> state rows
+  int64_t so = T.sel_off[leaf];
+  for (int k = threadIdx.x; k < m_sel; k += blockDim.x) T.tperm[so + k] = s_row[k];
+}
+
+// tile boxes (FP32, leaf frame) and hmax, one warp per tile
+__global__ void k_tile_boxes(int64_t n_tiles, const int64_t* n_tiles_dev, Tiling T,
+                             const double* state, const int8_t* pshift, double L) {
+  int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (t >= *n_tiles_dev) return;
+  int leaf = T.tile_leaf[t];
+  int n = T.tile_n[t];
+  int ks = T.tile_start[t];
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  float hm = 0.0f;
+  if (lane < n) {
+    int64_t r = T.tperm[ks + lane];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double v = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+      float c = (float)(v - T.origin[3 * leaf + d]);
+      lo[d] = c; hi[d] = c;
+    }
+    hm = (float)state[r * NCOL + C_H];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+    hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  }
+  if (lane == 0) {
+    T.tile_lo[t] = make_float4(lo[0], lo[1], lo[2], hm);
+    T.tile_hi[t] = make_float4(hi[0], hi[1], hi[2], 0.0f);
+  }
+}
+
+// ---------------------------------------------------------------- packing
+__global__ void k_pack(int kid, int64_t n_tiles_cap, const int64_t* n_tiles_dev, Tiling T,
+                       const double* state, const int8_t* pshift, const double* aux, int naux,
+                       double L, float4* P0, float4* P1, float4* P2) {
+  int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (t >= *n_tiles_dev) return;
+  if (lane >= T.tile_n[t]) return;
+  int leaf = T.tile_leaf[t];
+  int64_t k = T.tile_start[t] + lane;
+  int64_t r = T.tperm[k];
+  const double* st = state + r * NCOL;
+  float c[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double v = bin_coord(st[d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+    c[d] = (float)(v - T.origin[3 * leaf + d]);
+  }
+  double m = st[C_M], h = st[C_H], rho = st[C_RHO];
+  double sig = 0.31830988618379067;
+  double norm3 = h > 0 ? sig / (h * h * h) : 0.0;
+  double hinv = h > 0 ? 1.0 / h : 0.0;
+  double vol = rho > 0 ? m / rho : 0.0;
+  switch (kid) {
+    case KID_DENSITY:
+    case KID_NEIGHBOR_COUNT:
+      P0[k] = make_float4(c[0], c[1], c[2], (float)m);
+      P1[k] = make_float4((float)h, (float)norm3, (float)hinv, 0.0f);
+      break;
+    case KID_CRK_MOMENTS:
+      P0[k] = make_float4(c[0], c[1], c[2], (float)vol);
+      P1[k] = make_float4((float)h, (float)norm3, (float)hinv, 0.0f);
+      break;
+    case KID_HYDRO_FORCE: {
+      double fpart = rho > 0 ? st[C_P] / (rho * rho) : 0.0;
+      double norm5 = h > 0 ? sig / (h * h * h * h * h) : 0.0;
+      P0[k] = make_float4(c[0], c[1], c[2], (float)m);
+      P1[k] = make_float4((float)st[C_VX], (float)st[C_VY], (float)st[C_VZ], (float)h);
+      P2[k] = make_float4((float)fpart, (float)st[C_CS], (float)rho, (float)norm5);
+      break;
+    }
+    case KID_CRK_INTERP: {
+      const double* ax = aux + r * naux;
+      P0[k] = make_float4(c[0], c[1], c[2], (float)vol);
+      P1[k] = make_float4((float)h, (float)norm3, (float)hinv, (float)ax[1]);
+      P2[k] = make_float4((float)ax[2], (float)ax[3], (float)ax[4], (float)ax[0]);
+      break;
+    }
+    default:
+      P0[k] = make_float4(c[0], c[1], c[2], (float)m);
+  }
+}
+
+// ---------------------------------------------------------------- entry CSR
+__global__ void k_expand(int64_t n_pairs, int mirror, const int64_t* pa, const int64_t* pb,
+                         const int8_t* ps, const int64_t* rev_off, uint64_t* keys, uint32_t* vals,
+                         int32_t* e_src, int32_t* e_code, int32_t* e_orig) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pairs) return;
+  int64_t a = pa[i], b = pb[i];
+  int sx = ps[3 * i], sy = ps[3 * i + 1], sz = ps[3 * i + 2];
+  int code = (sx + 1) * 9 + (sy + 1) * 3 + (sz + 1);
+  keys[i] = (uint64_t)a; vals[i] = (uint32_t)i;
+  e_src[i] = (int32_t)b; e_code[i] = code | (1 << 8); e_orig[i] = (int32_t)i;
+  if (mirror && (a != b || code != 13)) {
+    int64_t j = n_pairs + rev_off[i];
+    keys[j] = (uint64_t)b; vals[j] = (uint32_t)j;
+    e_src[j] = (int32_t)a; e_code[j] = 26 - code; e_orig[j] = (int32_t)i;
+  }
+}
+__global__ void k_rev_flags(int64_t n_pairs, const int64_t* pa, const int64_t* pb,
+                            const int8_t* ps, int64_t* flag) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pairs) return;
+  bool shifted = ps[3 * i] != 0 || ps[3 * i + 1] != 0 || ps[3 * i + 2] != 0;
+  flag[i] = (pa[i] != pb[i] || shifted) ? 1 : 0;
+}
+__global__ void k_recv_hist(int64_t E, const uint64_t* keys_sorted, int64_t* cnt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  atomicAdd((unsigned long long*)&cnt[keys_sorted[i]], 1ull);
+}
+__global__ void k_gather_entries(int64_t E, const uint32_t* vals, const int32_t* src,
+                                 const int32_t* code, const int32_t* orig, int32_t* o_src,
+                                 int32_t* o_code, int32_t* o_orig) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  uint32_t v = vals[i];
+  o_src[i] = src[v]; o_code[i] = code[v]; o_orig[i] = orig[v];
+}
+
+// FLOP-proxy counters of the lane-split schedule (hb/kernels.py:319-343)
+__global__ void k_sched_counters(int64_t n_pairs, const int64_t* pa, const int64_t* pb,
+                                 const int64_t* ls, const int64_t* le, int W2,
+                                 unsigned long long* cnt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long f = 0, g = 0;
+  if (i < n_pairs) {
+    int64_t na = le[pa[i]] - ls[pa[i]], nb = le[pb[i]] - ls[pb[i]];
+    int64_t nit = (na + W2 - 1) / W2, njt = (nb + W2 - 1) / W2;
+    f = (unsigned long long)nit;
+    g = (unsigned long long)(nit * njt);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    f += __shfl_xor_sync(0xffffffffu, f, o);
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&cnt[0], f);
+    atomicAdd(&cnt[1], g);
+  }
+}
+
+// ---------------------------------------------------------------- the gather kernel
+struct EvalDev {
+  Tiling T;
+  const int64_t* ent_ptr;  // (n_leaves+1)
+  const int32_t* ent_src;
+  const int32_t* ent_code;  // shift code | fwd << 8
+  const float4 *P0, *P1, *P2;
+  const double* state;
+  const int8_t* pshift;
+  double L, reach;
+  PairParams pp;
+  float cull_reach;
+  int include_self;
+  int nchan;
+  float scale[10];
+  double* out_flt;
+  int64_t* out_int;
+  int write_out;
+  unsigned long long* in_count;
+  unsigned long long* err_key;  // min (entry*4 + kind)
+};
+
+__device__ __forceinline__ float box_gap2(float x, float y, float z, float4 lo, float4 hi) {
+  float gx = fmaxf(fmaxf(lo.x - x, x - hi.x), 0.0f);
+  float gy = fmaxf(fmaxf(lo.y - y, y - hi.y), 0.0f);
+  float gz = fmaxf(fmaxf(lo.z - z, z - hi.z), 0.0f);
+  return fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+}
+
+// exact float64 separation of rows i, j for image code (hb/kernels.py:346-356)
+__device__ __forceinline__ double exact_r2(const EvalDev& a, int64_t i, int64_t j, int code) {
+  int s[3] = {code / 9 - 1, (code / 3) % 3 - 1, code % 3 - 1};
+  double r2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    int64_t pi = a.pshift ? a.pshift[3 * i + d] : 0, pj = a.pshift ? a.pshift[3 * j + d] : 0;
+    int64_t tau = pi - pj - s[d];
+    double dx = __dadd_rn(__dsub_rn(a.state[i * NCOL + d], a.state[j * NCOL + d]),
+                          __dmul_rn((double)tau, a.L));
+    r2 = d == 0 ? __dmul_rn(dx, dx) : __dadd_rn(r2, __dmul_rn(dx, dx));
+  }
+  return r2;
+}
+
+template <int KID, bool DET>
+__global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_tiles_cap,
+                                                          const int64_t* n_tiles_dev) {
+  using P = Pol<KID>;
+  constexpr int NP = P::NP, NC = P::NC;
+  __shared__ float4 s_rec[kEvalWarps][kStage][NP];
+  __shared__ int2 s_meta[kEvalWarps][kStage];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = (int64_t)blockIdx.x * kEvalWarps + wid;
+  if (t >= *n_tiles_dev) return;
+  const Tiling& T = a.T;
+  int A = T.tile_leaf[t];
+  int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
+  if (e0 == e1) return;
+  int n_t = T.tile_n[t];
+  bool live = lane < n_t;
+  int k_i = T.tile_start[t] + (live ? lane : 0);
+  int64_t row_i = T.tperm[k_i];
+  float4 ti[NP];
+  ti[0] = a.P0[k_i];
+  if (NP > 1) ti[1] = a.P1[k_i];
+  if (NP > 2) ti[2] = a.P2[k_i];
+  float4 tlo = T.tile_lo[t], thi = T.tile_hi[t];
+  float hmax_t = tlo.w;
+  float Rt = a.cull_reach;
+  if (P::HVAR && KID != KID_HYDRO_FORCE) Rt = fminf(Rt, 2.0f * hmax_t * 1.0001f);
+  float acc[NC];
+  long long iacc[DET ? NC : 1];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < (DET ? NC : 1); ++c) iacc[c] = 0;
+  unsigned long long nin = 0;
+  double oA[3] = {T.origin[3 * A], T.origin[3 * A + 1], T.origin[3 * A + 2]};
+  float thr_n = 0.0f;
+  double thr_n64 = 0.0;
+  if (KID == KID_NEIGHBOR_COUNT) {
+    double h = a.state[row_i * NCOL + C_H];
+    thr_n64 = __dmul_rn(__dmul_rn(4.0, h), h);
+    thr_n = (float)thr_n64;
+  }
+  double reach2_64 = __dmul_rn(a.reach, a.reach);
+  int bad = 0;
+  int cnt = 0;
+  // evaluate the staged sources against this lane's target
+  auto flush = [&]() {
+    __syncwarp();
+    for (int q = 0; q < cnt; ++q) {
+      const float4* rec = s_rec[wid][q];
+      int2 meta = s_meta[wid][q];
+      float dx = ti[0].x - rec[0].x, dy = ti[0].y - rec[0].y, dz = ti[0].z - rec[0].z;
+      float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      bool in = r2 <= a.pp.reach2;
+      int64_t row_j = -1;
+      if (live && fabsf(r2 - a.pp.reach2) <= a.pp.reach2 * 2.44140625e-4f) {
+        row_j = T.tperm[meta.x];
+        in = exact_r2(a, row_i, row_j, meta.y & 31) <= reach2_64;
+      }
+      if (!a.include_self && meta.x == k_i && (meta.y & 31) == 13) in = false;
+      if (!in) continue;
+      if (live && (meta.y >> 8)) nin += 1;
+      float phi[NC];
+      if (KID == KID_NEIGHBOR_COUNT) {
+        bool c4 = r2 <= thr_n;
+        if (live && fabsf(r2 - thr_n) <= thr_n * 2.44140625e-4f) {
+          if (row_j < 0) row_j = T.tperm[meta.x];
+          c4 = exact_r2(a, row_i, row_j, meta.y & 31) <= thr_n64;
+        }
+        phi[0] = c4 ? 1.0f : 0.0f;
+      } else {
+        P::pair(ti, rec, dx, dy, dz, r2, a.pp, phi);
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (DET) {
+          float v = phi[c] * a.scale[c];
+          if (!(fabsf(v) <= 7.2057594e16f)) bad |= (v == v && fabsf(v) != INFINITY) ? 2 : 1;
+          else iacc[c] += __float2ll_rn(v);
+        } else {
+          acc[c] += phi[c];
+        }
+      }
+    }
+    __syncwarp();
+    cnt = 0;
+  };
+  for (int64_t e = e0; e < e1; ++e) {
+    int B = a.ent_src[e];
+    int cw = a.ent_code[e];
+    int code = cw & 31;
+    double oB[3] = {T.origin[3 * B], T.origin[3 * B + 1], T.origin[3 * B + 2]};
+    int sh[3] = {code / 9 - 1, (code / 3) % 3 - 1, code % 3 - 1};
+    float D[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) D[d] = (float)((oA[d] - oB[d]) - (double)sh[d] * a.L);
+    int64_t u0 = T.tile_ptr[B], u1 = T.tile_ptr[B + 1];
+    for (int64_t ub = u0; ub < u1; ub += 32) {
+      int64_t u = ub + lane;
+      bool pass = false;
+      if (u < u1) {
+        float4 lo = T.tile_lo[u], hi = T.tile_hi[u];
+        float R = Rt;
+        if (KID == KID_HYDRO_FORCE) R = fminf(a.cull_reach, 2.0f * fmaxf(hmax_t, lo.w) * 1.0001f);
+        float gx = fmaxf(fmaxf((lo.x - D[0]) - thi.x, tlo.x - (hi.x - D[0])), 0.0f);
+        float gy = fmaxf(fmaxf((lo.y - D[1]) - thi.y, tlo.y - (hi.y - D[1])), 0.0f);
+        float gz = fmaxf(fmaxf((lo.z - D[2]) - thi.z, tlo.z - (hi.z - D[2])), 0.0f);
+        pass = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) <= R * R;
+      }
+      unsigned tm = __ballot_sync(0xffffffffu, pass);
+      while (tm) {
+        int j = __ffs(tm) - 1;
+        tm &= tm - 1;
+        int64_t uu = ub + j;
+        int n_u = T.tile_n[uu];
+        int k_j = T.tile_start[uu] + lane;
+        bool ok = false;
+        float4 sj[NP];
+        if (lane < n_u) {
+          sj[0] = a.P0[k_j];
+          if (NP > 1) sj[1] = a.P1[k_j];
+          if (NP > 2) sj[2] = a.P2[k_j];
+          sj[0].x -= D[0]; sj[0].y -= D[1]; sj[0].z -= D[2];
+          float R = Rt;
+          if (KID == KID_HYDRO_FORCE) R = fminf(a.cull_reach, 2.0f * fmaxf(hmax_t, sj[1].w) * 1.0001f);
+          ok = box_gap2(sj[0].x, sj[0].y, sj[0].z, tlo, thi) <= R * R;
+        }
+        unsigned sm = __ballot_sync(0xffffffffu, ok);
+        if (cnt + __popc(sm) > kStage) flush();
+        if (ok) {
+          int slot = cnt + __popc(sm & lanemask_lt());
+#pragma unroll
+          for (int p = 0; p < NP; ++p) s_rec[wid][slot][p] = sj[p];
+          s_meta[wid][slot] = make_int2(k_j, cw);
+        }
+        cnt += __popc(sm);
+      }
+    }
+    flush();  // per entry: keeps error attribution per leaf pair
+    if (!DET) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) if (!isfinite(acc[c])) bad |= 1;
+    }
+    unsigned bm = __ballot_sync(0xffffffffu, live && bad);
+    if (bm) {
+      int kind = __shfl_sync(0xffffffffu, bad, __ffs(bm) - 1);
+      if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e * 4 + ((kind & 1) ? 1 : 2)));
+      return;
+    }
+  }
+  if (live && a.write_out) {
+    if (DET) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c < a.nchan) a.out_int[row_i * a.nchan + c] += iacc[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c < a.nchan) a.out_flt[row_i * a.nchan + c] += (double)acc[c];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nin += __shfl_xor_sync(0xffffffffu, nin, o);
+  if (lane == 0 && nin) atomicAdd(a.in_count, nin);
+}
+
+// ---------------------------------------------------------------- driver
+struct EvalWs {
+  Tiling T;
+  uint64_t* keys; uint32_t* vals;
+  int32_t *e_src, *e_code, *e_orig, *s_src, *s_code, *s_orig;
+  int64_t *rev_flag, *rev_off, *ent_cnt, *ent_ptr, *n_tiles_dev, *tot;
+  float4 *P0, *P1, *P2;
+  unsigned long long* dev_cnt;  // [0]=f [1]=g [2]=in_count [3]=err_key
+};
+
+static int64_t eval_tile_cap(int64_t n, int64_t n_leaves) { return n / kTileMax + n_leaves + 1; }
+
+static void carve_eval(Arena& ws, const HbEvalArgs* a, EvalWs& w, int64_t E) {
+  int64_t n = a->n, nl = a->n_leaves, tc = eval_tile_cap(n, nl);
+  Tiling& T = w.T;
+  T.n_leaves = nl; T.n_tiles_cap = tc;
+  T.sel_cnt = ws.take<int64_t>(nl + 1); T.sel_off = ws.take<int64_t>(nl + 1);
+  T.tile_cnt = ws.take<int64_t>(nl + 1); T.tile_ptr = ws.take<int64_t>(nl + 1);
+  T.tperm = ws.take<int32_t>(n + 1);
+  T.tile_start = ws.take<int32_t>(tc); T.tile_n = ws.take<int32_t>(tc); T.tile_leaf = ws.take<int32_t>(tc);
+  T.tile_lo = ws.take<float4>(tc); T.tile_hi = ws.take<float4>(tc);
+  T.origin = ws.take<double>(3 * nl + 3);
+  T.overflow = ws.take<int>(1);
+  w.keys = ws.take<uint64_t>(E + 1); w.vals = ws.take<uint32_t>(E + 1);
+  w.e_src = ws.take<int32_t>(E + 1); w.e_code = ws.take<int32_t>(E + 1); w.e_orig = ws.take<int32_t>(E + 1);
+  w.s_src = ws.take<int32_t>(E + 1); w.s_code = ws.take<int32_t>(E + 1); w.s_orig = ws.take<int32_t>(E + 1);
+  w.rev_flag = ws.take<int64_t>(a->n_pairs + 1); w.rev_off = ws.take<int64_t>(a->n_pairs + 1);
+  w.ent_cnt = ws.take<int64_t>(nl + 1); w.ent_ptr = ws.take<int64_t>(nl + 1);
+  w.n_tiles_dev = ws.take<int64_t>(1); w.tot = ws.take<int64_t>(1);
+  w.P0 = ws.take<float4>(n + 1); w.P1 = ws.take<float4>(n + 1); w.P2 = ws.take<float4>(n + 1);
+  w.dev_cnt = ws.take<unsigned long long>(5);
+}
+
+template <int KID>
+static void launch_eval(const EvalDev& d, int64_t tcap, const int64_t* ntd, bool det, cudaStream_t st) {
+  unsigned grid = grid_for(tcap, kEvalWarps);
+  if (det) k_eval<KID, true><<<grid, kEvalWarps * 32, 0, st>>>(d, tcap, ntd);
+  else k_eval<KID, false><<<grid, kEvalWarps * 32, 0, st>>>(d, tcap, ntd);
+}
+
+static int kid_selects_gas(int kid) {
+  return kid == KID_DENSITY || kid == KID_NEIGHBOR_COUNT || kid == KID_CRK_MOMENTS ||
+         kid == KID_HYDRO_FORCE || kid == KID_CRK_INTERP;
+}
+
+static int build_tiling(const HbEvalArgs* a, EvalWs& w, int sel, int kid, Arena& ws,
+                        cudaStream_t st, HbError* err) {
+  int64_t nl = a->n_leaves;
+  Tiling& T = w.T;
+  HB_CUDA_TRY(cudaMemsetAsync(T.overflow, 0, sizeof(int), st));
+  k_tile_count<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, a->leaf_start, a->leaf_end, a->state,
+                                                       sel, T.sel_cnt, T.tile_cnt);
+  HB_LAUNCH_CHECK();
+  {
+    Arena s = ws;
+    int rc = exclusive_scan_i64(T.sel_cnt, T.sel_off, nl, T.sel_off + nl, s, st, err);
+    if (rc) return rc;
+    Arena s2 = ws;
+    rc = exclusive_scan_i64(T.tile_cnt, T.tile_ptr, nl, w.n_tiles_dev, s2, st, err);
+    if (rc) return rc;
+    HB_CUDA_TRY(cudaMemcpyAsync(T.tile_ptr + nl, w.n_tiles_dev, sizeof(int64_t),
+                                cudaMemcpyDeviceToDevice, st));
+  }
+  k_tile_build<<<(unsigned)nl, kTileBuildBlock, 0, st>>>(T, a->leaf_start, a->leaf_end, a->state,
+                                                         a->pshift, a->side_length, sel);
+  HB_LAUNCH_CHECK();
+  int64_t tcap = T.n_tiles_cap;
+  k_tile_boxes<<<grid_for(tcap * 32, 256), 256, 0, st>>>(tcap, w.n_tiles_dev, T, a->state,
+                                                        a->pshift, a->side_length);
+  HB_LAUNCH_CHECK();
+  k_pack<<<grid_for(tcap * 32, 256), 256, 0, st>>>(kid, tcap, w.n_tiles_dev, T, a->state,
+                                                   a->pshift, a->aux, a->naux, a->side_length,
+                                                   w.P0, w.P1, w.P2);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
+
+int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
+  int64_t E = a->n_pairs * (a->mirror ? 2 : 1);
+  EvalWs w;
+  carve_eval(ws, a, w, E);
+  if (ws.dry) {
+    Arena s1 = ws, s2 = ws, s3 = ws;
+    radix_sort_u64_u32(w.keys, w.vals, E, 40, s1, st, err);
+    exclusive_scan_i64(nullptr, nullptr, a->n_leaves + 1, nullptr, s2, st, err);
+    exclusive_scan_i64(nullptr, nullptr, a->n_pairs + 1, nullptr, s3, st, err);
+    size_t mx = s1.used;
+    if (s2.used > mx) mx = s2.used;
+    if (s3.used > mx) mx = s3.used;
+    ws.used = mx;
+    return HB_OK;
+  }
+  if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (eval)");
+  for (int k = 0; k < 8; ++k) a->counters[k] = 0;
+  if (a->nchan < 1 || a->nchan > 10) return set_err(err, HB_CONTRACT, "nchan must be 1..10");
+  if (a->n <= 0 || a->n_pairs <= 0 || a->n_leaves <= 0) return HB_OK;
+  if (a->n >= (1LL << 31)) return set_err(err, HB_CONTRACT, "too many rows for one evaluation");
+  int sel = kid_selects_gas(a->kid);
+  int64_t nl = a->n_leaves, n = a->n;
+  // receiver CSR
+  int64_t n_rev = 0;
+  if (a->mirror) {
+    k_rev_flags<<<grid_for(a->n_pairs, 256), 256, 0, st>>>(a->n_pairs, a->pair_a, a->pair_b,
+                                                           a->pair_shift, w.rev_flag);
+    HB_LAUNCH_CHECK();
+    Arena s = ws;
+    int rc = exclusive_scan_i64(w.rev_flag, w.rev_off, a->n_pairs, w.tot, s, st, err);
+    if (rc) return rc;
+    HB_CUDA_TRY(cudaMemcpyAsync(&n_rev, w.tot, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HB_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  int64_t En = a->n_pairs + n_rev;
+  k_expand<<<grid_for(a->n_pairs, 256), 256, 0, st>>>(a->n_pairs, a->mirror, a->pair_a, a->pair_b,
+                                                      a->pair_shift, w.rev_off, w.keys, w.vals,
+                                                      w.e_src, w.e_code, w.e_orig);
+  HB_LAUNCH_CHECK();
+  {
+    int bits = 1;
+    while ((1LL << bits) < nl) ++bits;
+    Arena s = ws;
+    int rc = radix_sort_u64_u32(w.keys, w.vals, En, bits, s, st, err);
+    if (rc) return rc;
+  }
+  HB_CUDA_TRY(cudaMemsetAsync(w.ent_cnt, 0, (nl + 1) * sizeof(int64_t), st));
+  k_recv_hist<<<grid_for(En, 256), 256, 0, st>>>(En, w.keys, w.ent_cnt);
+  HB_LAUNCH_CHECK();
+  {
+    Arena s = ws;
+    int rc = exclusive_scan_i64(w.ent_cnt, w.ent_ptr, nl + 1, nullptr, s, st, err);
+    if (rc) return rc;
+  }
+  k_gather_entries<<<grid_for(En, 256), 256, 0, st>>>(En, w.vals, w.e_src, w.e_code, w.e_orig,
+                                                      w.s_src, w.s_code, w.s_orig);
+  HB_LAUNCH_CHECK();
+  Tiling& T = w.T;
+  int rc0 = build_tiling(a, w, sel, a->kid, ws, st, err);
+  if (rc0) return rc0;
+  int64_t tcap = T.n_tiles_cap;
+  HB_CUDA_TRY(cudaMemsetAsync(w.dev_cnt, 0, 3 * sizeof(unsigned long long), st));
+  HB_CUDA_TRY(cudaMemsetAsync(w.dev_cnt + 3, 0xff, sizeof(unsigned long long), st));
+  k_sched_counters<<<grid_for(a->n_pairs, 256), 256, 0, st>>>(a->n_pairs, a->pair_a, a->pair_b,
+                                                              a->leaf_start, a->leaf_end, a->W2,
+                                                              w.dev_cnt);
+  HB_LAUNCH_CHECK();
+  EvalDev d;
+  d.T = T; d.ent_ptr = w.ent_ptr; d.ent_src = w.s_src; d.ent_code = w.s_code;
+  d.P0 = w.P0; d.P1 = w.P1; d.P2 = w.P2; d.state = a->state; d.pshift = a->pshift;
+  d.L = a->side_length; d.reach = a->reach;
+  d.pp.p0 = (float)a->params[0]; d.pp.p1 = (float)a->params[1];
+  d.pp.inv_rs = a->params[0] != 0.0 ? (float)(1.0 / a->params[0]) : 0.0f;
+  d.pp.reach2 = (float)(a->reach * a->reach);
+  d.cull_reach = (float)(a->reach * (1.0 + 1e-4)) + 1e-30f;
+  d.include_self = a->include_self; d.nchan = a->nchan;
+  for (int c = 0; c < 10; ++c) d.scale[c] = (float)a->scales[c];
+  d.out_flt = a->out_flt; d.out_int = a->out_int; d.write_out = 1;
+  d.in_count = w.dev_cnt + 2; d.err_key = w.dev_cnt + 3;
+  bool det = a->deterministic != 0;
+  switch (a->kid) {
+    case KID_COUNTING: launch_eval<KID_COUNTING>(d, tcap, w.n_tiles_dev, det, st); break;
+    case KID_GRAVITY: launch_eval<KID_GRAVITY>(d, tcap, w.n_tiles_dev, det, st); break;
+    case KID_GRAV_POT: launch_eval<KID_GRAV_POT>(d, tcap, w.n_tiles_dev, det, st); break;
+    case KID_DENSITY: launch_eval<KID_DENSITY>(d, tcap, w.n_tiles_dev, det, st); break;
+    case KID_CRK_MOMENTS: launch_eval<KID_CRK_MOMENTS>(d, tcap, w.n_tiles_dev, det, st); break;
+    case KID_HYDRO_FORCE: launch_eval<KID_HYDRO_FORCE>(d, tcap, w.n_tiles_dev, det, st); break;
+    case KID_NEIGHBOR_COUNT: launch_eval<KID_NEIGHBOR_COUNT>(d, tcap, w.n_tiles_dev, det, st); break;
+    case KID_STUB_ZERO: launch_eval<KID_STUB_ZERO>(d, tcap, w.n_tiles_dev, det, st); break;
+    case KID_CRK_INTERP: launch_eval<KID_CRK_INTERP>(d, tcap, w.n_tiles_dev, det, st); break;
+    default: return set_err(err, HB_CONTRACT, "unknown kernel id");
+  }
+  HB_LAUNCH_CHECK();
+  if (a->exact_counters && sel) {
+    // the reference counts pairs in reach over every species (hb/kernels.py:356-359)
+    HB_CUDA_TRY(cudaMemsetAsync(w.dev_cnt + 2, 0, sizeof(unsigned long long), st));
+    int rc = build_tiling(a, w, 0, KID_COUNTING, ws, st, err);
+    if (rc) return rc;
+    EvalDev c = d;
+    c.T = w.T;
+    c.write_out = 0;
+    c.err_key = w.dev_cnt + 4;
+    launch_eval<KID_COUNTING>(c, T.n_tiles_cap, w.n_tiles_dev, false, st);
+    HB_LAUNCH_CHECK();
+  }
+  unsigned long long hc[4];
+  int ovf = 0;
+  HB_CUDA_TRY(cudaMemcpyAsync(hc, w.dev_cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  HB_CUDA_TRY(cudaMemcpyAsync(&ovf, T.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HB_CUDA_TRY(cudaStreamSynchronize(st));
+  if (ovf) return set_err(err, HB_CONTRACT, "leaf exceeds the tiling capacity (2048 members)");
+  int64_t W2 = a->W2;
+  a->counters[0] = (int64_t)hc[0];
+  a->counters[1] = (int64_t)hc[1];
+  a->counters[2] = (int64_t)hc[1] * W2;
+  a->counters[3] = (int64_t)hc[1] * W2 * W2;
+  a->counters[4] = (int64_t)hc[2];
+  if (hc[3] != ~0ull) {
+    int64_t e = (int64_t)(hc[3] / 4);
+    int kind = (int)(hc[3] % 4);
+    int32_t orig = 0;
+    HB_CUDA_TRY(cudaMemcpy(&orig, w.s_orig + e, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    int64_t la = 0, lb = 0;
+    HB_CUDA_TRY(cudaMemcpy(&la, a->pair_a + orig, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    HB_CUDA_TRY(cudaMemcpy(&lb, a->pair_b + orig, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    a->counters[5] = kind; a->counters[6] = la; a->counters[7] = lb;
+    if (err) { err->leaf_a = la; err->leaf_b = lb; }
+    return set_err(err, kind == 1 ? HB_NONFINITE : HB_OVERFLOW,
+                   kind == 1 ? "non-finite partial" : "accumulator overflow");
+  }
+  return HB_OK;
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" size_t hb_eval_pairs_workspace(const HbEvalArgs* a) {
+  Arena ws;
+  ws.dry = true;
+  HbEvalArgs c = *a;
+  eval_pairs(&c, ws, nullptr, nullptr);
+  return ws.used + 1024;
+}
+
+extern "C" int hb_eval_pairs(HbEvalArgs* a, void* wsp, size_t ws_bytes, void* stream, HbError* err) {
+  if (err) *err = HbError{};
+  Arena ws;
+  ws.base = (char*)wsp; ws.cap = ws_bytes;
+  return eval_pairs(a, ws, (cudaStream_t)stream, err);
+}

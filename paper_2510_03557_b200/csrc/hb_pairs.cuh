@@ -1,0 +1,167 @@
+// hb_pairs.cuh -- pair-kernel physics on FP32 leaf-relative coordinates.
+//
+// Each policy restates one branch of _pair_phi (hb/kernels.py:143-278) with
+// its _fill_partials pieces (hb/kernels.py:102-140), as a per-ordered-pair
+// function over packed per-particle float4 records.  Operation counts follow
+// the FP32 pipe, not the reference's float64; tolerances are stated in tests.
+#pragma once
+#include "hb_common.cuh"
+
+namespace hb {
+
+enum {
+  KID_COUNTING = 0, KID_GRAVITY = 1, KID_GRAV_POT = 2, KID_DENSITY = 3, KID_CRK_MOMENTS = 4,
+  KID_HYDRO_FORCE = 5, KID_NEIGHBOR_COUNT = 6, KID_STUB_ZERO = 7, KID_CRK_INTERP = 8
+};
+enum { C_X = 0, C_Y, C_Z, C_VX, C_VY, C_VZ, C_M, C_H, C_RHO, C_P, C_CS, C_SP, NCOL };
+
+constexpr float kSigma = 0.318309886183790671f;  // 1/pi (hb/kernels.py:63)
+
+struct PairParams {
+  float p0, p1;        // kernel params (rs, eps2) or (alpha, beta)
+  float inv_rs;
+  float reach2;        // reach^2 in FP32
+};
+
+// cubic spline body: W(q) h^3/sigma, q < 2 (hb/kernels.py:71-81)
+__device__ __forceinline__ float w_body(float q) {
+  float t = 2.0f - q;
+  float outer = 0.25f * t * t * t;
+  float inner = fmaf(q * q, fmaf(0.75f, q, -1.5f), 1.0f);
+  return q < 1.0f ? inner : (q < 2.0f ? outer : 0.0f);
+}
+
+// (dW/dr)/r * h^5/sigma for the cubic spline (hb/kernels.py:83-93); finite at 0
+__device__ __forceinline__ float gradw_body(float q) {
+  float t = 2.0f - q;
+  float outer = -0.75f * t * t * __frcp_rn(fmaxf(q, 1e-30f));
+  float inner = fmaf(2.25f, q, -3.0f);
+  return q < 1.0f ? inner : (q < 2.0f ? outer : 0.0f);
+}
+
+// S(x) = erfc(x) + 2x/sqrt(pi) exp(-x^2) (hb/kernels.py:96-99)
+__device__ __forceinline__ float grav_s(float x) {
+  return erfcf(x) + 1.1283791670955126f * x * __expf(-x * x);
+}
+
+// Policies: NP = float4 records per particle, NC channels, SEL = 1 gas-only.
+// pair(): returns phi for target i (ti) and source j (sj) given dx = x_i - x_j.
+template <int KID> struct Pol;
+
+template <> struct Pol<KID_COUNTING> {
+  static constexpr int NP = 1, NC = 1, SEL = 0;
+  static constexpr bool HVAR = false;
+  __device__ static void pair(const float4*, const float4*, float, float, float, float,
+                              const PairParams&, float* phi) { phi[0] = 1.0f; }
+};
+template <> struct Pol<KID_STUB_ZERO> {
+  static constexpr int NP = 1, NC = 1, SEL = 0;
+  static constexpr bool HVAR = false;
+  __device__ static void pair(const float4*, const float4*, float, float, float, float,
+                              const PairParams&, float* phi) { phi[0] = 0.0f; }
+};
+// gravity: record P0 = (x, y, z, m)
+template <> struct Pol<KID_GRAVITY> {
+  static constexpr int NP = 1, NC = 3, SEL = 0;
+  static constexpr bool HVAR = false;
+  __device__ static void pair(const float4* ti, const float4* sj, float dx, float dy, float dz,
+                              float r2, const PairParams& pp, float* phi) {
+    float soft = r2 + pp.p1;
+    float rinv = rsqrtf(soft);
+    float r = r2 > 0.0f ? r2 * rsqrtf(r2) : 0.0f;
+    float s = grav_s(r * pp.inv_rs) * (rinv * rinv * rinv);
+    float w = (ti[0].w * sj[0].w) * s;
+    phi[0] = -(w * dx); phi[1] = -(w * dy); phi[2] = -(w * dz);
+  }
+};
+template <> struct Pol<KID_GRAV_POT> {
+  static constexpr int NP = 1, NC = 1, SEL = 0;
+  static constexpr bool HVAR = false;
+  __device__ static void pair(const float4* ti, const float4* sj, float, float, float, float r2,
+                              const PairParams& pp, float* phi) {
+    float r = r2 > 0.0f ? r2 * rsqrtf(r2) : 0.0f;
+    phi[0] = -(ti[0].w * sj[0].w) * erfcf(r * pp.inv_rs) * rsqrtf(r2 + pp.p1);
+  }
+};
+// density: target P0 = (x,y,z,h), P1.x = sigma/h^3 ; source P0.w = m ... both share layout:
+// P0 = (x, y, z, m), P1 = (h, sigma/h^3, 1/h, 0)
+template <> struct Pol<KID_DENSITY> {
+  static constexpr int NP = 2, NC = 1, SEL = 1;
+  static constexpr bool HVAR = true;
+  __device__ static void pair(const float4* ti, const float4* sj, float, float, float, float r2,
+                              const PairParams&, float* phi) {
+    float q = sqrtf(r2) * ti[1].z;
+    phi[0] = sj[0].w * (ti[1].y * w_body(q));
+  }
+};
+template <> struct Pol<KID_NEIGHBOR_COUNT> {
+  static constexpr int NP = 2, NC = 1, SEL = 1;
+  static constexpr bool HVAR = true;
+  __device__ static void pair(const float4* ti, const float4*, float, float, float, float r2,
+                              const PairParams&, float* phi) {
+    float h = ti[1].x;
+    phi[0] = r2 <= 4.0f * h * h ? 1.0f : 0.0f;  // exact predicate re-checked in float64 near the edge
+  }
+};
+// CRK moments: source P0.w = V = m/rho (hb/kernels.py:119-121)
+template <> struct Pol<KID_CRK_MOMENTS> {
+  static constexpr int NP = 2, NC = 10, SEL = 1;
+  static constexpr bool HVAR = true;
+  __device__ static void pair(const float4* ti, const float4* sj, float dx, float dy, float dz,
+                              float r2, const PairParams&, float* phi) {
+    float q = sqrtf(r2) * ti[1].z;
+    float w = sj[0].w * (ti[1].y * w_body(q));
+    phi[0] = w;
+    phi[1] = -(w * dx); phi[2] = -(w * dy); phi[3] = -(w * dz);
+    float wx = w * dx, wy = w * dy;
+    phi[4] = wx * dx; phi[5] = wx * dy; phi[6] = wx * dz;
+    phi[7] = wy * dy; phi[8] = wy * dz; phi[9] = (w * dz) * dz;
+  }
+};
+// hydro: P0 = (x,y,z,m), P1 = (vx,vy,vz,h), P2 = (P/rho^2, c_s, rho, sigma/h^5)
+template <> struct Pol<KID_HYDRO_FORCE> {
+  static constexpr int NP = 3, NC = 5, SEL = 1;
+  static constexpr bool HVAR = true;
+  __device__ static void pair(const float4* ti, const float4* sj, float dx, float dy, float dz,
+                              float r2, const PairParams& pp, float* phi) {
+    float r = sqrtf(r2);
+    float hi = ti[1].w, hj = sj[1].w;
+    float gi = gradw_body(r * __frcp_rn(hi)) * ti[2].w;
+    float gj = gradw_body(r * __frcp_rn(hj)) * sj[2].w;
+    float gw = 0.5f * (gi + gj);
+    float vx = ti[1].x - sj[1].x, vy = ti[1].y - sj[1].y, vz = ti[1].z - sj[1].z;
+    float vdotr = fmaf(vz, dz, fmaf(vy, dy, vx * dx));
+    float visc = 0.0f;
+    if (vdotr < 0.0f) {
+      float hbar = 0.5f * (hi + hj);
+      float cbar = 0.5f * (ti[2].y + sj[2].y);
+      float rhobar = 0.5f * (ti[2].z + sj[2].z);
+      float mu = hbar * vdotr / fmaf(0.01f * hbar, hbar, r2);
+      visc = fmaf(pp.p1 * mu, mu, -(pp.p0 * cbar * mu)) / rhobar;
+    }
+    float mm = ti[0].w * sj[0].w;
+    float w = mm * (ti[2].x + sj[2].x + visc) * gw;
+    bool z = gw == 0.0f;
+    phi[0] = z ? 0.0f : -(w * dx);
+    phi[1] = z ? 0.0f : -(w * dy);
+    phi[2] = z ? 0.0f : -(w * dz);
+    float work = mm * vdotr * gw;
+    phi[3] = z ? 0.0f : fmaf(0.5f, visc, ti[2].x) * work;
+    phi[4] = z ? 0.0f : fmaf(0.5f, visc, sj[2].x) * work;
+  }
+};
+// corrected interpolation: target P1 = (h, sigma/h^3, 1/h, A), P2 = (Bx, By, Bz, 0);
+// source P0.w = V = m/rho, P1.x... source F in P2.w  (aux columns [F, A, Bx, By, Bz])
+template <> struct Pol<KID_CRK_INTERP> {
+  static constexpr int NP = 3, NC = 1, SEL = 1;
+  static constexpr bool HVAR = true;
+  __device__ static void pair(const float4* ti, const float4* sj, float dx, float dy, float dz,
+                              float r2, const PairParams&, float* phi) {
+    float q = sqrtf(r2) * ti[1].z;
+    float wk = ti[1].y * w_body(q);
+    float corr = ti[1].w * fmaf(ti[2].z, dz, fmaf(ti[2].y, dy, fmaf(ti[2].x, dx, 1.0f)));
+    phi[0] = sj[0].w * sj[2].w * corr * wk;
+  }
+};
+
+}  // namespace hb

@@ -1,0 +1,272 @@
+"""Generate the golden vectors that pin the oracle and the CUDA path.
+
+Runs the REFERENCE implementation (hydrobox, /root/reference/pkg/src) in this
+container and stores its inputs and outputs as small compressed .npz files in
+tests/golden/.  The reference cannot travel to the GPU box; these fixtures do.
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Every fixture stores raw arrays only (no pickled objects).  Sources for each
+recipe are cited inline (hb/ = /root/reference/pkg/src/hydrobox/).
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+from hydrobox.box import BoxGeometry  # noqa: E402
+from hydrobox.checks import _mixed_set  # noqa: E402  (hb/checks.py:90-97)
+from hydrobox.cmtree import (InteractionList, assemble_interaction_lists,  # noqa: E402
+                             build_mesh_and_leaves)
+from hydrobox.config import SimConfig  # noqa: E402
+from hydrobox.domain import build_overload, decompose  # noqa: E402
+from hydrobox.gravity import ForceSplit, short_range_gravity_kernel  # noqa: E402
+from hydrobox.hydro import (adapt_smoothing_length, compute_crk_coefficients,  # noqa: E402
+                            compute_density, compute_hydro_accel,
+                            corrected_interpolate, refresh_eos_columns)
+from hydrobox.ic import make_clustered_ic, make_lattice_ic  # noqa: E402
+from hydrobox.kernels import (counting_kernel, crk_interp_kernel,  # noqa: E402
+                              crk_moments_kernel, density_kernel,
+                              gravity_potential_kernel, hydro_force_kernel,
+                              neighbor_count_kernel)
+from hydrobox.lane import EvalMode, eval_interaction_list, reference_pair_sum  # noqa: E402
+from hydrobox.stepper import unordered_due_pairs  # noqa: E402
+
+REL, DET = EvalMode.RELAXED, EvalMode.DETERMINISTIC
+
+
+def particle_arrays(p, prefix=""):
+    return {prefix + "pos": p.pos.copy(), prefix + "vel": p.vel.copy(),
+            prefix + "mass": p.mass.copy(), prefix + "smoothing": p.smoothing.copy(),
+            prefix + "internal_energy": p.internal_energy.copy(),
+            prefix + "density": p.density.copy(), prefix + "species": p.species.copy(),
+            prefix + "ghost": p.ghost.copy(), prefix + "image_shift": p.image_shift.copy(),
+            prefix + "global_id": p.global_id.copy(), prefix + "ghost_src": p.ghost_src.copy(),
+            prefix + "timestep_level": p.timestep_level.copy()}
+
+
+def mesh_arrays(mesh, prefix="mesh_"):
+    return {prefix + "leaf_start": mesh.leaf_start, prefix + "leaf_end": mesh.leaf_end,
+            prefix + "leaf_lo": mesh.leaf_lo, prefix + "leaf_hi": mesh.leaf_hi,
+            prefix + "leaf_ghost_only": mesh.leaf_ghost_only,
+            prefix + "leaf_bin": mesh.leaf_bin, prefix + "leaf_level": mesh.leaf_level,
+            prefix + "bin_count": mesh.bin_count, prefix + "bin_width": mesh.bin_width,
+            prefix + "periodic": mesh.periodic_axis, prefix + "bin_ptr": mesh._bin_ptr,
+            prefix + "bin_ids": mesh._bin_ids}
+
+
+def lane_fixture():
+    """check_lane_oracle recipe (hb/checks.py:103-134) for three configs, both modes."""
+    box = BoxGeometry(1.0)
+    out = {}
+    rng = np.random.default_rng(101)
+    cfg_ns = []
+    for c in range(20):
+        n = int(rng.integers(100, 2200))
+        cfg_ns.append(n)
+    picks = [c for c in range(20) if cfg_ns[c] <= 1300][:3]
+    out["configs"] = np.array(picks)
+    for c in picks:
+        n = cfg_ns[c]
+        p = _mixed_set(n, 101 + c, box)
+        spacing = 1.0 / n ** (1 / 3)
+        reach = min(4.0 * spacing, 0.45)
+        mesh = build_mesh_and_leaves(p, box, max(reach, 0.2), 48)
+        state = p.state_matrix(5.0 / 3.0)
+        ilist = assemble_interaction_lists(mesh, reach, 0)
+        k = f"c{c}_"
+        out[k + "state"] = state
+        out[k + "reach"] = np.float64(reach)
+        out[k + "spacing"] = np.float64(spacing)
+        out[k + "la"], out[k + "lb"], out[k + "ls"] = ilist.leaf_a, ilist.leaf_b, ilist.shift
+        out.update(mesh_arrays(mesh, k + "mesh_"))
+        aux = np.zeros((n, 5))
+        arng = np.random.default_rng(7 + c)
+        aux[:, 0] = arng.normal(size=n)
+        aux[:, 1] = arng.uniform(0.5, 1.5, n)
+        aux[:, 2:5] = arng.normal(0, 0.3, (n, 3))
+        out[k + "aux"] = aux
+        kernels = {
+            "counting": counting_kernel(reach),
+            "gravity": short_range_gravity_kernel(ForceSplit(r_s=reach / 5.0, r_cut=reach),
+                                                  spacing / 50),
+            "grav_pot": gravity_potential_kernel(reach / 5.0, reach, spacing / 50),
+            "density": density_kernel(reach),
+            "neighbor_count": neighbor_count_kernel(reach),
+            "crk_moments": crk_moments_kernel(reach),
+            "hydro": hydro_force_kernel(reach),
+            "crk_interp": crk_interp_kernel(reach),
+        }
+        for name, ker in kernels.items():
+            kx = aux if ker.n_aux else None
+            for mode, tag in ((REL, "rel"), (DET, "det")):
+                res = eval_interaction_list(ker, ilist, state, mesh, mode=mode,
+                                            workers=1, aux=kx)
+                out[k + f"{name}_{tag}"] = res.values
+                if tag == "det":
+                    out[k + f"{name}_detint"] = res.int_acc
+                out[k + f"{name}_{tag}_counters"] = np.array(
+                    [res.counters[x] for x in ("f_evals", "g_evals", "rotations",
+                                               "pairs_scheduled", "pairs_in_reach")])
+            # worker split (relaxed merge order) for one kernel
+            if name == "gravity":
+                res3 = eval_interaction_list(ker, ilist, state, mesh, mode=REL, workers=3)
+                out[k + "gravity_rel_w3"] = res3.values
+            ref, absum = reference_pair_sum(ker, state, box.side_length, mode=REL, aux=kx)
+            out[k + f"{name}_allpairs"] = ref
+            out[k + f"{name}_allpairs_abs"] = absum
+        # mirror evaluation over the unordered list (hb/stepper.py:79-100,136)
+        pa, pb, psh, plev = unordered_due_pairs(ilist, mesh)
+        out[k + "ua"], out[k + "ub"], out[k + "us"] = pa, pb, psh
+        sub = InteractionList(pa, pb, ilist.reach, 0, psh)
+        for name in ("gravity", "hydro"):
+            ker = kernels[name]
+            for mode, tag in ((REL, "rel"), (DET, "det")):
+                res = eval_interaction_list(ker, sub, state, mesh, mode=mode, mirror=True)
+                out[k + f"{name}_mirror_{tag}"] = res.values
+    return out
+
+
+def mesh_fixture():
+    """build_mesh_and_leaves + assemble_interaction_lists (hb/cmtree.py:125-196, 303-337)."""
+    box = BoxGeometry(1.0)
+    out = {}
+    cases = []
+    # (a) random mixed set on the bare periodic mesh, leaf size 48
+    p = _mixed_set(3000, 77, box)
+    cases.append(("rand", p, 0.2, 48, None, None, [0.07, 0.2]))
+    # (b) unjittered two-species lattice with (1,1,1) overload: exact coordinate ties
+    p = make_lattice_ic(6, box, 0.0, seed=1)
+    w = 0.3
+    doms = decompose(box, (1, 1, 1), w)
+    rs = build_overload(p, doms, box, (1, 1, 1))[0][0]
+    cases.append(("lat", rs, 0.32, 64, doms[0].lo - w, doms[0].hi + w, [0.3]))
+    # (c) clustered set: deep k-d recursion inside dense bins
+    p = make_clustered_ic(10, box, seed=5)
+    cases.append(("clu", p, 0.2, 32, None, None, [0.1]))
+    # (d) 2x2x1 rank grid: one rank's overloaded working set (non-periodic x,y; periodic z)
+    p = make_lattice_ic(8, box, 0.02, seed=3)
+    w = 0.15
+    doms = decompose(box, (2, 2, 1), w)
+    rs = build_overload(p, doms, box, (2, 2, 1))[0][1]
+    d1 = doms[1]
+    cases.append(("r221", rs, 0.16, 40, d1.lo - w, d1.hi + w, [0.15]))
+    for tag, ps, bw, leaf, lo, hi, reaches in cases:
+        k = tag + "_"
+        out.update(particle_arrays(ps, k + "in_"))
+        out[k + "bin_width"] = np.float64(bw)
+        out[k + "max_leaf"] = np.int64(leaf)
+        out[k + "bounds_lo"] = np.zeros(3) if lo is None else np.asarray(lo, float)
+        out[k + "bounds_hi"] = np.ones(3) if hi is None else np.asarray(hi, float)
+        q = ps.copy()
+        mesh = build_mesh_and_leaves(q, box, bw, leaf, lo, hi)
+        out[k + "out_global_id"] = q.global_id.copy()
+        out[k + "out_image_shift"] = q.image_shift.copy()
+        out[k + "out_ghost_src"] = q.ghost_src.copy()
+        out.update(mesh_arrays(mesh, k + "mesh_"))
+        # levels for an active-depth list: deterministic pseudo-levels
+        lev = (np.arange(mesh.n_leaves) * 7919) % 3
+        out[k + "levels"] = lev
+        for ri, reach in enumerate(reaches):
+            il = assemble_interaction_lists(mesh, reach, 0)
+            out[k + f"list{ri}_reach"] = np.float64(reach)
+            out[k + f"list{ri}_a"], out[k + f"list{ri}_b"], out[k + f"list{ri}_s"] = \
+                il.leaf_a, il.leaf_b, il.shift
+        mesh.leaf_level[:] = lev
+        il = assemble_interaction_lists(mesh, reaches[0], 1)
+        out[k + "listd1_a"], out[k + "listd1_b"], out[k + "listd1_s"] = \
+            il.leaf_a, il.leaf_b, il.shift
+    return out
+
+
+def step_fixture():
+    """One s=0 force evaluation on a jittered 2x8^3 lattice, (1,1,1) overload
+    (SURVEY.md Appendix B recipe; correct ordered paths per SURVEY.md 8c)."""
+    box = BoxGeometry(1.0)
+    npd = 8
+    cfg = SimConfig()
+    cfg.n_per_dim = npd
+    cfg.pm_grid_n = 4 * npd     # r_cut = 2.5 spacings keeps the 2x8^3 overload legal
+    p = make_lattice_ic(npd, box, 0.1 / npd, seed=1234)
+    rng = np.random.default_rng(99)
+    p.vel = rng.normal(0, 0.05, p.pos.shape)     # exercise the viscosity branch
+    p.internal_energy[p.species == 1] = rng.uniform(0.5e-4, 2e-4, int((p.species == 1).sum()))
+    split = ForceSplit(r_s=cfg.split_scale, r_cut=cfg.r_cut)
+    eps = cfg.softening_for(p.n)
+    reach = max(split.r_cut, 2 * p.smoothing.max())
+    w = 1.25 * reach
+    doms = decompose(box, (1, 1, 1), w)
+    rs = build_overload(p, doms, box, (1, 1, 1))[0][0]
+    out = {}
+    out.update(particle_arrays(rs, "in_"))
+    bw = max(cfg.cm_bin_width, reach * (1 + 1e-9))
+    lo, hi = doms[0].lo - w, doms[0].hi + w
+    out["bin_width"], out["bounds_lo"], out["bounds_hi"] = np.float64(bw), lo, hi
+    out["reach"], out["r_s"], out["r_cut"], out["eps"] = (np.float64(reach), np.float64(split.r_s),
+                                                          np.float64(split.r_cut), np.float64(eps))
+    mesh = build_mesh_and_leaves(rs, box, bw, 256, lo, hi)
+    out.update(particle_arrays(rs, "built_"))
+    out.update(mesh_arrays(mesh))
+    il = assemble_interaction_lists(mesh, reach, 0)
+    out["la"], out["lb"], out["ls"] = il.leaf_a, il.leaf_b, il.shift
+    st = rs.state_matrix(5 / 3)
+    h_max = rs.smoothing.max()
+    nc = eval_interaction_list(neighbor_count_kernel(2 * h_max), il, st, mesh, mode=DET,
+                               pshift=rs.image_shift)
+    out["ncount"] = nc.values[:, 0]
+    rho = compute_density(rs, mesh, st, il, mode=REL)
+    out["rho_raw"] = rho
+    out["density"] = rs.density.copy()
+    refresh_eos_columns(st, rs, 5 / 3)
+    out["state_eos"] = st.copy()
+    crk = compute_crk_coefficients(rs, mesh, st, il, mode=REL)
+    out["crk_A"], out["crk_B"], out["crk_fallback"] = crk.A, crk.B, crk.fallback
+    out["crk_m0"], out["crk_m1"], out["crk_m2"] = crk.m0, crk.m1, crk.m2
+    g = eval_interaction_list(short_range_gravity_kernel(split, eps), il, st, mesh,
+                              mode=REL, pshift=rs.image_shift)
+    out["grav"] = g.values
+    out["grav_counters"] = np.array([g.counters["pairs_scheduled"], g.counters["pairs_in_reach"]])
+    f, e, hres = compute_hydro_accel(rs, mesh, st, il, mode=REL, mirror=False)
+    out["hydro_force"], out["hydro_edot"] = f, e
+    # corrected interpolation of a linear field (hb/hydro.py:162-178)
+    fld = 0.3 + rs.pos @ np.array([1.0, -2.0, 0.5])
+    out["interp_field"] = fld
+    out["interp"] = corrected_interpolate(rs, mesh, st, il, crk, fld, mode=REL)
+    return out
+
+
+def adapt_fixture():
+    """adapt_smoothing_length on a jittered gas lattice (hb/hydro.py:199-248)."""
+    box = BoxGeometry(1.0)
+    p = make_lattice_ic(8, box, 0.15 / 8, seed=21)
+    w = 0.3
+    doms = decompose(box, (1, 1, 1), w)
+    rs = build_overload(p, doms, box, (1, 1, 1))[0][0]
+    out = {}
+    bw = 0.32
+    mesh = build_mesh_and_leaves(rs, box, bw, 64, doms[0].lo - w, doms[0].hi + w)
+    out.update(particle_arrays(rs, "in_"))
+    out.update(mesh_arrays(mesh))
+    out["bin_width"] = np.float64(bw)
+    h = adapt_smoothing_length(rs, mesh, lambda: rs.state_matrix(5 / 3), 40, bw, mode=DET)
+    out["h_out"] = h.copy()
+    return out
+
+
+def main():
+    os.makedirs(HERE, exist_ok=True)
+    for name, fn in (("lane", lane_fixture), ("mesh", mesh_fixture),
+                     ("step", step_fixture), ("adapt", adapt_fixture)):
+        data = fn()
+        path = os.path.join(HERE, f"{name}.npz")
+        np.savez_compressed(path, **data)
+        print(f"{path}: {os.path.getsize(path) / 1e3:.0f} kB, {len(data)} arrays")
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,112 @@
+"""CPU: library loads and exports every symbol of include/hb.h; host-side
+logic (geometry, ICs, decomposition, workspace queries) without a GPU."""
+import re
+import os
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT
+
+
+def test_library_exports_header_symbols():
+    from paper_2510_03557_b200 import _native
+    lib = _native.lib()
+    header = open(os.path.join(ROOT, "include", "hb.h")).read()
+    declared = set(re.findall(r"\b(hb_[a-z0-9_]+)\s*\(", header))
+    assert declared, "no declarations parsed"
+    assert declared == set(_native.EXPORTS), declared ^ set(_native.EXPORTS)
+    for sym in declared:
+        getattr(lib, sym)
+
+
+def test_workspace_queries_are_host_only():
+    import ctypes as C
+    from paper_2510_03557_b200 import _native as N
+    lib = N.lib()
+    nb = (C.c_int64 * 3)(25, 25, 25)
+    assert lib.hb_build_mesh_workspace(1_000_000, nb, 256) > 24 * 1_000_000
+    assert lib.hb_assemble_lists_workspace(10_000, 300_000) > 0
+    assert lib.hb_leaf_capacity(1000, 8, 256) >= 8
+    a = N.HbEvalArgs()
+    a.n, a.n_pairs, a.n_leaves, a.nchan = 10_000, 5_000, 200, 3
+    assert lib.hb_eval_pairs_workspace(C.byref(a)) > 10_000 * 16
+
+
+def test_leaf_capacity_bounds_the_split():
+    from paper_2510_03557_b200 import _native as N
+    lib = N.lib()
+
+    def leaves(n, m):
+        if n == 0:
+            return 0
+        if n <= m:
+            return 1
+        mid = (n + 1) // 2
+        return leaves(mid, m) + leaves(n - mid, m)
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        nbins = int(rng.integers(1, 50))
+        m = int(rng.integers(2, 300))
+        counts = rng.integers(0, 3000, nbins)
+        assert sum(leaves(int(c), m) for c in counts) <= lib.hb_leaf_capacity(int(counts.sum()), nbins, m)
+
+
+def test_no_gpu_means_loud_failure():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2510_03557_b200 import _native
+    from paper_2510_03557_b200.errors import HydroboxError
+    with pytest.raises(HydroboxError, match="no CPU fallback"):
+        _native.torch_cuda()
+
+
+def test_zeldovich_ic_deterministic_and_normalised():
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.ic import make_zeldovich_ic, zeldovich_displacement
+    box = BoxGeometry(1.0)
+    psi = zeldovich_displacement(16, box, 0.05 / 16)
+    assert np.isclose(np.sqrt(np.mean(np.sum(psi ** 2, 1))), 0.05 / 16)
+    a = make_zeldovich_ic(16, box, 2.0)
+    b = make_zeldovich_ic(16, box, 2.0)
+    assert np.array_equal(a.pos, b.pos)
+    assert a.n == 2 * 16 ** 3 and np.all((a.pos >= 0) & (a.pos < 1))
+    assert np.isclose(a.mass.sum(), 1.0)
+    # same displacement for both species at their lattice sites
+    d = 1 / 16
+    n3 = 16 ** 3
+    diff = (a.pos[n3:] - a.pos[:n3] - 0.5 * d + 0.5) % 1.0 - 0.5
+    assert np.allclose(diff, 0, atol=1e-12)
+
+
+def test_overload_matches_golden(golden):
+    """Host-side overload construction reproduces the reference rank set."""
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.domain import build_overload, decompose
+    from paper_2510_03557_b200.ic import make_lattice_ic
+    g = golden("mesh")
+    box = BoxGeometry(1.0)
+    p = make_lattice_ic(6, box, 0.0, seed=1)
+    rs = build_overload(p, decompose(box, (1, 1, 1), 0.3), box, (1, 1, 1))[0][0]
+    for f in ("pos", "image_shift", "global_id", "ghost", "ghost_src"):
+        np.testing.assert_array_equal(getattr(rs, f), g["lat_in_" + f], err_msg=f)
+    p = make_lattice_ic(8, box, 0.02, seed=3)
+    rs = build_overload(p, decompose(box, (2, 2, 1), 0.15), box, (2, 2, 1))[0][1]
+    for f in ("pos", "image_shift", "global_id", "ghost", "ghost_src"):
+        np.testing.assert_array_equal(getattr(rs, f), g["r221_in_" + f], err_msg=f)
+
+
+def test_unordered_pairs_match_golden(golden):
+    from paper_2510_03557_b200.cmtree import InteractionList
+    from paper_2510_03557_b200.stepper import unordered_due_pairs
+    from tests.conftest import MeshView
+    g = golden("lane")
+    for c in g["configs"]:
+        k = f"c{c}_"
+        mesh = MeshView(g, k + "mesh_")
+        il = InteractionList(g[k + "la"], g[k + "lb"], 1.0, 0, g[k + "ls"])
+        a, b, s, _ = unordered_due_pairs(il, mesh)
+        np.testing.assert_array_equal(a, g[k + "ua"])
+        np.testing.assert_array_equal(b, g[k + "ub"])
+        np.testing.assert_array_equal(s, g[k + "us"])

@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA engine against the reference's golden vectors and the
+pinned C oracle.  Integer outputs (leaves, permutations, lists, counts,
+pairs_in_reach) must be bit-exact; floating outputs meet the FP32 tolerance
+stated in tolerances.py (normalised by the reference's own sum_j |phi_ij|)."""
+import numpy as np
+import pytest
+
+from tests.conftest import MeshView
+from tests.test_oracle_golden import KERNELS, make_kernel
+from tests.tolerances import assert_fp32_close
+
+pytestmark = pytest.mark.gpu
+
+INTEGER_KERNELS = ("counting", "neighbor_count")
+
+
+def particle_set(g, prefix):
+    from paper_2510_03557_b200.particles import FIELD_SPECS, ParticleSet
+    n = g[prefix + "pos"].shape[0]
+    p = ParticleSet(n)
+    for name, _, _ in FIELD_SPECS:
+        if prefix + name in g:
+            setattr(p, name, np.array(g[prefix + name]))
+    return p
+
+
+@pytest.mark.parametrize("case", ["rand", "lat", "clu", "r221"])
+def test_gpu_mesh_and_lists_bitwise(golden, case):
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.cmtree import assemble_interaction_lists, build_mesh_and_leaves
+    g = golden("mesh")
+    k = case + "_"
+    p = particle_set(g, k + "in_")
+    mesh = build_mesh_and_leaves(p, BoxGeometry(1.0), float(g[k + "bin_width"]),
+                                 int(g[k + "max_leaf"]), g[k + "bounds_lo"], g[k + "bounds_hi"])
+    np.testing.assert_array_equal(p.global_id, g[k + "out_global_id"])
+    np.testing.assert_array_equal(p.image_shift, g[k + "out_image_shift"])
+    np.testing.assert_array_equal(p.ghost_src, g[k + "out_ghost_src"])
+    for f in ("leaf_start", "leaf_end", "leaf_lo", "leaf_hi", "leaf_ghost_only", "leaf_bin"):
+        np.testing.assert_array_equal(getattr(mesh, f), g[k + "mesh_" + f], err_msg=f)
+    np.testing.assert_array_equal(mesh._bin_ptr, g[k + "mesh_bin_ptr"])
+    ri = 0
+    while k + f"list{ri}_a" in g:
+        il = assemble_interaction_lists(mesh, float(g[k + f"list{ri}_reach"]), 0)
+        np.testing.assert_array_equal(il.leaf_a, g[k + f"list{ri}_a"])
+        np.testing.assert_array_equal(il.leaf_b, g[k + f"list{ri}_b"])
+        np.testing.assert_array_equal(il.shift, g[k + f"list{ri}_s"])
+        ri += 1
+    mesh.leaf_level[:] = g[k + "levels"]
+    il = assemble_interaction_lists(mesh, float(g[k + "list0_reach"]), 1)
+    np.testing.assert_array_equal(il.leaf_a, g[k + "listd1_a"])
+    np.testing.assert_array_equal(il.leaf_b, g[k + "listd1_b"])
+    np.testing.assert_array_equal(il.shift, g[k + "listd1_s"])
+
+
+@pytest.mark.parametrize("name", KERNELS)
+def test_gpu_lane_kernels(golden, oracle, name):
+    from paper_2510_03557_b200.cmtree import InteractionList
+    from paper_2510_03557_b200.lane import EvalMode, eval_interaction_list
+    g = golden("lane")
+    for c in g["configs"]:
+        k = f"c{c}_"
+        st = g[k + "state"]
+        ker = make_kernel(name, float(g[k + "reach"]), float(g[k + "spacing"]))
+        aux = g[k + "aux"] if ker.n_aux else None
+        mesh = MeshView(g, k + "mesh_")
+        il = InteractionList(g[k + "la"], g[k + "lb"], ker.reach, 0, g[k + "ls"])
+        res = eval_interaction_list(ker, il, st, mesh, mode=EvalMode.RELAXED, aux=aux)
+        ref_c = g[k + f"{name}_rel_counters"]
+        got_c = [res.counters[x] for x in ("f_evals", "g_evals", "rotations", "pairs_scheduled",
+                                           "pairs_in_reach")]
+        np.testing.assert_array_equal(got_c, ref_c, err_msg="counters")
+        ref = g[k + f"{name}_rel"]
+        if name in INTEGER_KERNELS:
+            np.testing.assert_array_equal(res.values, ref)
+            det = eval_interaction_list(ker, il, st, mesh, mode=EvalMode.DETERMINISTIC, aux=aux)
+            np.testing.assert_array_equal(det.values, g[k + f"{name}_det"])
+            np.testing.assert_array_equal(det.int_acc, g[k + f"{name}_detint"])
+        else:
+            absum = oracle.eval_abs_sums(ker, g[k + "la"], g[k + "lb"], g[k + "ls"], st,
+                                         mesh.leaf_start, mesh.leaf_end, 1.0, aux=aux)
+            assert_fp32_close(res.values, ref, absum, what=f"{name} c{c}")
+            # deterministic mode: int64 quanta of the FP32 pair terms
+            det = eval_interaction_list(ker, il, st, mesh, mode=EvalMode.DETERMINISTIC, aux=aux)
+            assert_fp32_close(det.values, g[k + f"{name}_det"], absum, what=f"{name} det c{c}")
+
+
+@pytest.mark.parametrize("name", ["gravity", "hydro"])
+def test_gpu_mirror_equals_ordered(golden, oracle, name):
+    """Mirror evaluation over unordered pairs == reference mirror output."""
+    from paper_2510_03557_b200.cmtree import InteractionList
+    from paper_2510_03557_b200.lane import EvalMode, eval_interaction_list
+    g = golden("lane")
+    for c in g["configs"]:
+        k = f"c{c}_"
+        ker = make_kernel(name, float(g[k + "reach"]), float(g[k + "spacing"]))
+        mesh = MeshView(g, k + "mesh_")
+        il = InteractionList(g[k + "ua"], g[k + "ub"], ker.reach, 0, g[k + "us"])
+        res = eval_interaction_list(ker, il, g[k + "state"], mesh, mode=EvalMode.RELAXED,
+                                    mirror=True)
+        absum = oracle.eval_abs_sums(ker, g[k + "ua"], g[k + "ub"], g[k + "us"], g[k + "state"],
+                                     mesh.leaf_start, mesh.leaf_end, 1.0, mirror=True)
+        assert_fp32_close(res.values, g[k + f"{name}_mirror_rel"], absum, what=f"mirror {name}")
+
+
+def test_gpu_step_fixture(golden, oracle):
+    """Overloaded 2x8^3 lattice: density, CRK, gravity, hydro, counts."""
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.cmtree import assemble_interaction_lists, build_mesh_and_leaves
+    from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
+    from paper_2510_03557_b200.hydro import (compute_crk_coefficients, compute_density,
+                                             compute_hydro_accel, corrected_interpolate,
+                                             refresh_eos_columns)
+    from paper_2510_03557_b200.kernels import hydro_force_kernel, neighbor_count_kernel
+    from paper_2510_03557_b200.lane import EvalMode, eval_interaction_list
+    g = golden("step")
+    box = BoxGeometry(1.0)
+    p = particle_set(g, "in_")
+    mesh = build_mesh_and_leaves(p, box, float(g["bin_width"]), 256, g["bounds_lo"],
+                                 g["bounds_hi"])
+    np.testing.assert_array_equal(p.global_id, g["built_global_id"])
+    il = assemble_interaction_lists(mesh, float(g["reach"]), 0)
+    np.testing.assert_array_equal(il.leaf_a, g["la"])
+    np.testing.assert_array_equal(il.leaf_b, g["lb"])
+    st = p.state_matrix(5 / 3)
+    nc = eval_interaction_list(neighbor_count_kernel(2 * p.smoothing.max()), il, st, mesh,
+                               mode=EvalMode.DETERMINISTIC, pshift=p.image_shift)
+    np.testing.assert_array_equal(nc.values[:, 0], g["ncount"])
+    rho = compute_density(p, mesh, st, il, mode=EvalMode.RELAXED)
+    rel = np.abs(rho - g["rho_raw"]) / np.maximum(np.abs(g["rho_raw"]), 1e-300)
+    gas = p.species == 1
+    assert np.median(rel[gas]) <= 1e-6 and np.quantile(rel[gas], 0.999) <= 1e-5, rel[gas].max()
+    np.testing.assert_allclose(p.density, g["density"], rtol=1e-5, atol=0)
+    refresh_eos_columns(st, p, 5 / 3)
+    crk = compute_crk_coefficients(p, mesh, st, il, mode=EvalMode.RELAXED)
+    ok = gas & (g["crk_m0"] > 0)
+    np.testing.assert_array_equal(crk.fallback, g["crk_fallback"])
+    relA = np.abs(crk.A - g["crk_A"])[ok] / np.abs(g["crk_A"][ok])
+    assert np.median(relA) <= 1e-6 and np.quantile(relA, 0.999) <= 1e-5, relA.max()
+    dB = (np.abs(crk.B - g["crk_B"]).max(axis=1) * p.smoothing)[ok]
+    assert dB.max() <= 1e-5, dB.max()
+    split = ForceSplit(r_s=float(g["r_s"]), r_cut=float(g["r_cut"]))
+    gk = short_range_gravity_kernel(split, float(g["eps"]))
+    grav = eval_interaction_list(gk, il, st, mesh, mode=EvalMode.RELAXED, pshift=p.image_shift)
+    absg = oracle.eval_abs_sums(gk, il.leaf_a, il.leaf_b, il.shift, st, mesh.leaf_start,
+                                mesh.leaf_end, 1.0, pshift=p.image_shift)
+    own = p.ghost == 0
+    assert_fp32_close(grav.values[own], g["grav"][own], absg[own], what="step gravity")
+    f, e, _ = compute_hydro_accel(p, mesh, st, il, mode=EvalMode.RELAXED)
+    hk = hydro_force_kernel(2 * p.smoothing.max())
+    absh = oracle.eval_abs_sums(hk, il.leaf_a, il.leaf_b, il.shift, st, mesh.leaf_start,
+                                mesh.leaf_end, 1.0, pshift=p.image_shift)
+    assert_fp32_close(np.column_stack([f, e])[own], np.column_stack(
+        [g["hydro_force"], g["hydro_edot"]])[own], absh[own, :4], what="step hydro")
+    fh = corrected_interpolate(p, mesh, st, il, crk, g["interp_field"], mode=EvalMode.RELAXED)
+    inner = own & gas & ~crk.fallback
+    err = np.abs(fh - g["interp"])[inner] / np.abs(g["interp"][inner]).max()
+    assert err.max() <= 1e-5, err.max()
+
+
+def test_gpu_adapt_smoothing_bitwise(golden):
+    """Exact neighbour counts make the h iteration identical to the reference."""
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.cmtree import ChainingMesh
+    from paper_2510_03557_b200.hydro import adapt_smoothing_length
+    from paper_2510_03557_b200.lane import EvalMode
+    g = golden("adapt")
+    p = particle_set(g, "in_")
+    mv = MeshView(g, "mesh_")
+    mesh = ChainingMesh(box=BoxGeometry(1.0), bounds_lo=None, bounds_hi=None,
+                        bin_count=mv.bin_count, bin_width=mv.bin_width,
+                        periodic_axis=mv.periodic_axis, n_particles=p.n,
+                        leaf_start=mv.leaf_start, leaf_end=mv.leaf_end, leaf_lo=mv.leaf_lo,
+                        leaf_hi=mv.leaf_hi, leaf_level=mv.leaf_level.copy(),
+                        leaf_ghost_only=mv.leaf_ghost_only, leaf_bin=mv.leaf_bin,
+                        _bin_ptr=mv._bin_ptr, _bin_ids=mv._bin_ids)
+    h = adapt_smoothing_length(p, mesh, lambda: p.state_matrix(5 / 3), 40, float(g["bin_width"]),
+                               mode=EvalMode.DETERMINISTIC)
+    np.testing.assert_array_equal(h, g["h_out"])
+
+
+def test_gpu_nonfinite_raises(golden):
+    from paper_2510_03557_b200.cmtree import InteractionList
+    from paper_2510_03557_b200.errors import KernelEvalError
+    from paper_2510_03557_b200.lane import EvalMode, eval_interaction_list
+    g = golden("lane")
+    k = f"c{g['configs'][0]}_"
+    st = g[k + "state"].copy()
+    st[:, 6] = np.nan  # NaN masses poison every gravity term
+    ker = make_kernel("gravity", float(g[k + "reach"]), float(g[k + "spacing"]))
+    il = InteractionList(g[k + "la"], g[k + "lb"], ker.reach, 0, g[k + "ls"])
+    with pytest.raises(KernelEvalError, match="non-finite partial in leaf pair"):
+        eval_interaction_list(ker, il, st, MeshView(g, k + "mesh_"), mode=EvalMode.RELAXED)
