@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark: particle-updates/s of the short-range gravity + CRK-SPH force
+evaluation (BASELINE.json metric), on synthetic Zel'dovich-displaced
+two-species lattices.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one force evaluation at depth 0: bin sort + k-d leaf
+build + reorder, leaf-pair lists, one neighbour-count pass, density + EOS, CRK
+moments + 3x3 solve, short-range gravity, hydro force.  ``value`` times
+hb_force_step on device-resident inputs (CUDA events, max over ranks);
+``e2e`` times the same through host buffers (pinned H2D of the particle fields,
+the step, D2H of the results).  ``--impl reference`` times the reference
+algorithm's CPU restatement (oracle/, pinned bitwise to the reference) on the
+host cores: there is no other CPU implementation that can travel to the box.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-updates/sec (short-range grav+CRK-SPH) at 1/2/4/8 B200; % FP32 peak"
+UNIT = "particle-updates/s"
+# reference OpCost per in-support ordered pair (FMA = 2): hb/kernels.py:523,544,555,567,601
+OPCOST = {"gravity": 29, "density": 16, "ncount": 7, "crk": 29, "hydro": 57}
+
+CONFIGS = {
+    # name: (npd, sigma_psi in lattice spacings, species, description)
+    "c1": (32, 0.05, "both", "2x32^3 particles (DM + baryon), one short-range gravity + CRK-SPH step"),
+    "c2": (128, 0.05, "both", "2x128^3 particles, z=10 near-uniform Zel'dovich ICs, single B200"),
+    "c3": (256, 2.0, "both", "2x256^3 particles, z=0 strongly clustered (neighbour-count imbalance)"),
+    "c4": (512, 0.05, "both", "2x512^3 particles, spatial decomposition"),
+}
+
+
+def peaks():
+    """FP32 roofline denominator: FFMA peak measured on this pool's B200
+    (profiles/peaks_r01.json; MEASURED_PEAKS.json carries no FP32 entry)."""
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "peaks_r01.json")))
+        return float(rec["ffma_reg_tflops"]), "measured FFMA (profiles/peaks_r01.json)"
+    except Exception:
+        return 148 * 128 * 2 * 1.965e9 / 1e12, "nominal 148 SM x 128 lanes x 2 x 1.965 GHz"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(cfg_name: str, rank: int = 0, world: int = 1):
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.ic import make_zeldovich_ic
+    from paper_2510_03557_b200.resident import StepConfig
+    npd, sigma, species, desc = CONFIGS[cfg_name]
+    box = BoxGeometry(1.0)
+    p = make_zeldovich_ic(npd, box, sigma, species=species)
+    d = 1.0 / npd
+    pm_grid = 2 * npd                       # pm_grid_n = 2 npd
+    pm_cell = 1.0 / pm_grid
+    r_s = 2.0 * pm_cell                     # hb/config.py:87-90
+    r_cut = 5.0 * r_s                       # hb/config.py:91-93
+    eps = (1.0 / p.n ** (1.0 / 3.0)) / 50.0  # hb/config.py:95-99
+    h_max = float(p.smoothing.max())
+    reach = max(r_cut, 2.0 * h_max)
+    bin_width = max(4.0 * pm_cell, reach * (1 + 1e-9))  # hb/driver.py:147-150
+    cfg = StepConfig(box=box, bin_width=bin_width, max_leaf_size=256, r_s=r_s, r_cut=r_cut,
+                     softening=eps)
+    meta = {"workload": desc, "config": cfg_name, "n_particles": int(p.n),
+            "n_per_dim": npd, "sigma_psi_spacings": sigma, "smoothing": "h = 1.3 d (unadapted)",
+            "r_s": "d", "r_cut": "5 d", "softening": "L/N^(1/3)/50", "max_leaf_size": 256,
+            "mesh": "bare periodic box, bin width max(4 PM cells, reach)",
+            "bins_per_axis": int(np.floor(1.0 / bin_width)),
+            "ic": "Zel'dovich, seed 2510035570, P(k)~k^-2 exp(-(kd)^2)",
+            "l2": "working set > 126 MB L2 (no flush needed)"}
+    return p, cfg, meta
+
+
+def pair_counts(p, cfg):
+    """Exact in-support ordered pair counts for the algorithmic-FLOP roofline
+    (untimed; uses the compat API's exact pairs_in_reach)."""
+    from paper_2510_03557_b200.cmtree import assemble_interaction_lists, build_mesh_and_leaves
+    from paper_2510_03557_b200.kernels import counting_kernel, neighbor_count_kernel
+    from paper_2510_03557_b200.lane import EvalMode, eval_interaction_list
+    q = p.copy()
+    mesh = build_mesh_and_leaves(q, cfg.box, cfg.bin_width, cfg.max_leaf_size)
+    reach = max(cfg.r_cut, 2 * float(q.smoothing.max()))
+    il = assemble_interaction_lists(mesh, reach, 0)
+    st = q.state_matrix(cfg.eos_gamma)
+    g = eval_interaction_list(counting_kernel(cfg.r_cut), il, st, mesh, mode=EvalMode.RELAXED)
+    nc = eval_interaction_list(neighbor_count_kernel(2 * float(q.smoothing.max())), il, st, mesh,
+                               mode=EvalMode.DETERMINISTIC)
+    gas = q.species == 1
+    sph_in = int(nc.values[gas, 0].sum())          # r <= 2 h_i, gas-gas, incl. self
+    n_gas = int(gas.sum())
+    return {"gravity": int(g.values[:, 0].sum()), "density": sph_in, "ncount": sph_in,
+            "crk": sph_in, "hydro": sph_in - n_gas,
+            "gravity_scheduled_leafpairs": int(g.counters["pairs_scheduled"])}
+
+
+def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None):
+    """The reference algorithm (oracle/ C restatement, bitwise-pinned to the
+    reference) on the host cores: full build + lists, a contiguous 1/32 slice
+    of each kernel's list scaled up (fixed per-call cost measured separately),
+    full CRK solve.  Gravity and hydro use the reference driver's mirror mode
+    over unordered pairs (half the pair work)."""
+    from oracle import oracle as O
+    from paper_2510_03557_b200.kernels import (crk_moments_kernel, density_kernel,
+                                               hydro_force_kernel, neighbor_count_kernel)
+    from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
+    threads = threads or os.cpu_count() or 1
+    O.set_threads(threads)
+    L = cfg.box.side_length
+    t0 = time.perf_counter()
+    m = O.build_mesh(p.pos, p.image_shift, p.ghost, L, cfg.bin_width, cfg.max_leaf_size)
+    t_build = time.perf_counter() - t0
+    h_max = float(p.smoothing.max())
+    reach = max(cfg.r_cut, 2 * h_max)
+    t0 = time.perf_counter()
+    la, lb, ls = O.assemble(m, L, reach)
+    t_list = time.perf_counter() - t0
+    perm = m["perm"]
+    st = O.state_matrix(p.pos[perm], p.vel[perm], p.mass[perm], p.smoothing[perm],
+                        p.density[perm], p.internal_energy[perm], p.species[perm], cfg.eos_gamma)
+    ua, ub, us, _ = O.unordered_due_pairs(la, lb, ls, m["leaf_start"].shape[0])
+    gk = short_range_gravity_kernel(ForceSplit(r_s=cfg.r_s, r_cut=cfg.r_cut), cfg.softening)
+    jobs = [("ncount", neighbor_count_kernel(2 * h_max), False),
+            ("density", density_kernel(2 * h_max), False),
+            ("crk", crk_moments_kernel(2 * h_max), False),
+            ("gravity", gk, True),
+            ("hydro", hydro_force_kernel(2 * h_max), True)]
+    times = {}
+    for name, ker, mirror in jobs:
+        A, B, S = (ua, ub, us) if mirror else (la, lb, ls)
+        k = max(1, int(len(A) * frac))
+        mode = "deterministic" if name == "ncount" else "relaxed"
+        t0 = time.perf_counter()
+        O.eval_pairs(ker, A[:0], B[:0], S[:0], st, m["leaf_start"], m["leaf_end"], L, mode=mode,
+                     workers=threads, mirror=mirror)
+        t_fixed = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.eval_pairs(ker, A[:k], B[:k], S[:k], st, m["leaf_start"], m["leaf_end"], L, mode=mode,
+                     workers=threads, mirror=mirror)
+        t_s = time.perf_counter() - t0
+        times[name] = t_fixed + max(t_s - t_fixed, 0.0) * len(A) / k
+    t0 = time.perf_counter()
+    vals = np.zeros((p.n, 10))
+    vals[:, 0] = 1.0
+    vals[:, 4] = vals[:, 7] = vals[:, 9] = 1.0
+    O.crk_solve(vals, p.species[perm] == 1)
+    times["crk_solve"] = time.perf_counter() - t0
+    total = t_build + t_list + sum(times.values())
+    n_owned = int(np.count_nonzero(p.ghost == 0))
+    return {"value": n_owned / total, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": (f"full build+lists ({t_build:.2f}+{t_list:.2f} s), first {frac:.4g} of each "
+                       f"kernel's list (ordered: ncount/density/crk; mirror-unordered: "
+                       f"gravity/hydro) scaled to the full list, full CRK solve; "
+                       f"est. step {total:.1f} s"),
+            "seconds": {"build": t_build, "list": t_list, **times, "total_est": total}}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    p, cfg, meta = make_workload(args.config)
+    vals = []
+    base = None
+    for _ in range(args.warmup):
+        cpu_baseline(p, cfg, frac=args.cpu_frac / 4)
+    for _ in range(args.steps):
+        base = cpu_baseline(p, cfg, frac=args.cpu_frac)
+        vals.append(base["value"])
+    v = float(np.median(vals))
+    n_owned = meta["n_particles"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_owned / v * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": meta,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "port",
+                             "sample": base["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu_arm(args):
+    import torch
+    from paper_2510_03557_b200 import _native as N
+    from paper_2510_03557_b200.resident import PASS_ALL, STEP_FIELDS, ResidentRank
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p, cfg, meta = make_workload(args.config, rank, world)
+    n_owned = int(np.count_nonzero(p.ghost == 0))
+    rr = ResidentRank(p, cfg)
+    lib = N.lib()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        rr.step(PASS_ALL)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    l0 = lib.hb_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phases = []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rr.step(PASS_ALL, timing=True)
+            phases.append(rr.last["ms_phase"])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.hb_launch_count() - l0
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = n_owned * world / (ms_step * 1e-3) if world > 1 else n_owned / (ms_step * 1e-3)
+    ph = {k: float(np.mean([x[k] for x in phases])) for k in phases[0]}
+
+    # ---- e2e: pinned host buffers -> device -> step -> results back to host
+    pinned_in = {f: torch.from_numpy(np.ascontiguousarray(getattr(p, f))).pin_memory()
+                 for f in STEP_FIELDS}
+    out_names = ("grav", "hydro", "ncount", "crk_A", "crk_B", "perm")
+    pinned_out = {k: torch.empty(rr.out[k].shape, dtype=rr.out[k].dtype).pin_memory()
+                  for k in out_names}
+    pinned_out["density"] = torch.empty(rr.n, dtype=torch.float64).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in pinned_in.values())
+    d2h = sum(t.numel() * t.element_size() for t in pinned_out.values())
+
+    def e2e_step():
+        src = rr.buf[rr.cur]
+        for f in STEP_FIELDS:
+            src[f].copy_(pinned_in[f], non_blocking=True)
+        out = rr.step(PASS_ALL)
+        for k in out_names:
+            pinned_out[k].copy_(out[k], non_blocking=True)
+        pinned_out["density"].copy_(rr.fields()["density"], non_blocking=True)
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e_value = n_owned * world / (ms_e2e * 1e-3) if world > 1 else n_owned / (ms_e2e * 1e-3)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    # ---- roofline of the dominant kernel (gravity phase, timed live above)
+    counts = pair_counts(p, cfg) if world == 1 else None
+    peak, peak_src = peaks()
+    roof = None
+    if counts is not None:
+        alg_flops = counts["gravity"] * OPCOST["gravity"]
+        achieved = alg_flops / (ph["gravity"] * 1e-3) / 1e12
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get("gravity_dram_bytes")
+        roof = {"bound": "fp32", "kernel": "k_eval<GRAVITY> (gravity phase incl. record pack)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_flops_per_launch": alg_flops,
+                "in_support_pairs": counts["gravity"], "flops_per_pair": OPCOST["gravity"]}
+        step_flops = sum(counts[k] * OPCOST[k] for k in OPCOST)
+        roof["step_algorithmic_tflops"] = step_flops / (ms_step * 1e-3) / 1e12
+        roof["step_frac"] = roof["step_algorithmic_tflops"] / peak
+        roof["kflop_per_update"] = step_flops / n_owned / 1e3
+    base = None
+    if world == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(p, cfg, frac=args.cpu_frac)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Zel'dovich-displaced two-species lattice)",
+            "config": meta, "phases_ms": ph,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e},
+            "gpu_launches": int(launches), "roofline": roof, "clocks": clocks.summary(),
+            "mesh": rr.last and {"n_leaves": rr.last["n_leaves"], "n_entries": rr.last["n_entries"]},
+            "pair_counts": counts}
+    if base is not None:
+        line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"]["seconds"] = base["seconds"]
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-frac", type=float, default=1 / 32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

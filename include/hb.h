@@ -41,6 +41,8 @@ typedef struct HbError {
 } HbError;
 
 int hb_abi_version(void);
+/* number of kernels this library has launched in the process (bench accounting) */
+int64_t hb_launch_count(void);
 /* SM count and compute capability of the current device (host outputs). */
 int hb_device_query(int* sm_count, int* cc_major, int* cc_minor);
 
@@ -193,12 +195,59 @@ int hb_crk_solve(int64_t n, const double* moments, int64_t stride, const uint8_t
                  HbError* err);
 
 /* ---------------------------------------------------------------------------
- * Resident force evaluation (the s = 0 boundary of subcycle_pm_step,
- * hb/stepper.py:113-179, with the reference's ordered, single-count
- * semantics -- SURVEY.md 8c): mesh build, lists, neighbour count,
- * density (+ EOS), CRK moments + solve, short-range gravity, hydro force.
- * All buffers stay on device; see HbStepArgs in hb_step.h.
+ * Resident force evaluation: the s = 0 boundary of subcycle_pm_step
+ * (hb/stepper.py:113-179) with the reference's ordered, single-count pair
+ * semantics: build_mesh_and_leaves -> assemble_interaction_lists
+ * -> neighbour count -> compute_density (+ alias sync) -> refresh_eos_columns ->
+ * CRK moments + solve -> short-range gravity -> hydro force, all on device.
+ * Particle fields are read from *_in and written reordered (leaf order, as
+ * the reference reorders its ParticleSet in place) to the output fields.
  * ------------------------------------------------------------------------- */
+#define HB_PASS_NCOUNT 1
+#define HB_PASS_DENSITY 2
+#define HB_PASS_CRK 4
+#define HB_PASS_GRAVITY 8
+#define HB_PASS_HYDRO 16
+#define HB_PASS_ALL 31
+
+typedef struct HbStepArgs {
+  int64_t n;
+  /* inputs (n rows, ParticleSet layout) */
+  const double* pos_in; const double* vel_in; const double* mass_in;
+  const double* smoothing_in; const double* internal_energy_in; const double* density_in;
+  const uint8_t* species_in; const uint8_t* ghost_in; const int8_t* image_shift_in;
+  const int64_t* global_id_in; const int64_t* ghost_src_in; /* ghost_src may be NULL */
+  /* reordered outputs (may not alias the inputs) */
+  double* pos; double* vel; double* mass; double* smoothing; double* internal_energy;
+  double* density; uint8_t* species; uint8_t* ghost; int8_t* image_shift; int64_t* global_id;
+  int64_t* ghost_src;
+  /* mesh (host scalars) */
+  double side_length; double lo[3]; double width[3]; int64_t nb[3]; uint8_t periodic[3];
+  int64_t max_leaf_size;
+  /* physics (host scalars) */
+  double reach;      /* list reach = max(r_cut, 2 h_max)                       */
+  double h_max;      /* max smoothing length (kernel supports 2 h_max)        */
+  double r_s, r_cut, softening, eos_gamma, visc_alpha, visc_beta;
+  int32_t passes;    /* HB_PASS_* mask                                        */
+  int32_t timing;    /* 1: fill ms_phase with per-phase device times          */
+  int64_t list_capacity; /* entries the workspace was sized for              */
+  /* outputs (device, leaf order) */
+  int64_t* perm;        /* (n) row k = input row perm[k]                    */
+  double* ncount;       /* (n)                                                */
+  double* grav;         /* (n,3) m_i a_i short-range gravity                  */
+  double* hydro;        /* (n,5) fx fy fz m du/dt (edot_i) edot_j             */
+  double* crk_moments;  /* (n,10)                                             */
+  double* crk_A;        /* (n)                                                */
+  double* crk_B;        /* (n,3)                                              */
+  uint8_t* crk_fallback;/* (n)                                                */
+  /* host outputs */
+  int64_t n_leaves, n_entries, list_capacity_needed;
+  float ms_phase[8];    /* build, list, ncount, density+eos, crk, gravity, hydro, total */
+} HbStepArgs;
+
+size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,
+                               int64_t list_capacity);
+int hb_force_step(HbStepArgs* args, void* ws, size_t ws_bytes, void* stream, HbError* err);
 
 #ifdef __cplusplus
 }

@@ -82,16 +82,17 @@ def lib():
             lb.hb_permute_rows.argtypes = [C.c_int64, P, P, P, C.c_int64, P, P]
             lb.hb_remap_through_inverse.argtypes = [C.c_int64, P, P, P, P, P]
             lb.hb_grow_aabbs.argtypes = [C.c_int64, P, P, P, P, C.c_double, P, P, P, P]
+            lb.hb_launch_count.restype = C.c_int64
             lb.hb_crk_solve.argtypes = [C.c_int64, P, C.c_int64, P, C.c_double, P, P, P, P, P]
             _lib = lb
         return _lib
 
 
 # every symbol include/hb.h declares (tests check the library exports them)
-EXPORTS = ("hb_abi_version", "hb_device_query", "hb_build_mesh_workspace", "hb_leaf_capacity",
+EXPORTS = ("hb_abi_version", "hb_launch_count", "hb_device_query", "hb_build_mesh_workspace", "hb_leaf_capacity",
            "hb_build_mesh", "hb_permute_rows", "hb_remap_through_inverse", "hb_grow_aabbs",
            "hb_assemble_lists_workspace", "hb_assemble_lists", "hb_eval_pairs_workspace",
-           "hb_eval_pairs", "hb_crk_solve")
+           "hb_eval_pairs", "hb_crk_solve", "hb_force_step_workspace", "hb_force_step")
 
 
 def torch_cuda():

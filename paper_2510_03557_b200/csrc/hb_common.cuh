@@ -49,8 +49,11 @@ inline int set_err(HbError* e, int status, const char* msg, int cuda_err = 0) {
     if (_e != cudaSuccess) return ::hb::set_err(err, HB_CUDA, cudaGetErrorString(_e), (int)_e); \
   } while (0)
 
+extern unsigned long long g_launches;  // kernels launched (hb_crk.cu)
+#define HB_COUNT_LAUNCH(k) (::hb::g_launches += (k))
 #define HB_LAUNCH_CHECK()                                                   \
   do {                                                                      \
+    ::hb::g_launches += 1;                                                  \
     cudaError_t _e = cudaGetLastError();                                    \
     if (_e != cudaSuccess) return ::hb::set_err(err, HB_CUDA, cudaGetErrorString(_e), (int)_e); \
   } while (0)

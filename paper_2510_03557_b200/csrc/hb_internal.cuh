@@ -1,0 +1,28 @@
+// hb_internal.cuh -- internal (non-ABI) entry points shared by the translation
+// units: mesh build, list sweep into a receiver CSR, pair-engine pieces.
+#pragma once
+#include "hb_pairs.cuh"
+
+namespace hb {
+
+struct ListGeom {
+  int64_t nb[3];
+  int periodic[3];
+  double L, reach;
+  int64_t active_depth;
+};
+
+struct ListArgsDev {
+  int64_t n_leaves;
+  const int64_t *leaf_bin, *leaf_level, *bin_ptr, *bin_ids;
+  const double *leaf_lo, *leaf_hi;
+  const uint8_t* ghost_only;
+  ListGeom g;
+};
+
+int build_mesh(const HbMeshArgs* a, Arena& ws, cudaStream_t st, HbError* err);
+// ordered list as a receiver CSR: ent_ptr (n_leaves+1), partner, code|fwd<<8
+int assemble_csr(const ListArgsDev& d, int64_t capacity, int32_t* ent_src, int32_t* ent_code,
+                 int64_t* ent_ptr, int64_t* total_host, Arena& ws, cudaStream_t st, HbError* err);
+
+}  // namespace hb

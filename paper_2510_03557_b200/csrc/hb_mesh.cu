@@ -14,7 +14,7 @@
 //   * lists: 27-stencil sweep, periodic wrap with image shift on full-box
 //     axes, duplicate (bin,shift) suppression, per-axis gap test, ordered by
 //     (a, b, sx, sy, sz) (hb/cmtree.py:210-337).
-#include "hb_common.cuh"
+#include "hb_internal.cuh"
 
 namespace hb {
 
@@ -435,12 +435,7 @@ __global__ void k_grow(int64_t n_leaves, const int64_t* leaf_start, const int64_
 }
 
 // ------------------------------------------------------------------ lists
-struct ListGeom {
-  int64_t nb[3];
-  int periodic[3];
-  double L, reach;
-  int64_t active_depth;
-};
+
 
 // stencil cell o (0..26) of bin (bx,by,bz): returns false if off-mesh; flat bin, shift code
 __device__ __forceinline__ bool stencil_cell(const ListGeom& g, int64_t bx, int64_t by, int64_t bz,
@@ -474,13 +469,7 @@ __device__ __forceinline__ bool gap_ok(const double* lo_a, const double* hi_a, c
   return true;
 }
 
-struct ListArgsDev {
-  int64_t n_leaves;
-  const int64_t *leaf_bin, *leaf_level, *bin_ptr, *bin_ids;
-  const double *leaf_lo, *leaf_hi;
-  const uint8_t* ghost_only;
-  ListGeom g;
-};
+
 
 template <bool EMIT>
 __global__ void k_list_sweep(ListArgsDev a, int64_t* cnt, const int64_t* off, int64_t* tmp_b,
@@ -552,6 +541,57 @@ __global__ void k_list_order(int64_t n_leaves, const int64_t* cnt, const int64_t
     out_s[3 * (o + rank) + 1] = (int8_t)((code / 3) % 3 - 1);
     out_s[3 * (o + rank) + 2] = (int8_t)(code % 3 - 1);
   }
+}
+
+// receiver-CSR output for the resident step: entries already grouped by
+// receiver (leaf order), partner as int32, code | fwd<<8 as the pair engine reads
+__global__ void k_list_order_csr(int64_t n_leaves, const int64_t* cnt, const int64_t* off,
+                                 const int64_t* tmp_b, const int32_t* tmp_code, int32_t* ent_src,
+                                 int32_t* ent_code) {
+  int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (leaf >= n_leaves) return;
+  int64_t m = cnt[leaf], o = off[leaf];
+  for (int64_t e = lane; e < m; e += 32) {
+    int64_t ke = tmp_b[o + e] * 27 + tmp_code[o + e];
+    int64_t rank = 0;
+    for (int64_t f = 0; f < m; ++f) rank += (tmp_b[o + f] * 27 + tmp_code[o + f]) < ke;
+    ent_src[o + rank] = (int32_t)tmp_b[o + e];
+    ent_code[o + rank] = tmp_code[o + e] | (1 << 8);
+  }
+}
+
+int assemble_csr(const ListArgsDev& d, int64_t capacity, int32_t* ent_src, int32_t* ent_code,
+                 int64_t* ent_ptr, int64_t* total_host, Arena& ws, cudaStream_t st, HbError* err) {
+  int64_t nl = d.n_leaves;
+  int64_t* cnt = ws.take<int64_t>(nl + 1);
+  int64_t* tmp_b = ws.take<int64_t>(capacity > 0 ? capacity : 1);
+  int32_t* tmp_code = ws.take<int32_t>(capacity > 0 ? capacity : 1);
+  if (ws.dry) {
+    Arena sub = ws;
+    exclusive_scan_i64(nullptr, nullptr, nl, nullptr, sub, st, err);
+    ws.used = sub.used;
+    return HB_OK;
+  }
+  if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (list csr)");
+  k_list_sweep<false><<<grid_for(nl * 32, 256), 256, 0, st>>>(d, cnt, nullptr, nullptr, nullptr);
+  HB_LAUNCH_CHECK();
+  {
+    Arena sub = ws;
+    int rc = exclusive_scan_i64(cnt, ent_ptr, nl, ent_ptr + nl, sub, st, err);
+    if (rc) return rc;
+  }
+  int64_t total = 0;
+  HB_CUDA_TRY(cudaMemcpyAsync(&total, ent_ptr + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  HB_CUDA_TRY(cudaStreamSynchronize(st));
+  *total_host = total;
+  if (total > capacity) return set_err(err, HB_CONTRACT, "list capacity below entry count");
+  k_list_sweep<true><<<grid_for(nl * 32, 256), 256, 0, st>>>(d, cnt, ent_ptr, tmp_b, tmp_code);
+  HB_LAUNCH_CHECK();
+  k_list_order_csr<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, cnt, ent_ptr, tmp_b, tmp_code,
+                                                          ent_src, ent_code);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
 }
 
 int assemble_lists(const HbListArgs* a, Arena& ws, cudaStream_t st, HbError* err) {

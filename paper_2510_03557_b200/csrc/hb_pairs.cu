@@ -21,27 +21,12 @@
 
 namespace hb {
 
-constexpr int kTileMax = 32;
 constexpr int kTileBuildBlock = 256;
 constexpr int kTileBuildCap = 2048;  // selected members per leaf held in shared memory
 constexpr int kEvalWarps = 4;
 constexpr int kStage = 64;           // staged sources per warp
 
-struct Tiling {
-  int64_t n_leaves, n_tiles_cap;
-  int64_t* sel_cnt;     // (n_leaves+1)
-  int64_t* sel_off;     // (n_leaves+1)
-  int64_t* tile_cnt;    // (n_leaves+1)
-  int64_t* tile_ptr;    // (n_leaves+1)  CSR leaf -> tiles
-  int32_t* tperm;       // (n) internal -> state row
-  int32_t* tile_start;  // (cap) internal index
-  int32_t* tile_n;
-  int32_t* tile_leaf;
-  float4* tile_lo;      // w = hmax
-  float4* tile_hi;
-  double* origin;       // (n_leaves,3)
-  int* overflow;        // device flag: a leaf exceeded kTileBuildCap
-};
+
 
 // ---------------------------------------------------------------- tiling
 __global__ void k_tile_count(int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
@@ -273,7 +258,7 @@ __global__ void k_tile_boxes(int64_t n_tiles, const int64_t* n_tiles_dev, Tiling
 }
 
 // ---------------------------------------------------------------- packing
-__global__ void k_pack(int kid, int64_t n_tiles_cap, const int64_t* n_tiles_dev, Tiling T,
+__global__ void k_pack(int kid, int64_t n_tiles_cap, const int64_t* n_tiles_dev, const Tiling T,
                        const double* state, const int8_t* pshift, const double* aux, int naux,
                        double L, float4* P0, float4* P1, float4* P2) {
   int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -387,26 +372,7 @@ __global__ void k_sched_counters(int64_t n_pairs, const int64_t* pa, const int64
 }
 
 // ---------------------------------------------------------------- the gather kernel
-struct EvalDev {
-  Tiling T;
-  const int64_t* ent_ptr;  // (n_leaves+1)
-  const int32_t* ent_src;
-  const int32_t* ent_code;  // shift code | fwd << 8
-  const float4 *P0, *P1, *P2;
-  const double* state;
-  const int8_t* pshift;
-  double L, reach;
-  PairParams pp;
-  float cull_reach;
-  int include_self;
-  int nchan;
-  float scale[10];
-  double* out_flt;
-  int64_t* out_int;
-  int write_out;
-  unsigned long long* in_count;
-  unsigned long long* err_key;  // min (entry*4 + kind)
-};
+
 
 __device__ __forceinline__ float box_gap2(float x, float y, float z, float4 lo, float4 hi) {
   float gx = fmaxf(fmaxf(lo.x - x, x - hi.x), 0.0f);
@@ -430,7 +396,11 @@ __device__ __forceinline__ double exact_r2(const EvalDev& a, int64_t i, int64_t 
   return r2;
 }
 
-template <int KID, bool DET>
+// LEAN (resident hot path): no float64 reach recheck (only the integer kernel
+// keeps it), no index-based self test (r = 0 terms vanish or are included by
+// the kernel's own definition), no pairs_in_reach tally, staged sources are
+// flushed only when the stage fills, finiteness checked once at the end.
+template <int KID, bool DET, bool LEAN>
 __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_tiles_cap,
                                                           const int64_t* n_tiles_dev) {
   using P = Pol<KID>;
@@ -484,13 +454,14 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
       bool in = r2 <= a.pp.reach2;
       int64_t row_j = -1;
-      if (live && fabsf(r2 - a.pp.reach2) <= a.pp.reach2 * 2.44140625e-4f) {
+      if ((!LEAN || KID == KID_NEIGHBOR_COUNT) && live &&
+          fabsf(r2 - a.pp.reach2) <= a.pp.reach2 * 2.44140625e-4f) {
         row_j = T.tperm[meta.x];
         in = exact_r2(a, row_i, row_j, meta.y & 31) <= reach2_64;
       }
-      if (!a.include_self && meta.x == k_i && (meta.y & 31) == 13) in = false;
+      if (!LEAN && !a.include_self && meta.x == k_i && (meta.y & 31) == 13) in = false;
       if (!in) continue;
-      if (live && (meta.y >> 8)) nin += 1;
+      if (!LEAN && live && (meta.y >> 8)) nin += 1;
       float phi[NC];
       if (KID == KID_NEIGHBOR_COUNT) {
         bool c4 = r2 <= thr_n;
@@ -567,7 +538,22 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
         cnt += __popc(sm);
       }
     }
-    flush();  // per entry: keeps error attribution per leaf pair
+    if (!LEAN) {
+      flush();  // per entry: keeps error attribution per leaf pair
+      if (!DET) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) if (!isfinite(acc[c])) bad |= 1;
+      }
+      unsigned bm = __ballot_sync(0xffffffffu, live && bad);
+      if (bm) {
+        int kind = __shfl_sync(0xffffffffu, bad, __ffs(bm) - 1);
+        if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e * 4 + ((kind & 1) ? 1 : 2)));
+        return;
+      }
+    }
+  }
+  if (LEAN) {
+    flush();
     if (!DET) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) if (!isfinite(acc[c])) bad |= 1;
@@ -575,7 +561,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
     unsigned bm = __ballot_sync(0xffffffffu, live && bad);
     if (bm) {
       int kind = __shfl_sync(0xffffffffu, bad, __ffs(bm) - 1);
-      if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e * 4 + ((kind & 1) ? 1 : 2)));
+      if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e0 * 4 + ((kind & 1) ? 1 : 2)));
       return;
     }
   }
@@ -590,34 +576,120 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
         if (c < a.nchan) a.out_flt[row_i * a.nchan + c] += (double)acc[c];
     }
   }
+  if (!LEAN) {
 #pragma unroll
-  for (int o = 16; o; o >>= 1) nin += __shfl_xor_sync(0xffffffffu, nin, o);
-  if (lane == 0 && nin) atomicAdd(a.in_count, nin);
+    for (int o = 16; o; o >>= 1) nin += __shfl_xor_sync(0xffffffffu, nin, o);
+    if (lane == 0 && nin) atomicAdd(a.in_count, nin);
+  }
 }
 
-// ---------------------------------------------------------------- driver
+// ---------------------------------------------------------------- driver pieces
+int64_t tile_capacity(int64_t n, int64_t n_leaves) { return n / kTileMax + n_leaves + 1; }
+
+void carve_tiling(Arena& ws, int64_t n, int64_t nl, Tiling& T) {
+  int64_t tc = tile_capacity(n, nl);
+  T.n_leaves = nl; T.n_tiles_cap = tc;
+  T.sel_cnt = ws.take<int64_t>(nl + 1); T.sel_off = ws.take<int64_t>(nl + 1);
+  T.tile_cnt = ws.take<int64_t>(nl + 1); T.tile_ptr = ws.take<int64_t>(nl + 1);
+  T.tperm = ws.take<int32_t>(n + 1);
+  T.tile_start = ws.take<int32_t>(tc); T.tile_n = ws.take<int32_t>(tc);
+  T.tile_leaf = ws.take<int32_t>(tc);
+  T.tile_lo = ws.take<float4>(tc); T.tile_hi = ws.take<float4>(tc);
+  T.origin = ws.take<double>(3 * nl + 3);
+  T.overflow = ws.take<int>(1);
+}
+
+int kid_selects_gas(int kid) {
+  return kid == KID_DENSITY || kid == KID_NEIGHBOR_COUNT || kid == KID_CRK_MOMENTS ||
+         kid == KID_HYDRO_FORCE || kid == KID_CRK_INTERP;
+}
+
+int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t* leaf_end,
+                 const double* state, const int8_t* pshift, double L, int sel,
+                 int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err) {
+  if (ws.dry) {
+    Arena s = ws;
+    exclusive_scan_i64(nullptr, nullptr, nl, nullptr, s, st, err);
+    ws.used = s.used;
+    return HB_OK;
+  }
+  HB_CUDA_TRY(cudaMemsetAsync(T.overflow, 0, sizeof(int), st));
+  k_tile_count<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, leaf_start, leaf_end, state, sel,
+                                                       T.sel_cnt, T.tile_cnt);
+  HB_LAUNCH_CHECK();
+  {
+    Arena s = ws;
+    int rc = exclusive_scan_i64(T.sel_cnt, T.sel_off, nl, T.sel_off + nl, s, st, err);
+    if (rc) return rc;
+    Arena s2 = ws;
+    rc = exclusive_scan_i64(T.tile_cnt, T.tile_ptr, nl, n_tiles_dev, s2, st, err);
+    if (rc) return rc;
+    HB_CUDA_TRY(cudaMemcpyAsync(T.tile_ptr + nl, n_tiles_dev, sizeof(int64_t),
+                                cudaMemcpyDeviceToDevice, st));
+  }
+  k_tile_build<<<(unsigned)nl, kTileBuildBlock, 0, st>>>(T, leaf_start, leaf_end, state, pshift,
+                                                         L, sel);
+  HB_LAUNCH_CHECK();
+  int64_t tcap = T.n_tiles_cap;
+  k_tile_boxes<<<grid_for(tcap * 32, 256), 256, 0, st>>>(tcap, n_tiles_dev, T, state, pshift, L);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
+
+int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, const double* state,
+                 const int8_t* pshift, const double* aux, int naux, double L, float4* P0,
+                 float4* P1, float4* P2, cudaStream_t st, HbError* err) {
+  int64_t tcap = T.n_tiles_cap;
+  k_pack<<<grid_for(tcap * 32, 256), 256, 0, st>>>(kid, tcap, n_tiles_dev, T, state, pshift, aux,
+                                                   naux, L, P0, P1, P2);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
+
+template <int KID>
+static void launch_kid(const EvalDev& d, int64_t tcap, const int64_t* ntd, bool det, bool lean,
+                       cudaStream_t st) {
+  unsigned grid = grid_for(tcap, kEvalWarps);
+  if (lean) {
+    if (det) k_eval<KID, true, true><<<grid, kEvalWarps * 32, 0, st>>>(d, tcap, ntd);
+    else k_eval<KID, false, true><<<grid, kEvalWarps * 32, 0, st>>>(d, tcap, ntd);
+  } else {
+    if (det) k_eval<KID, true, false><<<grid, kEvalWarps * 32, 0, st>>>(d, tcap, ntd);
+    else k_eval<KID, false, false><<<grid, kEvalWarps * 32, 0, st>>>(d, tcap, ntd);
+  }
+}
+
+int launch_pairs(int kid, bool det, bool lean, const EvalDev& d, int64_t tcap,
+                 const int64_t* ntd, cudaStream_t st, HbError* err) {
+  switch (kid) {
+    case KID_COUNTING: launch_kid<KID_COUNTING>(d, tcap, ntd, det, lean, st); break;
+    case KID_GRAVITY: launch_kid<KID_GRAVITY>(d, tcap, ntd, det, lean, st); break;
+    case KID_GRAV_POT: launch_kid<KID_GRAV_POT>(d, tcap, ntd, det, lean, st); break;
+    case KID_DENSITY: launch_kid<KID_DENSITY>(d, tcap, ntd, det, lean, st); break;
+    case KID_CRK_MOMENTS: launch_kid<KID_CRK_MOMENTS>(d, tcap, ntd, det, lean, st); break;
+    case KID_HYDRO_FORCE: launch_kid<KID_HYDRO_FORCE>(d, tcap, ntd, det, lean, st); break;
+    case KID_NEIGHBOR_COUNT: launch_kid<KID_NEIGHBOR_COUNT>(d, tcap, ntd, det, lean, st); break;
+    case KID_STUB_ZERO: launch_kid<KID_STUB_ZERO>(d, tcap, ntd, det, lean, st); break;
+    case KID_CRK_INTERP: launch_kid<KID_CRK_INTERP>(d, tcap, ntd, det, lean, st); break;
+    default: return set_err(err, HB_CONTRACT, "unknown kernel id");
+  }
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
+
+// ---------------------------------------------------------------- hb_eval_pairs driver
 struct EvalWs {
   Tiling T;
   uint64_t* keys; uint32_t* vals;
   int32_t *e_src, *e_code, *e_orig, *s_src, *s_code, *s_orig;
   int64_t *rev_flag, *rev_off, *ent_cnt, *ent_ptr, *n_tiles_dev, *tot;
   float4 *P0, *P1, *P2;
-  unsigned long long* dev_cnt;  // [0]=f [1]=g [2]=in_count [3]=err_key
+  unsigned long long* dev_cnt;  // [0]=f [1]=g [2]=in_count [3]=err_key [4]=scratch
 };
 
-static int64_t eval_tile_cap(int64_t n, int64_t n_leaves) { return n / kTileMax + n_leaves + 1; }
-
 static void carve_eval(Arena& ws, const HbEvalArgs* a, EvalWs& w, int64_t E) {
-  int64_t n = a->n, nl = a->n_leaves, tc = eval_tile_cap(n, nl);
-  Tiling& T = w.T;
-  T.n_leaves = nl; T.n_tiles_cap = tc;
-  T.sel_cnt = ws.take<int64_t>(nl + 1); T.sel_off = ws.take<int64_t>(nl + 1);
-  T.tile_cnt = ws.take<int64_t>(nl + 1); T.tile_ptr = ws.take<int64_t>(nl + 1);
-  T.tperm = ws.take<int32_t>(n + 1);
-  T.tile_start = ws.take<int32_t>(tc); T.tile_n = ws.take<int32_t>(tc); T.tile_leaf = ws.take<int32_t>(tc);
-  T.tile_lo = ws.take<float4>(tc); T.tile_hi = ws.take<float4>(tc);
-  T.origin = ws.take<double>(3 * nl + 3);
-  T.overflow = ws.take<int>(1);
+  int64_t n = a->n, nl = a->n_leaves;
+  carve_tiling(ws, n, nl, w.T);
   w.keys = ws.take<uint64_t>(E + 1); w.vals = ws.take<uint32_t>(E + 1);
   w.e_src = ws.take<int32_t>(E + 1); w.e_code = ws.take<int32_t>(E + 1); w.e_orig = ws.take<int32_t>(E + 1);
   w.s_src = ws.take<int32_t>(E + 1); w.s_code = ws.take<int32_t>(E + 1); w.s_orig = ws.take<int32_t>(E + 1);
@@ -628,62 +700,20 @@ static void carve_eval(Arena& ws, const HbEvalArgs* a, EvalWs& w, int64_t E) {
   w.dev_cnt = ws.take<unsigned long long>(5);
 }
 
-template <int KID>
-static void launch_eval(const EvalDev& d, int64_t tcap, const int64_t* ntd, bool det, cudaStream_t st) {
-  unsigned grid = grid_for(tcap, kEvalWarps);
-  if (det) k_eval<KID, true><<<grid, kEvalWarps * 32, 0, st>>>(d, tcap, ntd);
-  else k_eval<KID, false><<<grid, kEvalWarps * 32, 0, st>>>(d, tcap, ntd);
-}
-
-static int kid_selects_gas(int kid) {
-  return kid == KID_DENSITY || kid == KID_NEIGHBOR_COUNT || kid == KID_CRK_MOMENTS ||
-         kid == KID_HYDRO_FORCE || kid == KID_CRK_INTERP;
-}
-
-static int build_tiling(const HbEvalArgs* a, EvalWs& w, int sel, int kid, Arena& ws,
-                        cudaStream_t st, HbError* err) {
-  int64_t nl = a->n_leaves;
-  Tiling& T = w.T;
-  HB_CUDA_TRY(cudaMemsetAsync(T.overflow, 0, sizeof(int), st));
-  k_tile_count<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, a->leaf_start, a->leaf_end, a->state,
-                                                       sel, T.sel_cnt, T.tile_cnt);
-  HB_LAUNCH_CHECK();
-  {
-    Arena s = ws;
-    int rc = exclusive_scan_i64(T.sel_cnt, T.sel_off, nl, T.sel_off + nl, s, st, err);
-    if (rc) return rc;
-    Arena s2 = ws;
-    rc = exclusive_scan_i64(T.tile_cnt, T.tile_ptr, nl, w.n_tiles_dev, s2, st, err);
-    if (rc) return rc;
-    HB_CUDA_TRY(cudaMemcpyAsync(T.tile_ptr + nl, w.n_tiles_dev, sizeof(int64_t),
-                                cudaMemcpyDeviceToDevice, st));
-  }
-  k_tile_build<<<(unsigned)nl, kTileBuildBlock, 0, st>>>(T, a->leaf_start, a->leaf_end, a->state,
-                                                         a->pshift, a->side_length, sel);
-  HB_LAUNCH_CHECK();
-  int64_t tcap = T.n_tiles_cap;
-  k_tile_boxes<<<grid_for(tcap * 32, 256), 256, 0, st>>>(tcap, w.n_tiles_dev, T, a->state,
-                                                        a->pshift, a->side_length);
-  HB_LAUNCH_CHECK();
-  k_pack<<<grid_for(tcap * 32, 256), 256, 0, st>>>(kid, tcap, w.n_tiles_dev, T, a->state,
-                                                   a->pshift, a->aux, a->naux, a->side_length,
-                                                   w.P0, w.P1, w.P2);
-  HB_LAUNCH_CHECK();
-  return HB_OK;
-}
-
 int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   int64_t E = a->n_pairs * (a->mirror ? 2 : 1);
   EvalWs w;
   carve_eval(ws, a, w, E);
   if (ws.dry) {
-    Arena s1 = ws, s2 = ws, s3 = ws;
+    Arena s1 = ws, s2 = ws, s3 = ws, s4 = ws;
     radix_sort_u64_u32(w.keys, w.vals, E, 40, s1, st, err);
     exclusive_scan_i64(nullptr, nullptr, a->n_leaves + 1, nullptr, s2, st, err);
     exclusive_scan_i64(nullptr, nullptr, a->n_pairs + 1, nullptr, s3, st, err);
+    build_tiling(w.T, a->n_leaves, nullptr, nullptr, nullptr, nullptr, 0.0, 0, nullptr, s4, st, err);
     size_t mx = s1.used;
     if (s2.used > mx) mx = s2.used;
     if (s3.used > mx) mx = s3.used;
+    if (s4.used > mx) mx = s4.used;
     ws.used = mx;
     return HB_OK;
   }
@@ -693,8 +723,8 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->n <= 0 || a->n_pairs <= 0 || a->n_leaves <= 0) return HB_OK;
   if (a->n >= (1LL << 31)) return set_err(err, HB_CONTRACT, "too many rows for one evaluation");
   int sel = kid_selects_gas(a->kid);
-  int64_t nl = a->n_leaves, n = a->n;
-  // receiver CSR
+  int64_t nl = a->n_leaves;
+  // receiver CSR (stable: deterministic accumulation order)
   int64_t n_rev = 0;
   if (a->mirror) {
     k_rev_flags<<<grid_for(a->n_pairs, 256), 256, 0, st>>>(a->n_pairs, a->pair_a, a->pair_b,
@@ -730,7 +760,11 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                                                       w.s_src, w.s_code, w.s_orig);
   HB_LAUNCH_CHECK();
   Tiling& T = w.T;
-  int rc0 = build_tiling(a, w, sel, a->kid, ws, st, err);
+  int rc0 = build_tiling(T, nl, a->leaf_start, a->leaf_end, a->state, a->pshift, a->side_length,
+                         sel, w.n_tiles_dev, ws, st, err);
+  if (rc0) return rc0;
+  rc0 = pack_records(a->kid, T, w.n_tiles_dev, a->state, a->pshift, a->aux, a->naux,
+                     a->side_length, w.P0, w.P1, w.P2, st, err);
   if (rc0) return rc0;
   int64_t tcap = T.n_tiles_cap;
   HB_CUDA_TRY(cudaMemsetAsync(w.dev_cnt, 0, 3 * sizeof(unsigned long long), st));
@@ -751,31 +785,23 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   for (int c = 0; c < 10; ++c) d.scale[c] = (float)a->scales[c];
   d.out_flt = a->out_flt; d.out_int = a->out_int; d.write_out = 1;
   d.in_count = w.dev_cnt + 2; d.err_key = w.dev_cnt + 3;
-  bool det = a->deterministic != 0;
-  switch (a->kid) {
-    case KID_COUNTING: launch_eval<KID_COUNTING>(d, tcap, w.n_tiles_dev, det, st); break;
-    case KID_GRAVITY: launch_eval<KID_GRAVITY>(d, tcap, w.n_tiles_dev, det, st); break;
-    case KID_GRAV_POT: launch_eval<KID_GRAV_POT>(d, tcap, w.n_tiles_dev, det, st); break;
-    case KID_DENSITY: launch_eval<KID_DENSITY>(d, tcap, w.n_tiles_dev, det, st); break;
-    case KID_CRK_MOMENTS: launch_eval<KID_CRK_MOMENTS>(d, tcap, w.n_tiles_dev, det, st); break;
-    case KID_HYDRO_FORCE: launch_eval<KID_HYDRO_FORCE>(d, tcap, w.n_tiles_dev, det, st); break;
-    case KID_NEIGHBOR_COUNT: launch_eval<KID_NEIGHBOR_COUNT>(d, tcap, w.n_tiles_dev, det, st); break;
-    case KID_STUB_ZERO: launch_eval<KID_STUB_ZERO>(d, tcap, w.n_tiles_dev, det, st); break;
-    case KID_CRK_INTERP: launch_eval<KID_CRK_INTERP>(d, tcap, w.n_tiles_dev, det, st); break;
-    default: return set_err(err, HB_CONTRACT, "unknown kernel id");
-  }
-  HB_LAUNCH_CHECK();
+  int rc = launch_pairs(a->kid, a->deterministic != 0, false, d, tcap, w.n_tiles_dev, st, err);
+  if (rc) return rc;
   if (a->exact_counters && sel) {
     // the reference counts pairs in reach over every species (hb/kernels.py:356-359)
     HB_CUDA_TRY(cudaMemsetAsync(w.dev_cnt + 2, 0, sizeof(unsigned long long), st));
-    int rc = build_tiling(a, w, 0, KID_COUNTING, ws, st, err);
+    rc = build_tiling(T, nl, a->leaf_start, a->leaf_end, a->state, a->pshift, a->side_length, 0,
+                      w.n_tiles_dev, ws, st, err);
+    if (rc) return rc;
+    rc = pack_records(KID_COUNTING, T, w.n_tiles_dev, a->state, a->pshift, nullptr, 0,
+                      a->side_length, w.P0, w.P1, w.P2, st, err);
     if (rc) return rc;
     EvalDev c = d;
-    c.T = w.T;
+    c.T = T;
     c.write_out = 0;
     c.err_key = w.dev_cnt + 4;
-    launch_eval<KID_COUNTING>(c, T.n_tiles_cap, w.n_tiles_dev, false, st);
-    HB_LAUNCH_CHECK();
+    rc = launch_pairs(KID_COUNTING, false, false, c, tcap, w.n_tiles_dev, st, err);
+    if (rc) return rc;
   }
   unsigned long long hc[4];
   int ovf = 0;

@@ -8,6 +8,10 @@
 #include "hb_common.cuh"
 
 namespace hb {
+struct Tiling;
+}
+
+namespace hb {
 
 enum {
   KID_COUNTING = 0, KID_GRAVITY = 1, KID_GRAV_POT = 2, KID_DENSITY = 3, KID_CRK_MOMENTS = 4,
@@ -163,5 +167,61 @@ template <> struct Pol<KID_CRK_INTERP> {
     phi[0] = sj[0].w * sj[2].w * corr * wk;
   }
 };
+
+constexpr int kTileMax = 32;
+
+// Per-leaf tiling of the selected particles (all, or gas only) into spatially
+// compact tiles of <= 32 (one warp each); internal order = tile order.
+struct Tiling {
+  int64_t n_leaves, n_tiles_cap;
+  int64_t* sel_cnt;     // (n_leaves+1)
+  int64_t* sel_off;     // (n_leaves+1)
+  int64_t* tile_cnt;    // (n_leaves+1)
+  int64_t* tile_ptr;    // (n_leaves+1)  CSR leaf -> tiles
+  int32_t* tperm;       // (n) internal -> state row
+  int32_t* tile_start;  // (cap) internal index
+  int32_t* tile_n;
+  int32_t* tile_leaf;
+  float4* tile_lo;      // w = hmax
+  float4* tile_hi;
+  double* origin;       // (n_leaves,3)
+  int* overflow;        // device flag: a leaf exceeded kTileBuildCap
+};
+
+// Everything one pair-kernel launch reads.
+struct EvalDev {
+  Tiling T;
+  const int64_t* ent_ptr;  // (n_leaves+1)
+  const int32_t* ent_src;
+  const int32_t* ent_code;  // shift code | fwd << 8
+  const float4 *P0, *P1, *P2;
+  const double* state;
+  const int8_t* pshift;
+  double L, reach;
+  PairParams pp;
+  float cull_reach;
+  int include_self;
+  int nchan;
+  float scale[10];
+  double* out_flt;
+  int64_t* out_int;
+  int write_out;
+  unsigned long long* in_count;
+  unsigned long long* err_key;  // min (entry*4 + kind)
+};
+
+// ---- internal driver pieces shared by hb_eval_pairs and hb_force_step ----
+int64_t tile_capacity(int64_t n, int64_t n_leaves);
+void carve_tiling(Arena& ws, int64_t n, int64_t n_leaves, Tiling& T);
+int build_tiling(Tiling& T, int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
+                 const double* state, const int8_t* pshift, double L, int sel,
+                 int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err);
+int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, const double* state,
+                 const int8_t* pshift, const double* aux, int naux, double L, float4* P0,
+                 float4* P1, float4* P2, cudaStream_t st, HbError* err);
+// lean: resident hot path (no exact counters / per-entry error attribution)
+int launch_pairs(int kid, bool det, bool lean, const EvalDev& d, int64_t tile_cap,
+                 const int64_t* n_tiles_dev, cudaStream_t st, HbError* err);
+int kid_selects_gas(int kid);
 
 }  // namespace hb

@@ -1,0 +1,346 @@
+// hb_step.cu -- device-resident force evaluation (hb_force_step, include/hb.h).
+//
+// One call = the s = 0 boundary of subcycle_pm_step (hb/stepper.py:113-179)
+// with ordered single-count pair semantics: mesh build + reorder, list sweep
+// straight into a receiver CSR (the list is born grouped by receiver), two
+// tilings shared by all passes (gas-only for the SPH kernels, all species for
+// gravity), then ncount -> density (+EOS) -> CRK moments + solve -> gravity ->
+// hydro with the lean pair kernels.  Host syncs: the leaf count and the list
+// entry count (both needed to size launches); everything else is stream-ordered.
+#include "hb_internal.cuh"
+
+namespace hb {
+
+__global__ void k_state_matrix(int64_t n, const double* pos, const double* vel, const double* mass,
+                               const double* h, const double* u, const double* rho,
+                               const uint8_t* species, double gamma, double* st) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* s = st + i * NCOL;
+  s[C_X] = pos[3 * i]; s[C_Y] = pos[3 * i + 1]; s[C_Z] = pos[3 * i + 2];
+  s[C_VX] = vel[3 * i]; s[C_VY] = vel[3 * i + 1]; s[C_VZ] = vel[3 * i + 2];
+  s[C_M] = mass[i];
+  s[C_H] = h[i];
+  double gm1 = gamma - 1.0;
+  s[C_RHO] = rho[i];
+  s[C_P] = gm1 * rho[i] * u[i];
+  s[C_CS] = sqrt(fmax(gamma * gm1 * u[i], 0.0));
+  s[C_SP] = (double)species[i];
+}
+
+// density write-back for gas rows of active leaves (hb/hydro.py:73-80), then
+// EOS columns for every row (hb/hydro.py:48-57)
+__global__ void k_density_update(int64_t n_leaves, const int64_t* leaf_start,
+                                 const int64_t* leaf_end, const uint8_t* ghost_only,
+                                 const uint8_t* species, const double* rho_new, double* density) {
+  int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (leaf >= n_leaves || ghost_only[leaf]) return;
+  for (int64_t r = leaf_start[leaf] + lane; r < leaf_end[leaf]; r += 32)
+    if (species[r] == 1) density[r] = rho_new[r];
+}
+__global__ void k_alias_sync(int64_t n, const int64_t* ghost_src, double* density) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && ghost_src[i] >= 0) density[i] = density[ghost_src[i]];
+}
+__global__ void k_eos(int64_t n, const double* rho, const double* u, double gamma, double* st) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double gm1 = gamma - 1.0;
+  st[i * NCOL + C_RHO] = rho[i];
+  st[i * NCOL + C_P] = gm1 * rho[i] * u[i];
+  st[i * NCOL + C_CS] = sqrt(fmax(gamma * gm1 * u[i], 0.0));
+}
+
+__global__ void k_gather_inverse(int64_t n, const int64_t* perm, int64_t* inv) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) inv[perm[k]] = k;
+}
+__global__ void k_ghost_src(int64_t n, const int64_t* perm, const int64_t* inv,
+                            const int64_t* src_in, int64_t* src_out) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int64_t g = src_in[perm[k]];
+  src_out[k] = g >= 0 ? inv[g] : -1;
+}
+
+template <class T>
+__global__ void k_gather(int64_t n, int w, const int64_t* perm, const T* in, T* out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * w) return;
+  int64_t r = t / w, c = t - r * w;
+  out[t] = in[perm[r] * w + c];
+}
+
+struct StepWs {
+  // mesh
+  int64_t *leaf_start, *leaf_end, *leaf_bin, *bin_ptr, *n_leaves_dev;
+  double *leaf_lo, *leaf_hi;
+  uint8_t* ghost_only;
+  // list csr
+  int64_t* ent_ptr;
+  int32_t *ent_src, *ent_code;
+  // engine
+  Tiling Tg, Ta;
+  int64_t *ntg, *nta;
+  double *state, *rho_new, *inv_tmp;
+  float4 *P0, *P1, *P2;
+  unsigned long long* err_key;
+  int64_t* inv;
+};
+
+static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t lcap, StepWs& w) {
+  w.leaf_start = ws.take<int64_t>(cap); w.leaf_end = ws.take<int64_t>(cap);
+  w.leaf_bin = ws.take<int64_t>(cap); w.bin_ptr = ws.take<int64_t>(nbins + 1);
+  w.n_leaves_dev = ws.take<int64_t>(1);
+  w.leaf_lo = ws.take<double>(3 * cap); w.leaf_hi = ws.take<double>(3 * cap);
+  w.ghost_only = ws.take<uint8_t>(cap);
+  w.ent_ptr = ws.take<int64_t>(cap + 1);
+  w.ent_src = ws.take<int32_t>(lcap + 1); w.ent_code = ws.take<int32_t>(lcap + 1);
+  carve_tiling(ws, n, cap, w.Tg);
+  carve_tiling(ws, n, cap, w.Ta);
+  w.ntg = ws.take<int64_t>(1); w.nta = ws.take<int64_t>(1);
+  w.state = ws.take<double>(n * NCOL + 1);
+  w.rho_new = ws.take<double>(n + 1);
+  w.P0 = ws.take<float4>(n + 1); w.P1 = ws.take<float4>(n + 1); w.P2 = ws.take<float4>(n + 1);
+  w.err_key = ws.take<unsigned long long>(1);
+  w.inv = ws.take<int64_t>(n + 1);
+}
+
+struct PhaseTimer {
+  bool on;
+  cudaStream_t st;
+  cudaEvent_t ev[9];
+  int k = 0;
+  PhaseTimer(bool on_, cudaStream_t s) : on(on_), st(s) {
+    if (on) for (int i = 0; i < 9; ++i) cudaEventCreate(&ev[i]);
+  }
+  ~PhaseTimer() { if (on) for (int i = 0; i < 9; ++i) cudaEventDestroy(ev[i]); }
+  void mark(int i) { if (on) cudaEventRecord(ev[i], st); }
+};
+
+int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
+  int64_t n = a->n;
+  int64_t nbins = a->nb[0] * a->nb[1] * a->nb[2];
+  int64_t cap = hb_leaf_capacity(n, nbins, a->max_leaf_size);
+  StepWs w;
+  carve_step(ws, n, nbins, cap, a->list_capacity, w);
+  // nested arenas (mesh build, list csr, tilings) reuse the space after the carve
+  HbMeshArgs m = {};
+  m.n = n; m.pos = a->pos_in; m.image_shift = a->image_shift_in; m.ghost = a->ghost_in;
+  m.side_length = a->side_length;
+  for (int d = 0; d < 3; ++d) { m.lo[d] = a->lo[d]; m.width[d] = a->width[d]; m.nb[d] = a->nb[d]; }
+  m.max_leaf_size = a->max_leaf_size; m.leaf_cap = cap;
+  m.perm = a->perm; m.leaf_start = w.leaf_start; m.leaf_end = w.leaf_end; m.leaf_lo = w.leaf_lo;
+  m.leaf_hi = w.leaf_hi; m.leaf_ghost_only = w.ghost_only; m.leaf_bin = w.leaf_bin;
+  m.bin_ptr = w.bin_ptr; m.n_leaves_dev = w.n_leaves_dev;
+  int64_t nl = 0;
+  m.n_leaves_host = &nl;
+  ListArgsDev ld;
+  if (ws.dry) {
+    size_t mx = ws.used;
+    Arena s1 = ws; build_mesh(&m, s1, st, err); if (s1.used > mx) mx = s1.used;
+    ld.n_leaves = cap;
+    Arena s2 = ws; assemble_csr(ld, a->list_capacity, nullptr, nullptr, nullptr, nullptr, s2, st, err);
+    if (s2.used > mx) mx = s2.used;
+    Arena s3 = ws;
+    build_tiling(w.Tg, cap, nullptr, nullptr, nullptr, nullptr, 0.0, 1, nullptr, s3, st, err);
+    if (s3.used > mx) mx = s3.used;
+    ws.used = mx;
+    return HB_OK;
+  }
+  if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (step)");
+  if (n <= 0) return HB_OK;
+  if (n >= (1LL << 31)) return set_err(err, HB_CONTRACT, "too many rows for one rank");
+  PhaseTimer tm(a->timing != 0, st);
+  tm.mark(0);
+  // 1. mesh + reorder
+  {
+    Arena s = ws;
+    int rc = build_mesh(&m, s, st, err);
+    if (rc) return rc;
+  }
+  a->n_leaves = nl;
+  {
+    unsigned g3 = grid_for(n * 3, 256), g1 = grid_for(n, 256);
+    k_gather<double><<<g3, 256, 0, st>>>(n, 3, a->perm, a->pos_in, a->pos);
+    k_gather<double><<<g3, 256, 0, st>>>(n, 3, a->perm, a->vel_in, a->vel);
+    k_gather<double><<<g1, 256, 0, st>>>(n, 1, a->perm, a->mass_in, a->mass);
+    k_gather<double><<<g1, 256, 0, st>>>(n, 1, a->perm, a->smoothing_in, a->smoothing);
+    k_gather<double><<<g1, 256, 0, st>>>(n, 1, a->perm, a->internal_energy_in, a->internal_energy);
+    k_gather<double><<<g1, 256, 0, st>>>(n, 1, a->perm, a->density_in, a->density);
+    k_gather<uint8_t><<<g1, 256, 0, st>>>(n, 1, a->perm, a->species_in, a->species);
+    k_gather<uint8_t><<<g1, 256, 0, st>>>(n, 1, a->perm, a->ghost_in, a->ghost);
+    k_gather<int8_t><<<g3, 256, 0, st>>>(n, 3, a->perm, a->image_shift_in, a->image_shift);
+    k_gather<int64_t><<<g1, 256, 0, st>>>(n, 1, a->perm, a->global_id_in, a->global_id);
+    if (a->ghost_src_in && a->ghost_src) {
+      k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
+      k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
+      HB_COUNT_LAUNCH(2);
+    }
+    HB_COUNT_LAUNCH(9);
+    HB_LAUNCH_CHECK();
+  }
+  tm.mark(1);
+  // 2. ordered list as a receiver CSR
+  ld.n_leaves = nl; ld.leaf_bin = w.leaf_bin; ld.leaf_level = nullptr; ld.bin_ptr = w.bin_ptr;
+  ld.bin_ids = nullptr; ld.leaf_lo = w.leaf_lo; ld.leaf_hi = w.leaf_hi; ld.ghost_only = w.ghost_only;
+  for (int d = 0; d < 3; ++d) { ld.g.nb[d] = a->nb[d]; ld.g.periodic[d] = a->periodic[d]; }
+  ld.g.L = a->side_length; ld.g.reach = a->reach; ld.g.active_depth = 0;
+  {
+    Arena s = ws;
+    int64_t total = 0;
+    int rc = assemble_csr(ld, a->list_capacity, w.ent_src, w.ent_code, w.ent_ptr, &total, s, st, err);
+    a->n_entries = total;
+    a->list_capacity_needed = total;
+    if (rc) return rc;
+  }
+  tm.mark(2);
+  // 3. state matrix, tilings
+  k_state_matrix<<<grid_for(n, 256), 256, 0, st>>>(n, a->pos, a->vel, a->mass, a->smoothing,
+                                                   a->internal_energy, a->density, a->species,
+                                                   a->eos_gamma, w.state);
+  HB_LAUNCH_CHECK();
+  w.Tg.n_leaves = nl; w.Ta.n_leaves = nl;
+  {
+    Arena s = ws;
+    int rc = build_tiling(w.Tg, nl, w.leaf_start, w.leaf_end, w.state, a->image_shift,
+                          a->side_length, 1, w.ntg, s, st, err);
+    if (rc) return rc;
+    Arena s2 = ws;
+    rc = build_tiling(w.Ta, nl, w.leaf_start, w.leaf_end, w.state, a->image_shift,
+                      a->side_length, 0, w.nta, s2, st, err);
+    if (rc) return rc;
+  }
+  HB_CUDA_TRY(cudaMemsetAsync(w.err_key, 0xff, sizeof(unsigned long long), st));
+  EvalDev d = {};
+  d.ent_ptr = w.ent_ptr; d.ent_src = w.ent_src; d.ent_code = w.ent_code;
+  d.P0 = w.P0; d.P1 = w.P1; d.P2 = w.P2; d.state = w.state; d.pshift = a->image_shift;
+  d.L = a->side_length; d.include_self = 1; d.write_out = 1; d.err_key = w.err_key;
+  d.in_count = nullptr; d.out_int = nullptr;
+  double sph_reach = 2.0 * a->h_max;
+  auto setup = [&](int kid, double reach, double p0, double p1, int nchan, const Tiling& T,
+                   double* out) {
+    d.T = T;
+    d.reach = reach;
+    d.pp.p0 = (float)p0; d.pp.p1 = (float)p1;
+    d.pp.inv_rs = p0 != 0.0 ? (float)(1.0 / p0) : 0.0f;
+    d.pp.reach2 = (float)(reach * reach);
+    d.cull_reach = (float)(reach * (1.0 + 1e-4)) + 1e-30f;
+    d.nchan = nchan;
+    d.out_flt = out;
+    (void)kid;
+  };
+  int rc = HB_OK;
+  int64_t tcap = w.Tg.n_tiles_cap;
+  // 4. neighbour count (hb/hydro.py:223-227)
+  if (a->passes & HB_PASS_NCOUNT) {
+    HB_CUDA_TRY(cudaMemsetAsync(a->ncount, 0, n * sizeof(double), st));
+    rc = pack_records(KID_NEIGHBOR_COUNT, w.Tg, w.ntg, w.state, a->image_shift, nullptr, 0,
+                      a->side_length, w.P0, w.P1, w.P2, st, err);
+    if (rc) return rc;
+    setup(KID_NEIGHBOR_COUNT, sph_reach, 0.0, 0.0, 1, w.Tg, a->ncount);
+    rc = launch_pairs(KID_NEIGHBOR_COUNT, false, true, d, tcap, w.ntg, st, err);
+    if (rc) return rc;
+  }
+  tm.mark(3);
+  // 5. density + alias sync + EOS (hb/hydro.py:60-84, 48-57)
+  if (a->passes & HB_PASS_DENSITY) {
+    HB_CUDA_TRY(cudaMemsetAsync(w.rho_new, 0, n * sizeof(double), st));
+    rc = pack_records(KID_DENSITY, w.Tg, w.ntg, w.state, a->image_shift, nullptr, 0,
+                      a->side_length, w.P0, w.P1, w.P2, st, err);
+    if (rc) return rc;
+    setup(KID_DENSITY, sph_reach, 0.0, 0.0, 1, w.Tg, w.rho_new);
+    rc = launch_pairs(KID_DENSITY, false, true, d, tcap, w.ntg, st, err);
+    if (rc) return rc;
+    k_density_update<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, w.leaf_start, w.leaf_end,
+                                                             w.ghost_only, a->species, w.rho_new,
+                                                             a->density);
+    if (a->ghost_src_in && a->ghost_src) {
+      k_alias_sync<<<grid_for(n, 256), 256, 0, st>>>(n, a->ghost_src, a->density);
+      HB_COUNT_LAUNCH(1);
+    }
+    HB_COUNT_LAUNCH(1);
+    k_eos<<<grid_for(n, 256), 256, 0, st>>>(n, a->density, a->internal_energy, a->eos_gamma,
+                                            w.state);
+    HB_LAUNCH_CHECK();
+  }
+  tm.mark(4);
+  // 6. CRK moments + solve (hb/hydro.py:99-150)
+  if (a->passes & HB_PASS_CRK) {
+    HB_CUDA_TRY(cudaMemsetAsync(a->crk_moments, 0, n * 10 * sizeof(double), st));
+    rc = pack_records(KID_CRK_MOMENTS, w.Tg, w.ntg, w.state, a->image_shift, nullptr, 0,
+                      a->side_length, w.P0, w.P1, w.P2, st, err);
+    if (rc) return rc;
+    setup(KID_CRK_MOMENTS, sph_reach, 0.0, 0.0, 10, w.Tg, a->crk_moments);
+    rc = launch_pairs(KID_CRK_MOMENTS, false, true, d, tcap, w.ntg, st, err);
+    if (rc) return rc;
+    rc = hb_crk_solve(n, a->crk_moments, 10, a->species, 1e8, a->crk_A, a->crk_B,
+                      a->crk_fallback, st, err);
+    if (rc) return rc;
+  }
+  tm.mark(5);
+  // 7. short-range gravity (hb/kernels.py:152-163)
+  if (a->passes & HB_PASS_GRAVITY) {
+    HB_CUDA_TRY(cudaMemsetAsync(a->grav, 0, n * 3 * sizeof(double), st));
+    rc = pack_records(KID_GRAVITY, w.Ta, w.nta, w.state, a->image_shift, nullptr, 0,
+                      a->side_length, w.P0, w.P1, w.P2, st, err);
+    if (rc) return rc;
+    setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
+    rc = launch_pairs(KID_GRAVITY, false, true, d, w.Ta.n_tiles_cap, w.nta, st, err);
+    if (rc) return rc;
+  }
+  tm.mark(6);
+  // 8. hydro force (hb/kernels.py:222-258)
+  if (a->passes & HB_PASS_HYDRO) {
+    HB_CUDA_TRY(cudaMemsetAsync(a->hydro, 0, n * 5 * sizeof(double), st));
+    rc = pack_records(KID_HYDRO_FORCE, w.Tg, w.ntg, w.state, a->image_shift, nullptr, 0,
+                      a->side_length, w.P0, w.P1, w.P2, st, err);
+    if (rc) return rc;
+    setup(KID_HYDRO_FORCE, sph_reach, a->visc_alpha, a->visc_beta, 5, w.Tg, a->hydro);
+    rc = launch_pairs(KID_HYDRO_FORCE, false, true, d, tcap, w.ntg, st, err);
+    if (rc) return rc;
+  }
+  tm.mark(7);
+  unsigned long long ek = 0;
+  int ovf = 0, ovf2 = 0;
+  HB_CUDA_TRY(cudaMemcpyAsync(&ek, w.err_key, sizeof(ek), cudaMemcpyDeviceToHost, st));
+  HB_CUDA_TRY(cudaMemcpyAsync(&ovf, w.Tg.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HB_CUDA_TRY(cudaMemcpyAsync(&ovf2, w.Ta.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HB_CUDA_TRY(cudaStreamSynchronize(st));
+  if (tm.on) {
+    for (int i = 0; i < 7; ++i) cudaEventElapsedTime(&a->ms_phase[i], tm.ev[i], tm.ev[i + 1]);
+    cudaEventElapsedTime(&a->ms_phase[7], tm.ev[0], tm.ev[7]);
+  }
+  if (ovf || ovf2) return set_err(err, HB_CONTRACT, "leaf exceeds the tiling capacity (2048 members)");
+  if (ek != ~0ull) {
+    if (err) { err->leaf_a = -1; err->leaf_b = -1; }
+    return set_err(err, (ek % 4) == 1 ? HB_NONFINITE : HB_OVERFLOW,
+                   (ek % 4) == 1 ? "non-finite partial" : "accumulator overflow");
+  }
+  return HB_OK;
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,
+                                          int64_t list_capacity) {
+  HbStepArgs a = {};
+  a.n = n;
+  for (int d = 0; d < 3; ++d) a.nb[d] = nb[d];
+  a.max_leaf_size = max_leaf_size;
+  a.list_capacity = list_capacity;
+  Arena ws;
+  ws.dry = true;
+  force_step(&a, ws, nullptr, nullptr);
+  return ws.used + 4096;
+}
+
+extern "C" int hb_force_step(HbStepArgs* a, void* wsp, size_t ws_bytes, void* stream, HbError* err) {
+  if (err) *err = HbError{};
+  Arena ws;
+  ws.base = (char*)wsp; ws.cap = ws_bytes;
+  return force_step(a, ws, (cudaStream_t)stream, err);
+}

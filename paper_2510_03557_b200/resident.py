@@ -1,0 +1,194 @@
+"""Device-resident force evaluation (the benchmark's hot path).
+
+``ResidentRank`` holds one rank's particle fields as CUDA tensors and runs
+``hb_force_step`` (include/hb.h): the s = 0 boundary of subcycle_pm_step
+(hb/stepper.py:113-179) -- mesh build + reorder, lists, neighbour count,
+density + EOS, CRK moments + solve, short-range gravity, hydro force -- with
+the reference's ordered single-count semantics.  Fields ping-pong between two
+buffer sets because the build reorders them (the reference reorders its
+ParticleSet in place, hb/cmtree.py:171-172).
+
+``force_step(particles, ...)`` is the host-level convenience wrapper: numpy in,
+ParticleSet reordered in place, numpy outputs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .box import BoxGeometry
+from .cmtree import mesh_geometry
+from .errors import HydroboxError
+from .particles import FIELD_SPECS, ParticleSet
+
+PASS_NCOUNT, PASS_DENSITY, PASS_CRK, PASS_GRAVITY, PASS_HYDRO = 1, 2, 4, 8, 16
+PASS_ALL = 31
+PHASES = ("build", "list", "ncount", "density_eos", "crk", "gravity", "hydro", "total")
+
+STEP_FIELDS = ("pos", "vel", "mass", "smoothing", "internal_energy", "density", "species",
+               "ghost", "image_shift", "global_id", "ghost_src")
+
+
+P = C.c_void_p
+
+
+class HbStepArgs(C.Structure):
+    _fields_ = ([("n", C.c_int64)] + [(f + "_in", P) for f in STEP_FIELDS]
+                + [(f, P) for f in STEP_FIELDS]
+                + [("side_length", C.c_double), ("lo", C.c_double * 3), ("width", C.c_double * 3),
+                   ("nb", C.c_int64 * 3), ("periodic", C.c_uint8 * 3), ("max_leaf_size", C.c_int64),
+                   ("reach", C.c_double), ("h_max", C.c_double), ("r_s", C.c_double),
+                   ("r_cut", C.c_double), ("softening", C.c_double), ("eos_gamma", C.c_double),
+                   ("visc_alpha", C.c_double), ("visc_beta", C.c_double), ("passes", C.c_int32),
+                   ("timing", C.c_int32), ("list_capacity", C.c_int64),
+                   ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
+                   ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
+                   ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
+                   ("ms_phase", C.c_float * 8)])
+
+
+def _bind(lib):
+    if getattr(lib, "_step_bound", False):
+        return
+    lib.hb_force_step_workspace.restype = C.c_size_t
+    lib.hb_force_step_workspace.argtypes = [C.c_int64, C.c_void_p, C.c_int64, C.c_int64]
+    lib.hb_force_step.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+    lib._step_bound = True
+
+
+@dataclass
+class StepConfig:
+    """Scales of one force evaluation (derived as hb/config.py:79-99 and
+    hb/driver.py:121-150 derive them)."""
+
+    box: BoxGeometry
+    bin_width: float
+    max_leaf_size: int
+    r_s: float
+    r_cut: float
+    softening: float
+    eos_gamma: float = 5.0 / 3.0
+    visc_alpha: float = 1.0
+    visc_beta: float = 2.0
+    bounds_lo: np.ndarray | None = None
+    bounds_hi: np.ndarray | None = None
+
+
+class ResidentRank:
+    """One rank's working set on the current CUDA device."""
+
+    def __init__(self, particles: ParticleSet, cfg: StepConfig):
+        torch = N.torch_cuda()
+        self.cfg = cfg
+        self.n = particles.n
+        self.buf = [self._alloc(particles), None]
+        self.buf[1] = {k: torch.empty_like(v) for k, v in self.buf[0].items()}
+        self.cur = 0
+        gas = particles.species == 1
+        self.h_max = float(particles.smoothing.max()) if particles.n else 0.0
+        if not np.any(gas):
+            self.h_max = 0.0
+        lo, hi, nb, width, periodic = mesh_geometry(cfg.box, cfg.bin_width, cfg.bounds_lo,
+                                                    cfg.bounds_hi)
+        self.lo, self.nb, self.width, self.periodic = lo, nb, width, periodic
+        n = max(self.n, 1)
+        f64 = torch.float64
+        self.out = {
+            "perm": torch.empty(n, dtype=torch.int64, device="cuda"),
+            "ncount": torch.zeros(n, dtype=f64, device="cuda"),
+            "grav": torch.zeros((n, 3), dtype=f64, device="cuda"),
+            "hydro": torch.zeros((n, 5), dtype=f64, device="cuda"),
+            "crk_moments": torch.zeros((n, 10), dtype=f64, device="cuda"),
+            "crk_A": torch.zeros(n, dtype=f64, device="cuda"),
+            "crk_B": torch.zeros((n, 3), dtype=f64, device="cuda"),
+            "crk_fallback": torch.zeros(n, dtype=torch.uint8, device="cuda"),
+        }
+        self.lib = N.lib()
+        _bind(self.lib)
+        nbins = int(np.prod(nb))
+        cap = int(self.lib.hb_leaf_capacity(self.n, nbins, cfg.max_leaf_size))
+        self.list_capacity = max(1024, cap * 64)
+        self._ws = None
+        self._ws_cap = -1
+        self.last = None
+
+    @staticmethod
+    def _alloc(p: ParticleSet) -> dict:
+        torch = N.torch_cuda()
+        return {name: N.dev(np.ascontiguousarray(getattr(p, name))) for name, _, _ in FIELD_SPECS
+                if name in STEP_FIELDS}
+
+    def _workspace(self):
+        if self._ws is None or self._ws_cap != self.list_capacity:
+            nb3 = (C.c_int64 * 3)(*[int(v) for v in self.nb])
+            sz = self.lib.hb_force_step_workspace(self.n, nb3, self.cfg.max_leaf_size,
+                                                  self.list_capacity)
+            self._ws = None
+            self._ws = N.workspace(sz)
+            self._ws_cap = self.list_capacity
+        return self._ws
+
+    def fields(self) -> dict:
+        """Current (leaf-ordered after a step) device fields."""
+        return self.buf[self.cur]
+
+    def step(self, passes: int = PASS_ALL, timing: bool = False) -> dict:
+        """One force evaluation; returns the device outputs (leaf order)."""
+        cfg = self.cfg
+        src, dst = self.buf[self.cur], self.buf[1 - self.cur]
+        a = HbStepArgs()
+        a.n = self.n
+        for f in STEP_FIELDS:
+            setattr(a, f + "_in", N.ptr(src[f]))
+            setattr(a, f, N.ptr(dst[f]))
+        a.side_length = float(cfg.box.side_length)
+        for d in range(3):
+            a.lo[d], a.width[d], a.nb[d] = float(self.lo[d]), float(self.width[d]), int(self.nb[d])
+            a.periodic[d] = 1 if self.periodic[d] else 0
+        a.max_leaf_size = int(cfg.max_leaf_size)
+        a.h_max = self.h_max
+        a.reach = max(cfg.r_cut if passes & PASS_GRAVITY else 0.0, 2.0 * self.h_max)
+        a.r_s, a.r_cut, a.softening = cfg.r_s, cfg.r_cut, cfg.softening
+        a.eos_gamma, a.visc_alpha, a.visc_beta = cfg.eos_gamma, cfg.visc_alpha, cfg.visc_beta
+        a.passes = int(passes)
+        a.timing = 1 if timing else 0
+        for k in ("perm", "ncount", "grav", "hydro", "crk_moments", "crk_A", "crk_B",
+                  "crk_fallback"):
+            setattr(a, k, N.ptr(self.out[k]))
+        for d in range(3):
+            if a.reach > self.width[d] and self.nb[d] > 3:
+                raise HydroboxError(f"reach {a.reach:.4g} exceeds bin width "
+                                    f"{self.width[d]:.4g} on axis {d}")
+        for _attempt in range(3):
+            ws = self._workspace()
+            a.list_capacity = self.list_capacity
+            err = N.HbError()
+            st = self.lib.hb_force_step(C.byref(a), N.ptr(ws), C.c_size_t(ws.numel()),
+                                        N.stream_ptr(), C.byref(err))
+            if st == N.HB_CONTRACT and a.list_capacity_needed > self.list_capacity:
+                self.list_capacity = int(a.list_capacity_needed * 1.25) + 1024
+                continue
+            N.check(st, err, "force_step")
+            break
+        self.cur = 1 - self.cur
+        self.last = {"n_leaves": int(a.n_leaves), "n_entries": int(a.n_entries),
+                     "ms_phase": dict(zip(PHASES, list(a.ms_phase))) if timing else None}
+        return self.out
+
+
+def force_step(particles: ParticleSet, cfg: StepConfig, passes: int = PASS_ALL) -> dict:
+    """Host-level force evaluation: reorders ``particles`` in place (leaf
+    order) and returns numpy outputs; density is updated as compute_density
+    updates it."""
+    rank = ResidentRank(particles, cfg)
+    out = rank.step(passes)
+    fields = rank.fields()
+    for name in STEP_FIELDS:
+        setattr(particles, name, fields[name].cpu().numpy())
+    res = {k: v[:particles.n].cpu().numpy() for k, v in out.items()}
+    res["crk_fallback"] = res["crk_fallback"].astype(bool)
+    res.update(rank.last)
+    return res

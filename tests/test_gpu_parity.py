@@ -191,3 +191,43 @@ def test_gpu_nonfinite_raises(golden):
     il = InteractionList(g[k + "la"], g[k + "lb"], ker.reach, 0, g[k + "ls"])
     with pytest.raises(KernelEvalError, match="non-finite partial in leaf pair"):
         eval_interaction_list(ker, il, st, MeshView(g, k + "mesh_"), mode=EvalMode.RELAXED)
+
+
+def test_gpu_resident_force_step(golden, oracle):
+    """hb_force_step (the benchmark hot path) reproduces the reference step:
+    same reorder, exact counts, density/CRK/gravity/hydro within tolerance."""
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.cmtree import InteractionList
+    from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
+    from paper_2510_03557_b200.kernels import hydro_force_kernel
+    from paper_2510_03557_b200.resident import StepConfig, force_step
+    g = golden("step")
+    p = particle_set(g, "in_")
+    cfg = StepConfig(box=BoxGeometry(1.0), bin_width=float(g["bin_width"]), max_leaf_size=256,
+                     r_s=float(g["r_s"]), r_cut=float(g["r_cut"]), softening=float(g["eps"]),
+                     bounds_lo=g["bounds_lo"], bounds_hi=g["bounds_hi"])
+    out = force_step(p, cfg)
+    np.testing.assert_array_equal(p.global_id, g["built_global_id"])
+    np.testing.assert_array_equal(p.ghost_src, g["built_ghost_src"])
+    assert out["n_entries"] == g["la"].shape[0]
+    np.testing.assert_array_equal(out["ncount"], g["ncount"])
+    gas = p.species == 1
+    rel = np.abs(p.density - g["density"])[gas] / g["density"][gas]
+    assert np.median(rel) <= 1e-6 and rel.max() <= 1e-5, rel.max()
+    np.testing.assert_array_equal(out["crk_fallback"], g["crk_fallback"])
+    ok = gas & (g["crk_m0"] > 0)
+    relA = np.abs(out["crk_A"] - g["crk_A"])[ok] / np.abs(g["crk_A"][ok])
+    assert np.median(relA) <= 1e-6 and np.quantile(relA, 0.999) <= 1e-5, relA.max()
+    own = p.ghost == 0
+    st = g["state_eos"]
+    ms = MeshView(g, "mesh_")
+    gk = short_range_gravity_kernel(ForceSplit(r_s=float(g["r_s"]), r_cut=float(g["r_cut"])),
+                                    float(g["eps"]))
+    absg = oracle.eval_abs_sums(gk, g["la"], g["lb"], g["ls"], st, ms.leaf_start, ms.leaf_end, 1.0,
+                                pshift=g["built_image_shift"])
+    assert_fp32_close(out["grav"][own], g["grav"][own], absg[own], what="resident gravity")
+    hk = hydro_force_kernel(2 * p.smoothing.max())
+    absh = oracle.eval_abs_sums(hk, g["la"], g["lb"], g["ls"], st, ms.leaf_start, ms.leaf_end, 1.0,
+                                pshift=g["built_image_shift"])
+    ref_h = np.column_stack([g["hydro_force"], g["hydro_edot"]])
+    assert_fp32_close(out["hydro"][own, :4], ref_h[own], absh[own, :4], what="resident hydro")
