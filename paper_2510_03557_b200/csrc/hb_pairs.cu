@@ -583,6 +583,158 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
   }
 }
 
+// ---------------------------------------------------------------- fast gravity
+// Resident-path short-range gravity.  Same tiling, culling and staging as
+// k_eval<KID_GRAVITY>, but S(r/r_s) comes from a 128-interval cubic table in
+// shared memory (centred intervals, Chebyshev-node interpolation of
+// erfc(x) + 2x/sqrt(pi) exp(-x^2) in float64 on the host; FP32 abs. error
+// < 1e-7) indexed with the float magic-number trick (no F2I), and the m_i
+// factor is applied once per target.  Per pair: 21 FMA-pipe + 2 MUFU + 4 ALU
+// + 2 LDS.  Entries beyond r_cut (plus half an interval) read a zero row.
+constexpr int kGravWarps = 8;
+constexpr int kGravStage = 128;
+
+__global__ void __launch_bounds__(kGravWarps * 32)
+k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_last,
+          const int64_t* n_tiles_dev) {
+  __shared__ float4 s_tab[kGravTableMax];
+  __shared__ float4 s_src[kGravWarps][kGravStage];
+  for (int k = threadIdx.x; k <= tab_last; k += blockDim.x) s_tab[k] = table[k];
+  __syncthreads();
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = (int64_t)blockIdx.x * kGravWarps + wid;
+  if (t >= *n_tiles_dev) return;
+  const Tiling& T = a.T;
+  int A = T.tile_leaf[t];
+  int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
+  if (e0 == e1) return;
+  int n_t = T.tile_n[t];
+  bool live = lane < n_t;
+  int k_i = T.tile_start[t] + (live ? lane : 0);
+  float4 ti = a.P0[k_i];
+  float4 tlo = T.tile_lo[t], thi = T.tile_hi[t];
+  float R2 = a.cull_reach * a.cull_reach;
+  float eps2 = a.pp.p1;
+  float ax = 0.0f, ay = 0.0f, az = 0.0f;
+  double oA[3] = {T.origin[3 * A], T.origin[3 * A + 1], T.origin[3 * A + 2]};
+  float4* stage = s_src[wid];
+  int cnt = 0;
+  auto flush = [&]() {
+    __syncwarp();
+#pragma unroll 4
+    for (int q = 0; q < cnt; ++q) {
+      float4 s = stage[q];
+      float dx = ti.x - s.x, dy = ti.y - s.y, dz = ti.z - s.z;
+      float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      float ri = rsqrt_ftz(r2 + eps2);
+      float rr = r2 * rsqrt_ftz(fmaxf(r2, 1e-30f));
+      float fm = fmaf(rr, tab_scale, 12582912.0f);
+      int k = min(__float_as_int(fm) - 0x4B400000, tab_last);
+      float u = fmaf(rr, tab_scale, 12582912.0f - fm);
+      float4 c = s_tab[k];
+      float S = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x);
+      float w = (S * (ri * ri)) * (ri * s.w);
+      ax = fmaf(w, dx, ax);
+      ay = fmaf(w, dy, ay);
+      az = fmaf(w, dz, az);
+    }
+    __syncwarp();
+    cnt = 0;
+  };
+  for (int64_t e = e0; e < e1; ++e) {
+    int B = a.ent_src[e];
+    int code = a.ent_code[e] & 31;
+    int sh0 = code / 9 - 1, sh1 = (code / 3) % 3 - 1, sh2 = code % 3 - 1;
+    float D0 = (float)((oA[0] - T.origin[3 * B]) - (double)sh0 * a.L);
+    float D1 = (float)((oA[1] - T.origin[3 * B + 1]) - (double)sh1 * a.L);
+    float D2 = (float)((oA[2] - T.origin[3 * B + 2]) - (double)sh2 * a.L);
+    int64_t u0 = T.tile_ptr[B], u1 = T.tile_ptr[B + 1];
+    for (int64_t ub = u0; ub < u1; ub += 32) {
+      int64_t u = ub + lane;
+      bool pass = false;
+      if (u < u1) {
+        float4 lo = T.tile_lo[u], hi = T.tile_hi[u];
+        float gx = fmaxf(fmaxf((lo.x - D0) - thi.x, tlo.x - (hi.x - D0)), 0.0f);
+        float gy = fmaxf(fmaxf((lo.y - D1) - thi.y, tlo.y - (hi.y - D1)), 0.0f);
+        float gz = fmaxf(fmaxf((lo.z - D2) - thi.z, tlo.z - (hi.z - D2)), 0.0f);
+        pass = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) <= R2;
+      }
+      unsigned tm = __ballot_sync(0xffffffffu, pass);
+      while (tm) {
+        int j = __ffs(tm) - 1;
+        tm &= tm - 1;
+        int64_t uu = ub + j;
+        int n_u = T.tile_n[uu];
+        bool ok = false;
+        float4 sj;
+        if (lane < n_u) {
+          sj = a.P0[T.tile_start[uu] + lane];
+          sj.x -= D0; sj.y -= D1; sj.z -= D2;
+          ok = box_gap2(sj.x, sj.y, sj.z, tlo, thi) <= R2;
+        }
+        unsigned sm = __ballot_sync(0xffffffffu, ok);
+        if (cnt + 32 > kGravStage) flush();
+        if (ok) stage[cnt + __popc(sm & lanemask_lt())] = sj;
+        cnt += __popc(sm);
+      }
+    }
+  }
+  flush();
+  bool bad = !(isfinite(ax) && isfinite(ay) && isfinite(az));
+  unsigned bm = __ballot_sync(0xffffffffu, live && bad);
+  if (bm) {
+    if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e0 * 4 + 1));
+    return;
+  }
+  if (live && a.write_out) {
+    int64_t row = T.tperm[k_i];
+    double mi = -(double)ti.w;
+    a.out_flt[row * 3 + 0] += mi * (double)ax;
+    a.out_flt[row * 3 + 1] += mi * (double)ay;
+    a.out_flt[row * 3 + 2] += mi * (double)az;
+  }
+}
+
+int launch_gravity_fast(const EvalDev& d, const float4* table, float tab_scale, int tab_last,
+                        int64_t tcap, const int64_t* ntd, cudaStream_t st, HbError* err) {
+  k_gravity<<<grid_for(tcap, kGravWarps), kGravWarps * 32, 0, st>>>(d, table, tab_scale, tab_last,
+                                                                    ntd);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
+
+// cubic-per-interval table of S(r / r_s) over r in [0, r_cut] (float64 fit)
+int gravity_table(double r_s, double r_cut, int nt, float4* host_out, float* tab_scale) {
+  double dr = r_cut / nt;
+  const double node[4] = {0.5 * cos(M_PI * 0.5 / 4), 0.5 * cos(M_PI * 1.5 / 4),
+                          0.5 * cos(M_PI * 2.5 / 4), 0.5 * cos(M_PI * 3.5 / 4)};
+  for (int k = 0; k <= nt; ++k) {
+    double m[4][5];
+    for (int i = 0; i < 4; ++i) {
+      double x = (k + node[i]) * dr / r_s;
+      double sv = erfc(x) + 1.1283791670955126 * x * exp(-x * x);
+      double p = 1.0;
+      for (int j = 0; j < 4; ++j) { m[i][j] = p; p *= node[i]; }
+      m[i][4] = sv;
+    }
+    for (int c = 0; c < 4; ++c) {  // Gauss-Jordan on the 4x4 Vandermonde
+      int piv = c;
+      for (int r = c + 1; r < 4; ++r) if (fabs(m[r][c]) > fabs(m[piv][c])) piv = r;
+      for (int j = 0; j < 5; ++j) { double tmp = m[c][j]; m[c][j] = m[piv][j]; m[piv][j] = tmp; }
+      for (int r = 0; r < 4; ++r) {
+        if (r == c) continue;
+        double f = m[r][c] / m[c][c];
+        for (int j = c; j < 5; ++j) m[r][j] -= f * m[c][j];
+      }
+    }
+    host_out[k] = make_float4((float)(m[0][4] / m[0][0]), (float)(m[1][4] / m[1][1]),
+                              (float)(m[2][4] / m[2][2]), (float)(m[3][4] / m[3][3]));
+  }
+  host_out[nt + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  *tab_scale = (float)(nt / r_cut);
+  return nt + 1;
+}
+
 // ---------------------------------------------------------------- driver pieces
 int64_t tile_capacity(int64_t n, int64_t n_leaves) { return n / kTileMax + n_leaves + 1; }
 

@@ -21,6 +21,14 @@ enum { C_X = 0, C_Y, C_Z, C_VX, C_VY, C_VZ, C_M, C_H, C_RHO, C_P, C_CS, C_SP, NC
 
 constexpr float kSigma = 0.318309886183790671f;  // 1/pi (hb/kernels.py:63)
 
+// MUFU.RSQ without the denormal fix-up rsqrtf() wraps around it (inputs here
+// are >= 1e-30, normal in FP32)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 struct PairParams {
   float p0, p1;        // kernel params (rs, eps2) or (alpha, beta)
   float inv_rs;
@@ -223,5 +231,11 @@ int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, const dou
 int launch_pairs(int kid, bool det, bool lean, const EvalDev& d, int64_t tile_cap,
                  const int64_t* n_tiles_dev, cudaStream_t st, HbError* err);
 int kid_selects_gas(int kid);
+// resident fast gravity: table of S(r/r_s), 128 cubic intervals over [0, r_cut]
+constexpr int kGravTableN = 128;
+constexpr int kGravTableMax = kGravTableN + 2;
+int gravity_table(double r_s, double r_cut, int nt, float4* host_out, float* tab_scale);
+int launch_gravity_fast(const EvalDev& d, const float4* table, float tab_scale, int tab_last,
+                        int64_t tcap, const int64_t* ntd, cudaStream_t st, HbError* err);
 
 }  // namespace hb

@@ -87,6 +87,7 @@ struct StepWs {
   float4 *P0, *P1, *P2;
   unsigned long long* err_key;
   int64_t* inv;
+  float4* gtab;
 };
 
 static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t lcap, StepWs& w) {
@@ -105,6 +106,7 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
   w.P0 = ws.take<float4>(n + 1); w.P1 = ws.take<float4>(n + 1); w.P2 = ws.take<float4>(n + 1);
   w.err_key = ws.take<unsigned long long>(1);
   w.inv = ws.take<int64_t>(n + 1);
+  w.gtab = ws.take<float4>(kGravTableMax);
 }
 
 struct PhaseTimer {
@@ -287,7 +289,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                       a->side_length, w.P0, w.P1, w.P2, st, err);
     if (rc) return rc;
     setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
-    rc = launch_pairs(KID_GRAVITY, false, true, d, w.Ta.n_tiles_cap, w.nta, st, err);
+    static float4 host_tab[kGravTableMax];
+    float tab_scale = 0.f;
+    int tab_last = gravity_table(a->r_s, a->r_cut, kGravTableN, host_tab, &tab_scale);
+    HB_CUDA_TRY(cudaMemcpyAsync(w.gtab, host_tab, sizeof(host_tab), cudaMemcpyHostToDevice, st));
+    rc = launch_gravity_fast(d, w.gtab, tab_scale, tab_last, w.Ta.n_tiles_cap, w.nta, st, err);
     if (rc) return rc;
   }
   tm.mark(6);
