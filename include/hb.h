@@ -227,6 +227,7 @@ typedef struct HbStepArgs {
   /* physics (host scalars) */
   double reach;      /* list reach = max(r_cut, 2 h_max)                       */
   double h_max;      /* max smoothing length (kernel supports 2 h_max)        */
+  double h_min;      /* min gas smoothing length (sizes the float64 re-check band) */
   double r_s, r_cut, softening, eos_gamma, visc_alpha, visc_beta;
   int32_t passes;    /* HB_PASS_* mask                                        */
   int32_t timing;    /* 1: fill ms_phase with per-phase device times          */
@@ -242,7 +243,8 @@ typedef struct HbStepArgs {
   uint8_t* crk_fallback;/* (n)                                                */
   /* host outputs */
   int64_t n_leaves, n_entries, list_capacity_needed;
-  float ms_phase[8];    /* build, list, ncount, density+eos, crk, gravity, hydro, total */
+  float ms_phase[8];    /* build, list, tiling, sph A (count+density+eos),
+                           sph B (crk+hydro+solve), gravity, tail, total */
 } HbStepArgs;
 
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,

@@ -25,4 +25,25 @@ int build_mesh(const HbMeshArgs* a, Arena& ws, cudaStream_t st, HbError* err);
 int assemble_csr(const ListArgsDev& d, int64_t capacity, int32_t* ent_src, int32_t* ent_code,
                  int64_t* ent_ptr, int64_t* total_host, Arena& ws, cudaStream_t st, HbError* err);
 
+// fused SPH passes (hb_sph.cu): pass 0 = neighbour count + density,
+// pass 1 = CRK moments + hydro force; gas tiling, gas records P0..P2
+struct SphArgs {
+  const Tiling* T;
+  const int64_t* n_tiles_dev;
+  const int64_t* ent_ptr;
+  const int32_t* ent_src;
+  const int32_t* ent_code;
+  const float4 *P0, *P1, *P2;
+  const double* state;
+  const int8_t* pshift;
+  double L, reach;
+  float band;  // relative band of r^2 around a threshold decided in float64
+  double alpha, beta;
+  double *ncount, *rho, *moments, *hydro;
+  unsigned long long* err_key;
+};
+int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
+             double L, float4* P0, float4* P1, float4* P2, cudaStream_t st, HbError* err);
+int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err);
+
 }  // namespace hb

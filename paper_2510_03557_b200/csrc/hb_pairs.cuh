@@ -46,7 +46,9 @@ __device__ __forceinline__ float w_body(float q) {
 // (dW/dr)/r * h^5/sigma for the cubic spline (hb/kernels.py:83-93); finite at 0
 __device__ __forceinline__ float gradw_body(float q) {
   float t = 2.0f - q;
-  float outer = -0.75f * t * t * __frcp_rn(fmaxf(q, 1e-30f));
+  float rq;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"(fmaxf(q, 1e-30f)));
+  float outer = -0.75f * t * t * rq;
   float inner = fmaf(2.25f, q, -3.0f);
   return q < 1.0f ? inner : (q < 2.0f ? outer : 0.0f);
 }

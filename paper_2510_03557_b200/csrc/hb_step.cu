@@ -235,26 +235,28 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   };
   int rc = HB_OK;
   int64_t tcap = w.Tg.n_tiles_cap;
-  // 4. neighbour count (hb/hydro.py:223-227)
-  if (a->passes & HB_PASS_NCOUNT) {
+  tm.mark(3);
+  // geometry-derived band: FP32 r^2 error <= ~6 * 2^-24 * bin width * r; decide
+  // in float64 within 64x that of a threshold (exact counts, hb/kernels.py:191,357)
+  double wmax = fmax(a->width[0], fmax(a->width[1], a->width[2]));
+  double rmin = fmax(fmin(a->reach, 2.0 * a->h_min), 1e-300);
+  float band = (float)fmax(64.0 * 5.9604644775390625e-08 * wmax / rmin, 9.5367431640625e-07);
+  SphArgs sa;
+  sa.T = &w.Tg; sa.n_tiles_dev = w.ntg; sa.ent_ptr = w.ent_ptr; sa.ent_src = w.ent_src;
+  sa.ent_code = w.ent_code; sa.P0 = w.P0; sa.P1 = w.P1; sa.P2 = w.P2; sa.state = w.state;
+  sa.pshift = a->image_shift; sa.L = a->side_length; sa.reach = sph_reach; sa.band = band;
+  sa.alpha = a->visc_alpha; sa.beta = a->visc_beta; sa.err_key = w.err_key;
+  sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = a->crk_moments; sa.hydro = a->hydro;
+  // 4. pass A: neighbour count + density (hb/hydro.py:223-227, 60-84), EOS (48-57)
+  if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY)) {
     HB_CUDA_TRY(cudaMemsetAsync(a->ncount, 0, n * sizeof(double), st));
-    rc = pack_records(KID_NEIGHBOR_COUNT, w.Tg, w.ntg, w.state, a->image_shift, nullptr, 0,
-                      a->side_length, w.P0, w.P1, w.P2, st, err);
+    HB_CUDA_TRY(cudaMemsetAsync(w.rho_new, 0, n * sizeof(double), st));
+    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, st, err);
     if (rc) return rc;
-    setup(KID_NEIGHBOR_COUNT, sph_reach, 0.0, 0.0, 1, w.Tg, a->ncount);
-    rc = launch_pairs(KID_NEIGHBOR_COUNT, false, true, d, tcap, w.ntg, st, err);
+    rc = launch_sph(0, sa, st, err);
     if (rc) return rc;
   }
-  tm.mark(3);
-  // 5. density + alias sync + EOS (hb/hydro.py:60-84, 48-57)
   if (a->passes & HB_PASS_DENSITY) {
-    HB_CUDA_TRY(cudaMemsetAsync(w.rho_new, 0, n * sizeof(double), st));
-    rc = pack_records(KID_DENSITY, w.Tg, w.ntg, w.state, a->image_shift, nullptr, 0,
-                      a->side_length, w.P0, w.P1, w.P2, st, err);
-    if (rc) return rc;
-    setup(KID_DENSITY, sph_reach, 0.0, 0.0, 1, w.Tg, w.rho_new);
-    rc = launch_pairs(KID_DENSITY, false, true, d, tcap, w.ntg, st, err);
-    if (rc) return rc;
     k_density_update<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, w.leaf_start, w.leaf_end,
                                                              w.ghost_only, a->species, w.rho_new,
                                                              a->density);
@@ -268,14 +270,13 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     HB_LAUNCH_CHECK();
   }
   tm.mark(4);
-  // 6. CRK moments + solve (hb/hydro.py:99-150)
-  if (a->passes & HB_PASS_CRK) {
+  // 5. pass B: CRK moments (+ 3x3 solve, hb/hydro.py:99-150) + hydro force (hb/kernels.py:222-258)
+  if (a->passes & (HB_PASS_CRK | HB_PASS_HYDRO)) {
     HB_CUDA_TRY(cudaMemsetAsync(a->crk_moments, 0, n * 10 * sizeof(double), st));
-    rc = pack_records(KID_CRK_MOMENTS, w.Tg, w.ntg, w.state, a->image_shift, nullptr, 0,
-                      a->side_length, w.P0, w.P1, w.P2, st, err);
+    HB_CUDA_TRY(cudaMemsetAsync(a->hydro, 0, n * 5 * sizeof(double), st));
+    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, st, err);
     if (rc) return rc;
-    setup(KID_CRK_MOMENTS, sph_reach, 0.0, 0.0, 10, w.Tg, a->crk_moments);
-    rc = launch_pairs(KID_CRK_MOMENTS, false, true, d, tcap, w.ntg, st, err);
+    rc = launch_sph(1, sa, st, err);
     if (rc) return rc;
     rc = hb_crk_solve(n, a->crk_moments, 10, a->species, 1e8, a->crk_A, a->crk_B,
                       a->crk_fallback, st, err);
@@ -297,16 +298,6 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     if (rc) return rc;
   }
   tm.mark(6);
-  // 8. hydro force (hb/kernels.py:222-258)
-  if (a->passes & HB_PASS_HYDRO) {
-    HB_CUDA_TRY(cudaMemsetAsync(a->hydro, 0, n * 5 * sizeof(double), st));
-    rc = pack_records(KID_HYDRO_FORCE, w.Tg, w.ntg, w.state, a->image_shift, nullptr, 0,
-                      a->side_length, w.P0, w.P1, w.P2, st, err);
-    if (rc) return rc;
-    setup(KID_HYDRO_FORCE, sph_reach, a->visc_alpha, a->visc_beta, 5, w.Tg, a->hydro);
-    rc = launch_pairs(KID_HYDRO_FORCE, false, true, d, tcap, w.ntg, st, err);
-    if (rc) return rc;
-  }
   tm.mark(7);
   unsigned long long ek = 0;
   int ovf = 0, ovf2 = 0;

@@ -26,7 +26,7 @@ from .particles import FIELD_SPECS, ParticleSet
 
 PASS_NCOUNT, PASS_DENSITY, PASS_CRK, PASS_GRAVITY, PASS_HYDRO = 1, 2, 4, 8, 16
 PASS_ALL = 31
-PHASES = ("build", "list", "ncount", "density_eos", "crk", "gravity", "hydro", "total")
+PHASES = ("build", "list", "tiling", "sph_density", "sph_force", "gravity", "tail", "total")
 
 STEP_FIELDS = ("pos", "vel", "mass", "smoothing", "internal_energy", "density", "species",
                "ghost", "image_shift", "global_id", "ghost_src")
@@ -40,7 +40,8 @@ class HbStepArgs(C.Structure):
                 + [(f, P) for f in STEP_FIELDS]
                 + [("side_length", C.c_double), ("lo", C.c_double * 3), ("width", C.c_double * 3),
                    ("nb", C.c_int64 * 3), ("periodic", C.c_uint8 * 3), ("max_leaf_size", C.c_int64),
-                   ("reach", C.c_double), ("h_max", C.c_double), ("r_s", C.c_double),
+                   ("reach", C.c_double), ("h_max", C.c_double), ("h_min", C.c_double),
+                   ("r_s", C.c_double),
                    ("r_cut", C.c_double), ("softening", C.c_double), ("eos_gamma", C.c_double),
                    ("visc_alpha", C.c_double), ("visc_beta", C.c_double), ("passes", C.c_int32),
                    ("timing", C.c_int32), ("list_capacity", C.c_int64),
@@ -91,6 +92,7 @@ class ResidentRank:
         self.h_max = float(particles.smoothing.max()) if particles.n else 0.0
         if not np.any(gas):
             self.h_max = 0.0
+        self.h_min = float(particles.smoothing[gas].min()) if np.any(gas) else 0.0
         lo, hi, nb, width, periodic = mesh_geometry(cfg.box, cfg.bin_width, cfg.bounds_lo,
                                                     cfg.bounds_hi)
         self.lo, self.nb, self.width, self.periodic = lo, nb, width, periodic
@@ -150,6 +152,7 @@ class ResidentRank:
             a.periodic[d] = 1 if self.periodic[d] else 0
         a.max_leaf_size = int(cfg.max_leaf_size)
         a.h_max = self.h_max
+        a.h_min = self.h_min
         a.reach = max(cfg.r_cut if passes & PASS_GRAVITY else 0.0, 2.0 * self.h_max)
         a.r_s, a.r_cut, a.softening = cfg.r_s, cfg.r_cut, cfg.softening
         a.eos_gamma, a.visc_alpha, a.visc_beta = cfg.eos_gamma, cfg.visc_alpha, cfg.visc_beta

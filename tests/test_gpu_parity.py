@@ -231,3 +231,63 @@ def test_gpu_resident_force_step(golden, oracle):
                                 pshift=g["built_image_shift"])
     ref_h = np.column_stack([g["hydro_force"], g["hydro_edot"]])
     assert_fp32_close(out["hydro"][own, :4], ref_h[own], absh[own, :4], what="resident hydro")
+
+
+@pytest.mark.parametrize("sigma", [0.05, 1.0])
+def test_gpu_force_step_vs_oracle_c1(oracle, sigma):
+    """hb_force_step at 2x32^3 (config C1, near-uniform and shell-crossing
+    Zel'dovich ICs) against the oracle's ordered evaluation of the same step:
+    leaf order and neighbour counts bit-exact, the rest within FP32 tolerance."""
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
+    from paper_2510_03557_b200.ic import make_zeldovich_ic
+    from paper_2510_03557_b200.kernels import (crk_moments_kernel, density_kernel,
+                                               hydro_force_kernel, neighbor_count_kernel)
+    from paper_2510_03557_b200.resident import StepConfig, force_step
+    npd = 32
+    box = BoxGeometry(1.0)
+    p0 = make_zeldovich_ic(npd, box, sigma)
+    pm = 1.0 / (2 * npd)
+    r_s, r_cut = 2 * pm, 10 * pm
+    eps = (1.0 / p0.n ** (1 / 3)) / 50
+    h_max = float(p0.smoothing.max())
+    reach = max(r_cut, 2 * h_max)
+    bw = max(4 * pm, reach * (1 + 1e-9))
+    cfg = StepConfig(box=box, bin_width=bw, max_leaf_size=256, r_s=r_s, r_cut=r_cut, softening=eps)
+    p = p0.copy()
+    out = force_step(p, cfg)
+    m = oracle.build_mesh(p0.pos, p0.image_shift, p0.ghost, 1.0, bw, 256)
+    perm = m["perm"]
+    np.testing.assert_array_equal(p.global_id, p0.global_id[perm])
+    la, lb, ls = oracle.assemble(m, 1.0, reach)
+    assert out["n_entries"] == la.shape[0]
+    q = p0.select(perm)
+    st = q.state_matrix(5 / 3)
+    L = 1.0
+    args = (la, lb, ls, st, m["leaf_start"], m["leaf_end"], L)
+    nc, _, _, _ = oracle.eval_pairs(neighbor_count_kernel(2 * h_max), *args, mode="deterministic",
+                                    workers=8)
+    np.testing.assert_array_equal(out["ncount"], nc[:, 0])
+    dk = density_kernel(2 * h_max)
+    rho, _, _, _ = oracle.eval_pairs(dk, *args, mode="relaxed", workers=8)
+    gas = q.species == 1
+    rel = np.abs(p.density - rho[:, 0])[gas] / rho[gas, 0]
+    assert np.median(rel) <= 1e-6 and np.quantile(rel, 0.999) <= 1e-5, rel.max()
+    q.density[gas] = rho[gas, 0]
+    oracle.refresh_eos(st, q.density, q.internal_energy, 5 / 3)
+    ck = crk_moments_kernel(2 * h_max)
+    mom, _, _, _ = oracle.eval_pairs(ck, *args, mode="relaxed", workers=8)
+    mabs = oracle.eval_abs_sums(ck, *args)
+    assert_fp32_close(out["crk_moments"], mom, mabs, what="crk moments")
+    A, B, fb, *_ = oracle.crk_solve(mom, gas)
+    np.testing.assert_array_equal(out["crk_fallback"], fb)
+    relA = np.abs(out["crk_A"] - A)[gas] / np.abs(A[gas])
+    assert np.median(relA) <= 1e-5 and np.quantile(relA, 0.999) <= 1e-4, relA.max()
+    gk = short_range_gravity_kernel(ForceSplit(r_s=r_s, r_cut=r_cut), eps)
+    g, _, _, _ = oracle.eval_pairs(gk, *args, mode="relaxed", workers=8)
+    gabs = oracle.eval_abs_sums(gk, *args)
+    assert_fp32_close(out["grav"], g, gabs, what="gravity")
+    hk = hydro_force_kernel(2 * h_max)
+    hy, _, _, _ = oracle.eval_pairs(hk, *args, mode="relaxed", workers=8)
+    habs = oracle.eval_abs_sums(hk, *args)
+    assert_fp32_close(out["hydro"], hy, habs, what="hydro")
