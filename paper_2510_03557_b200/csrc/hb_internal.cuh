@@ -43,7 +43,8 @@ struct SphArgs {
   unsigned long long* err_key;
 };
 int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
-             double L, float4* P0, float4* P1, float4* P2, cudaStream_t st, HbError* err);
+             double L, float4* P0, float4* P1, float4* P2, int layout, cudaStream_t st,
+             HbError* err);
 int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err);
 
 }  // namespace hb

@@ -471,6 +471,9 @@ __device__ __forceinline__ bool gap_ok(const double* lo_a, const double* hi_a, c
 
 
 
+// one warp per receiving leaf, lane o < 27 owns stencil cell o; duplicate
+// (bin, shift) cells (tiny periodic meshes) keep the lowest offset, as the
+// reference's sequential sweep does (hb/cmtree.py:218-245)
 template <bool EMIT>
 __global__ void k_list_sweep(ListArgsDev a, int64_t* cnt, const int64_t* off, int64_t* tmp_b,
                              int32_t* tmp_code) {
@@ -484,42 +487,46 @@ __global__ void k_list_sweep(ListArgsDev a, int64_t* cnt, const int64_t* off, in
   }
   int64_t bf = a.leaf_bin[leaf];
   int64_t bz = bf % a.g.nb[2], by = (bf / a.g.nb[2]) % a.g.nb[1], bx = bf / (a.g.nb[1] * a.g.nb[2]);
+  int64_t flat = 0;
+  int code = 0, s[3] = {0, 0, 0};
+  bool valid = lane < 27 && stencil_cell(a.g, bx, by, bz, lane, flat, code, s);
+  long long key = valid ? (long long)(flat * 27 + code) : -1 - lane;
+  unsigned peers = __match_any_sync(0xffffffffu, key);
+  valid = valid && (__ffs(peers) - 1 == lane);
   double lo_a[3], hi_a[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) { lo_a[d] = a.leaf_lo[3 * leaf + d]; hi_a[d] = a.leaf_hi[3 * leaf + d]; }
-  int64_t count = 0;
-  int64_t base = EMIT ? off[leaf] : 0;
-  for (int o = 0; o < 27; ++o) {
-    int64_t flat; int code; int s[3];
-    if (!stencil_cell(a.g, bx, by, bz, o, flat, code, s)) continue;
-    bool dup = false;  // earlier offset with the same (bin, shift)?
-    for (int o2 = 0; o2 < o && !dup; ++o2) {
-      int64_t f2; int c2; int s2[3];
-      if (stencil_cell(a.g, bx, by, bz, o2, f2, c2, s2) && f2 == flat && c2 == code) dup = true;
-    }
-    if (dup) continue;
-    int64_t p0 = a.bin_ptr[flat], p1 = a.bin_ptr[flat + 1];
-    for (int64_t pb = p0; pb < p1; pb += 32) {
-      int64_t p = pb + lane;
-      bool hit = false;
-      int64_t b = 0;
-      if (p < p1) {
-        b = a.bin_ids ? a.bin_ids[p] : p;
-        double lo_b[3], hi_b[3];
+  int64_t p0 = valid ? a.bin_ptr[flat] : 0, p1 = valid ? a.bin_ptr[flat + 1] : 0;
+  int mine = 0;
+  for (int64_t p = p0; p < p1; ++p) {
+    int64_t b = a.bin_ids ? a.bin_ids[p] : p;
+    double lo_b[3], hi_b[3];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) { lo_b[d] = a.leaf_lo[3 * b + d]; hi_b[d] = a.leaf_hi[3 * b + d]; }
-        hit = gap_ok(lo_a, hi_a, lo_b, hi_b, s, a.g.L, a.g.reach);
-      }
-      unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (EMIT && hit) {
-        int64_t slot = base + count + __popc(m & lanemask_lt());
-        tmp_b[slot] = b;
-        tmp_code[slot] = code;
-      }
-      count += __popc(m);
+    for (int d = 0; d < 3; ++d) { lo_b[d] = a.leaf_lo[3 * b + d]; hi_b[d] = a.leaf_hi[3 * b + d]; }
+    mine += gap_ok(lo_a, hi_a, lo_b, hi_b, s, a.g.L, a.g.reach);
+  }
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (!EMIT) {
+    if (lane == 31) cnt[leaf] = incl;
+    return;
+  }
+  int64_t slot = off[leaf] + incl - mine;
+  for (int64_t p = p0; p < p1; ++p) {
+    int64_t b = a.bin_ids ? a.bin_ids[p] : p;
+    double lo_b[3], hi_b[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) { lo_b[d] = a.leaf_lo[3 * b + d]; hi_b[d] = a.leaf_hi[3 * b + d]; }
+    if (gap_ok(lo_a, hi_a, lo_b, hi_b, s, a.g.L, a.g.reach)) {
+      tmp_b[slot] = b;
+      tmp_code[slot] = code;
+      ++slot;
     }
   }
-  if (!EMIT && lane == 0) cnt[leaf] = count;
 }
 
 // order each receiver's entries by (b, code); keys are unique per receiver

@@ -23,6 +23,7 @@ namespace hb {
 
 constexpr int kTileBuildBlock = 256;
 constexpr int kTileBuildCap = 2048;  // selected members per leaf held in shared memory
+constexpr int kTileWarpCapBlock = 256;  // leaves up to this many go to the warp kernel
 constexpr int kEvalWarps = 4;
 constexpr int kStage = 64;           // staged sources per warp
 
@@ -68,6 +69,7 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
     if (threadIdx.x < 3) T.origin[3 * leaf + threadIdx.x] = 0.0;
     return;
   }
+  if (m_sel <= kTileWarpCapBlock) return;  // k_tile_build_warp's leaves
   if (m_sel > kTileBuildCap) {
     if (threadIdx.x == 0) atomicExch(T.overflow, 1);
     return;
@@ -219,6 +221,136 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
   // 4. internal order -> state rows
   int64_t so = T.sel_off[leaf];
   for (int k = threadIdx.x; k < m_sel; k += blockDim.x) T.tperm[so + k] = s_row[k];
+}
+
+// Same tiling as k_tile_build, one WARP per leaf (leaves with <= 256 selected
+// members -- the common case -- without block barriers); larger leaves are
+// left to k_tile_build (flagged by big != 0).
+constexpr int kTileWarpCap = 256;
+constexpr int kTileWarps = 8;
+__global__ void __launch_bounds__(kTileWarps * 32)
+k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
+                  const double* state, const int8_t* pshift, double L, int sel, int nl) {
+  __shared__ int32_t s_row[kTileWarps][kTileWarpCap];
+  __shared__ int32_t s_tmp[kTileWarps][kTileWarpCap];
+  __shared__ float s_c[kTileWarps][3][kTileWarpCap];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t leaf = (int64_t)blockIdx.x * kTileWarps + wid;
+  if (leaf >= nl) return;
+  int m_sel = (int)T.sel_cnt[leaf];
+  if (m_sel > kTileWarpCap) return;  // handled by the block kernel
+  if (m_sel == 0) {
+    if (lane < 3) T.origin[3 * leaf + lane] = 0.0;
+    return;
+  }
+  int32_t* row = s_row[wid];
+  int32_t* tmp = s_tmp[wid];
+  float (*cc)[kTileWarpCap] = s_c[wid];
+  int64_t s = leaf_start[leaf], e = leaf_end[leaf];
+  int base = 0;
+  for (int64_t r0 = s; r0 < e; r0 += 32) {
+    int64_t r = r0 + lane;
+    bool f = r < e && (sel == 0 || state[r * NCOL + C_SP] == 1.0);
+    unsigned b = __ballot_sync(0xffffffffu, f);
+    if (f) row[base + __popc(b & lanemask_lt())] = (int32_t)r;
+    base += __popc(b);
+  }
+  __syncwarp();
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  double v[8][3];
+  int nloc = 0;
+  for (int k = lane; k < m_sel; k += 32, ++nloc) {
+    int64_t r = row[k];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      v[nloc][d] = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+      mn[d] = fmin(mn[d], v[nloc][d]); mx[d] = fmax(mx[d], v[nloc][d]);
+    }
+  }
+  double org[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mn[d] = fmin(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
+      mx[d] = fmax(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
+    }
+    org[d] = 0.5 * (mn[d] + mx[d]);
+  }
+  if (lane < 3) T.origin[3 * leaf + lane] = org[lane];
+  nloc = 0;
+  for (int k = lane; k < m_sel; k += 32, ++nloc)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) cc[d][k] = (float)(v[nloc][d] - org[d]);
+  __syncwarp();
+  // proportional median splits into ceil(m/32) tiles (DFS left-first)
+  int stk_a[16], stk_m[16], stk_k[16];  // warp-uniform stack in registers
+  int sp = 1, tile_j = 0;
+  stk_a[0] = 0; stk_m[0] = m_sel; stk_k[0] = (m_sel + kTileMax - 1) / kTileMax;
+  int64_t tbase = T.tile_ptr[leaf], so = T.sel_off[leaf];
+  while (sp) {
+    --sp;
+    int a0 = stk_a[sp], m = stk_m[sp], kk = stk_k[sp];
+    if (kk == 1) {
+      if (lane == 0) {
+        int64_t t = tbase + tile_j;
+        T.tile_start[t] = (int32_t)(so + a0);
+        T.tile_n[t] = m;
+        T.tile_leaf[t] = (int32_t)leaf;
+      }
+      ++tile_j;
+      continue;
+    }
+    float lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int k = lane; k < m; k += 32)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        float x = cc[d][a0 + k];
+        lo3[d] = fminf(lo3[d], x); hi3[d] = fmaxf(hi3[d], x);
+      }
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        lo3[d] = fminf(lo3[d], __shfl_xor_sync(0xffffffffu, lo3[d], o));
+        hi3[d] = fmaxf(hi3[d], __shfl_xor_sync(0xffffffffu, hi3[d], o));
+      }
+    float ex0 = hi3[0] - lo3[0], ex1 = hi3[1] - lo3[1], ex2 = hi3[2] - lo3[2];
+    int axis = ex1 > ex0 ? 1 : 0;
+    if (ex2 > (axis ? ex1 : ex0)) axis = 2;
+    for (int k = lane; k < m; k += 32) {
+      float x = cc[axis][a0 + k];
+      int rank = 0;
+      for (int q = 0; q < m; ++q) {
+        float y = cc[axis][a0 + q];
+        rank += (y < x) || (y == x && q < k);
+      }
+      tmp[a0 + rank] = a0 + k;
+    }
+    __syncwarp();
+    int32_t rr[8];
+    float c3[8][3];
+    nloc = 0;
+    for (int k = lane; k < m; k += 32, ++nloc) {
+      int src = tmp[a0 + k];
+      rr[nloc] = row[src];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) c3[nloc][d] = cc[d][src];
+    }
+    __syncwarp();
+    nloc = 0;
+    for (int k = lane; k < m; k += 32, ++nloc) {
+      row[a0 + k] = rr[nloc];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) cc[d][a0 + k] = c3[nloc][d];
+    }
+    __syncwarp();
+    int k1 = (kk + 1) / 2, k2 = kk - k1;
+    int left = (int)(((int64_t)m * k1 + kk - 1) / kk);
+    stk_a[sp] = a0 + left; stk_m[sp] = m - left; stk_k[sp] = k2; ++sp;   // right (popped last)
+    stk_a[sp] = a0; stk_m[sp] = left; stk_k[sp] = k1; ++sp;              // left first
+  }
+  for (int k = lane; k < m_sel; k += 32) T.tperm[so + k] = row[k];
 }
 
 // tile boxes (FP32, leaf frame) and hmax, one warp per tile
@@ -779,6 +911,9 @@ int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t
     HB_CUDA_TRY(cudaMemcpyAsync(T.tile_ptr + nl, n_tiles_dev, sizeof(int64_t),
                                 cudaMemcpyDeviceToDevice, st));
   }
+  k_tile_build_warp<<<grid_for(nl, kTileWarps), kTileWarps * 32, 0, st>>>(
+      T, leaf_start, leaf_end, state, pshift, L, sel, (int)nl);
+  HB_LAUNCH_CHECK();
   k_tile_build<<<(unsigned)nl, kTileBuildBlock, 0, st>>>(T, leaf_start, leaf_end, state, pshift,
                                                          L, sel);
   HB_LAUNCH_CHECK();

@@ -20,7 +20,8 @@
 namespace hb {
 
 constexpr int kSphWarps = 4;
-constexpr int kSphStage = 64;  // two 32-bit mask words per lane
+constexpr int kStageA = 256;  // pass A staged sources per warp (8 mask words per lane)
+constexpr int kStageB = 192;  // pass B (3 records per source)
 
 struct SphDev {
   Tiling T;
@@ -59,7 +60,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // staging shared by both passes: walks the receiver's entries, culls source
 // tiles and sources against the target box, calls consume() when the stage
 // would overflow and at the end.
-template <int NP, bool HYDRO, class Consume>
+template <int NP, bool HYDRO, int CAP, class Consume>
 __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, int64_t e1,
                                           float4 tlo, float4 thi, float hmax_t, float Rcap,
                                           float4 (*stage)[NP], int2* meta, int& cnt,
@@ -102,14 +103,14 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
           if (NP > 1) sj[1] = a.P1[k_j];
           if (NP > 2) sj[2] = a.P2[k_j];
           sj[0].x -= D0; sj[0].y -= D1; sj[0].z -= D2;
-          float R = HYDRO ? fminf(Rcap, 2.0f * fmaxf(hmax_t, sj[1].w) * 1.0001f) : Rt;
+          float R = HYDRO ? fminf(Rcap, 2.0f * fmaxf(hmax_t, sj[0].w) * 1.0001f) : Rt;
           float gx = fmaxf(fmaxf(tlo.x - sj[0].x, sj[0].x - thi.x), 0.0f);
           float gy = fmaxf(fmaxf(tlo.y - sj[0].y, sj[0].y - thi.y), 0.0f);
           float gz = fmaxf(fmaxf(tlo.z - sj[0].z, sj[0].z - thi.z), 0.0f);
           ok = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) <= R * R;
         }
         unsigned sm = __ballot_sync(0xffffffffu, ok);
-        if (cnt + 32 > kSphStage) consume();
+        if (cnt + 32 > CAP) consume();
         if (ok) {
           int slot = cnt + __popc(sm & lanemask_lt());
 #pragma unroll
@@ -123,38 +124,60 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
   consume();
 }
 
-// per-lane in-support mask over the stage (r^2 against the lane's threshold)
+// per-lane in-support bitmask over the stage, stored word-major in shared
+// memory (mask[w][lane], conflict-free); threshold on r^2 per lane (and per
+// source h_j for hydro's 2 max(h_i, h_j) support)
 template <int NP, bool HYDRO>
-__device__ __forceinline__ void stage_masks(const float4 (*stage)[NP], int cnt, float4 ti0,
+__device__ __forceinline__ void build_masks(const float4 (*stage)[NP], int cnt, float4 ti0,
                                             float hi, float thr_i, float reach2c,
-                                            unsigned& m0, unsigned& m1) {
-  m0 = 0u; m1 = 0u;
-  for (int q = 0; q < cnt; ++q) {
-    float4 s = stage[q][0];
-    float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
-    float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    float thr = thr_i;
-    if (HYDRO) {
-      float hm = fmaxf(hi, stage[q][1].w);
-      thr = fminf(reach2c, 4.0f * hm * hm * 1.0002f);
+                                            unsigned (*mask)[32]) {
+  int lane = threadIdx.x & 31;
+  int nw = (cnt + 31) >> 5;
+  for (int w = 0; w < nw; ++w) {
+    unsigned bits = 0u;
+    int qmax = min(32, cnt - w * 32);
+    for (int b = 0; b < qmax; ++b) {
+      float4 s = stage[w * 32 + b][0];
+      float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
+      float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      float thr = thr_i;
+      if (HYDRO) {
+        float hm = fmaxf(hi, s.w);
+        thr = fminf(reach2c, 4.0f * hm * hm * 1.0002f);
+      }
+      bits |= (r2 <= thr ? 1u : 0u) << b;
     }
-    unsigned bit = r2 <= thr ? 1u : 0u;
-    if (q < 32) m0 |= bit << q;
-    else m1 |= bit << (q - 32);
+    mask[w][lane] = bits;
   }
+  __syncwarp();
 }
 
-__device__ __forceinline__ bool pop_bit(unsigned& m0, unsigned& m1, int& q) {
-  if (m0) { q = __ffs(m0) - 1; m0 &= m0 - 1; return true; }
-  if (m1) { q = 32 + __ffs(m1) - 1; m1 &= m1 - 1; return true; }
-  return false;
+// walk this lane's set bits across all words; body(q) per in-support source.
+// The warp loops max-over-lanes(total bits) times: balanced over the stage.
+template <class Body>
+__device__ __forceinline__ void walk_masks(const unsigned (*mask)[32], int cnt, Body body) {
+  int lane = threadIdx.x & 31;
+  int nw = (cnt + 31) >> 5;
+  int wi = 0;
+  unsigned m = nw > 0 ? mask[0][lane] : 0u;
+  while (true) {
+    while (m == 0u && ++wi < nw) m = mask[wi][lane];
+    bool has = m != 0u;
+    if (!__any_sync(0xffffffffu, has)) break;
+    if (has) {
+      int q = wi * 32 + __ffs(m) - 1;
+      m &= m - 1;
+      body(q);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- pass A
 __global__ void __launch_bounds__(kSphWarps * 32)
 k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
-  __shared__ float4 s_stage[kSphWarps][kSphStage][1];
-  __shared__ int2 s_meta[kSphWarps][kSphStage];
+  __shared__ float4 s_stage[kSphWarps][kStageA][1];
+  __shared__ int2 s_meta[kSphWarps][kStageA];
+  __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
   if (t >= *n_tiles_dev) return;
@@ -180,13 +203,11 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   int cnt = 0;
   float4(*stage)[1] = s_stage[wid];
   int2* meta = s_meta[wid];
+  unsigned(*mask)[32] = s_mask[wid];
   auto consume = [&]() {
     __syncwarp();
-    unsigned m0, m1;
-    stage_masks<1, false>(stage, cnt, ti0, h, live ? thr_mask : -1.0f, 0.0f, m0, m1);
-    int q;
-    while (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
-      if (!pop_bit(m0, m1, q)) continue;
+    build_masks<1, false>(stage, cnt, ti0, h, live ? thr_mask : -1.0f, 0.0f, mask);
+    walk_masks(mask, cnt, [&](int q) {
       float4 s = stage[q][0];
       float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
@@ -204,11 +225,12 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
         float qq = sqrtf(r2) * hinv;
         rho = fmaf(s.w, w_body(qq), rho);
       }
-    }
+    });
     __syncwarp();
     cnt = 0;
   };
-  sph_sweep<1, false>(a, A, e0, e1, tlo, thi, h, a.reach * 1.0001f, stage, meta, cnt, consume);
+  sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, h, a.reach * 1.0001f, stage, meta, cnt,
+                               consume);
   if (live) {
     float norm3 = h > 0.0f ? kSigma * hinv * hinv * hinv : 0.0f;
     a.ncount[row_i] += (double)count;
@@ -219,8 +241,9 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
 // ---------------------------------------------------------------- pass B
 __global__ void __launch_bounds__(kSphWarps * 32)
 k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
-  __shared__ float4 s_stage[kSphWarps][kSphStage][3];
-  __shared__ int2 s_meta[kSphWarps][kSphStage];
+  __shared__ float4 s_stage[kSphWarps][kStageB][3];
+  __shared__ int2 s_meta[kSphWarps][kStageB];
+  __shared__ unsigned s_mask[kSphWarps][kStageB / 32][32];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
   if (t >= *n_tiles_dev) return;
@@ -231,12 +254,12 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   int n_t = T.tile_n[t];
   bool live = lane < n_t;
   int k_i = T.tile_start[t] + (live ? lane : 0);
+  // records: P0 = (x, y, z, h), P1 = (vx, vy, vz, m), P2 = (P/rho^2, c_s, rho, sigma/h^5)
   float4 ti0 = a.P0[k_i], ti1 = a.P1[k_i], ti2 = a.P2[k_i];
-  float hi = ti1.w;
+  float hi = ti0.w;
   float hinv = hi > 0.0f ? 1.0f / hi : 0.0f;
   float reach2c = a.reach2 * (1.0f + 2.0f * a.band);
   float4 tlo = a.T.tile_lo[t], thi = a.T.tile_hi[t];
-  // accumulators: CRK moments (scaled by sigma/h_i^3 at the end), hydro (scaled by m_i)
   float mo[10];
 #pragma unroll
   for (int c = 0; c < 10; ++c) mo[c] = 0.0f;
@@ -244,22 +267,21 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   int cnt = 0;
   float4(*stage)[3] = s_stage[wid];
   int2* meta = s_meta[wid];
+  unsigned(*mask)[32] = s_mask[wid];
   auto consume = [&]() {
     __syncwarp();
-    unsigned m0, m1;
-    stage_masks<3, true>(stage, cnt, ti0, live ? hi : -1.0f, 0.0f, live ? reach2c : -1.0f, m0, m1);
-    int q;
-    while (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
-      if (!pop_bit(m0, m1, q)) continue;
+    build_masks<3, true>(stage, cnt, ti0, live ? hi : -1.0f, 0.0f, live ? reach2c : -1.0f, mask);
+    walk_masks(mask, cnt, [&](int q) {
       float4 s0 = stage[q][0], s1 = stage[q][1], s2 = stage[q][2];
       float dx = ti0.x - s0.x, dy = ti0.y - s0.y, dz = ti0.z - s0.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      if (!(r2 <= a.reach2)) continue;
+      if (!(r2 <= a.reach2)) return;
       float rinv = rsqrt_ftz(fmaxf(r2, 1e-30f));
       float r = r2 * rinv;
       // CRK moments: w = V_j W(r, h_i) (hb/kernels.py:205-220)
       float qi = r * hinv;
-      float vj = s2.z > 0.0f ? s0.w * rcp_approx(s2.z) : 0.0f;
+      float mj = s1.w;
+      float vj = s2.z > 0.0f ? mj * rcp_approx(s2.z) : 0.0f;
       float wk = vj * w_body(qi);
       float wx = wk * dx, wy = wk * dy, wz = wk * dz;
       mo[0] += wk;
@@ -267,7 +289,7 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
       mo[4] = fmaf(wx, dx, mo[4]); mo[5] = fmaf(wx, dy, mo[5]); mo[6] = fmaf(wx, dz, mo[6]);
       mo[7] = fmaf(wy, dy, mo[7]); mo[8] = fmaf(wy, dz, mo[8]); mo[9] = fmaf(wz, dz, mo[9]);
       // hydro (hb/kernels.py:227-258), m_i factored out
-      float hj = s1.w;
+      float hj = s0.w;
       float qj = r * rcp_approx(hj);
       float gw = 0.5f * (gradw_body(qi) * ti2.w + gradw_body(qj) * s2.w);
       float vx = ti1.x - s1.x, vy = ti1.y - s1.y, vz = ti1.z - s1.z;
@@ -280,16 +302,17 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
         float mu = hbar * vdotr * rcp_approx(fmaf(0.01f * hbar, hbar, r2));
         visc = fmaf(a.beta * mu, mu, -(a.alpha * cbar * mu)) * rcp_approx(rhobar);
       }
-      float w = s0.w * (ti2.x + s2.x + visc) * gw;
+      float w = mj * (ti2.x + s2.x + visc) * gw;
       fx = fmaf(-w, dx, fx); fy = fmaf(-w, dy, fy); fz = fmaf(-w, dz, fz);
-      float work = s0.w * vdotr * gw;
+      float work = mj * vdotr * gw;
       ei = fmaf(fmaf(0.5f, visc, ti2.x), work, ei);
       ej = fmaf(fmaf(0.5f, visc, s2.x), work, ej);
-    }
+    });
     __syncwarp();
     cnt = 0;
   };
-  sph_sweep<3, true>(a, A, e0, e1, tlo, thi, hi, a.reach * 1.0001f, stage, meta, cnt, consume);
+  sph_sweep<3, true, kStageB>(a, A, e0, e1, tlo, thi, hi, a.reach * 1.0001f, stage, meta, cnt,
+                              consume);
   bool bad = !(isfinite(fx) && isfinite(fy) && isfinite(fz) && isfinite(ei) && isfinite(mo[0]));
   if (__ballot_sync(0xffffffffu, live && bad)) {
     if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e0 * 4 + 1));
@@ -299,7 +322,7 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
     int64_t row = T.tperm[k_i];
     double norm3 = hi > 0.0f ? (double)kSigma * (double)hinv * (double)hinv * (double)hinv : 0.0;
     for (int c = 0; c < 10; ++c) a.moments[row * 10 + c] += norm3 * (double)mo[c];
-    double mi = (double)ti0.w;
+    double mi = (double)ti1.w;
     a.hydro[row * 5 + 0] += mi * (double)fx;
     a.hydro[row * 5 + 1] += mi * (double)fy;
     a.hydro[row * 5 + 2] += mi * (double)fz;
@@ -309,9 +332,11 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
 }
 
 // gas records for both passes
+// layout 0 (pass A): P0 = (x, y, z, m), P1 = (.., .., .., h)
+// layout 1 (pass B): P0 = (x, y, z, h), P1 = (vx, vy, vz, m), P2 = (P/rho^2, c_s, rho, sigma/h^5)
 __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tiling T,
                            const double* state, const int8_t* pshift, double L, float4* P0,
-                           float4* P1, float4* P2) {
+                           float4* P1, float4* P2, int layout) {
   int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (t >= *n_tiles_dev || lane >= T.tile_n[t]) return;
@@ -328,15 +353,21 @@ __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tilin
   double h = st[C_H], rho = st[C_RHO];
   double norm5 = h > 0 ? 0.31830988618379067 / (h * h * h * h * h) : 0.0;
   double fpart = rho > 0 ? st[C_P] / (rho * rho) : 0.0;
-  P0[k] = make_float4(c[0], c[1], c[2], (float)st[C_M]);
-  P1[k] = make_float4((float)st[C_VX], (float)st[C_VY], (float)st[C_VZ], (float)h);
-  P2[k] = make_float4((float)fpart, (float)st[C_CS], (float)rho, (float)norm5);
+  if (layout == 0) {
+    P0[k] = make_float4(c[0], c[1], c[2], (float)st[C_M]);
+    P1[k] = make_float4(0.f, 0.f, 0.f, (float)h);
+  } else {
+    P0[k] = make_float4(c[0], c[1], c[2], (float)h);
+    P1[k] = make_float4((float)st[C_VX], (float)st[C_VY], (float)st[C_VZ], (float)st[C_M]);
+    P2[k] = make_float4((float)fpart, (float)st[C_CS], (float)rho, (float)norm5);
+  }
 }
 
 int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
-             double L, float4* P0, float4* P1, float4* P2, cudaStream_t st, HbError* err) {
+             double L, float4* P0, float4* P1, float4* P2, int layout, cudaStream_t st,
+             HbError* err) {
   k_pack_sph<<<grid_for(T.n_tiles_cap * 32, 256), 256, 0, st>>>(T.n_tiles_cap, ntd, T, state,
-                                                                pshift, L, P0, P1, P2);
+                                                                pshift, L, P0, P1, P2, layout);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }

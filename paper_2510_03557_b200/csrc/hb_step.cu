@@ -251,7 +251,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY)) {
     HB_CUDA_TRY(cudaMemsetAsync(a->ncount, 0, n * sizeof(double), st));
     HB_CUDA_TRY(cudaMemsetAsync(w.rho_new, 0, n * sizeof(double), st));
-    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, st, err);
+    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, 0, st,
+                  err);
     if (rc) return rc;
     rc = launch_sph(0, sa, st, err);
     if (rc) return rc;
@@ -274,7 +275,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->passes & (HB_PASS_CRK | HB_PASS_HYDRO)) {
     HB_CUDA_TRY(cudaMemsetAsync(a->crk_moments, 0, n * 10 * sizeof(double), st));
     HB_CUDA_TRY(cudaMemsetAsync(a->hydro, 0, n * 5 * sizeof(double), st));
-    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, st, err);
+    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, 1, st,
+                  err);
     if (rc) return rc;
     rc = launch_sph(1, sa, st, err);
     if (rc) return rc;
