@@ -231,6 +231,10 @@ typedef struct HbStepArgs {
   double r_s, r_cut, softening, eos_gamma, visc_alpha, visc_beta;
   int32_t passes;    /* HB_PASS_* mask                                        */
   int32_t timing;    /* 1: fill ms_phase with per-phase device times          */
+  int32_t ghost_density; /* 1: ghost-only leaves are density receivers too, so
+                            ghost rows near the rank face get fresh rho, P, c_s
+                            (multi-rank; fixes SURVEY.md finding 4); gravity,
+                            CRK and hydro still skip ghost-only receivers     */
   int64_t list_capacity; /* entries the workspace was sized for              */
   /* outputs (device, leaf order) */
   int64_t* perm;        /* (n) row k = input row perm[k]                    */
@@ -250,6 +254,36 @@ typedef struct HbStepArgs {
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,
                                int64_t list_capacity);
 int hb_force_step(HbStepArgs* args, void* ws, size_t ws_bytes, void* stream, HbError* err);
+
+/* ---------------------------------------------------------------------------
+ * Overload-shell exchange (multi-GPU ranks).  Distributed build_overload /
+ * refresh_overload (hb/domain.py:88-189): cuboid ranks of grid g (x-major ids),
+ * ghost copy of an owned particle for every (rank r, image s) with pos + s L
+ * strictly inside r's bounds widened by w (except its owned copy), owned copy
+ * to its (new) owner; DriftError flag for > 1 domain hop.  Records are
+ * hb_halo_record_bytes() wide; slots = dest * 28 + code (27 = owned).
+ * hb_halo_select: mode 0 counts per slot, mode 1 emits rows/slots at `fill`
+ * offsets.  hb_halo_unpack orders owned rows by global_id then ghosts by
+ * (global_id, shift) (hb/domain.py:135-138) into SoA rank fields.
+ * ------------------------------------------------------------------------- */
+int64_t hb_halo_record_bytes(void);
+int hb_halo_select(int64_t n, const double* pos, const uint8_t* ghost, const int32_t g[3],
+                   double side_length, double overload_width, int32_t self, int32_t mode,
+                   uint64_t* counts, uint64_t* fill, int64_t* out_row, int32_t* out_slot,
+                   int32_t* drift_flag, void* stream, HbError* err);
+int hb_halo_pack(int64_t m, const int64_t* rows, const int32_t* slots, const double* pos,
+                 const double* vel, const double* mass, const double* smoothing,
+                 const double* internal_energy, const double* density, const uint8_t* species,
+                 const int64_t* global_id, const int32_t g[3], double side_length, int32_t self,
+                 void* out, void* stream, HbError* err);
+size_t hb_halo_unpack_workspace(int64_t m);
+int hb_halo_unpack(int64_t m, const void* recs, int32_t sort_by_gid, int64_t row0, double* pos,
+                   double* vel, double* mass, double* smoothing, double* internal_energy,
+                   double* density, uint8_t* species, uint8_t* ghost, int8_t* image_shift,
+                   int64_t* global_id, int64_t* ghost_src, void* ws, size_t ws_bytes,
+                   void* stream, HbError* err);
+int hb_halo_resolve_sources(int64_t n_owned, int64_t m, const int64_t* global_id,
+                            int64_t* ghost_src, void* stream, HbError* err);
 
 #ifdef __cplusplus
 }

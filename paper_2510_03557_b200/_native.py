@@ -83,6 +83,16 @@ def lib():
             lb.hb_remap_through_inverse.argtypes = [C.c_int64, P, P, P, P, P]
             lb.hb_grow_aabbs.argtypes = [C.c_int64, P, P, P, P, C.c_double, P, P, P, P]
             lb.hb_launch_count.restype = C.c_int64
+            lb.hb_halo_record_bytes.restype = C.c_int64
+            lb.hb_halo_select.argtypes = [C.c_int64, P, P, P, C.c_double, C.c_double, C.c_int32,
+                                          C.c_int32, P, P, P, P, P, P, P]
+            lb.hb_halo_pack.argtypes = [C.c_int64, P, P, P, P, P, P, P, P, P, P, P, C.c_double,
+                                        C.c_int32, P, P, P]
+            lb.hb_halo_unpack_workspace.restype = C.c_size_t
+            lb.hb_halo_unpack_workspace.argtypes = [C.c_int64]
+            lb.hb_halo_unpack.argtypes = [C.c_int64, P, C.c_int32, C.c_int64] + [P] * 11 + [
+                P, C.c_size_t, P, P]
+            lb.hb_halo_resolve_sources.argtypes = [C.c_int64, C.c_int64, P, P, P, P]
             lb.hb_crk_solve.argtypes = [C.c_int64, P, C.c_int64, P, C.c_double, P, P, P, P, P]
             _lib = lb
         return _lib
@@ -92,7 +102,9 @@ def lib():
 EXPORTS = ("hb_abi_version", "hb_launch_count", "hb_device_query", "hb_build_mesh_workspace", "hb_leaf_capacity",
            "hb_build_mesh", "hb_permute_rows", "hb_remap_through_inverse", "hb_grow_aabbs",
            "hb_assemble_lists_workspace", "hb_assemble_lists", "hb_eval_pairs_workspace",
-           "hb_eval_pairs", "hb_crk_solve", "hb_force_step_workspace", "hb_force_step")
+           "hb_eval_pairs", "hb_crk_solve", "hb_force_step_workspace", "hb_force_step",
+           "hb_halo_record_bytes", "hb_halo_select", "hb_halo_pack", "hb_halo_unpack_workspace",
+           "hb_halo_unpack", "hb_halo_resolve_sources")
 
 
 def torch_cuda():

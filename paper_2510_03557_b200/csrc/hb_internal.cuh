@@ -41,6 +41,7 @@ struct SphArgs {
   double alpha, beta;
   double *ncount, *rho, *moments, *hydro;
   unsigned long long* err_key;
+  const uint8_t* skip_leaf;
 };
 int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
              double L, float4* P0, float4* P1, float4* P2, int layout, cudaStream_t st,

@@ -726,6 +726,11 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 constexpr int kGravWarps = 8;
 constexpr int kGravStage = 128;
 
+// TVAR: the table is indexed by t = sqrt(r^2 + eps^2) = soft * rsqrt(soft) and
+// stores S(sqrt(t^2 - eps^2) / r_s) (one MUFU per pair; used when eps/r_s <=
+// 0.05, where the cusp at t = eps costs < 4e-6 abs. in S for r < 2 eps only);
+// otherwise by r = r^2 * rsqrt(r^2).
+template <bool TVAR>
 __global__ void __launch_bounds__(kGravWarps * 32)
 k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_last,
           const int64_t* n_tiles_dev) {
@@ -738,6 +743,7 @@ k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_
   if (t >= *n_tiles_dev) return;
   const Tiling& T = a.T;
   int A = T.tile_leaf[t];
+  if (a.skip_leaf && a.skip_leaf[A]) return;
   int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
   if (e0 == e1) return;
   int n_t = T.tile_n[t];
@@ -758,8 +764,9 @@ k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_
       float4 s = stage[q];
       float dx = ti.x - s.x, dy = ti.y - s.y, dz = ti.z - s.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      float ri = rsqrt_ftz(r2 + eps2);
-      float rr = r2 * rsqrt_ftz(fmaxf(r2, 1e-30f));
+      float soft = r2 + eps2;
+      float ri = rsqrt_ftz(soft);
+      float rr = TVAR ? soft * ri : r2 * rsqrt_ftz(fmaxf(r2, 1e-30f));
       float fm = fmaf(rr, tab_scale, 12582912.0f);
       int k = min(__float_as_int(fm) - 0x4B400000, tab_last);
       float u = fmaf(rr, tab_scale, 12582912.0f - fm);
@@ -828,22 +835,30 @@ k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_
 }
 
 int launch_gravity_fast(const EvalDev& d, const float4* table, float tab_scale, int tab_last,
-                        int64_t tcap, const int64_t* ntd, cudaStream_t st, HbError* err) {
-  k_gravity<<<grid_for(tcap, kGravWarps), kGravWarps * 32, 0, st>>>(d, table, tab_scale, tab_last,
-                                                                    ntd);
+                        bool tvar, int64_t tcap, const int64_t* ntd, cudaStream_t st,
+                        HbError* err) {
+  if (tvar)
+    k_gravity<true><<<grid_for(tcap, kGravWarps), kGravWarps * 32, 0, st>>>(d, table, tab_scale,
+                                                                           tab_last, ntd);
+  else
+    k_gravity<false><<<grid_for(tcap, kGravWarps), kGravWarps * 32, 0, st>>>(d, table, tab_scale,
+                                                                            tab_last, ntd);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
 
 // cubic-per-interval table of S(r / r_s) over r in [0, r_cut] (float64 fit)
-int gravity_table(double r_s, double r_cut, int nt, float4* host_out, float* tab_scale) {
+int gravity_table(double r_s, double r_cut, double eps, bool tvar, int nt, float4* host_out,
+                  float* tab_scale) {
   double dr = r_cut / nt;
   const double node[4] = {0.5 * cos(M_PI * 0.5 / 4), 0.5 * cos(M_PI * 1.5 / 4),
                           0.5 * cos(M_PI * 2.5 / 4), 0.5 * cos(M_PI * 3.5 / 4)};
   for (int k = 0; k <= nt; ++k) {
     double m[4][5];
     for (int i = 0; i < 4; ++i) {
-      double x = (k + node[i]) * dr / r_s;
+      double rv = (k + node[i]) * dr;
+      if (tvar) rv = sqrt(fmax(rv * rv - eps * eps, 0.0));
+      double x = rv / r_s;
       double sv = erfc(x) + 1.1283791670955126 * x * exp(-x * x);
       double p = 1.0;
       for (int j = 0; j < 4; ++j) { m[i][j] = p; p *= node[i]; }
@@ -1070,7 +1085,7 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   d.cull_reach = (float)(a->reach * (1.0 + 1e-4)) + 1e-30f;
   d.include_self = a->include_self; d.nchan = a->nchan;
   for (int c = 0; c < 10; ++c) d.scale[c] = (float)a->scales[c];
-  d.out_flt = a->out_flt; d.out_int = a->out_int; d.write_out = 1;
+  d.out_flt = a->out_flt; d.out_int = a->out_int; d.write_out = 1; d.skip_leaf = nullptr;
   d.in_count = w.dev_cnt + 2; d.err_key = w.dev_cnt + 3;
   int rc = launch_pairs(a->kid, a->deterministic != 0, false, d, tcap, w.n_tiles_dev, st, err);
   if (rc) return rc;

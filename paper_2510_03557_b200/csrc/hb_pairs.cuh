@@ -216,6 +216,7 @@ struct EvalDev {
   double* out_flt;
   int64_t* out_int;
   int write_out;
+  const uint8_t* skip_leaf;  // receivers to skip (ghost-only leaves), or null
   unsigned long long* in_count;
   unsigned long long* err_key;  // min (entry*4 + kind)
 };
@@ -236,8 +237,10 @@ int kid_selects_gas(int kid);
 // resident fast gravity: table of S(r/r_s), 128 cubic intervals over [0, r_cut]
 constexpr int kGravTableN = 128;
 constexpr int kGravTableMax = kGravTableN + 2;
-int gravity_table(double r_s, double r_cut, int nt, float4* host_out, float* tab_scale);
+int gravity_table(double r_s, double r_cut, double eps, bool tvar, int nt, float4* host_out,
+                  float* tab_scale);
 int launch_gravity_fast(const EvalDev& d, const float4* table, float tab_scale, int tab_last,
-                        int64_t tcap, const int64_t* ntd, cudaStream_t st, HbError* err);
+                        bool tvar, int64_t tcap, const int64_t* ntd, cudaStream_t st,
+                        HbError* err);
 
 }  // namespace hb

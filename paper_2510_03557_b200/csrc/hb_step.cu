@@ -88,6 +88,7 @@ struct StepWs {
   unsigned long long* err_key;
   int64_t* inv;
   float4* gtab;
+  uint8_t* no_ghost;
 };
 
 static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t lcap, StepWs& w) {
@@ -107,6 +108,7 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
   w.err_key = ws.take<unsigned long long>(1);
   w.inv = ws.take<int64_t>(n + 1);
   w.gtab = ws.take<float4>(kGravTableMax);
+  w.no_ghost = ws.take<uint8_t>(cap + 1);
 }
 
 struct PhaseTimer {
@@ -187,6 +189,10 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   // 2. ordered list as a receiver CSR
   ld.n_leaves = nl; ld.leaf_bin = w.leaf_bin; ld.leaf_level = nullptr; ld.bin_ptr = w.bin_ptr;
   ld.bin_ids = nullptr; ld.leaf_lo = w.leaf_lo; ld.leaf_hi = w.leaf_hi; ld.ghost_only = w.ghost_only;
+  if (a->ghost_density) {  // every leaf receives (ghost-only ones feed fresh ghost densities)
+    HB_CUDA_TRY(cudaMemsetAsync(w.no_ghost, 0, nl + 1, st));
+    ld.ghost_only = w.no_ghost;
+  }
   for (int d = 0; d < 3; ++d) { ld.g.nb[d] = a->nb[d]; ld.g.periodic[d] = a->periodic[d]; }
   ld.g.L = a->side_length; ld.g.reach = a->reach; ld.g.active_depth = 0;
   {
@@ -247,6 +253,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   sa.pshift = a->image_shift; sa.L = a->side_length; sa.reach = sph_reach; sa.band = band;
   sa.alpha = a->visc_alpha; sa.beta = a->visc_beta; sa.err_key = w.err_key;
   sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = a->crk_moments; sa.hydro = a->hydro;
+  sa.skip_leaf = a->ghost_density ? w.ghost_only : nullptr;
+  d.skip_leaf = a->ghost_density ? w.ghost_only : nullptr;
   // 4. pass A: neighbour count + density (hb/hydro.py:223-227, 60-84), EOS (48-57)
   if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY)) {
     HB_CUDA_TRY(cudaMemsetAsync(a->ncount, 0, n * sizeof(double), st));
@@ -258,9 +266,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     if (rc) return rc;
   }
   if (a->passes & HB_PASS_DENSITY) {
-    k_density_update<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, w.leaf_start, w.leaf_end,
-                                                             w.ghost_only, a->species, w.rho_new,
-                                                             a->density);
+    k_density_update<<<grid_for(nl * 32, 256), 256, 0, st>>>(
+        nl, w.leaf_start, w.leaf_end, a->ghost_density ? w.no_ghost : w.ghost_only, a->species,
+        w.rho_new, a->density);
     if (a->ghost_src_in && a->ghost_src) {
       k_alias_sync<<<grid_for(n, 256), 256, 0, st>>>(n, a->ghost_src, a->density);
       HB_COUNT_LAUNCH(1);
@@ -294,9 +302,12 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
     static float4 host_tab[kGravTableMax];
     float tab_scale = 0.f;
-    int tab_last = gravity_table(a->r_s, a->r_cut, kGravTableN, host_tab, &tab_scale);
+    bool tvar = a->softening <= 0.05 * a->r_s;
+    int tab_last = gravity_table(a->r_s, a->r_cut, a->softening, tvar, kGravTableN, host_tab,
+                                 &tab_scale);
     HB_CUDA_TRY(cudaMemcpyAsync(w.gtab, host_tab, sizeof(host_tab), cudaMemcpyHostToDevice, st));
-    rc = launch_gravity_fast(d, w.gtab, tab_scale, tab_last, w.Ta.n_tiles_cap, w.nta, st, err);
+    rc = launch_gravity_fast(d, w.gtab, tab_scale, tab_last, tvar, w.Ta.n_tiles_cap, w.nta, st,
+                             err);
     if (rc) return rc;
   }
   tm.mark(6);

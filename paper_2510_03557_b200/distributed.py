@@ -1,0 +1,221 @@
+"""Multi-GPU force evaluation: cuboid ranks with an overload-shell exchange.
+
+One process per GPU.  Each rank owns the particles of one cuboid of the box
+(decompose, hb/domain.py:53-69: x-major rank ids, half-open bounds) and, per
+step, refreshes its overload shell (refresh_overload / build_overload,
+hb/domain.py:88-189) with ONE all-to-all of fixed-width records:
+
+  hb_halo_select (count, emit)   ghost copy for every (rank, image shift) whose
+                                 shifted position lies strictly inside the
+                                 rank's bounds widened by w; owned copy to the
+                                 (new) owner (migration, DriftError on >1 hop)
+  hb_halo_pack                   104-byte records, grouped by destination
+  all_to_all_single (NCCL)       counts, then bytes (the only collective)
+  hb_halo_unpack (+ sort)        owned rows by global_id, ghosts by
+                                 (global_id, shift) -- the reference's order
+  hb_force_step                  with ghost-only leaves as density receivers,
+                                 so ghost rows near the face carry fresh rho,
+                                 P, c_s (SURVEY.md finding 4)
+
+The overload width is max(1.25 reach, reach + 2 h_max): the reference's
+1.25 x reach (hb/driver.py:135-145) widened so every ghost within reach of an
+owned particle has its whole density neighbourhood on the rank.  Results for
+owned rows equal the single-domain evaluation within FP32 tolerance.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .box import BoxGeometry
+from .errors import DriftError, HydroboxError
+from .particles import ParticleSet
+from .resident import STEP_FIELDS, ResidentRank, StepConfig
+
+RANK_GRIDS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+
+_FIELD_DTYPES = {"pos": ("float64", 3), "vel": ("float64", 3), "mass": ("float64", 1),
+                 "smoothing": ("float64", 1), "internal_energy": ("float64", 1),
+                 "density": ("float64", 1), "species": ("uint8", 1), "ghost": ("uint8", 1),
+                 "image_shift": ("int8", 3), "global_id": ("int64", 1),
+                 "ghost_src": ("int64", 1)}
+
+
+def rank_grid_for(world: int) -> tuple:
+    if world in RANK_GRIDS:
+        return RANK_GRIDS[world]
+    raise HydroboxError(f"no cuboid rank grid for {world} ranks (supported: 1, 2, 4, 8)")
+
+
+def domain_bounds(box: BoxGeometry, grid, rank: int):
+    """Bounds of rank `rank` exactly as decompose() computes them."""
+    g = np.asarray(grid, dtype=np.int64)
+    L = box.side_length
+    c = np.array([rank // (g[1] * g[2]), (rank // g[2]) % g[1], rank % g[2]])
+    lo = np.array([L * c[d] / g[d] for d in range(3)])
+    hi = np.array([L * (c[d] + 1) / g[d] for d in range(3)])
+    return lo, hi
+
+
+def overload_width(r_cut: float, h_max: float) -> float:
+    reach = max(r_cut, 2.0 * h_max)
+    return max(1.25 * reach, reach + 2.0 * h_max)
+
+
+def alltoallv_bytes(send, send_counts: list, group=None):
+    """Variable all-to-all of a uint8 tensor (NCCL on GPU, gloo on CPU).
+    Returns (recv tensor, recv_counts)."""
+    import torch
+    import torch.distributed as dist
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=send.device)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = [int(x) for x in rc.tolist()]
+    out = torch.empty(sum(recv_counts), dtype=torch.uint8, device=send.device)
+    dist.all_to_all_single(out, send, recv_counts, [int(x) for x in send_counts], group=group)
+    return out, recv_counts
+
+
+def empty_fields(n: int) -> dict:
+    import torch
+    out = {}
+    for f, (dt, w) in _FIELD_DTYPES.items():
+        shape = (n,) if w == 1 else (n, w)
+        out[f] = torch.empty(shape, dtype=getattr(torch, dt), device="cuda")
+    return out
+
+
+class HaloExchange:
+    """Overload refresh of one rank (world ranks, cuboid grid)."""
+
+    def __init__(self, box: BoxGeometry, grid, w: float, rank: int, world: int, group=None,
+                 transport=None):
+        self.box, self.grid, self.w = box, tuple(int(x) for x in grid), float(w)
+        self.rank, self.world, self.group = rank, world, group
+        self.transport = transport  # callable(send, counts) -> (recv, counts); None = NCCL/gloo
+        self.lib = N.lib()
+        self.rec = int(self.lib.hb_halo_record_bytes())
+        lo, hi = domain_bounds(box, self.grid, rank)
+        if w >= 0.5 * float(np.min(hi - lo)):
+            raise HydroboxError(f"overload_width {w:.4g} >= half the smallest domain extent "
+                                f"{float(np.min(hi - lo)):.4g}: a particle would be duplicated "
+                                "twice within one rank")
+
+    def pack(self, fields: dict):
+        """Select + pack this rank's owned rows; returns (send bytes, per-dest byte counts)."""
+        import torch
+        n = int(fields["pos"].shape[0])
+        nslot = self.world * 28
+        g = (C.c_int32 * 3)(*self.grid)
+        counts = torch.zeros(nslot, dtype=torch.int64, device="cuda")
+        drift = torch.zeros(1, dtype=torch.int32, device="cuda")
+        err = N.HbError()
+        st = N.stream_ptr()
+        N.check(self.lib.hb_halo_select(n, N.ptr(fields["pos"]), N.ptr(fields["ghost"]), g,
+                                        float(self.box.side_length), self.w, self.rank, 0,
+                                        N.ptr(counts), N.ptr(counts), None, None, N.ptr(drift),
+                                        st, C.byref(err)), err)
+        ch = counts.cpu().numpy()
+        if int(drift.item()):
+            raise DriftError("particle crossed more than one domain in one PM step")
+        offs = np.concatenate([[0], np.cumsum(ch)]).astype(np.int64)
+        m = int(offs[-1])
+        rows = torch.empty(max(m, 1), dtype=torch.int64, device="cuda")
+        slots = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        fill = torch.from_numpy(offs[:-1].copy()).cuda()
+        N.check(self.lib.hb_halo_select(n, N.ptr(fields["pos"]), N.ptr(fields["ghost"]), g,
+                                        float(self.box.side_length), self.w, self.rank, 1,
+                                        N.ptr(counts), N.ptr(fill), N.ptr(rows), N.ptr(slots),
+                                        N.ptr(drift), st, C.byref(err)), err)
+        send = torch.empty(max(m, 1) * self.rec, dtype=torch.uint8, device="cuda")
+        N.check(self.lib.hb_halo_pack(m, N.ptr(rows), N.ptr(slots), N.ptr(fields["pos"]),
+                                      N.ptr(fields["vel"]), N.ptr(fields["mass"]),
+                                      N.ptr(fields["smoothing"]), N.ptr(fields["internal_energy"]),
+                                      N.ptr(fields["density"]), N.ptr(fields["species"]),
+                                      N.ptr(fields["global_id"]), g, float(self.box.side_length),
+                                      self.rank, N.ptr(send), st, C.byref(err)), err)
+        per_dest = ch.reshape(self.world, 28).sum(axis=1) * self.rec
+        return send[:m * self.rec], [int(x) for x in per_dest]
+
+    def unpack(self, recv) -> tuple[dict, int]:
+        """Records -> new rank field set (owned by gid, then ghosts by (gid, shift))."""
+        import torch
+        m = int(recv.numel()) // self.rec
+        out = empty_fields(max(m, 1))
+        ws = N.workspace(self.lib.hb_halo_unpack_workspace(m))
+        err = N.HbError()
+        st = N.stream_ptr()
+        N.check(self.lib.hb_halo_unpack(m, N.ptr(recv), 1, 0, *[N.ptr(out[f]) for f in (
+            "pos", "vel", "mass", "smoothing", "internal_energy", "density", "species", "ghost",
+            "image_shift", "global_id", "ghost_src")], N.ptr(ws), C.c_size_t(ws.numel()), st,
+            C.byref(err)), err)
+        out = {k: v[:m] for k, v in out.items()}
+        n_owned = int((out["ghost"] == 0).sum().item())
+        N.check(self.lib.hb_halo_resolve_sources(n_owned, m, N.ptr(out["global_id"]),
+                                                 N.ptr(out["ghost_src"]), st, C.byref(err)), err)
+        return out, n_owned
+
+    def exchange(self, fields: dict) -> tuple[dict, int]:
+        send, counts = self.pack(fields)
+        if self.transport is not None:
+            recv, _ = self.transport(send, counts)
+        elif self.world == 1:
+            recv = send
+        else:
+            recv, _ = alltoallv_bytes(send, counts, self.group)
+        return self.unpack(recv)
+
+
+class DistributedRank:
+    """One rank of a multi-GPU force evaluation (device-resident)."""
+
+    def __init__(self, owned: ParticleSet, box: BoxGeometry, rank: int, world: int, r_s: float,
+                 r_cut: float, softening: float, h_max: float, h_min: float,
+                 max_leaf_size: int = 256, cm_bin_width: float = 0.0, group=None,
+                 transport=None, eos_gamma: float = 5.0 / 3.0):
+        import torch
+        self.box, self.rank, self.world = box, rank, world
+        self.grid = rank_grid_for(world)
+        self.w = overload_width(r_cut, h_max)
+        reach = max(r_cut, 2.0 * h_max)
+        lo, hi = domain_bounds(box, self.grid, rank)
+        self.lo, self.hi = lo, hi
+        bin_width = max(cm_bin_width, reach * (1 + 1e-9))
+        self.cfg = StepConfig(box=box, bin_width=bin_width, max_leaf_size=max_leaf_size,
+                              r_s=r_s, r_cut=r_cut, softening=softening, eos_gamma=eos_gamma,
+                              bounds_lo=lo - self.w, bounds_hi=hi + self.w)
+        self.h_range = (h_min, h_max)
+        self.halo = HaloExchange(box, self.grid, self.w, rank, world, group, transport)
+        fields = {}
+        for f in STEP_FIELDS:
+            arr = np.ascontiguousarray(getattr(owned, f))
+            fields[f] = torch.from_numpy(arr).cuda()
+        fields["ghost"].zero_()
+        fields["image_shift"].zero_()
+        fields["ghost_src"].fill_(-1)
+        self.owned_fields = fields
+        self.engine = None
+        self.n_owned = int(owned.n)
+
+    def exchange(self):
+        new, n_owned = self.halo.exchange(self.owned_fields)
+        self.n_owned = n_owned
+        if self.engine is None:
+            self.engine = ResidentRank(None, self.cfg, fields=new, ghost_density=self.world > 1,
+                                       h_range=self.h_range)
+        else:
+            self.engine.set_fields(new, self.h_range)
+        return new
+
+    def step(self, timing: bool = False):
+        """Exchange + force evaluation; returns device outputs (leaf order of
+        the rank set) and the reordered fields."""
+        self.exchange()
+        out = self.engine.step(timing=timing)
+        fields = self.engine.fields()
+        # keep only owned rows (leaf order) as next step's owned set
+        own = fields["ghost"] == 0
+        self.owned_fields = {k: v[own].contiguous() for k, v in fields.items()}
+        return out, fields

@@ -44,7 +44,8 @@ class HbStepArgs(C.Structure):
                    ("r_s", C.c_double),
                    ("r_cut", C.c_double), ("softening", C.c_double), ("eos_gamma", C.c_double),
                    ("visc_alpha", C.c_double), ("visc_beta", C.c_double), ("passes", C.c_int32),
-                   ("timing", C.c_int32), ("list_capacity", C.c_int64),
+                   ("timing", C.c_int32), ("ghost_density", C.c_int32),
+                   ("list_capacity", C.c_int64),
                    ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
                    ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
@@ -81,41 +82,57 @@ class StepConfig:
 class ResidentRank:
     """One rank's working set on the current CUDA device."""
 
-    def __init__(self, particles: ParticleSet, cfg: StepConfig):
+    def __init__(self, particles: ParticleSet | None, cfg: StepConfig, fields: dict | None = None,
+                 ghost_density: bool = False, h_range: tuple | None = None):
+        """Either host ``particles`` or device ``fields`` (dict of STEP_FIELDS
+        tensors).  ``h_range`` = (h_min_gas, h_max) when given as fields."""
         torch = N.torch_cuda()
         self.cfg = cfg
-        self.n = particles.n
-        self.buf = [self._alloc(particles), None]
-        self.buf[1] = {k: torch.empty_like(v) for k, v in self.buf[0].items()}
-        self.cur = 0
-        gas = particles.species == 1
-        self.h_max = float(particles.smoothing.max()) if particles.n else 0.0
-        if not np.any(gas):
-            self.h_max = 0.0
-        self.h_min = float(particles.smoothing[gas].min()) if np.any(gas) else 0.0
+        self.ghost_density = ghost_density
         lo, hi, nb, width, periodic = mesh_geometry(cfg.box, cfg.bin_width, cfg.bounds_lo,
                                                     cfg.bounds_hi)
         self.lo, self.nb, self.width, self.periodic = lo, nb, width, periodic
-        n = max(self.n, 1)
-        f64 = torch.float64
-        self.out = {
-            "perm": torch.empty(n, dtype=torch.int64, device="cuda"),
-            "ncount": torch.zeros(n, dtype=f64, device="cuda"),
-            "grav": torch.zeros((n, 3), dtype=f64, device="cuda"),
-            "hydro": torch.zeros((n, 5), dtype=f64, device="cuda"),
-            "crk_moments": torch.zeros((n, 10), dtype=f64, device="cuda"),
-            "crk_A": torch.zeros(n, dtype=f64, device="cuda"),
-            "crk_B": torch.zeros((n, 3), dtype=f64, device="cuda"),
-            "crk_fallback": torch.zeros(n, dtype=torch.uint8, device="cuda"),
-        }
         self.lib = N.lib()
         _bind(self.lib)
-        nbins = int(np.prod(nb))
-        cap = int(self.lib.hb_leaf_capacity(self.n, nbins, cfg.max_leaf_size))
-        self.list_capacity = max(1024, cap * 64)
         self._ws = None
-        self._ws_cap = -1
+        self._ws_key = None
+        self.list_capacity = 0
         self.last = None
+        self.out = {}
+        self.buf = [None, None]
+        if particles is not None:
+            gas = particles.species == 1
+            h_range = ((float(particles.smoothing[gas].min()), float(particles.smoothing.max()))
+                       if np.any(gas) else (0.0, 0.0))
+            fields = self._alloc(particles)
+        self.set_fields(fields, h_range)
+
+    def set_fields(self, fields: dict, h_range: tuple) -> None:
+        """Adopt a device field set (n rows); (re)size outputs and buffers."""
+        torch = N.torch_cuda()
+        n = int(fields["pos"].shape[0])
+        self.h_min, self.h_max = float(h_range[0]), float(h_range[1])
+        self.buf[0] = fields
+        self.cur = 0
+        if self.buf[1] is None or int(self.buf[1]["pos"].shape[0]) != n:
+            self.buf[1] = {k: torch.empty_like(v) for k, v in fields.items()}
+        if self.out.get("perm") is None or int(self.out["perm"].shape[0]) != max(n, 1):
+            m = max(n, 1)
+            f64 = torch.float64
+            self.out = {
+                "perm": torch.empty(m, dtype=torch.int64, device="cuda"),
+                "ncount": torch.zeros(m, dtype=f64, device="cuda"),
+                "grav": torch.zeros((m, 3), dtype=f64, device="cuda"),
+                "hydro": torch.zeros((m, 5), dtype=f64, device="cuda"),
+                "crk_moments": torch.zeros((m, 10), dtype=f64, device="cuda"),
+                "crk_A": torch.zeros(m, dtype=f64, device="cuda"),
+                "crk_B": torch.zeros((m, 3), dtype=f64, device="cuda"),
+                "crk_fallback": torch.zeros(m, dtype=torch.uint8, device="cuda"),
+            }
+        self.n = n
+        nbins = int(np.prod(self.nb))
+        cap = int(self.lib.hb_leaf_capacity(self.n, nbins, self.cfg.max_leaf_size))
+        self.list_capacity = max(self.list_capacity, 1024, cap * 64)
 
     @staticmethod
     def _alloc(p: ParticleSet) -> dict:
@@ -124,13 +141,15 @@ class ResidentRank:
                 if name in STEP_FIELDS}
 
     def _workspace(self):
-        if self._ws is None or self._ws_cap != self.list_capacity:
+        key = (self.n, self.list_capacity)
+        if self._ws is None or self._ws_key != key:
             nb3 = (C.c_int64 * 3)(*[int(v) for v in self.nb])
             sz = self.lib.hb_force_step_workspace(self.n, nb3, self.cfg.max_leaf_size,
                                                   self.list_capacity)
-            self._ws = None
-            self._ws = N.workspace(sz)
-            self._ws_cap = self.list_capacity
+            if self._ws is None or self._ws.numel() < sz:
+                self._ws = None
+                self._ws = N.workspace(sz)
+            self._ws_key = key
         return self._ws
 
     def fields(self) -> dict:
@@ -158,6 +177,7 @@ class ResidentRank:
         a.eos_gamma, a.visc_alpha, a.visc_beta = cfg.eos_gamma, cfg.visc_alpha, cfg.visc_beta
         a.passes = int(passes)
         a.timing = 1 if timing else 0
+        a.ghost_density = 1 if self.ghost_density else 0
         for k in ("perm", "ncount", "grav", "hydro", "crk_moments", "crk_A", "crk_B",
                   "crk_fallback"):
             setattr(a, k, N.ptr(self.out[k]))

@@ -1,0 +1,78 @@
+"""GPU: the multi-rank force evaluation, emulated with R ranks in one process
+(the all-to-all is routed in-process; the NCCL path is exercised by bench.py
+under torchrun).  Rank sets must equal the reference's build_overload
+bit-for-bit; owned-row outputs must equal the single-domain evaluation."""
+import numpy as np
+import pytest
+
+from tests.tolerances import assert_fp32_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(npd=32, sigma=0.3):
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.ic import make_zeldovich_ic
+    box = BoxGeometry(1.0)
+    p = make_zeldovich_ic(npd, box, sigma)
+    pm = 1.0 / (2 * npd)
+    r_s, r_cut = 2 * pm, 10 * pm
+    eps = (1.0 / p.n ** (1 / 3)) / 50
+    return box, p, r_s, r_cut, eps
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_emulated_ranks_match_single_domain(world, oracle):
+    import torch
+    from paper_2510_03557_b200.distributed import DistributedRank, rank_grid_for
+    from paper_2510_03557_b200.domain import build_overload, decompose, owner_ranks
+    from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
+    from paper_2510_03557_b200.resident import StepConfig, force_step
+    box, p, r_s, r_cut, eps = _setup()
+    h_max = float(p.smoothing.max())
+    h_min = float(p.smoothing[p.species == 1].min())
+    reach = max(r_cut, 2 * h_max)
+    grid = rank_grid_for(world)
+    # single-domain reference evaluation (bare periodic mesh)
+    q = p.copy()
+    cfg = StepConfig(box=box, bin_width=reach * (1 + 1e-9), max_leaf_size=256, r_s=r_s,
+                     r_cut=r_cut, softening=eps)
+    ref = force_step(q, cfg)
+    by_gid = np.argsort(q.global_id)
+    owner = owner_ranks(p.pos, box, grid)
+    ranks = [DistributedRank(p.select(np.nonzero(owner == r)[0]), box, r, world, r_s, r_cut, eps,
+                             h_max, h_min) for r in range(world)]
+    sends = [rk.halo.pack(rk.owned_fields) for rk in ranks]
+    doms = decompose(box, grid, ranks[0].w)
+    ref_sets, _ = build_overload(p.copy(), doms, box, grid)
+    m = oracle  # noqa: F841  (oracle fixture builds the checker library)
+    gk = short_range_gravity_kernel(ForceSplit(r_s=r_s, r_cut=r_cut), eps)
+    for r, rk in enumerate(ranks):
+        chunks = []
+        for src, (buf, counts) in enumerate(sends):
+            off = sum(counts[:r])
+            chunks.append(buf[off:off + counts[r]])
+        new, n_owned = rk.halo.unpack(torch.cat(chunks))
+        rs = ref_sets[r]
+        for f in ("pos", "image_shift", "global_id", "ghost", "ghost_src", "smoothing"):
+            np.testing.assert_array_equal(new[f].cpu().numpy(), getattr(rs, f), err_msg=f)
+        from paper_2510_03557_b200.resident import ResidentRank
+        eng = ResidentRank(None, rk.cfg, fields=new, ghost_density=world > 1,
+                           h_range=(h_min, h_max))
+        out = eng.step()
+        flds = eng.fields()
+        gid = flds["global_id"].cpu().numpy()
+        own = flds["ghost"].cpu().numpy() == 0
+        g = gid[own]
+        np.testing.assert_array_equal(out["ncount"].cpu().numpy()[own], ref["ncount"][by_gid][g])
+        dens = flds["density"].cpu().numpy()[own]
+        rd = q.density[by_gid][g]
+        gas = q.species[by_gid][g] == 1
+        rel = np.abs(dens - rd)[gas] / rd[gas]
+        assert rel.max() <= 1e-5, rel.max()
+        scale = np.abs(ref["grav"]).mean()
+        dg = np.abs(out["grav"].cpu().numpy()[own] - ref["grav"][by_gid][g])
+        assert np.median(dg) <= 1e-5 * scale and dg.max() <= 1e-3 * scale, dg.max() / scale
+        hs = np.abs(ref["hydro"][:, :4]).mean()
+        dh = np.abs(out["hydro"].cpu().numpy()[own, :4] - ref["hydro"][by_gid][g][:, :4])
+        assert np.median(dh) <= 1e-5 * hs and dh.max() <= 1e-3 * hs, dh.max() / hs
