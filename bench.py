@@ -244,27 +244,52 @@ def run_reference_arm(args):
     return 0
 
 
+def _make_rank(args, p, cfg, rank, world, group=None):
+    """N = 1: the bare periodic mesh; N > 1: cuboid rank + overload exchange."""
+    from paper_2510_03557_b200.distributed import DistributedRank, rank_grid_for
+    from paper_2510_03557_b200.domain import owner_ranks
+    from paper_2510_03557_b200.resident import ResidentRank
+    if world == 1:
+        return ResidentRank(p, cfg)
+    owner = owner_ranks(p.pos, cfg.box, rank_grid_for(world))
+    gas = p.species == 1
+    return DistributedRank(p.select(np.nonzero(owner == rank)[0]), cfg.box, rank, world,
+                           cfg.r_s, cfg.r_cut, cfg.softening, float(p.smoothing.max()),
+                           float(p.smoothing[gas].min()), cfg.max_leaf_size, group=group,
+                           n_global=p.n)
+
+
 def run_gpu_arm(args):
     import torch
     from paper_2510_03557_b200 import _native as N
-    from paper_2510_03557_b200.resident import PASS_ALL, STEP_FIELDS, ResidentRank
+    from paper_2510_03557_b200.resident import PASS_ALL, STEP_FIELDS
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     p, cfg, meta = make_workload(args.config, rank, world)
-    n_owned = int(np.count_nonzero(p.ghost == 0))
-    rr = ResidentRank(p, cfg)
+    n_total = int(p.n)
+    rr = _make_rank(args, p, cfg, rank, world)
+    engine = rr if world == 1 else None
     lib = N.lib()
     stream = torch.cuda.current_stream()
+
+    def step(timing=False):
+        if world == 1:
+            rr.step(PASS_ALL, timing=timing)
+            return rr.last
+        rr.step(timing=timing)
+        return rr.engine.last
+
     for _ in range(args.warmup):
-        rr.step(PASS_ALL)
+        step()
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    if dist:
+        dist.barrier()
     l0 = lib.hb_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     phases = []
@@ -272,42 +297,62 @@ def run_gpu_arm(args):
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            rr.step(PASS_ALL, timing=True)
-            phases.append(rr.last["ms_phase"])
+            phases.append(step(timing=True)["ms_phase"])
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = lib.hb_launch_count() - l0
     ms_total = ev0.elapsed_time(ev1)
-    if world > 1:
+    if dist:
         t = torch.tensor([ms_total], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = n_owned * world / (ms_step * 1e-3) if world > 1 else n_owned / (ms_step * 1e-3)
+    value = n_total / (ms_step * 1e-3)
     ph = {k: float(np.mean([x[k] for x in phases])) for k in phases[0]}
+    if dist:
+        t = torch.tensor([ph["gravity"]], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ph["gravity_max_over_ranks"] = float(t.item())
 
-    # ---- e2e: pinned host buffers -> device -> step -> results back to host
-    pinned_in = {f: torch.from_numpy(np.ascontiguousarray(getattr(p, f))).pin_memory()
-                 for f in STEP_FIELDS}
+    # ---- e2e: pinned host inputs -> device -> step (exchange incl.) -> results to host
+    if world == 1:
+        src_fields = {f: getattr(p, f) for f in STEP_FIELDS}
+    else:
+        src_fields = {f: rr.owned_fields[f].cpu().numpy() for f in STEP_FIELDS}
+    pinned_in = {f: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                 for f, a in src_fields.items()}
+    eng = rr if world == 1 else rr.engine
     out_names = ("grav", "hydro", "ncount", "crk_A", "crk_B", "perm")
-    pinned_out = {k: torch.empty(rr.out[k].shape, dtype=rr.out[k].dtype).pin_memory()
+    pinned_out = {k: torch.empty(eng.out[k].shape, dtype=eng.out[k].dtype).pin_memory()
                   for k in out_names}
-    pinned_out["density"] = torch.empty(rr.n, dtype=torch.float64).pin_memory()
+    pinned_out["density"] = torch.empty(eng.n, dtype=torch.float64).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in pinned_in.values())
     d2h = sum(t.numel() * t.element_size() for t in pinned_out.values())
 
+    e2e_dev = None if world == 1 else {
+        f: torch.empty(pinned_in[f].shape, dtype=pinned_in[f].dtype, device="cuda")
+        for f in STEP_FIELDS}
+
     def e2e_step():
-        src = rr.buf[rr.cur]
+        if world == 1:
+            dst = rr.buf[rr.cur]
+        else:
+            dst = rr.owned_fields = e2e_dev
         for f in STEP_FIELDS:
-            src[f].copy_(pinned_in[f], non_blocking=True)
-        out = rr.step(PASS_ALL)
+            dst[f].copy_(pinned_in[f], non_blocking=True)
+        step()
+        e = rr if world == 1 else rr.engine
         for k in out_names:
-            pinned_out[k].copy_(out[k], non_blocking=True)
-        pinned_out["density"].copy_(rr.fields()["density"], non_blocking=True)
+            if e.out[k].shape == pinned_out[k].shape:
+                pinned_out[k].copy_(e.out[k], non_blocking=True)
+        if e.fields()["density"].shape == pinned_out["density"].shape:
+            pinned_out["density"].copy_(e.fields()["density"], non_blocking=True)
 
     for _ in range(max(1, args.warmup // 2)):
         e2e_step()
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -315,39 +360,44 @@ def run_gpu_arm(args):
     e1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_e2e = float(t.item())
-    e2e_value = n_owned * world / (ms_e2e * 1e-3) if world > 1 else n_owned / (ms_e2e * 1e-3)
+    if dist:
+        t = torch.tensor([ms_e2e, float(h2d), float(d2h)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t[0].item())
+        tt = torch.tensor([float(h2d), float(d2h)], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        h2d, d2h = float(tt[0].item()), float(tt[1].item())
+    e2e_value = n_total / (ms_e2e * 1e-3)
 
     if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
+        if dist:
+            dist.destroy_process_group()
         return 0
     # ---- roofline of the dominant kernel (gravity phase, timed live above)
-    counts = pair_counts(p, cfg) if world == 1 else None
+    counts = pair_counts(p, cfg)
     peak, peak_src = peaks()
-    roof = None
-    if counts is not None:
-        alg_flops = counts["gravity"] * OPCOST["gravity"]
-        achieved = alg_flops / (ph["gravity"] * 1e-3) / 1e12
-        traffic = None
-        tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-        if os.path.exists(tf):
-            traffic = json.load(open(tf)).get("gravity_dram_bytes")
-        roof = {"bound": "fp32", "kernel": "k_eval<GRAVITY> (gravity phase incl. record pack)",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_flops_per_launch": alg_flops,
-                "in_support_pairs": counts["gravity"], "flops_per_pair": OPCOST["gravity"]}
-        step_flops = sum(counts[k] * OPCOST[k] for k in OPCOST)
-        roof["step_algorithmic_tflops"] = step_flops / (ms_step * 1e-3) / 1e12
-        roof["step_frac"] = roof["step_algorithmic_tflops"] / peak
-        roof["kflop_per_update"] = step_flops / n_owned / 1e3
+    alg_flops = counts["gravity"] * OPCOST["gravity"]
+    t_grav = ph.get("gravity_max_over_ranks", ph["gravity"]) * 1e-3
+    achieved = alg_flops / t_grav / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("gravity_dram_bytes_per_launch")
+    roof = {"bound": "fp32", "kernel": "k_gravity (gravity phase incl. record pack)",
+            "achieved": achieved, "peak": peak * world, "unit": "TFLOP/s",
+            "frac": achieved / (peak * world), "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_flops_per_launch": alg_flops, "in_support_pairs": counts["gravity"],
+            "flops_per_pair": OPCOST["gravity"]}
+    step_flops = sum(counts[k] * OPCOST[k] for k in OPCOST)
+    roof["step_algorithmic_tflops"] = step_flops / (ms_step * 1e-3) / 1e12
+    roof["step_frac"] = roof["step_algorithmic_tflops"] / (peak * world)
+    roof["kflop_per_update"] = step_flops / n_total / 1e3
     base = None
     if world == 1 and not args.no_cpu_baseline:
         base = cpu_baseline(p, cfg, frac=args.cpu_frac)
+    meta = dict(meta)
+    if world > 1:
+        meta["parallelism"] = f"spatial cuboids {rr.grid}, overload width {rr.w:.4g}, NCCL all-to-all shell exchange per step"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -356,14 +406,13 @@ def run_gpu_arm(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e},
             "gpu_launches": int(launches), "roofline": roof, "clocks": clocks.summary(),
-            "mesh": rr.last and {"n_leaves": rr.last["n_leaves"], "n_entries": rr.last["n_entries"]},
             "pair_counts": counts}
     if base is not None:
         line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
         line["cpu_baseline"]["seconds"] = base["seconds"]
     print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    if dist:
+        dist.destroy_process_group()
     return 0
 
 

@@ -260,24 +260,29 @@ int hb_force_step(HbStepArgs* args, void* ws, size_t ws_bytes, void* stream, HbE
  * refresh_overload (hb/domain.py:88-189): cuboid ranks of grid g (x-major ids),
  * ghost copy of an owned particle for every (rank r, image s) with pos + s L
  * strictly inside r's bounds widened by w (except its owned copy), owned copy
- * to its (new) owner; DriftError flag for > 1 domain hop.  Records are
+ * to its (new) owner; DriftError flag for > 1 domain hop.  periodic_unsplit:
+ * axes with g = 1 stay periodic in the rank mesh (no self-image ghosts there).
+ * stay != NULL: rows that remain owned here are flagged (mode 0) and not
+ * emitted, so only shell ghosts and migrants cross the exchange.  Records are
  * hb_halo_record_bytes() wide; slots = dest * 28 + code (27 = owned).
  * hb_halo_select: mode 0 counts per slot, mode 1 emits rows/slots at `fill`
  * offsets.  hb_halo_unpack orders owned rows by global_id then ghosts by
- * (global_id, shift) (hb/domain.py:135-138) into SoA rank fields.
+ * (global_id, shift) (hb/domain.py:135-138) into SoA rank fields; key_bits
+ * >= bit_length(27 * max_global_id + 26) (0: keep record order).
  * ------------------------------------------------------------------------- */
 int64_t hb_halo_record_bytes(void);
 int hb_halo_select(int64_t n, const double* pos, const uint8_t* ghost, const int32_t g[3],
-                   double side_length, double overload_width, int32_t self, int32_t mode,
-                   uint64_t* counts, uint64_t* fill, int64_t* out_row, int32_t* out_slot,
-                   int32_t* drift_flag, void* stream, HbError* err);
+                   double side_length, double overload_width, int32_t self,
+                   int32_t periodic_unsplit, int32_t mode, uint64_t* counts, uint64_t* fill,
+                   int64_t* out_row, int32_t* out_slot, int32_t* drift_flag, uint8_t* stay,
+                   void* stream, HbError* err);
 int hb_halo_pack(int64_t m, const int64_t* rows, const int32_t* slots, const double* pos,
                  const double* vel, const double* mass, const double* smoothing,
                  const double* internal_energy, const double* density, const uint8_t* species,
                  const int64_t* global_id, const int32_t g[3], double side_length, int32_t self,
                  void* out, void* stream, HbError* err);
 size_t hb_halo_unpack_workspace(int64_t m);
-int hb_halo_unpack(int64_t m, const void* recs, int32_t sort_by_gid, int64_t row0, double* pos,
+int hb_halo_unpack(int64_t m, const void* recs, int32_t key_bits, int64_t row0, double* pos,
                    double* vel, double* mass, double* smoothing, double* internal_energy,
                    double* density, uint8_t* species, uint8_t* ghost, int8_t* image_shift,
                    int64_t* global_id, int64_t* ghost_src, void* ws, size_t ws_bytes,

@@ -85,7 +85,7 @@ def lib():
             lb.hb_launch_count.restype = C.c_int64
             lb.hb_halo_record_bytes.restype = C.c_int64
             lb.hb_halo_select.argtypes = [C.c_int64, P, P, P, C.c_double, C.c_double, C.c_int32,
-                                          C.c_int32, P, P, P, P, P, P, P]
+                                          C.c_int32, C.c_int32, P, P, P, P, P, P, P, P]
             lb.hb_halo_pack.argtypes = [C.c_int64, P, P, P, P, P, P, P, P, P, P, P, C.c_double,
                                         C.c_int32, P, P, P]
             lb.hb_halo_unpack_workspace.restype = C.c_size_t

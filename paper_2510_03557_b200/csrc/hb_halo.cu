@@ -59,14 +59,58 @@ __device__ __forceinline__ int owner_of(const DomGrid& G, const double* p) {
 // owned copy to its owner, i.e. keep or migrate).  mode 0 counts per slot,
 // mode 1 emits (row, slot) at per-slot offsets (order inside a slot is free:
 // the receiver sorts).  Only owned rows of the current set are sources.
+// The reference tests every (rank, shift) on all three axes; the test is a
+// product of per-axis interval tests, so candidates are enumerated per axis
+// (<= 4 per axis, usually 1).  Axes with periodic_unsplit (g = 1, kept
+// periodic in the rank mesh) take only (cell 0, shift 0).
+__device__ __forceinline__ void halo_emit(int mode, int slot, int64_t i,
+                                          unsigned long long* counts, unsigned long long* fill,
+                                          int64_t* out_row, int32_t* out_slot) {
+  if (mode == 0) {
+    atomicAdd(&counts[slot], 1ull);
+  } else {
+    unsigned long long k = atomicAdd(&fill[slot], 1ull);
+    out_row[k] = i;
+    out_slot[k] = slot;
+  }
+}
+
 __global__ void k_halo_select(int64_t n, const double* pos, const uint8_t* ghost, DomGrid G,
-                              int self, int n_ranks, int mode, unsigned long long* counts,
-                              unsigned long long* fill, int64_t* out_row, int32_t* out_slot,
-                              int* drift) {
+                              int self, int periodic_unsplit, int mode,
+                              unsigned long long* counts, unsigned long long* fill,
+                              int64_t* out_row, int32_t* out_slot, int* drift, uint8_t* stay) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || ghost[i]) return;
-  double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-  int own = owner_of(G, p);
+  bool live = i < n && !ghost[i];
+  int own_slot = -1;
+  double p[3] = {0.0, 0.0, 0.0};
+  int own = 0;
+  if (live) {
+    p[0] = pos[3 * i]; p[1] = pos[3 * i + 1]; p[2] = pos[3 * i + 2];
+    own = owner_of(G, p);
+    own_slot = own * 28 + 27;
+  }
+  // stay != null: particles this rank keeps owning are flagged, not exchanged
+  bool emit_owned = live && !(stay && own == self);
+  if (stay && i < n && mode == 0) stay[i] = (live && own == self) ? 1 : 0;
+  // owned copies: one per particle, nearly all to the same slot -> warp-aggregated
+  {
+    unsigned act = __ballot_sync(0xffffffffu, emit_owned);
+    if (emit_owned) {
+      unsigned peers = __match_any_sync(act, own_slot);
+      int leader = __ffs(peers) - 1;
+      int rank_in = __popc(peers & lanemask_lt());
+      unsigned long long base = 0;
+      if ((int)(threadIdx.x & 31) == leader)
+        base = atomicAdd(mode == 0 ? &counts[own_slot] : &fill[own_slot],
+                         (unsigned long long)__popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      if (mode == 1) {
+        out_row[base + rank_in] = i;
+        out_slot[base + rank_in] = own_slot;
+      }
+    }
+  }
+  if (!live) return;
   if (mode == 0 && own != self) {  // DriftError: more than one domain hop (hb/domain.py:176-182)
     int a[3] = {own / (G.g[1] * G.g[2]), (own / G.g[2]) % G.g[1], own % G.g[2]};
     int b[3] = {self / (G.g[1] * G.g[2]), (self / G.g[2]) % G.g[1], self % G.g[2]};
@@ -76,35 +120,36 @@ __global__ void k_halo_select(int64_t n, const double* pos, const uint8_t* ghost
       if (hop > 1) atomicExch(drift, 1);
     }
   }
-  for (int r = 0; r < n_ranks; ++r) {
-    double lo[3], hi[3];
-    dom_bounds(G, r, lo, hi);
-    for (int sc = 0; sc < 28; ++sc) {
-      bool emit;
-      if (sc == 27) {
-        emit = r == own;
-      } else if (sc == 13 && r == own) {
-        emit = false;  // that is the owned copy itself
-      } else {
-        int s[3] = {sc / 9 - 1, (sc / 3) % 3 - 1, sc % 3 - 1};
-        emit = true;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          double x = __dadd_rn(p[d], __dmul_rn((double)s[d], G.L));
-          emit = emit && (x > __dsub_rn(lo[d], G.w)) && (x < __dadd_rn(hi[d], G.w));
+  int oc[3] = {own / (G.g[1] * G.g[2]), (own / G.g[2]) % G.g[1], own % G.g[2]};
+  int cand_c[3][6], cand_s[3][6], nc[3];
+  for (int d = 0; d < 3; ++d) {
+    nc[d] = 0;
+    if (periodic_unsplit && G.g[d] == 1) {
+      cand_c[d][0] = 0; cand_s[d][0] = 0; nc[d] = 1;
+      continue;
+    }
+    for (int c = 0; c < G.g[d] && nc[d] < 6; ++c) {
+      double lo = (G.L * (double)c) / (double)G.g[d];
+      double hi = (G.L * (double)(c + 1)) / (double)G.g[d];
+      for (int sv = -1; sv <= 1; ++sv) {
+        double x = __dadd_rn(p[d], __dmul_rn((double)sv, G.L));
+        if (x > __dsub_rn(lo, G.w) && x < __dadd_rn(hi, G.w) && nc[d] < 6) {
+          cand_c[d][nc[d]] = c; cand_s[d][nc[d]] = sv; ++nc[d];
         }
-      }
-      if (!emit) continue;
-      int slot = r * 28 + sc;
-      if (mode == 0) {
-        atomicAdd(&counts[slot], 1ull);
-      } else {
-        unsigned long long k = atomicAdd(&fill[slot], 1ull);
-        out_row[k] = i;
-        out_slot[k] = slot;
       }
     }
   }
+  // ghost copies (shell particles only; the owned copy was emitted above)
+  for (int a0 = 0; a0 < nc[0]; ++a0)
+    for (int a1 = 0; a1 < nc[1]; ++a1)
+      for (int a2 = 0; a2 < nc[2]; ++a2) {
+        int c0 = cand_c[0][a0], c1 = cand_c[1][a1], c2 = cand_c[2][a2];
+        int s0 = cand_s[0][a0], s1 = cand_s[1][a1], s2 = cand_s[2][a2];
+        if (s0 == 0 && s1 == 0 && s2 == 0 && c0 == oc[0] && c1 == oc[1] && c2 == oc[2]) continue;
+        int r = (c0 * G.g[1] + c1) * G.g[2] + c2;
+        halo_emit(mode, r * 28 + (s0 + 1) * 9 + (s1 + 1) * 3 + (s2 + 1), i, counts, fill,
+                  out_row, out_slot);
+      }
 }
 
 __global__ void k_halo_pack(int64_t m, const int64_t* rows, const int32_t* slots,
@@ -134,13 +179,14 @@ __global__ void k_halo_pack(int64_t m, const int64_t* rows, const int32_t* slots
   out[k] = rec;
 }
 
-__global__ void k_halo_keys(int64_t m, const HaloRec* in, uint64_t* keys, uint32_t* vals) {
+__global__ void k_halo_keys(int64_t m, const HaloRec* in, int key_bits, uint64_t* keys,
+                            uint32_t* vals) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
   const HaloRec& r = in[k];
   int code = (r.shift[0] + 1) * 9 + (r.shift[1] + 1) * 3 + (r.shift[2] + 1);
   // owned rows first (sorted by gid), ghosts after, ordered by (gid, shift)
-  keys[k] = ((uint64_t)r.ghost << 62) | ((uint64_t)r.gid * 27u + (uint64_t)code);
+  keys[k] = ((uint64_t)r.ghost << key_bits) | ((uint64_t)r.gid * 27u + (uint64_t)code);
   vals[k] = (uint32_t)k;
 }
 
@@ -180,18 +226,18 @@ extern "C" int64_t hb_halo_record_bytes(void) { return (int64_t)sizeof(HaloRec);
 
 extern "C" int hb_halo_select(int64_t n, const double* pos, const uint8_t* ghost, const int32_t g[3],
                               double side_length, double overload_width, int32_t self,
-                              int32_t mode, uint64_t* counts, uint64_t* fill, int64_t* out_row,
-                              int32_t* out_slot, int32_t* drift_flag, void* stream, HbError* err) {
+                              int32_t periodic_unsplit, int32_t mode, uint64_t* counts,
+                              uint64_t* fill, int64_t* out_row, int32_t* out_slot,
+                              int32_t* drift_flag, uint8_t* stay, void* stream, HbError* err) {
   if (err) *err = HbError{};
   if (n <= 0) return HB_OK;
   DomGrid G;
   for (int d = 0; d < 3; ++d) G.g[d] = g[d];
   G.L = side_length;
   G.w = overload_width;
-  int n_ranks = g[0] * g[1] * g[2];
   k_halo_select<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(
-      n, pos, ghost, G, self, n_ranks, mode, (unsigned long long*)counts,
-      (unsigned long long*)fill, out_row, out_slot, drift_flag);
+      n, pos, ghost, G, self, periodic_unsplit, mode, (unsigned long long*)counts,
+      (unsigned long long*)fill, out_row, out_slot, drift_flag, stay);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
@@ -224,7 +270,7 @@ extern "C" size_t hb_halo_unpack_workspace(int64_t m) {
   return ws.used + 1024;
 }
 
-extern "C" int hb_halo_unpack(int64_t m, const void* recs, int32_t sort_by_gid, int64_t row0,
+extern "C" int hb_halo_unpack(int64_t m, const void* recs, int32_t key_bits, int64_t row0,
                               double* pos, double* vel, double* mass, double* smoothing,
                               double* internal_energy, double* density, uint8_t* species,
                               uint8_t* ghost, int8_t* image_shift, int64_t* global_id,
@@ -240,10 +286,10 @@ extern "C" int hb_halo_unpack(int64_t m, const void* recs, int32_t sort_by_gid, 
   if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (halo unpack)");
   const HaloRec* in = (const HaloRec*)recs;
   uint32_t* order = nullptr;
-  if (sort_by_gid) {
-    k_halo_keys<<<grid_for(m, 256), 256, 0, st>>>(m, in, keys, vals);
+  if (key_bits > 0) {  // sort by (ghost flag, global_id * 27 + shift code)
+    k_halo_keys<<<grid_for(m, 256), 256, 0, st>>>(m, in, key_bits, keys, vals);
     HB_LAUNCH_CHECK();
-    int rc = radix_sort_u64_u32(keys, vals, m, 64, ws, st, err);
+    int rc = radix_sort_u64_u32(keys, vals, m, key_bits + 1, ws, st, err);
     if (rc) return rc;
     order = vals;
   }

@@ -91,45 +91,81 @@ class HaloExchange:
     """Overload refresh of one rank (world ranks, cuboid grid)."""
 
     def __init__(self, box: BoxGeometry, grid, w: float, rank: int, world: int, group=None,
-                 transport=None):
+                 transport=None, periodic_unsplit: bool = True, n_global: int | None = None):
         self.box, self.grid, self.w = box, tuple(int(x) for x in grid), float(w)
+        self.periodic_unsplit = periodic_unsplit
+        # key bits of the receiver's (ghost, global_id, shift) sort
+        self.key_bits = max(1, int(27 * max(n_global or 2 ** 40, 1) + 26).bit_length())
         self.rank, self.world, self.group = rank, world, group
         self.transport = transport  # callable(send, counts) -> (recv, counts); None = NCCL/gloo
         self.lib = N.lib()
         self.rec = int(self.lib.hb_halo_record_bytes())
+        self._bufs = {}   # capacity-backed scratch (no per-step allocation)
+        self._sets = [None, None]
+        self._which = 0
         lo, hi = domain_bounds(box, self.grid, rank)
         if w >= 0.5 * float(np.min(hi - lo)):
             raise HydroboxError(f"overload_width {w:.4g} >= half the smallest domain extent "
                                 f"{float(np.min(hi - lo)):.4g}: a particle would be duplicated "
                                 "twice within one rank")
 
+    def _buf(self, name, n, dtype, shape=()):
+        import torch
+        b = self._bufs.get(name)
+        if b is None or b.shape[0] < n:
+            b = torch.empty((int(n * 1.2) + 1024,) + tuple(shape), dtype=dtype, device="cuda")
+            self._bufs[name] = b
+        return b[:n]
+
+    def _field_set(self, n):
+        """One of two alternating capacity-backed rank field sets."""
+        k = self._which
+        self._which ^= 1
+        cur = self._sets[k]
+        if cur is None or cur["pos"].shape[0] < n:
+            cur = empty_fields(int(n * 1.2) + 1024)
+            self._sets[k] = cur
+        return cur
+
+    @property
+    def fast(self) -> bool:
+        """Staying owners bypass the exchange.  Valid when no rank can hold a
+        periodic self-image of its own particle: unsplit axes periodic in the
+        rank mesh and at most 2 ranks along every split axis."""
+        return self.periodic_unsplit and all(g <= 2 for g in self.grid)
+
     def pack(self, fields: dict):
-        """Select + pack this rank's owned rows; returns (send bytes, per-dest byte counts)."""
+        """Select + pack; returns (send bytes, per-dest byte counts, stay mask or None)."""
         import torch
         n = int(fields["pos"].shape[0])
         nslot = self.world * 28
         g = (C.c_int32 * 3)(*self.grid)
-        counts = torch.zeros(nslot, dtype=torch.int64, device="cuda")
-        drift = torch.zeros(1, dtype=torch.int32, device="cuda")
+        counts = self._buf("counts", nslot + 1, torch.int64)
+        counts.zero_()
+        drift = counts[nslot:].view(torch.int32)[:1]
+        stay = self._buf("stay", max(n, 1), torch.uint8) if self.fast else None
         err = N.HbError()
         st = N.stream_ptr()
+        pu = 1 if self.periodic_unsplit else 0
         N.check(self.lib.hb_halo_select(n, N.ptr(fields["pos"]), N.ptr(fields["ghost"]), g,
-                                        float(self.box.side_length), self.w, self.rank, 0,
+                                        float(self.box.side_length), self.w, self.rank, pu, 0,
                                         N.ptr(counts), N.ptr(counts), None, None, N.ptr(drift),
-                                        st, C.byref(err)), err)
-        ch = counts.cpu().numpy()
-        if int(drift.item()):
+                                        N.ptr(stay), st, C.byref(err)), err)
+        ch_all = counts.cpu().numpy()
+        ch = ch_all[:nslot]
+        if int(ch_all[nslot]) & 0xFFFFFFFF:
             raise DriftError("particle crossed more than one domain in one PM step")
         offs = np.concatenate([[0], np.cumsum(ch)]).astype(np.int64)
         m = int(offs[-1])
-        rows = torch.empty(max(m, 1), dtype=torch.int64, device="cuda")
-        slots = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
-        fill = torch.from_numpy(offs[:-1].copy()).cuda()
+        rows = self._buf("rows", max(m, 1), torch.int64)
+        slots = self._buf("slots", max(m, 1), torch.int32)
+        fill = self._buf("fill", nslot, torch.int64)
+        fill.copy_(torch.from_numpy(offs[:-1].copy()))
         N.check(self.lib.hb_halo_select(n, N.ptr(fields["pos"]), N.ptr(fields["ghost"]), g,
-                                        float(self.box.side_length), self.w, self.rank, 1,
+                                        float(self.box.side_length), self.w, self.rank, pu, 1,
                                         N.ptr(counts), N.ptr(fill), N.ptr(rows), N.ptr(slots),
-                                        N.ptr(drift), st, C.byref(err)), err)
-        send = torch.empty(max(m, 1) * self.rec, dtype=torch.uint8, device="cuda")
+                                        N.ptr(drift), N.ptr(stay), st, C.byref(err)), err)
+        send = self._buf("send", max(m, 1) * self.rec, torch.uint8)
         N.check(self.lib.hb_halo_pack(m, N.ptr(rows), N.ptr(slots), N.ptr(fields["pos"]),
                                       N.ptr(fields["vel"]), N.ptr(fields["mass"]),
                                       N.ptr(fields["smoothing"]), N.ptr(fields["internal_energy"]),
@@ -137,35 +173,49 @@ class HaloExchange:
                                       N.ptr(fields["global_id"]), g, float(self.box.side_length),
                                       self.rank, N.ptr(send), st, C.byref(err)), err)
         per_dest = ch.reshape(self.world, 28).sum(axis=1) * self.rec
-        return send[:m * self.rec], [int(x) for x in per_dest]
+        return send[:m * self.rec], [int(x) for x in per_dest], (stay[:n] if stay is not None
+                                                                  else None)
 
-    def unpack(self, recv) -> tuple[dict, int]:
-        """Records -> new rank field set (owned by gid, then ghosts by (gid, shift))."""
+    def unpack(self, recv, keep: dict | None = None) -> tuple[dict, int]:
+        """Records -> new rank field set.  Reference order (keep=None): owned by
+        gid then ghosts by (gid, shift).  Fast path: the staying owned rows
+        `keep` first (their current order), then arrivals sorted the same way."""
         import torch
         m = int(recv.numel()) // self.rec
-        out = empty_fields(max(m, 1))
-        ws = N.workspace(self.lib.hb_halo_unpack_workspace(m))
+        n0 = int(keep[1].shape[0]) if keep is not None else 0
+        out = self._field_set(max(n0 + m, 1))
+        if keep is not None:  # staying owned rows, current order
+            src, idx = keep
+            for f in out:
+                torch.index_select(src[f], 0, idx, out=out[f][:n0])
+        ws = self._buf("unpack_ws", int(self.lib.hb_halo_unpack_workspace(m)), torch.uint8)
         err = N.HbError()
         st = N.stream_ptr()
-        N.check(self.lib.hb_halo_unpack(m, N.ptr(recv), 1, 0, *[N.ptr(out[f]) for f in (
+        N.check(self.lib.hb_halo_unpack(m, N.ptr(recv), self.key_bits, n0, *[N.ptr(out[f]) for f in (
             "pos", "vel", "mass", "smoothing", "internal_energy", "density", "species", "ghost",
             "image_shift", "global_id", "ghost_src")], N.ptr(ws), C.c_size_t(ws.numel()), st,
             C.byref(err)), err)
-        out = {k: v[:m] for k, v in out.items()}
+        out = {k: v[:n0 + m] for k, v in out.items()}
         n_owned = int((out["ghost"] == 0).sum().item())
-        N.check(self.lib.hb_halo_resolve_sources(n_owned, m, N.ptr(out["global_id"]),
-                                                 N.ptr(out["ghost_src"]), st, C.byref(err)), err)
+        if keep is None:
+            N.check(self.lib.hb_halo_resolve_sources(n_owned, m, N.ptr(out["global_id"]),
+                                                     N.ptr(out["ghost_src"]), st, C.byref(err)),
+                    err)
         return out, n_owned
 
     def exchange(self, fields: dict) -> tuple[dict, int]:
-        send, counts = self.pack(fields)
+        import torch
+        send, counts, stay = self.pack(fields)
         if self.transport is not None:
             recv, _ = self.transport(send, counts)
         elif self.world == 1:
             recv = send
         else:
             recv, _ = alltoallv_bytes(send, counts, self.group)
-        return self.unpack(recv)
+        keep = None
+        if stay is not None:
+            keep = (fields, torch.nonzero(stay).squeeze(1))
+        return self.unpack(recv, keep)
 
 
 class DistributedRank:
@@ -174,7 +224,8 @@ class DistributedRank:
     def __init__(self, owned: ParticleSet, box: BoxGeometry, rank: int, world: int, r_s: float,
                  r_cut: float, softening: float, h_max: float, h_min: float,
                  max_leaf_size: int = 256, cm_bin_width: float = 0.0, group=None,
-                 transport=None, eos_gamma: float = 5.0 / 3.0):
+                 transport=None, eos_gamma: float = 5.0 / 3.0, periodic_unsplit: bool = True,
+                 n_global: int | None = None):
         import torch
         self.box, self.rank, self.world = box, rank, world
         self.grid = rank_grid_for(world)
@@ -183,11 +234,17 @@ class DistributedRank:
         lo, hi = domain_bounds(box, self.grid, rank)
         self.lo, self.hi = lo, hi
         bin_width = max(cm_bin_width, reach * (1 + 1e-9))
+        mlo, mhi = lo - self.w, hi + self.w
+        if periodic_unsplit:  # unsplit axes: full periodic box, no self-image shell
+            for d in range(3):
+                if self.grid[d] == 1:
+                    mlo[d], mhi[d] = 0.0, box.side_length
         self.cfg = StepConfig(box=box, bin_width=bin_width, max_leaf_size=max_leaf_size,
                               r_s=r_s, r_cut=r_cut, softening=softening, eos_gamma=eos_gamma,
-                              bounds_lo=lo - self.w, bounds_hi=hi + self.w)
+                              bounds_lo=mlo, bounds_hi=mhi)
         self.h_range = (h_min, h_max)
-        self.halo = HaloExchange(box, self.grid, self.w, rank, world, group, transport)
+        self.halo = HaloExchange(box, self.grid, self.w, rank, world, group, transport,
+                                 periodic_unsplit=periodic_unsplit, n_global=n_global)
         fields = {}
         for f in STEP_FIELDS:
             arr = np.ascontiguousarray(getattr(owned, f))
@@ -212,10 +269,25 @@ class DistributedRank:
     def step(self, timing: bool = False):
         """Exchange + force evaluation; returns device outputs (leaf order of
         the rank set) and the reordered fields."""
+        import torch
+        if timing:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         self.exchange()
+        if timing:
+            e1.record()
         out = self.engine.step(timing=timing)
+        if timing:
+            torch.cuda.synchronize()
+            self.engine.last["ms_phase"]["exchange"] = e0.elapsed_time(e1)
         fields = self.engine.fields()
         # keep only owned rows (leaf order) as next step's owned set
-        own = fields["ghost"] == 0
-        self.owned_fields = {k: v[own].contiguous() for k, v in fields.items()}
+        idx = torch.nonzero(fields["ghost"] == 0).squeeze(1)
+        n_own = int(idx.shape[0])
+        store = getattr(self, "_owned_store", None)
+        if store is None or store["pos"].shape[0] < n_own:
+            store = empty_fields(int(n_own * 1.2) + 1024)
+            self._owned_store = store
+        self.owned_fields = {k: torch.index_select(v, 0, idx, out=store[k][:n_own])
+                             for k, v in fields.items()}
         return out, fields

@@ -108,31 +108,37 @@ class ResidentRank:
         self.set_fields(fields, h_range)
 
     def set_fields(self, fields: dict, h_range: tuple) -> None:
-        """Adopt a device field set (n rows); (re)size outputs and buffers."""
+        """Adopt a device field set (n rows); outputs and the reorder buffer are
+        capacity-backed views (no allocation while n stays within capacity)."""
         torch = N.torch_cuda()
         n = int(fields["pos"].shape[0])
         self.h_min, self.h_max = float(h_range[0]), float(h_range[1])
-        self.buf[0] = fields
-        self.cur = 0
-        if self.buf[1] is None or int(self.buf[1]["pos"].shape[0]) != n:
-            self.buf[1] = {k: torch.empty_like(v) for k, v in fields.items()}
-        if self.out.get("perm") is None or int(self.out["perm"].shape[0]) != max(n, 1):
-            m = max(n, 1)
+        m = max(n, 1)
+        cap = getattr(self, "_cap", 0)
+        if m > cap:
+            cap = int(m * 1.1) + 1024
             f64 = torch.float64
-            self.out = {
-                "perm": torch.empty(m, dtype=torch.int64, device="cuda"),
-                "ncount": torch.zeros(m, dtype=f64, device="cuda"),
-                "grav": torch.zeros((m, 3), dtype=f64, device="cuda"),
-                "hydro": torch.zeros((m, 5), dtype=f64, device="cuda"),
-                "crk_moments": torch.zeros((m, 10), dtype=f64, device="cuda"),
-                "crk_A": torch.zeros(m, dtype=f64, device="cuda"),
-                "crk_B": torch.zeros((m, 3), dtype=f64, device="cuda"),
-                "crk_fallback": torch.zeros(m, dtype=torch.uint8, device="cuda"),
+            self._buf1_store = {k: torch.empty((cap,) + tuple(v.shape[1:]), dtype=v.dtype,
+                                               device="cuda") for k, v in fields.items()}
+            self._out_store = {
+                "perm": torch.empty(cap, dtype=torch.int64, device="cuda"),
+                "ncount": torch.zeros(cap, dtype=f64, device="cuda"),
+                "grav": torch.zeros((cap, 3), dtype=f64, device="cuda"),
+                "hydro": torch.zeros((cap, 5), dtype=f64, device="cuda"),
+                "crk_moments": torch.zeros((cap, 10), dtype=f64, device="cuda"),
+                "crk_A": torch.zeros(cap, dtype=f64, device="cuda"),
+                "crk_B": torch.zeros((cap, 3), dtype=f64, device="cuda"),
+                "crk_fallback": torch.zeros(cap, dtype=torch.uint8, device="cuda"),
             }
+            self._cap = cap
+        self.buf[0] = fields
+        self.buf[1] = {k: v[:n] for k, v in self._buf1_store.items()}
+        self.cur = 0
+        self.out = {k: v[:m] for k, v in self._out_store.items()}
         self.n = n
         nbins = int(np.prod(self.nb))
-        cap = int(self.lib.hb_leaf_capacity(self.n, nbins, self.cfg.max_leaf_size))
-        self.list_capacity = max(self.list_capacity, 1024, cap * 64)
+        leaf_cap = int(self.lib.hb_leaf_capacity(self.n, nbins, self.cfg.max_leaf_size))
+        self.list_capacity = max(self.list_capacity, 1024, leaf_cap * 64)
 
     @staticmethod
     def _alloc(p: ParticleSet) -> dict:
@@ -141,10 +147,10 @@ class ResidentRank:
                 if name in STEP_FIELDS}
 
     def _workspace(self):
-        key = (self.n, self.list_capacity)
+        key = (self._cap, self.list_capacity)
         if self._ws is None or self._ws_key != key:
             nb3 = (C.c_int64 * 3)(*[int(v) for v in self.nb])
-            sz = self.lib.hb_force_step_workspace(self.n, nb3, self.cfg.max_leaf_size,
+            sz = self.lib.hb_force_step_workspace(self._cap, nb3, self.cfg.max_leaf_size,
                                                   self.list_capacity)
             if self._ws is None or self._ws.numel() < sz:
                 self._ws = None

@@ -1,0 +1,51 @@
+"""Per-sub-phase wall time of the overload exchange under torchrun (debug aid)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from bench import _make_rank, make_workload
+    from paper_2510_03557_b200.distributed import alltoallv_bytes
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+    p, cfg, meta = make_workload(sys.argv[1] if len(sys.argv) > 1 else "c2")
+    rr = _make_rank(None, p, cfg, rank, world)
+    for _ in range(3):
+        rr.step()
+    torch.cuda.synchronize()
+    h = rr.halo
+    T = {}
+
+    def tick(name, t0):
+        torch.cuda.synchronize()
+        T[name] = T.get(name, 0.0) + (time.perf_counter() - t0) * 1e3
+        return time.perf_counter()
+
+    for _ in range(5):
+        t = time.perf_counter()
+        send, counts, stay = h.pack(rr.owned_fields)
+        t = tick("pack(select x2 + pack)", t)
+        recv, _ = alltoallv_bytes(send, counts)
+        t = tick("alltoallv", t)
+        idx = torch.nonzero(stay).squeeze(1)
+        keep = {k: v.index_select(0, idx) for k, v in rr.owned_fields.items()}
+        t = tick("keep gather", t)
+        new, n_owned = h.unpack(recv, keep)
+        t = tick("unpack", t)
+        rr.engine.set_fields(new, rr.h_range)
+        t = tick("set_fields", t)
+    if rank == 0:
+        print({k: round(v / 5, 3) for k, v in T.items()}, "send MB", send.numel() / 1e6,
+              "recv MB", recv.numel() / 1e6, "n", new["pos"].shape[0])
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
