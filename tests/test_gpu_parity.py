@@ -233,7 +233,7 @@ def test_gpu_resident_force_step(golden, oracle):
     assert_fp32_close(out["hydro"][own, :4], ref_h[own], absh[own, :4], what="resident hydro")
 
 
-@pytest.mark.parametrize("sigma", [0.05, 1.0])
+@pytest.mark.parametrize("sigma", [0.05, 1.0, 2.5])
 def test_gpu_force_step_vs_oracle_c1(oracle, sigma):
     """hb_force_step at 2x32^3 (config C1, near-uniform and shell-crossing
     Zel'dovich ICs) against the oracle's ordered evaluation of the same step:
