@@ -79,6 +79,7 @@ typedef struct HbMeshArgs {
   int64_t* n_leaves_dev;     /* device scalar                                   */
   int64_t* n_leaves_host;    /* host scalar or NULL (NULL: no host sync)        */
   int64_t* max_bin_leaves_host; /* host scalar or NULL                          */
+  int64_t* max_bin_count_host;  /* host scalar or NULL: most particles in a bin  */
 } HbMeshArgs;
 
 size_t hb_build_mesh_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size);
@@ -231,6 +232,9 @@ typedef struct HbStepArgs {
   double r_s, r_cut, softening, eos_gamma, visc_alpha, visc_beta;
   int32_t passes;    /* HB_PASS_* mask                                        */
   int32_t timing;    /* 1: fill ms_phase with per-phase device times          */
+  int32_t gravity_mode; /* 0 auto (= 3 when every bin fits the tiler), 1 leaf tiles +
+                           leaf list, 2 bin half-warp tiles (k_gravity2), 3 bin tiles +
+                           27-bin stencil (k_gravity)                             */
   int32_t ghost_density; /* 1: ghost-only leaves are density receivers too, so
                             ghost rows near the rank face get fresh rho, P, c_s
                             (multi-rank; fixes SURVEY.md finding 4); gravity,

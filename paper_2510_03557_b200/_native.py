@@ -37,7 +37,7 @@ class HbMeshArgs(C.Structure):
                 ("nb", C.c_int64 * 3), ("max_leaf_size", C.c_int64), ("leaf_cap", C.c_int64),
                 ("perm", P), ("leaf_start", P), ("leaf_end", P), ("leaf_lo", P), ("leaf_hi", P),
                 ("leaf_ghost_only", P), ("leaf_bin", P), ("bin_ptr", P), ("n_leaves_dev", P),
-                ("n_leaves_host", P), ("max_bin_leaves_host", P)]
+                ("n_leaves_host", P), ("max_bin_leaves_host", P), ("max_bin_count_host", P)]
 
 
 class HbListArgs(C.Structure):

@@ -48,4 +48,24 @@ int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int
              HbError* err);
 int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err);
 
+// bin-level short-range gravity (hb_grav2.cu)
+struct GravBinArgs {
+  int64_t n, nbins;
+  const int64_t *bin_ptr, *leaf_start, *leaf_end;
+  ListGeom geom;
+  const double* state;
+  const int8_t* pshift;
+  double L, r_s, r_cut, eps;
+  double* out;
+  unsigned long long* err_key;
+  int* overflow_host;
+  bool half_warp;
+};
+int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);
+// bins as segments: row range per bin and the 27-bin stencil as a receiver CSR
+int bin_stencil_csr(int64_t nbins, const int64_t* bin_ptr, const int64_t* leaf_start,
+                    const int64_t* leaf_end, const ListGeom& g, int64_t* seg_s, int64_t* seg_e,
+                    int64_t* st_ptr, int32_t* st_src, int32_t* st_code, cudaStream_t st,
+                    HbError* err);
+
 }  // namespace hb

@@ -291,6 +291,7 @@ struct MeshWs {
   double *g_key, *g_tkey;
   uint32_t *g_idx, *g_tidx;
   unsigned long long* maxbl;
+  unsigned long long* maxbc;
 };
 
 static void carve_mesh(Arena& ws, int64_t n, int64_t nbins, MeshWs& m) {
@@ -303,6 +304,7 @@ static void carve_mesh(Arena& ws, int64_t n, int64_t nbins, MeshWs& m) {
   m.g_key = ws.take<double>(n); m.g_tkey = ws.take<double>(n);
   m.g_idx = ws.take<uint32_t>(n); m.g_tidx = ws.take<uint32_t>(n);
   m.maxbl = ws.take<unsigned long long>(1);
+  m.maxbc = ws.take<unsigned long long>(1);
 }
 
 static int bit_length(uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return b; }
@@ -330,6 +332,7 @@ int build_mesh(const HbMeshArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   for (int d = 0; d < 3; ++d) { g.lo[d] = a->lo[d]; g.width[d] = a->width[d]; g.nb[d] = a->nb[d]; }
   HB_CUDA_TRY(cudaMemsetAsync(m.bin_cnt, 0, nbins * sizeof(unsigned long long), st));
   HB_CUDA_TRY(cudaMemsetAsync(m.maxbl, 0, sizeof(unsigned long long), st));
+  HB_CUDA_TRY(cudaMemsetAsync(m.maxbc, 0, sizeof(unsigned long long), st));
   if (n > 0) {
     k_bin_keys<<<grid_for(n, 256), 256, 0, st>>>(n, a->pos, a->image_shift, g, m.bx, m.by, m.bz,
                                                   m.keys, m.vals, m.bin_cnt);
@@ -355,6 +358,8 @@ int build_mesh(const HbMeshArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                               cudaMemcpyDeviceToDevice, st));
   k_max_bin_leaves<<<grid_for(nbins, 256), 256, 0, st>>>(nbins, m.leaf_cnt, m.maxbl);
   HB_LAUNCH_CHECK();
+  k_max_bin_leaves<<<grid_for(nbins, 256), 256, 0, st>>>(nbins, m.bin_cnt64, m.maxbc);
+  HB_LAUNCH_CHECK();
   KdArgs k;
   k.bin_start = m.bin_start; k.leaf_off = a->bin_ptr; k.sorted_vals = m.vals;
   k.bx = m.bx; k.by = m.by; k.bz = m.bz; k.max_leaf = a->max_leaf_size;
@@ -367,14 +372,16 @@ int build_mesh(const HbMeshArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                                                          a->ghost, a->leaf_lo, a->leaf_hi,
                                                          a->leaf_ghost_only);
   HB_LAUNCH_CHECK();
-  if (a->n_leaves_host || a->max_bin_leaves_host) {
-    unsigned long long mbl = 0;
+  if (a->n_leaves_host || a->max_bin_leaves_host || a->max_bin_count_host) {
+    unsigned long long mbl = 0, mbc = 0;
     HB_CUDA_TRY(cudaMemcpyAsync(&mbl, m.maxbl, sizeof(mbl), cudaMemcpyDeviceToHost, st));
+    HB_CUDA_TRY(cudaMemcpyAsync(&mbc, m.maxbc, sizeof(mbc), cudaMemcpyDeviceToHost, st));
     int64_t nl = 0;
     HB_CUDA_TRY(cudaMemcpyAsync(&nl, a->n_leaves_dev, sizeof(nl), cudaMemcpyDeviceToHost, st));
     HB_CUDA_TRY(cudaStreamSynchronize(st));
     if (a->n_leaves_host) *a->n_leaves_host = nl;
     if (a->max_bin_leaves_host) *a->max_bin_leaves_host = (int64_t)mbl;
+    if (a->max_bin_count_host) *a->max_bin_count_host = (int64_t)mbc;
   }
   return HB_OK;
 }

@@ -23,7 +23,7 @@ namespace hb {
 
 constexpr int kTileBuildBlock = 256;
 constexpr int kTileBuildCap = 2048;  // selected members per leaf held in shared memory
-constexpr int kTileWarpCapBlock = 256;  // leaves up to this many go to the warp kernel
+constexpr int kTileWarpCapBlock = 512;  // leaves up to this many go to the warp kernel
 constexpr int kEvalWarps = 4;
 constexpr int kStage = 64;           // staged sources per warp
 
@@ -31,7 +31,8 @@ constexpr int kStage = 64;           // staged sources per warp
 
 // ---------------------------------------------------------------- tiling
 __global__ void k_tile_count(int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
-                             const double* state, int sel, int64_t* sel_cnt, int64_t* tile_cnt) {
+                             const double* state, int sel, int64_t* sel_cnt, int64_t* tile_cnt,
+                             int tile_max, int even) {
   int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (leaf >= n_leaves) return;
@@ -42,7 +43,7 @@ __global__ void k_tile_count(int64_t n_leaves, const int64_t* leaf_start, const 
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if (lane == 0) {
     sel_cnt[leaf] = c;
-    tile_cnt[leaf] = (c + kTileMax - 1) / kTileMax;
+    tile_cnt[leaf] = tiles_for(c, tile_max, even);
   }
 }
 
@@ -134,7 +135,7 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
       s_c[d][k] = (float)(v - org[d]);
     }
   }
-  int ntiles = (m_sel + kTileMax - 1) / kTileMax;
+  int ntiles = tiles_for(m_sel, T.tile_max, T.even);
   if (threadIdx.x == 0) { sp_sh = 1; stk_a[0] = 0; stk_m[0] = m_sel; stk_k[0] = ntiles; tile_j = 0; }
   __syncthreads();
   // 3. proportional median splits into ntiles tiles of <= 32 (DFS left-first)
@@ -226,8 +227,8 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
 // Same tiling as k_tile_build, one WARP per leaf (leaves with <= 256 selected
 // members -- the common case -- without block barriers); larger leaves are
 // left to k_tile_build (flagged by big != 0).
-constexpr int kTileWarpCap = 256;
-constexpr int kTileWarps = 8;
+constexpr int kTileWarpCap = 512;
+constexpr int kTileWarps = 4;
 __global__ void __launch_bounds__(kTileWarps * 32)
 k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
                   const double* state, const int8_t* pshift, double L, int sel, int nl) {
@@ -257,7 +258,7 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
   }
   __syncwarp();
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-  double v[8][3];
+  double v[kTileWarpCapBlock / 32][3];
   int nloc = 0;
   for (int k = lane; k < m_sel; k += 32, ++nloc) {
     int64_t r = row[k];
@@ -284,9 +285,9 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     for (int d = 0; d < 3; ++d) cc[d][k] = (float)(v[nloc][d] - org[d]);
   __syncwarp();
   // proportional median splits into ceil(m/32) tiles (DFS left-first)
-  int stk_a[16], stk_m[16], stk_k[16];  // warp-uniform stack in registers
+  int stk_a[24], stk_m[24], stk_k[24];  // warp-uniform stack
   int sp = 1, tile_j = 0;
-  stk_a[0] = 0; stk_m[0] = m_sel; stk_k[0] = (m_sel + kTileMax - 1) / kTileMax;
+  stk_a[0] = 0; stk_m[0] = m_sel; stk_k[0] = tiles_for(m_sel, T.tile_max, T.even);
   int64_t tbase = T.tile_ptr[leaf], so = T.sel_off[leaf];
   while (sp) {
     --sp;
@@ -328,8 +329,8 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
       tmp[a0 + rank] = a0 + k;
     }
     __syncwarp();
-    int32_t rr[8];
-    float c3[8][3];
+    int32_t rr[kTileWarpCapBlock / 32];
+    float c3[kTileWarpCapBlock / 32][3];
     nloc = 0;
     for (int k = lane; k < m; k += 32, ++nloc) {
       int src = tmp[a0 + k];
@@ -506,12 +507,6 @@ __global__ void k_sched_counters(int64_t n_pairs, const int64_t* pa, const int64
 // ---------------------------------------------------------------- the gather kernel
 
 
-__device__ __forceinline__ float box_gap2(float x, float y, float z, float4 lo, float4 hi) {
-  float gx = fmaxf(fmaxf(lo.x - x, x - hi.x), 0.0f);
-  float gy = fmaxf(fmaxf(lo.y - y, y - hi.y), 0.0f);
-  float gz = fmaxf(fmaxf(lo.z - z, z - hi.z), 0.0f);
-  return fmaf(gz, gz, fmaf(gy, gy, gx * gx));
-}
 
 // exact float64 separation of rows i, j for image code (hb/kernels.py:346-356)
 __device__ __forceinline__ double exact_r2(const EvalDev& a, int64_t i, int64_t j, int code) {
@@ -782,6 +777,7 @@ k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_
   };
   for (int64_t e = e0; e < e1; ++e) {
     int B = a.ent_src[e];
+    if (B < 0) continue;  // bin stencil: off-mesh / duplicate cell
     int code = a.ent_code[e] & 31;
     int sh0 = code / 9 - 1, sh1 = (code / 3) % 3 - 1, sh2 = code % 3 - 1;
     float D0 = (float)((oA[0] - T.origin[3 * B]) - (double)sh0 * a.L);
@@ -883,11 +879,12 @@ int gravity_table(double r_s, double r_cut, double eps, bool tvar, int nt, float
 }
 
 // ---------------------------------------------------------------- driver pieces
-int64_t tile_capacity(int64_t n, int64_t n_leaves) { return n / kTileMax + n_leaves + 1; }
+int64_t tile_capacity(int64_t n, int64_t n_leaves) { return n / 8 + 2 * n_leaves + 2; }
 
-void carve_tiling(Arena& ws, int64_t n, int64_t nl, Tiling& T) {
+void carve_tiling(Arena& ws, int64_t n, int64_t nl, Tiling& T, int tile_max, int even) {
   int64_t tc = tile_capacity(n, nl);
   T.n_leaves = nl; T.n_tiles_cap = tc;
+  T.tile_max = tile_max; T.even = even;
   T.sel_cnt = ws.take<int64_t>(nl + 1); T.sel_off = ws.take<int64_t>(nl + 1);
   T.tile_cnt = ws.take<int64_t>(nl + 1); T.tile_ptr = ws.take<int64_t>(nl + 1);
   T.tperm = ws.take<int32_t>(n + 1);
@@ -914,7 +911,7 @@ int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t
   }
   HB_CUDA_TRY(cudaMemsetAsync(T.overflow, 0, sizeof(int), st));
   k_tile_count<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, leaf_start, leaf_end, state, sel,
-                                                       T.sel_cnt, T.tile_cnt);
+                                                       T.sel_cnt, T.tile_cnt, T.tile_max, T.even);
   HB_LAUNCH_CHECK();
   {
     Arena s = ws;

@@ -180,10 +180,22 @@ template <> struct Pol<KID_CRK_INTERP> {
 
 constexpr int kTileMax = 32;
 
+// squared distance from a point to an axis-aligned box (0 inside)
+__device__ __forceinline__ float box_gap2(float x, float y, float z, float4 lo, float4 hi) {
+  float gx = fmaxf(fmaxf(lo.x - x, x - hi.x), 0.0f);
+  float gy = fmaxf(fmaxf(lo.y - y, y - hi.y), 0.0f);
+  float gz = fmaxf(fmaxf(lo.z - z, z - hi.z), 0.0f);
+  return fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+}
+
+
+
 // Per-leaf tiling of the selected particles (all, or gas only) into spatially
 // compact tiles of <= 32 (one warp each); internal order = tile order.
 struct Tiling {
   int64_t n_leaves, n_tiles_cap;
+  int tile_max = 32;    // members per tile
+  int even = 0;         // 1: even tile count per segment (half-warp tile pairs)
   int64_t* sel_cnt;     // (n_leaves+1)
   int64_t* sel_off;     // (n_leaves+1)
   int64_t* tile_cnt;    // (n_leaves+1)
@@ -223,7 +235,11 @@ struct EvalDev {
 
 // ---- internal driver pieces shared by hb_eval_pairs and hb_force_step ----
 int64_t tile_capacity(int64_t n, int64_t n_leaves);
-void carve_tiling(Arena& ws, int64_t n, int64_t n_leaves, Tiling& T);
+void carve_tiling(Arena& ws, int64_t n, int64_t n_leaves, Tiling& T, int tile_max = 32,
+                  int even = 0);
+__host__ __device__ inline int tiles_for(int m, int tile_max, int even) {
+  return even ? 2 * ((m + 2 * tile_max - 1) / (2 * tile_max)) : (m + tile_max - 1) / tile_max;
+}
 int build_tiling(Tiling& T, int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
                  const double* state, const int8_t* pshift, double L, int sel,
                  int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err);

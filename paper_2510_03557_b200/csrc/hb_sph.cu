@@ -72,6 +72,7 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
   float Rt = fminf(Rcap, 2.0f * hmax_t * 1.0001f);
   for (int64_t e = e0; e < e1; ++e) {
     int B = a.ent_src[e];
+    if (B < 0) continue;  // bin stencil: off-mesh / duplicate cell
     int cw = a.ent_code[e];
     int code = cw & 31;
     int sh0 = code / 9 - 1, sh1 = (code / 3) % 3 - 1, sh2 = code % 3 - 1;

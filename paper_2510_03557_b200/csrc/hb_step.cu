@@ -52,6 +52,20 @@ __global__ void k_eos(int64_t n, const double* rho, const double* u, double gamm
   st[i * NCOL + C_CS] = sqrt(fmax(gamma * gm1 * u[i], 0.0));
 }
 
+__global__ void k_zero_ghost_rows(int64_t n_leaves, const int64_t* leaf_start,
+                                  const int64_t* leaf_end, const uint8_t* ghost_only,
+                                  double* ncount, double* moments, double* hydro, double* grav) {
+  int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (leaf >= n_leaves || !ghost_only[leaf]) return;
+  for (int64_t r = leaf_start[leaf] + lane; r < leaf_end[leaf]; r += 32) {
+    if (ncount) ncount[r] = 0.0;
+    for (int c = 0; c < 10; ++c) moments[r * 10 + c] = 0.0;
+    for (int c = 0; c < 5; ++c) hydro[r * 5 + c] = 0.0;
+    for (int c = 0; c < 3; ++c) grav[r * 3 + c] = 0.0;
+  }
+}
+
 __global__ void k_gather_inverse(int64_t n, const int64_t* perm, int64_t* inv) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) inv[perm[k]] = k;
@@ -89,6 +103,8 @@ struct StepWs {
   int64_t* inv;
   float4* gtab;
   uint8_t* no_ghost;
+  int64_t *seg_s, *seg_e, *st_ptr;
+  int32_t *st_src, *st_code;
 };
 
 static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t lcap, StepWs& w) {
@@ -99,7 +115,7 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
   w.ghost_only = ws.take<uint8_t>(cap);
   w.ent_ptr = ws.take<int64_t>(cap + 1);
   w.ent_src = ws.take<int32_t>(lcap + 1); w.ent_code = ws.take<int32_t>(lcap + 1);
-  carve_tiling(ws, n, cap, w.Tg);
+  carve_tiling(ws, n, cap > nbins ? cap : nbins, w.Tg);
   carve_tiling(ws, n, cap, w.Ta);
   w.ntg = ws.take<int64_t>(1); w.nta = ws.take<int64_t>(1);
   w.state = ws.take<double>(n * NCOL + 1);
@@ -109,7 +125,12 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
   w.inv = ws.take<int64_t>(n + 1);
   w.gtab = ws.take<float4>(kGravTableMax);
   w.no_ghost = ws.take<uint8_t>(cap + 1);
+  w.seg_s = ws.take<int64_t>(nbins + 1); w.seg_e = ws.take<int64_t>(nbins + 1);
+  w.st_ptr = ws.take<int64_t>(nbins + 1);
+  w.st_src = ws.take<int32_t>(nbins * 27 + 1); w.st_code = ws.take<int32_t>(nbins * 27 + 1);
 }
+
+constexpr bool kGravityBinsDefault = true;
 
 struct PhaseTimer {
   bool on;
@@ -138,8 +159,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   m.perm = a->perm; m.leaf_start = w.leaf_start; m.leaf_end = w.leaf_end; m.leaf_lo = w.leaf_lo;
   m.leaf_hi = w.leaf_hi; m.leaf_ghost_only = w.ghost_only; m.leaf_bin = w.leaf_bin;
   m.bin_ptr = w.bin_ptr; m.n_leaves_dev = w.n_leaves_dev;
-  int64_t nl = 0;
+  int64_t nl = 0, max_bin_count = 0;
   m.n_leaves_host = &nl;
+  m.max_bin_count_host = &max_bin_count;
   ListArgsDev ld;
   if (ws.dry) {
     size_t mx = ws.used;
@@ -150,6 +172,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     Arena s3 = ws;
     build_tiling(w.Tg, cap, nullptr, nullptr, nullptr, nullptr, 0.0, 1, nullptr, s3, st, err);
     if (s3.used > mx) mx = s3.used;
+    GravBinArgs gb = {};
+    gb.n = n; gb.nbins = nbins; gb.half_warp = true;
+    Arena s4 = ws; gravity_bins(gb, s4, st, err); if (s4.used > mx) mx = s4.used;
     ws.used = mx;
     return HB_OK;
   }
@@ -210,15 +235,34 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                                                    a->eos_gamma, w.state);
   HB_LAUNCH_CHECK();
   w.Tg.n_leaves = nl; w.Ta.n_leaves = nl;
+  // gravity over bin segments (half-warp tiles) or leaf tiles; bins beyond the
+  // block tiler's capacity force the leaf path
+  bool use_leaf_gravity = a->gravity_mode == 1 || max_bin_count > 2048 ||
+                          (a->gravity_mode == 0 && !kGravityBinsDefault);
+  // SPH passes over bin segments too (fuller gas tiles); the leaf list stays the
+  // reference's product and the fallback when a bin outgrows the tiler
+  bool sph_bins = a->gravity_mode != 1 && max_bin_count <= 2048;
+  int64_t n_seg = sph_bins ? nbins : nl;
+  const int64_t* seg_s = w.leaf_start;
+  const int64_t* seg_e = w.leaf_end;
+  if (sph_bins) {
+    int rcb = bin_stencil_csr(nbins, w.bin_ptr, w.leaf_start, w.leaf_end, ld.g, w.seg_s, w.seg_e,
+                              w.st_ptr, w.st_src, w.st_code, st, err);
+    if (rcb) return rcb;
+    seg_s = w.seg_s;
+    seg_e = w.seg_e;
+  }
   {
     Arena s = ws;
-    int rc = build_tiling(w.Tg, nl, w.leaf_start, w.leaf_end, w.state, a->image_shift,
-                          a->side_length, 1, w.ntg, s, st, err);
+    int rc = build_tiling(w.Tg, n_seg, seg_s, seg_e, w.state, a->image_shift, a->side_length, 1,
+                          w.ntg, s, st, err);
     if (rc) return rc;
-    Arena s2 = ws;
-    rc = build_tiling(w.Ta, nl, w.leaf_start, w.leaf_end, w.state, a->image_shift,
-                      a->side_length, 0, w.nta, s2, st, err);
-    if (rc) return rc;
+    if ((a->passes & HB_PASS_GRAVITY) && use_leaf_gravity) {
+      Arena s2 = ws;
+      rc = build_tiling(w.Ta, nl, w.leaf_start, w.leaf_end, w.state, a->image_shift,
+                        a->side_length, 0, w.nta, s2, st, err);
+      if (rc) return rc;
+    }
   }
   HB_CUDA_TRY(cudaMemsetAsync(w.err_key, 0xff, sizeof(unsigned long long), st));
   EvalDev d = {};
@@ -248,12 +292,15 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   double rmin = fmax(fmin(a->reach, 2.0 * a->h_min), 1e-300);
   float band = (float)fmax(64.0 * 5.9604644775390625e-08 * wmax / rmin, 9.5367431640625e-07);
   SphArgs sa;
-  sa.T = &w.Tg; sa.n_tiles_dev = w.ntg; sa.ent_ptr = w.ent_ptr; sa.ent_src = w.ent_src;
-  sa.ent_code = w.ent_code; sa.P0 = w.P0; sa.P1 = w.P1; sa.P2 = w.P2; sa.state = w.state;
+  sa.T = &w.Tg; sa.n_tiles_dev = w.ntg;
+  sa.ent_ptr = sph_bins ? w.st_ptr : w.ent_ptr;
+  sa.ent_src = sph_bins ? w.st_src : w.ent_src;
+  sa.ent_code = sph_bins ? w.st_code : w.ent_code;
+  sa.P0 = w.P0; sa.P1 = w.P1; sa.P2 = w.P2; sa.state = w.state;
   sa.pshift = a->image_shift; sa.L = a->side_length; sa.reach = sph_reach; sa.band = band;
   sa.alpha = a->visc_alpha; sa.beta = a->visc_beta; sa.err_key = w.err_key;
   sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = a->crk_moments; sa.hydro = a->hydro;
-  sa.skip_leaf = a->ghost_density ? w.ghost_only : nullptr;
+  sa.skip_leaf = (a->ghost_density && !sph_bins) ? w.ghost_only : nullptr;
   d.skip_leaf = a->ghost_density ? w.ghost_only : nullptr;
   // 4. pass A: neighbour count + density (hb/hydro.py:223-227, 60-84), EOS (48-57)
   if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY)) {
@@ -293,30 +340,52 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     if (rc) return rc;
   }
   tm.mark(5);
-  // 7. short-range gravity (hb/kernels.py:152-163)
+  // 7. short-range gravity (hb/kernels.py:152-163): bin segments with half-warp
+  // tiles (hb_grav2.cu) unless a bin outgrows the block tiler, then leaf tiles
   if (a->passes & HB_PASS_GRAVITY) {
     HB_CUDA_TRY(cudaMemsetAsync(a->grav, 0, n * 3 * sizeof(double), st));
-    rc = pack_records(KID_GRAVITY, w.Ta, w.nta, w.state, a->image_shift, nullptr, 0,
-                      a->side_length, w.P0, w.P1, w.P2, st, err);
-    if (rc) return rc;
-    setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
-    static float4 host_tab[kGravTableMax];
-    float tab_scale = 0.f;
-    bool tvar = a->softening <= 0.05 * a->r_s;
-    int tab_last = gravity_table(a->r_s, a->r_cut, a->softening, tvar, kGravTableN, host_tab,
-                                 &tab_scale);
-    HB_CUDA_TRY(cudaMemcpyAsync(w.gtab, host_tab, sizeof(host_tab), cudaMemcpyHostToDevice, st));
-    rc = launch_gravity_fast(d, w.gtab, tab_scale, tab_last, tvar, w.Ta.n_tiles_cap, w.nta, st,
-                             err);
-    if (rc) return rc;
+    if (!use_leaf_gravity) {
+      GravBinArgs gb;
+      gb.n = n; gb.nbins = nbins; gb.bin_ptr = w.bin_ptr; gb.leaf_start = w.leaf_start;
+      gb.leaf_end = w.leaf_end; gb.geom = ld.g; gb.state = w.state; gb.pshift = a->image_shift;
+      gb.L = a->side_length; gb.r_s = a->r_s; gb.r_cut = a->r_cut; gb.eps = a->softening;
+      gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
+      gb.half_warp = a->gravity_mode == 2;
+      Arena s = ws;
+      rc = gravity_bins(gb, s, st, err);
+      if (rc) return rc;
+    } else {
+      rc = pack_records(KID_GRAVITY, w.Ta, w.nta, w.state, a->image_shift, nullptr, 0,
+                        a->side_length, w.P0, w.P1, w.P2, st, err);
+      if (rc) return rc;
+      setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
+      static float4 host_tab[kGravTableMax];
+      float tab_scale = 0.f;
+      bool tvar = a->softening <= 0.05 * a->r_s;
+      int tab_last = gravity_table(a->r_s, a->r_cut, a->softening, tvar, kGravTableN, host_tab,
+                                   &tab_scale);
+      HB_CUDA_TRY(cudaMemcpyAsync(w.gtab, host_tab, sizeof(host_tab), cudaMemcpyHostToDevice, st));
+      rc = launch_gravity_fast(d, w.gtab, tab_scale, tab_last, tvar, w.Ta.n_tiles_cap, w.nta, st,
+                               err);
+      if (rc) return rc;
+    }
   }
   tm.mark(6);
+  if (sph_bins || !use_leaf_gravity) {
+    // bin segments evaluate every row; the reference's receivers are the
+    // non-ghost-only leaves, so their ghost-only rows read zero (hb/cmtree.py:318)
+    k_zero_ghost_rows<<<grid_for(nl * 32, 256), 256, 0, st>>>(
+        nl, w.leaf_start, w.leaf_end, w.ghost_only, a->ghost_density ? nullptr : a->ncount,
+        a->crk_moments, a->hydro, a->grav);
+    HB_LAUNCH_CHECK();
+  }
   tm.mark(7);
   unsigned long long ek = 0;
   int ovf = 0, ovf2 = 0;
   HB_CUDA_TRY(cudaMemcpyAsync(&ek, w.err_key, sizeof(ek), cudaMemcpyDeviceToHost, st));
   HB_CUDA_TRY(cudaMemcpyAsync(&ovf, w.Tg.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-  HB_CUDA_TRY(cudaMemcpyAsync(&ovf2, w.Ta.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (use_leaf_gravity)
+    HB_CUDA_TRY(cudaMemcpyAsync(&ovf2, w.Ta.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
   HB_CUDA_TRY(cudaStreamSynchronize(st));
   if (tm.on) {
     for (int i = 0; i < 7; ++i) cudaEventElapsedTime(&a->ms_phase[i], tm.ev[i], tm.ev[i + 1]);

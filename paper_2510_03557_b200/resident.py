@@ -14,6 +14,7 @@ ParticleSet reordered in place, numpy outputs.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,7 +45,8 @@ class HbStepArgs(C.Structure):
                    ("r_s", C.c_double),
                    ("r_cut", C.c_double), ("softening", C.c_double), ("eos_gamma", C.c_double),
                    ("visc_alpha", C.c_double), ("visc_beta", C.c_double), ("passes", C.c_int32),
-                   ("timing", C.c_int32), ("ghost_density", C.c_int32),
+                   ("timing", C.c_int32), ("gravity_mode", C.c_int32),
+                   ("ghost_density", C.c_int32),
                    ("list_capacity", C.c_int64),
                    ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
                    ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
@@ -184,6 +186,7 @@ class ResidentRank:
         a.passes = int(passes)
         a.timing = 1 if timing else 0
         a.ghost_density = 1 if self.ghost_density else 0
+        a.gravity_mode = int(os.environ.get("HB_GRAVITY_MODE", "0"))
         for k in ("perm", "ncount", "grav", "hydro", "crk_moments", "crk_A", "crk_B",
                   "crk_fallback"):
             setattr(a, k, N.ptr(self.out[k]))
