@@ -240,6 +240,13 @@ typedef struct HbStepArgs {
                             (multi-rank; fixes SURVEY.md finding 4); gravity,
                             CRK and hydro still skip ghost-only receivers     */
   int64_t list_capacity; /* entries the workspace was sized for              */
+  /* optional cudaEvent_t handles (void*, NULL = unused) for overlapping host
+     copies with the step: the step waits on fields_ready before it first reads
+     any input field other than pos / image_shift / ghost (the mesh build only
+     needs those), and records sph_done once ncount, density, CRK and hydro
+     outputs are final (gravity still running) */
+  void* fields_ready_event;
+  void* sph_done_event;
   /* outputs (device, leaf order) */
   int64_t* perm;        /* (n) row k = input row perm[k]                    */
   double* ncount;       /* (n)                                                */

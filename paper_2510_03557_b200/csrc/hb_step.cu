@@ -190,6 +190,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     if (rc) return rc;
   }
   a->n_leaves = nl;
+  if (a->fields_ready_event)
+    HB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a->fields_ready_event, 0));
   {
     unsigned g3 = grid_for(n * 3, 256), g1 = grid_for(n, 256);
     k_gather<double><<<g3, 256, 0, st>>>(n, 3, a->perm, a->pos_in, a->pos);
@@ -339,6 +341,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                       a->crk_fallback, st, err);
     if (rc) return rc;
   }
+  if (a->sph_done_event) HB_CUDA_TRY(cudaEventRecord((cudaEvent_t)a->sph_done_event, st));
   tm.mark(5);
   // 7. short-range gravity (hb/kernels.py:152-163): bin segments with half-warp
   // tiles (hb_grav2.cu) unless a bin outgrows the block tiler, then leaf tiles

@@ -47,7 +47,8 @@ class HbStepArgs(C.Structure):
                    ("visc_alpha", C.c_double), ("visc_beta", C.c_double), ("passes", C.c_int32),
                    ("timing", C.c_int32), ("gravity_mode", C.c_int32),
                    ("ghost_density", C.c_int32),
-                   ("list_capacity", C.c_int64),
+                   ("list_capacity", C.c_int64), ("fields_ready_event", P),
+                   ("sph_done_event", P),
                    ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
                    ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
@@ -164,8 +165,11 @@ class ResidentRank:
         """Current (leaf-ordered after a step) device fields."""
         return self.buf[self.cur]
 
-    def step(self, passes: int = PASS_ALL, timing: bool = False) -> dict:
-        """One force evaluation; returns the device outputs (leaf order)."""
+    def step(self, passes: int = PASS_ALL, timing: bool = False, fields_ready=None,
+             sph_done=None) -> dict:
+        """One force evaluation; returns the device outputs (leaf order).
+        fields_ready / sph_done: optional torch.cuda.Event for copy overlap
+        (see HbStepArgs in include/hb.h)."""
         cfg = self.cfg
         src, dst = self.buf[self.cur], self.buf[1 - self.cur]
         a = HbStepArgs()
@@ -187,6 +191,8 @@ class ResidentRank:
         a.timing = 1 if timing else 0
         a.ghost_density = 1 if self.ghost_density else 0
         a.gravity_mode = int(os.environ.get("HB_GRAVITY_MODE", "0"))
+        a.fields_ready_event = P(fields_ready.cuda_event) if fields_ready is not None else P(0)
+        a.sph_done_event = P(sph_done.cuda_event) if sph_done is not None else P(0)
         for k in ("perm", "ncount", "grav", "hydro", "crk_moments", "crk_A", "crk_B",
                   "crk_fallback"):
             setattr(a, k, N.ptr(self.out[k]))
@@ -209,6 +215,59 @@ class ResidentRank:
         self.last = {"n_leaves": int(a.n_leaves), "n_entries": int(a.n_entries),
                      "ms_phase": dict(zip(PHASES, list(a.ms_phase))) if timing else None}
         return self.out
+
+
+SPH_OUTPUTS = ("ncount", "crk_A", "crk_B", "hydro")
+
+
+class HostStepper:
+    """End-to-end force evaluation from pinned host arrays (the e2e path).
+
+    Per call: H2D of the 11 input fields (positions/shift/ghost first, the
+    rest on a second copy stream while the mesh build runs), the step, and
+    D2H of the results -- the SPH outputs while gravity is still running, the
+    gravity output, permutation and density after.  Copies of one call overlap
+    that call's own compute; nothing is carried between calls."""
+
+    FIRST = ("pos", "image_shift", "ghost")
+
+    def __init__(self, rank: "ResidentRank", pinned_in: dict, pinned_out: dict):
+        torch = N.torch_cuda()
+        self.rank, self.pin_in, self.pin_out = rank, pinned_in, pinned_out
+        self.s_in = torch.cuda.Stream()
+        self.s_out = torch.cuda.Stream()
+        self.ev_first = torch.cuda.Event()
+        self.ev_fields = torch.cuda.Event()
+        self.ev_sph = torch.cuda.Event()
+        self.ev_done = torch.cuda.Event()
+
+    def __call__(self):
+        torch = N.torch_cuda()
+        rk = self.rank
+        dst = rk.buf[rk.cur]
+        main = torch.cuda.current_stream()
+        self.s_in.wait_stream(main)   # previous call's compute may still read dst
+        with torch.cuda.stream(self.s_in):
+            for f in self.FIRST:
+                dst[f].copy_(self.pin_in[f], non_blocking=True)
+            self.ev_first.record(self.s_in)
+            for f in STEP_FIELDS:
+                if f not in self.FIRST:
+                    dst[f].copy_(self.pin_in[f], non_blocking=True)
+            self.ev_fields.record(self.s_in)
+        main.wait_event(self.ev_first)
+        out = rk.step(PASS_ALL, fields_ready=self.ev_fields, sph_done=self.ev_sph)
+        self.ev_done.record(main)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.ev_sph)
+            for k in SPH_OUTPUTS:
+                self.pin_out[k].copy_(out[k], non_blocking=True)
+            self.pin_out["density"].copy_(rk.fields()["density"], non_blocking=True)
+            self.s_out.wait_event(self.ev_done)
+            for k in ("grav", "perm"):
+                self.pin_out[k].copy_(out[k], non_blocking=True)
+        main.wait_stream(self.s_out)
+        return self.pin_out
 
 
 def force_step(particles: ParticleSet, cfg: StepConfig, passes: int = PASS_ALL) -> dict:
