@@ -274,7 +274,9 @@ int hb_force_step(HbStepArgs* args, void* ws, size_t ws_bytes, void* stream, HbE
  * to its (new) owner; DriftError flag for > 1 domain hop.  periodic_unsplit:
  * axes with g = 1 stay periodic in the rank mesh (no self-image ghosts there).
  * stay != NULL: rows that remain owned here are flagged (mode 0) and not
- * emitted, so only shell ghosts and migrants cross the exchange.  Records are
+ * emitted, so only shell ghosts and migrants cross the exchange; their number
+ * is accumulated into counts[n_ranks * 28 + 1] (counts has n_ranks*28 + 2
+ * entries: slots, drift word, staying rows).  Records are
  * hb_halo_record_bytes() wide; slots = dest * 28 + code (27 = owned).
  * hb_halo_select: mode 0 counts per slot, mode 1 emits rows/slots at `fill`
  * offsets.  hb_halo_unpack orders owned rows by global_id then ghosts by
@@ -300,6 +302,11 @@ int hb_halo_unpack(int64_t m, const void* recs, int32_t key_bits, int64_t row0, 
                    void* stream, HbError* err);
 int hb_halo_resolve_sources(int64_t n_owned, int64_t m, const int64_t* global_id,
                             int64_t* ghost_src, void* stream, HbError* err);
+/* Row indices of the nonzero flags in row order (a device compaction whose
+ * size the caller already knows -- no host sync). */
+size_t hb_flag_indices_workspace(int64_t n);
+int hb_flag_indices(int64_t n, const uint8_t* flags, int64_t* idx, void* ws, size_t ws_bytes,
+                    void* stream, HbError* err);
 
 #ifdef __cplusplus
 }

@@ -93,6 +93,9 @@ def lib():
             lb.hb_halo_unpack.argtypes = [C.c_int64, P, C.c_int32, C.c_int64] + [P] * 11 + [
                 P, C.c_size_t, P, P]
             lb.hb_halo_resolve_sources.argtypes = [C.c_int64, C.c_int64, P, P, P, P]
+            lb.hb_flag_indices_workspace.restype = C.c_size_t
+            lb.hb_flag_indices_workspace.argtypes = [C.c_int64]
+            lb.hb_flag_indices.argtypes = [C.c_int64, P, P, P, C.c_size_t, P, P]
             lb.hb_crk_solve.argtypes = [C.c_int64, P, C.c_int64, P, C.c_double, P, P, P, P, P]
             _lib = lb
         return _lib
@@ -104,7 +107,8 @@ EXPORTS = ("hb_abi_version", "hb_launch_count", "hb_device_query", "hb_build_mes
            "hb_assemble_lists_workspace", "hb_assemble_lists", "hb_eval_pairs_workspace",
            "hb_eval_pairs", "hb_crk_solve", "hb_force_step_workspace", "hb_force_step",
            "hb_halo_record_bytes", "hb_halo_select", "hb_halo_pack", "hb_halo_unpack_workspace",
-           "hb_halo_unpack", "hb_halo_resolve_sources")
+           "hb_halo_unpack", "hb_halo_resolve_sources", "hb_flag_indices_workspace",
+           "hb_flag_indices")
 
 
 def torch_cuda():

@@ -89,9 +89,16 @@ __global__ void k_halo_select(int64_t n, const double* pos, const uint8_t* ghost
     own = owner_of(G, p);
     own_slot = own * 28 + 27;
   }
-  // stay != null: particles this rank keeps owning are flagged, not exchanged
+  // stay != null: particles this rank keeps owning are flagged, not exchanged;
+  // their number goes to counts[n_ranks * 28 + 1]
   bool emit_owned = live && !(stay && own == self);
-  if (stay && i < n && mode == 0) stay[i] = (live && own == self) ? 1 : 0;
+  if (stay && mode == 0) {
+    bool st = live && own == self;
+    if (i < n) stay[i] = st ? 1 : 0;
+    unsigned sm = __ballot_sync(0xffffffffu, st);
+    if ((threadIdx.x & 31) == 0 && sm)
+      atomicAdd(&counts[G.g[0] * G.g[1] * G.g[2] * 28 + 1], (unsigned long long)__popc(sm));
+  }
   // owned copies: one per particle, nearly all to the same slot -> warp-aggregated
   {
     unsigned act = __ballot_sync(0xffffffffu, emit_owned);
@@ -218,9 +225,45 @@ __global__ void k_halo_src_lookup(int64_t n_owned, int64_t m, const int64_t* gid
   ghost_src[k] = (lo < n_owned && gid[lo] == key) ? lo : -1;
 }
 
+__global__ void k_flag_scan_scatter(int64_t n, const uint8_t* flags, const int64_t* pos,
+                                    int64_t* idx) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flags[i]) idx[pos[i]] = i;
+}
+__global__ void k_flags_to_i64(int64_t n, const uint8_t* flags, int64_t* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = flags[i] ? 1 : 0;
+}
+
 }  // namespace hb
 
 using namespace hb;
+
+extern "C" size_t hb_flag_indices_workspace(int64_t n) {
+  Arena ws;
+  ws.dry = true;
+  ws.take<int64_t>(n + 1);
+  exclusive_scan_i64(nullptr, nullptr, n, nullptr, ws, nullptr, nullptr);
+  return ws.used + 1024;
+}
+
+extern "C" int hb_flag_indices(int64_t n, const uint8_t* flags, int64_t* idx, void* wsp,
+                               size_t ws_bytes, void* stream, HbError* err) {
+  if (err) *err = HbError{};
+  if (n <= 0) return HB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena ws;
+  ws.base = (char*)wsp; ws.cap = ws_bytes;
+  int64_t* pos = ws.take<int64_t>(n + 1);
+  if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (flag indices)");
+  k_flags_to_i64<<<grid_for(n, 256), 256, 0, st>>>(n, flags, pos);
+  HB_LAUNCH_CHECK();
+  int rc = exclusive_scan_i64(pos, pos, n, nullptr, ws, st, err);
+  if (rc) return rc;
+  k_flag_scan_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, flags, pos, idx);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
 
 extern "C" int64_t hb_halo_record_bytes(void) { return (int64_t)sizeof(HaloRec); }
 

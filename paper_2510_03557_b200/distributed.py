@@ -17,10 +17,10 @@ hb/domain.py:88-189) with ONE all-to-all of fixed-width records:
                                  so ghost rows near the face carry fresh rho,
                                  P, c_s (SURVEY.md finding 4)
 
-The overload width is max(1.25 reach, reach + 2 h_max): the reference's
-1.25 x reach (hb/driver.py:135-145) widened so every ghost within reach of an
-owned particle has its whole density neighbourhood on the rank.  Results for
-owned rows equal the single-domain evaluation within FP32 tolerance.
+The overload width is max(r_cut, 4 h_max) (overload_width()): every ghost
+within 2 h_max of an owned particle has its whole density neighbourhood on the
+rank, so its rho, P, c_s are fresh.  Results for owned rows equal the
+single-domain evaluation within FP32 tolerance.
 """
 from __future__ import annotations
 
@@ -59,9 +59,13 @@ def domain_bounds(box: BoxGeometry, grid, rank: int):
     return lo, hi
 
 
-def overload_width(r_cut: float, h_max: float) -> float:
-    reach = max(r_cut, 2.0 * h_max)
-    return max(1.25 * reach, reach + 2.0 * h_max)
+def overload_width(r_cut: float, h_max: float, headroom: float = 1.001) -> float:
+    """Smallest valid shell for one evaluation: gravity needs sources within
+    r_cut; hydro on an owned particle needs rho, P, c_s of ghosts within
+    2 h_max, whose own densities need neighbours within a further 2 h_max.
+    (The reference pads 1.25 x reach, hb/driver.py:135-145, for h growth
+    between PM-step refreshes; this engine refreshes every evaluation.)"""
+    return headroom * max(r_cut, 4.0 * h_max)
 
 
 def alltoallv_bytes(send, send_counts: list, group=None):
@@ -135,14 +139,15 @@ class HaloExchange:
         return self.periodic_unsplit and all(g <= 2 for g in self.grid)
 
     def pack(self, fields: dict):
-        """Select + pack; returns (send bytes, per-dest byte counts, stay mask or None)."""
+        """Select + pack.  Returns (send bytes, slot counts (world, 28) numpy,
+        stay flags or None, number of staying rows).  One host sync (counts)."""
         import torch
         n = int(fields["pos"].shape[0])
         nslot = self.world * 28
         g = (C.c_int32 * 3)(*self.grid)
-        counts = self._buf("counts", nslot + 1, torch.int64)
+        counts = self._buf("counts", nslot + 2, torch.int64)
         counts.zero_()
-        drift = counts[nslot:].view(torch.int32)[:1]
+        drift = counts[nslot:nslot + 1].view(torch.int32)[:1]
         stay = self._buf("stay", max(n, 1), torch.uint8) if self.fast else None
         err = N.HbError()
         st = N.stream_ptr()
@@ -155,12 +160,13 @@ class HaloExchange:
         ch = ch_all[:nslot]
         if int(ch_all[nslot]) & 0xFFFFFFFF:
             raise DriftError("particle crossed more than one domain in one PM step")
+        n_stay = int(ch_all[nslot + 1])
         offs = np.concatenate([[0], np.cumsum(ch)]).astype(np.int64)
         m = int(offs[-1])
         rows = self._buf("rows", max(m, 1), torch.int64)
         slots = self._buf("slots", max(m, 1), torch.int32)
         fill = self._buf("fill", nslot, torch.int64)
-        fill.copy_(torch.from_numpy(offs[:-1].copy()))
+        fill.copy_(torch.from_numpy(offs[:-1].copy()), non_blocking=False)
         N.check(self.lib.hb_halo_select(n, N.ptr(fields["pos"]), N.ptr(fields["ghost"]), g,
                                         float(self.box.side_length), self.w, self.rank, pu, 1,
                                         N.ptr(counts), N.ptr(fill), N.ptr(rows), N.ptr(slots),
@@ -172,20 +178,33 @@ class HaloExchange:
                                       N.ptr(fields["density"]), N.ptr(fields["species"]),
                                       N.ptr(fields["global_id"]), g, float(self.box.side_length),
                                       self.rank, N.ptr(send), st, C.byref(err)), err)
-        per_dest = ch.reshape(self.world, 28).sum(axis=1) * self.rec
-        return send[:m * self.rec], [int(x) for x in per_dest], (stay[:n] if stay is not None
-                                                                  else None)
+        return (send[:m * self.rec], ch.reshape(self.world, 28),
+                stay[:n] if stay is not None else None, n_stay)
 
-    def unpack(self, recv, keep: dict | None = None) -> tuple[dict, int]:
+    def flag_indices(self, flags, count: int, name: str):
+        """Row indices of nonzero flags (count known on the host: no sync)."""
+        import torch
+        n = int(flags.shape[0])
+        idx = self._buf(name, max(count, 1), torch.int64)[:count]
+        ws = self._buf(name + "_ws", int(self.lib.hb_flag_indices_workspace(n)), torch.uint8)
+        err = N.HbError()
+        N.check(self.lib.hb_flag_indices(n, N.ptr(flags), N.ptr(idx), N.ptr(ws),
+                                         C.c_size_t(ws.numel()), N.stream_ptr(), C.byref(err)),
+                err)
+        return idx
+
+    def unpack(self, recv, keep=None, n_owned: int | None = None) -> tuple[dict, int]:
         """Records -> new rank field set.  Reference order (keep=None): owned by
-        gid then ghosts by (gid, shift).  Fast path: the staying owned rows
-        `keep` first (their current order), then arrivals sorted the same way."""
+        gid then ghosts by (gid, shift).  Fast path keep = (fields, stay, n_stay):
+        the staying owned rows first (current order), then arrivals (migrants by
+        gid, ghosts by (gid, shift))."""
         import torch
         m = int(recv.numel()) // self.rec
-        n0 = int(keep[1].shape[0]) if keep is not None else 0
+        n0 = int(keep[2]) if keep is not None else 0
         out = self._field_set(max(n0 + m, 1))
         if keep is not None:  # staying owned rows, current order
-            src, idx = keep
+            src, stay, n_stay = keep
+            idx = self.flag_indices(stay, n_stay, "keep_idx")
             for f in out:
                 torch.index_select(src[f], 0, idx, out=out[f][:n0])
         ws = self._buf("unpack_ws", int(self.lib.hb_halo_unpack_workspace(m)), torch.uint8)
@@ -196,26 +215,40 @@ class HaloExchange:
             "image_shift", "global_id", "ghost_src")], N.ptr(ws), C.c_size_t(ws.numel()), st,
             C.byref(err)), err)
         out = {k: v[:n0 + m] for k, v in out.items()}
-        n_owned = int((out["ghost"] == 0).sum().item())
+        if n_owned is None:
+            n_owned = int((out["ghost"] == 0).sum().item())
         if keep is None:
             N.check(self.lib.hb_halo_resolve_sources(n_owned, m, N.ptr(out["global_id"]),
                                                      N.ptr(out["ghost_src"]), st, C.byref(err)),
                     err)
         return out, n_owned
 
-    def exchange(self, fields: dict) -> tuple[dict, int]:
+    def route(self, send, slot_counts):
+        """All-to-all of the records.  Returns (recv bytes, received slot
+        counts (world, 28)).  One host sync (the counts)."""
         import torch
-        send, counts, stay = self.pack(fields)
+        import torch.distributed as dist
+        if self.world == 1:
+            return send, slot_counts
+        sc = torch.from_numpy(np.ascontiguousarray(slot_counts.reshape(-1))).cuda()
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc, group=self.group)
+        recv_slots = rc.cpu().numpy().reshape(self.world, 28)
+        send_bytes = [int(x) * self.rec for x in slot_counts.sum(axis=1)]
+        recv_bytes = [int(x) * self.rec for x in recv_slots.sum(axis=1)]
+        out = self._buf("recv", max(sum(recv_bytes), 1), torch.uint8)[:sum(recv_bytes)]
+        dist.all_to_all_single(out, send, recv_bytes, send_bytes, group=self.group)
+        return out, recv_slots
+
+    def exchange(self, fields: dict) -> tuple[dict, int]:
+        send, slot_counts, stay, n_stay = self.pack(fields)
         if self.transport is not None:
-            recv, _ = self.transport(send, counts)
-        elif self.world == 1:
-            recv = send
+            recv, recv_slots = self.transport(send, slot_counts)
         else:
-            recv, _ = alltoallv_bytes(send, counts, self.group)
-        keep = None
-        if stay is not None:
-            keep = (fields, torch.nonzero(stay).squeeze(1))
-        return self.unpack(recv, keep)
+            recv, recv_slots = self.route(send, slot_counts)
+        owned_in = int(np.asarray(recv_slots)[:, 27].sum())
+        keep = (fields, stay, n_stay) if stay is not None else None
+        return self.unpack(recv, keep, n_stay + owned_in if stay is not None else owned_in)
 
 
 class DistributedRank:
@@ -282,8 +315,9 @@ class DistributedRank:
             self.engine.last["ms_phase"]["exchange"] = e0.elapsed_time(e1)
         fields = self.engine.fields()
         # keep only owned rows (leaf order) as next step's owned set
-        idx = torch.nonzero(fields["ghost"] == 0).squeeze(1)
-        n_own = int(idx.shape[0])
+        n_own = self.n_owned
+        own_flags = (fields["ghost"] == 0).to(torch.uint8)
+        idx = self.halo.flag_indices(own_flags, n_own, "own_idx")
         store = getattr(self, "_owned_store", None)
         if store is None or store["pos"].shape[0] < n_own:
             store = empty_fields(int(n_own * 1.2) + 1024)

@@ -65,7 +65,8 @@ def test_rank_grid_and_bounds_match_decompose():
             lo, hi = domain_bounds(box, g, d.rank_id)
             np.testing.assert_array_equal(lo, d.lo)
             np.testing.assert_array_equal(hi, d.hi)
-    # shell: reference 1.25 reach widened to reach + 2 h_max for fresh ghost densities
-    assert overload_width(5.0, 1.3) == pytest.approx(max(6.25, 7.6))
+    # shell: gravity reach or the 2h + 2h density neighbourhood of ghosts in reach
+    assert overload_width(5.0, 1.3, headroom=1.0) == pytest.approx(5.2)
+    assert overload_width(5.0, 1.0, headroom=1.0) == pytest.approx(5.0)
     with pytest.raises(Exception):
         rank_grid_for(3)

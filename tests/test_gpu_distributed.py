@@ -45,22 +45,23 @@ def test_emulated_ranks_match_single_domain(world, periodic_unsplit, oracle):
                              h_max, h_min, periodic_unsplit=periodic_unsplit, n_global=p.n)
              for r in range(world)]
     sends = [rk.halo.pack(rk.owned_fields) for rk in ranks]
-    keeps = []
-    for rk, (_, _, stay) in zip(ranks, sends):
-        if stay is None:
-            keeps.append(None)
-        else:
-            keeps.append((rk.owned_fields, torch.nonzero(stay).squeeze(1)))
+    keeps = [None if stay is None else (rk.owned_fields, stay, n_stay)
+             for rk, (_, _, stay, n_stay) in zip(ranks, sends)]
     doms = decompose(box, grid, ranks[0].w)
     ref_sets, _ = build_overload(p.copy(), doms, box, grid)
     m = oracle  # noqa: F841  (oracle fixture builds the checker library)
     gk = short_range_gravity_kernel(ForceSplit(r_s=r_s, r_cut=r_cut), eps)
     for r, rk in enumerate(ranks):
         chunks = []
-        for src, (buf, counts, _) in enumerate(sends):
-            off = sum(counts[:r])
-            chunks.append(buf[off:off + counts[r]])
-        new, n_owned = rk.halo.unpack(torch.cat(chunks), keeps[r])
+        owned_in = 0
+        for src, (buf, slot_counts, _, _) in enumerate(sends):
+            per_dest = slot_counts.sum(axis=1) * rk.halo.rec
+            off = int(per_dest[:r].sum())
+            chunks.append(buf[off:off + int(per_dest[r])])
+            owned_in += int(slot_counts[r, 27])
+        n_exp = owned_in + (keeps[r][2] if keeps[r] is not None else 0)
+        new, n_owned = rk.halo.unpack(torch.cat(chunks), keeps[r], n_exp)
+        assert n_owned == int((new["ghost"] == 0).sum())
         rs = ref_sets[r]
         if not periodic_unsplit:  # the reference's own rank set, bit for bit
             for f in ("pos", "image_shift", "global_id", "ghost", "ghost_src", "smoothing"):

@@ -30,20 +30,18 @@ def main():
 
     for _ in range(5):
         t = time.perf_counter()
-        send, counts, stay = h.pack(rr.owned_fields)
-        t = tick("pack(select x2 + pack)", t)
-        recv, _ = alltoallv_bytes(send, counts)
-        t = tick("alltoallv", t)
-        idx = torch.nonzero(stay).squeeze(1)
-        keep = {k: v.index_select(0, idx) for k, v in rr.owned_fields.items()}
-        t = tick("keep gather", t)
-        new, n_owned = h.unpack(recv, keep)
-        t = tick("unpack", t)
+        send, slot_counts, stay, n_stay = h.pack(rr.owned_fields)
+        t = tick("pack(select x2 + sync + pack)", t)
+        recv, recv_slots = h.route(send, slot_counts)
+        t = tick("route (2 NCCL a2a + sync)", t)
+        owned_in = int(recv_slots[:, 27].sum())
+        new, n_owned = h.unpack(recv, (rr.owned_fields, stay, n_stay), n_stay + owned_in)
+        t = tick("unpack (keep gather + sort + unpack)", t)
         rr.engine.set_fields(new, rr.h_range)
         t = tick("set_fields", t)
     if rank == 0:
         print({k: round(v / 5, 3) for k, v in T.items()}, "send MB", send.numel() / 1e6,
-              "recv MB", recv.numel() / 1e6, "n", new["pos"].shape[0])
+              "recv MB", recv.numel() / 1e6, "n", new["pos"].shape[0], "n_stay", n_stay)
     dist.destroy_process_group()
 
 
