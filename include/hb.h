@@ -232,9 +232,10 @@ typedef struct HbStepArgs {
   double r_s, r_cut, softening, eos_gamma, visc_alpha, visc_beta;
   int32_t passes;    /* HB_PASS_* mask                                        */
   int32_t timing;    /* 1: fill ms_phase with per-phase device times          */
-  int32_t gravity_mode; /* 0 auto (= 3 when every bin fits the tiler), 1 leaf tiles +
-                           leaf list, 2 bin half-warp tiles (k_gravity2), 3 bin tiles +
-                           27-bin stencil (k_gravity)                             */
+  int32_t gravity_mode; /* 0 auto (= 4 when every bin fits the tiler, else 1),
+                           1 leaf tiles + leaf list, 2 bin half-warp tiles
+                           (k_gravity2, r/t table), 3 bin tiles + 27-bin stencil
+                           (k_gravity, r/t table), 4 as 3 with the soft-bits table */
   int32_t ghost_density; /* 1: ghost-only leaves are density receivers too, so
                             ghost rows near the rank face get fresh rho, P, c_s
                             (multi-rank; fixes SURVEY.md finding 4); gravity,

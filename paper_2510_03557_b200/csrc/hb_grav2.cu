@@ -78,7 +78,7 @@ struct G2Dev {
 template <bool TVAR>
 __global__ void __launch_bounds__(kG2Warps * 32)
 k_gravity2(G2Dev a, const float4* __restrict__ table, const int64_t* n_tiles_dev) {
-  __shared__ float4 s_tab[kGravTableMax];
+  __shared__ float4 s_tab[kGravTableRMax];
   __shared__ float4 s_stage[kG2Warps][kG2Stage][2];
   for (int k = threadIdx.x; k <= a.tab_last; k += blockDim.x) s_tab[k] = table[k];
   __syncthreads();
@@ -243,10 +243,13 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
                         nullptr, st, err);
   if (rc) return rc;
   static float4 host_tab[kGravTableMax];
-  float tab_scale = 0.f;
-  bool tvar = g.eps <= 0.05 * g.r_s;
-  int tab_last = gravity_table(g.r_s, g.r_cut, g.eps, tvar, kGravTableN, host_tab, &tab_scale);
-  HB_CUDA_TRY(cudaMemcpyAsync(tab, host_tab, sizeof(host_tab), cudaMemcpyHostToDevice, st));
+  GravTab gt;
+  // k_gravity2 only has the r / t tables
+  int kind = g.half_warp ? (g.eps <= 0.05 * g.r_s ? GT_T : GT_R) : g.table_kind;
+  if (gravity_table(g.r_s, g.r_cut, g.eps, kind, host_tab, &gt) < 0)
+    return set_err(err, HB_CONTRACT, "gravity table: r_cut / softening not representable");
+  HB_CUDA_TRY(cudaMemcpyAsync(tab, host_tab, gt.rows * sizeof(float4), cudaMemcpyHostToDevice,
+                              st));
   if (!g.half_warp) {
     k_stride_ptr<<<grid_for(nbins + 1, 256), 256, 0, st>>>(nbins, 27, st_ptr);
     HB_LAUNCH_CHECK();
@@ -257,16 +260,16 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     e.cull_reach = (float)(g.r_cut * (1.0 + 1e-4)) + 1e-30f;
     e.nchan = 3; e.out_flt = g.out; e.write_out = 1; e.err_key = g.err_key;
     e.skip_leaf = nullptr;
-    return launch_gravity_fast(e, tab, tab_scale, tab_last, tvar, T.n_tiles_cap, ntd, st, err);
+    return launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err);
   }
   G2Dev d;
   d.T = T; d.st_src = st_src; d.st_code = st_code; d.P0 = P0; d.L = g.L;
   d.cull_reach = (float)(g.r_cut * (1.0 + 1e-4)) + 1e-30f;
   d.eps2 = (float)(g.eps * g.eps);
-  d.tab_scale = tab_scale; d.tab_last = tab_last;
+  d.tab_scale = gt.scale; d.tab_last = (int)gt.last;
   d.out = g.out; d.err_key = g.err_key;
   unsigned grid = grid_for((T.n_tiles_cap + 1) / 2, kG2Warps);
-  if (tvar) k_gravity2<true><<<grid, kG2Warps * 32, 0, st>>>(d, tab, ntd);
+  if (kind == GT_T) k_gravity2<true><<<grid, kG2Warps * 32, 0, st>>>(d, tab, ntd);
   else k_gravity2<false><<<grid, kG2Warps * 32, 0, st>>>(d, tab, ntd);
   HB_LAUNCH_CHECK();
   if (g.overflow_host) {

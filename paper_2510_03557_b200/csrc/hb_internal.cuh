@@ -60,6 +60,7 @@ struct GravBinArgs {
   unsigned long long* err_key;
   int* overflow_host;
   bool half_warp;
+  int table_kind;  // GT_* for k_gravity (hb_pairs.cuh)
 };
 int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);
 // bins as segments: row range per bin and the 27-bin stencil as a receiver CSR

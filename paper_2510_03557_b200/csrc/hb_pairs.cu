@@ -712,30 +712,30 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 
 // ---------------------------------------------------------------- fast gravity
 // Resident-path short-range gravity.  Same tiling, culling and staging as
-// k_eval<KID_GRAVITY>, but S(r/r_s) comes from a 128-interval cubic table in
-// shared memory (centred intervals, Chebyshev-node interpolation of
-// erfc(x) + 2x/sqrt(pi) exp(-x^2) in float64 on the host; FP32 abs. error
-// < 1e-7) indexed with the float magic-number trick (no F2I), and the m_i
-// factor is applied once per target.  Per pair: 21 FMA-pipe + 2 MUFU + 4 ALU
-// + 2 LDS.  Entries beyond r_cut (plus half an interval) read a zero row.
+// k_eval<KID_GRAVITY> (per entry: lane-parallel source-tile box cull, then a
+// per-source cull against the target tile box; survivors staged in shared
+// memory and broadcast to the 32 target lanes), but the pair function comes
+// from a cubic-per-interval table in shared memory and m_i is applied once
+// per target.  Table kinds (host fit in float64 at Chebyshev nodes):
+//   GT_SOFT: indexed by the float bits of soft = r^2 + eps^2 (32 intervals per
+//            octave: index = bits >> 18, in-interval variable = the low 18
+//            mantissa bits as a float in [1, 1+2^-5) minus 1), storing
+//            G(soft) = S(sqrt(soft - eps^2) / r_s) * soft^{-3/2}.  Per pair:
+//            3 FADD + 3 FFMA (soft) + SHF + VIADDMNMX + LOP3 + FADD + LDS +
+//            3 FFMA + FMUL + 3 FFMA, no MUFU.  FP32 abs. error in S < 1.2e-7.
+//   GT_T:    indexed by t = sqrt(r^2 + eps^2) = soft * rsqrt(soft) with the
+//            float magic-number trick, storing S(sqrt(t^2 - eps^2) / r_s)
+//            (eps <= 0.05 r_s); GT_R: by r = r^2 * rsqrt(r^2).  One or two MUFU.
+// Rows past r_cut (to the end of the interval holding r_cut) carry the smooth
+// continuation (|S| <= S(r_cut/r_s) < 1e-5 by the ForceSplit guard); the next
+// row is zero.  (A persistent grid loading the table once per CTA measured
+// 5% slower: static tile striding leaves warps idle at the tail.)
 constexpr int kGravWarps = 8;
 constexpr int kGravStage = 128;
 
-// TVAR: the table is indexed by t = sqrt(r^2 + eps^2) = soft * rsqrt(soft) and
-// stores S(sqrt(t^2 - eps^2) / r_s) (one MUFU per pair; used when eps/r_s <=
-// 0.05, where the cusp at t = eps costs < 4e-6 abs. in S for r < 2 eps only);
-// otherwise by r = r^2 * rsqrt(r^2).
-template <bool TVAR>
-__global__ void __launch_bounds__(kGravWarps * 32)
-k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_last,
-          const int64_t* n_tiles_dev) {
-  __shared__ float4 s_tab[kGravTableMax];
-  __shared__ float4 s_src[kGravWarps][kGravStage];
-  for (int k = threadIdx.x; k <= tab_last; k += blockDim.x) s_tab[k] = table[k];
-  __syncthreads();
-  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t t = (int64_t)blockIdx.x * kGravWarps + wid;
-  if (t >= *n_tiles_dev) return;
+template <int KIND>
+__device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
+                                          float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
   int A = T.tile_leaf[t];
   if (a.skip_leaf && a.skip_leaf[A]) return;
@@ -750,7 +750,6 @@ k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_
   float eps2 = a.pp.p1;
   float ax = 0.0f, ay = 0.0f, az = 0.0f;
   double oA[3] = {T.origin[3 * A], T.origin[3 * A + 1], T.origin[3 * A + 2]};
-  float4* stage = s_src[wid];
   int cnt = 0;
   auto flush = [&]() {
     __syncwarp();
@@ -758,16 +757,27 @@ k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_
     for (int q = 0; q < cnt; ++q) {
       float4 s = stage[q];
       float dx = ti.x - s.x, dy = ti.y - s.y, dz = ti.z - s.z;
-      float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      float soft = r2 + eps2;
-      float ri = rsqrt_ftz(soft);
-      float rr = TVAR ? soft * ri : r2 * rsqrt_ftz(fmaxf(r2, 1e-30f));
-      float fm = fmaf(rr, tab_scale, 12582912.0f);
-      int k = min(__float_as_int(fm) - 0x4B400000, tab_last);
-      float u = fmaf(rr, tab_scale, 12582912.0f - fm);
-      float4 c = s_tab[k];
-      float S = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x);
-      float w = (S * (ri * ri)) * (ri * s.w);
+      float w;
+      if (KIND == GT_SOFT) {
+        float soft = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
+        unsigned bits = __float_as_uint(soft);
+        unsigned k = min((bits >> (23 - kGravSoftBits)) - gt.base, gt.last);
+        float u = __uint_as_float((bits & ((1u << (23 - kGravSoftBits)) - 1u)) | 0x3F800000u) -
+                  1.0f;
+        float4 c = s_tab[k];
+        w = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x) * s.w;
+      } else {
+        float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        float soft = r2 + eps2;
+        float ri = rsqrt_ftz(soft);
+        float rr = KIND == GT_T ? soft * ri : r2 * rsqrt_ftz(fmaxf(r2, 1e-30f));
+        float fm = fmaf(rr, gt.scale, 12582912.0f);
+        int k = min(__float_as_int(fm) - 0x4B400000, (int)gt.last);
+        float u = fmaf(rr, gt.scale, 12582912.0f - fm);
+        float4 c = s_tab[k];
+        float S = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x);
+        w = (S * (ri * ri)) * (ri * s.w);
+      }
       ax = fmaf(w, dx, ax);
       ay = fmaf(w, dy, ay);
       az = fmaf(w, dz, az);
@@ -830,52 +840,113 @@ k_gravity(EvalDev a, const float4* __restrict__ table, float tab_scale, int tab_
   }
 }
 
-int launch_gravity_fast(const EvalDev& d, const float4* table, float tab_scale, int tab_last,
-                        bool tvar, int64_t tcap, const int64_t* ntd, cudaStream_t st,
-                        HbError* err) {
-  if (tvar)
-    k_gravity<true><<<grid_for(tcap, kGravWarps), kGravWarps * 32, 0, st>>>(d, table, tab_scale,
-                                                                           tab_last, ntd);
-  else
-    k_gravity<false><<<grid_for(tcap, kGravWarps), kGravWarps * 32, 0, st>>>(d, table, tab_scale,
-                                                                            tab_last, ntd);
+template <int KIND>
+__global__ void __launch_bounds__(kGravWarps * 32, 4)
+k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev) {
+  extern __shared__ float4 s_tab[];  // gt.rows
+  __shared__ float4 s_src[kGravWarps][kGravStage];
+  for (int k = threadIdx.x; k < gt.rows; k += blockDim.x) s_tab[k] = table[k];
+  __syncthreads();
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = (int64_t)blockIdx.x * kGravWarps + wid;
+  if (t < *n_tiles_dev) grav_tile<KIND>(a, s_tab, gt, s_src[wid], t, lane);
+}
+
+int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
+                        const int64_t* ntd, cudaStream_t st, HbError* err) {
+  unsigned grid = grid_for(tcap, kGravWarps), blk = kGravWarps * 32;
+  size_t sm = gt.rows * sizeof(float4);
+  if (gt.kind == GT_SOFT) k_gravity<GT_SOFT><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+  else if (gt.kind == GT_T) k_gravity<GT_T><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+  else k_gravity<GT_R><<<grid, blk, sm, st>>>(d, table, gt, ntd);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
 
-// cubic-per-interval table of S(r / r_s) over r in [0, r_cut] (float64 fit)
-int gravity_table(double r_s, double r_cut, double eps, bool tvar, int nt, float4* host_out,
-                  float* tab_scale) {
-  double dr = r_cut / nt;
-  const double node[4] = {0.5 * cos(M_PI * 0.5 / 4), 0.5 * cos(M_PI * 1.5 / 4),
-                          0.5 * cos(M_PI * 2.5 / 4), 0.5 * cos(M_PI * 3.5 / 4)};
-  for (int k = 0; k <= nt; ++k) {
-    double m[4][5];
-    for (int i = 0; i < 4; ++i) {
-      double rv = (k + node[i]) * dr;
-      if (tvar) rv = sqrt(fmax(rv * rv - eps * eps, 0.0));
-      double x = rv / r_s;
-      double sv = erfc(x) + 1.1283791670955126 * x * exp(-x * x);
-      double p = 1.0;
-      for (int j = 0; j < 4; ++j) { m[i][j] = p; p *= node[i]; }
-      m[i][4] = sv;
-    }
-    for (int c = 0; c < 4; ++c) {  // Gauss-Jordan on the 4x4 Vandermonde
-      int piv = c;
-      for (int r = c + 1; r < 4; ++r) if (fabs(m[r][c]) > fabs(m[piv][c])) piv = r;
-      for (int j = 0; j < 5; ++j) { double tmp = m[c][j]; m[c][j] = m[piv][j]; m[piv][j] = tmp; }
-      for (int r = 0; r < 4; ++r) {
-        if (r == c) continue;
-        double f = m[r][c] / m[c][c];
-        for (int j = c; j < 5; ++j) m[r][j] -= f * m[c][j];
-      }
-    }
-    host_out[k] = make_float4((float)(m[0][4] / m[0][0]), (float)(m[1][4] / m[1][1]),
-                              (float)(m[2][4] / m[2][2]), (float)(m[3][4] / m[3][3]));
+// cubic through f at the 4 Chebyshev nodes of [lo, hi]: coefficients in u
+static float4 cheb_cubic(double lo, double hi, double (*f)(double, const double*),
+                         const double* prm) {
+  double m[4][5];
+  for (int i = 0; i < 4; ++i) {
+    double x = 0.5 * (lo + hi) + 0.5 * (hi - lo) * cos(M_PI * (i + 0.5) / 4);
+    double p = 1.0;
+    for (int j = 0; j < 4; ++j) { m[i][j] = p; p *= x; }
+    m[i][4] = f(x, prm);
   }
-  host_out[nt + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-  *tab_scale = (float)(nt / r_cut);
-  return nt + 1;
+  for (int c = 0; c < 4; ++c) {  // Gauss-Jordan on the 4x4 Vandermonde
+    int piv = c;
+    for (int r = c + 1; r < 4; ++r) if (fabs(m[r][c]) > fabs(m[piv][c])) piv = r;
+    for (int j = 0; j < 5; ++j) { double tmp = m[c][j]; m[c][j] = m[piv][j]; m[piv][j] = tmp; }
+    for (int r = 0; r < 4; ++r) {
+      if (r == c) continue;
+      double q = m[r][c] / m[c][c];
+      for (int j = c; j < 5; ++j) m[r][j] -= q * m[c][j];
+    }
+  }
+  return make_float4((float)(m[0][4] / m[0][0]), (float)(m[1][4] / m[1][1]),
+                     (float)(m[2][4] / m[2][2]), (float)(m[3][4] / m[3][3]));
+}
+
+static double split_s(double x) { return erfc(x) + 1.1283791670955126 * x * exp(-x * x); }
+static unsigned f2u(float f) { unsigned u; memcpy(&u, &f, 4); return u; }
+static float u2f(unsigned u) { float f; memcpy(&f, &u, 4); return f; }
+// prm: r_s, eps, x0, kind, scale.  GT_SOFT: u in [0, 2^-5) is the in-interval
+// mantissa offset, soft = x0 + scale * u (x0 = interval start, scale = 2^exponent).
+// GT_R / GT_T: u in [-1/2, 1/2] interval units around x0 = k * dr, r = x0 + scale * u.
+static double tab_fn(double u, const double* p) {
+  double rs = p[0], eps = p[1], x0 = p[2], sc = p[4];
+  if ((int)p[3] == GT_SOFT) {
+    double soft = x0 + sc * u;
+    return split_s(sqrt(fmax(soft - eps * eps, 0.0)) / rs) * pow(soft, -1.5);
+  }
+  double rv = x0 + sc * u;
+  if ((int)p[3] == GT_T) rv = sqrt(fmax(rv * rv - eps * eps, 0.0));
+  return split_s(rv / rs);
+}
+
+int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_out, GravTab* gt) {
+  gt->kind = kind;
+  if (kind == GT_SOFT) {
+    const int sh = 23 - kGravSoftBits;
+    float scut = (float)(r_cut * r_cut + eps * eps);
+    // lowest row: eps^2, floored so the table spans <= kGravSoftOctaves octaves
+    // (soft below the floor -- only r < 2^-20 r_cut at eps = 0 -- reads zero)
+    double fl = fmax(eps * eps, ldexp((double)scut, -kGravSoftOctaves + 1));
+    float smin = (float)fl;
+    unsigned base = f2u(smin) >> sh;
+    unsigned kc = f2u(scut) >> sh;
+    unsigned rows = kc - base + 1;
+    if (rows + 1 > (unsigned)kGravTableMax) return -1;
+    for (unsigned k = 0; k < rows; ++k) {
+      unsigned b = (base + k) << sh;
+      float f0 = u2f(b);
+      int e = 0;
+      frexp((double)f0, &e);
+      double prm[5] = {r_s, eps, (double)f0, (double)GT_SOFT, ldexp(1.0, e - 1)};
+      host_out[k] = cheb_cubic(0.0, ldexp(1.0, -kGravSoftBits), tab_fn, prm);
+      if (!(isfinite(host_out[k].x) && isfinite(host_out[k].y) && isfinite(host_out[k].z) &&
+            isfinite(host_out[k].w)))
+        return -1;
+    }
+    host_out[rows] = make_float4(0.f, 0.f, 0.f, 0.f);
+    gt->base = base; gt->last = rows; gt->rows = (int)rows + 1; gt->scale = 0.f;
+    return gt->rows;
+  }
+  double dr = r_cut / kGravTableN;
+  for (int k = 0; k <= kGravTableN; ++k) {
+    double prm[5] = {r_s, eps, k * dr, (double)kind, dr};
+    host_out[k] = cheb_cubic(-0.5, 0.5, tab_fn, prm);
+  }
+  host_out[kGravTableN + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  gt->base = 0; gt->last = kGravTableN + 1; gt->rows = kGravTableN + 2;
+  gt->scale = (float)(kGravTableN / r_cut);
+  return gt->rows;
+}
+
+int gravity_kind(int gravity_mode, double eps, double r_s) {
+  if (gravity_mode == 3 || gravity_mode == 2 || !kGravitySoftTable)
+    return eps <= 0.05 * r_s ? GT_T : GT_R;
+  return GT_SOFT;
 }
 
 // ---------------------------------------------------------------- driver pieces

@@ -21,6 +21,25 @@ enum { C_X = 0, C_Y, C_Z, C_VX, C_VY, C_VZ, C_M, C_H, C_RHO, C_P, C_CS, C_SP, NC
 
 constexpr float kSigma = 0.318309886183790671f;  // 1/pi (hb/kernels.py:63)
 
+// walk this lane's set bits across all words; body(q) per in-support source.
+// The warp loops max-over-lanes(total bits) times: balanced over the stage.
+template <class Body>
+__device__ __forceinline__ void walk_masks(const unsigned (*mask)[32], int cnt, Body body) {
+  int lane = threadIdx.x & 31;
+  int nw = (cnt + 31) >> 5;
+  int wi = 0;
+  unsigned m = nw > 0 ? mask[0][lane] : 0u;
+  while (true) {
+    while (m == 0u && ++wi < nw) m = mask[wi][lane];
+    bool has = m != 0u;
+    if (!__any_sync(0xffffffffu, has)) break;
+    if (has) {
+      int q = wi * 32 + __ffs(m) - 1;
+      m &= m - 1;
+      body(q);
+    }
+  }
+}
 // MUFU.RSQ without the denormal fix-up rsqrtf() wraps around it (inputs here
 // are >= 1e-30, normal in FP32)
 __device__ __forceinline__ float rsqrt_ftz(float x) {
@@ -251,12 +270,23 @@ int launch_pairs(int kid, bool det, bool lean, const EvalDev& d, int64_t tile_ca
                  const int64_t* n_tiles_dev, cudaStream_t st, HbError* err);
 int kid_selects_gas(int kid);
 // resident fast gravity: table of S(r/r_s), 128 cubic intervals over [0, r_cut]
-constexpr int kGravTableN = 128;
-constexpr int kGravTableMax = kGravTableN + 2;
-int gravity_table(double r_s, double r_cut, double eps, bool tvar, int nt, float4* host_out,
-                  float* tab_scale);
-int launch_gravity_fast(const EvalDev& d, const float4* table, float tab_scale, int tab_last,
-                        bool tvar, int64_t tcap, const int64_t* ntd, cudaStream_t st,
-                        HbError* err);
+constexpr int kGravTableN = 128;            // GT_R / GT_T intervals over [0, r_cut]
+constexpr int kGravTableRMax = kGravTableN + 2;
+constexpr int kGravSoftBits = 5;            // GT_SOFT: 2^5 intervals per octave of soft
+constexpr int kGravSoftOctaves = 40;
+constexpr int kGravTableMax = (kGravSoftOctaves + 1) * (1 << kGravSoftBits) + 2;
+constexpr bool kGravitySoftTable = true;    // gravity_mode 0/1/4 use GT_SOFT
+enum { GT_R = 0, GT_T = 1, GT_SOFT = 2 };
+struct GravTab {
+  int kind, rows;  // rows to stage in shared memory (the last one is zero)
+  float scale;     // GT_R / GT_T: intervals per unit r (or t)
+  unsigned base;   // GT_SOFT: (bits of the lowest soft) >> (23 - kGravSoftBits)
+  unsigned last;   // zero row index
+};
+// host: fill host_out (kGravTableMax rows) and gt; returns rows or -1 (unrepresentable)
+int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_out, GravTab* gt);
+int gravity_kind(int gravity_mode, double eps, double r_s);
+int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
+                        const int64_t* ntd, cudaStream_t st, HbError* err);
 
 }  // namespace hb

@@ -154,26 +154,6 @@ __device__ __forceinline__ void build_masks(const float4 (*stage)[NP], int cnt, 
   __syncwarp();
 }
 
-// walk this lane's set bits across all words; body(q) per in-support source.
-// The warp loops max-over-lanes(total bits) times: balanced over the stage.
-template <class Body>
-__device__ __forceinline__ void walk_masks(const unsigned (*mask)[32], int cnt, Body body) {
-  int lane = threadIdx.x & 31;
-  int nw = (cnt + 31) >> 5;
-  int wi = 0;
-  unsigned m = nw > 0 ? mask[0][lane] : 0u;
-  while (true) {
-    while (m == 0u && ++wi < nw) m = mask[wi][lane];
-    bool has = m != 0u;
-    if (!__any_sync(0xffffffffu, has)) break;
-    if (has) {
-      int q = wi * 32 + __ffs(m) - 1;
-      m &= m - 1;
-      body(q);
-    }
-  }
-}
-
 // ---------------------------------------------------------------- pass A
 __global__ void __launch_bounds__(kSphWarps * 32)
 k_sph_density(SphDev a, const int64_t* n_tiles_dev) {

@@ -354,6 +354,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       gb.L = a->side_length; gb.r_s = a->r_s; gb.r_cut = a->r_cut; gb.eps = a->softening;
       gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
       gb.half_warp = a->gravity_mode == 2;
+      gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
       Arena s = ws;
       rc = gravity_bins(gb, s, st, err);
       if (rc) return rc;
@@ -363,13 +364,13 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       if (rc) return rc;
       setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
       static float4 host_tab[kGravTableMax];
-      float tab_scale = 0.f;
-      bool tvar = a->softening <= 0.05 * a->r_s;
-      int tab_last = gravity_table(a->r_s, a->r_cut, a->softening, tvar, kGravTableN, host_tab,
-                                   &tab_scale);
-      HB_CUDA_TRY(cudaMemcpyAsync(w.gtab, host_tab, sizeof(host_tab), cudaMemcpyHostToDevice, st));
-      rc = launch_gravity_fast(d, w.gtab, tab_scale, tab_last, tvar, w.Ta.n_tiles_cap, w.nta, st,
-                               err);
+      GravTab gt;
+      if (gravity_table(a->r_s, a->r_cut, a->softening,
+                        gravity_kind(a->gravity_mode, a->softening, a->r_s), host_tab, &gt) < 0)
+        return set_err(err, HB_CONTRACT, "gravity table: r_cut / softening not representable");
+      HB_CUDA_TRY(cudaMemcpyAsync(w.gtab, host_tab, gt.rows * sizeof(float4),
+                                  cudaMemcpyHostToDevice, st));
+      rc = launch_gravity_fast(d, w.gtab, gt, w.Ta.n_tiles_cap, w.nta, st, err);
       if (rc) return rc;
     }
   }
