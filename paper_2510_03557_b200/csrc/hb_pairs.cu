@@ -717,12 +717,15 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 // memory and broadcast to the 32 target lanes), but the pair function comes
 // from a cubic-per-interval table in shared memory and m_i is applied once
 // per target.  Table kinds (host fit in float64 at Chebyshev nodes):
-//   GT_SOFT: indexed by the float bits of soft = r^2 + eps^2 (32 intervals per
-//            octave: index = bits >> 18, in-interval variable = the low 18
-//            mantissa bits as a float in [1, 1+2^-5) minus 1), storing
-//            G(soft) = S(sqrt(soft - eps^2) / r_s) * soft^{-3/2}.  Per pair:
-//            3 FADD + 3 FFMA (soft) + SHF + VIADDMNMX + LOP3 + FADD + LDS +
-//            3 FFMA + FMUL + 3 FFMA, no MUFU.  FP32 abs. error in S < 1.2e-7.
+//   GT_SOFT: indexed by the float bits of soft = r^2 + eps^2 (2^JB intervals
+//            per octave: index = bits >> (23 - JB), in-interval variable = the
+//            low 23 - JB mantissa bits as a float in [1, 1 + 2^-JB) minus 1),
+//            storing G(soft) = S(sqrt(soft - eps^2) / r_s) * soft^{-3/2}.  Per
+//            pair: 3 FADD + 3 FFMA (soft) + LEA.HI + VIMNMX + 2 LOP3 + FADD +
+//            LEA + LDS + 3 FFMA + FMUL + 3 FFMA, no MUFU.  FP32 abs. error in S
+//            < 1.2e-7 (JB = 5) / 3.4e-7 (JB = 4).  The gather is the bound: its
+//            shared-memory wavefronts grow with the number of distinct rows the
+//            32 (nearby) targets touch, so the coarser JB = 4 table is cheaper.
 //   GT_T:    indexed by t = sqrt(r^2 + eps^2) = soft * rsqrt(soft) with the
 //            float magic-number trick, storing S(sqrt(t^2 - eps^2) / r_s)
 //            (eps <= 0.05 r_s); GT_R: by r = r^2 * rsqrt(r^2).  One or two MUFU.
@@ -733,7 +736,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 constexpr int kGravWarps = 8;
 constexpr int kGravStage = 128;
 
-template <int KIND>
+template <int KIND, int JB>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -761,9 +764,8 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
       if (KIND == GT_SOFT) {
         float soft = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
         unsigned bits = __float_as_uint(soft);
-        unsigned k = min((bits >> (23 - kGravSoftBits)) - gt.base, gt.last);
-        float u = __uint_as_float((bits & ((1u << (23 - kGravSoftBits)) - 1u)) | 0x3F800000u) -
-                  1.0f;
+        unsigned k = min((bits >> (23 - JB)) - gt.base, gt.last);
+        float u = __uint_as_float((bits & ((1u << (23 - JB)) - 1u)) | 0x3F800000u) - 1.0f;
         float4 c = s_tab[k];
         w = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x) * s.w;
       } else {
@@ -840,7 +842,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   }
 }
 
-template <int KIND>
+template <int KIND, int JB>
 __global__ void __launch_bounds__(kGravWarps * 32, 4)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev) {
   extern __shared__ float4 s_tab[];  // gt.rows
@@ -849,16 +851,21 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
   __syncthreads();
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * kGravWarps + wid;
-  if (t < *n_tiles_dev) grav_tile<KIND>(a, s_tab, gt, s_src[wid], t, lane);
+  if (t < *n_tiles_dev) grav_tile<KIND, JB>(a, s_tab, gt, s_src[wid], t, lane);
 }
 
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
                         const int64_t* ntd, cudaStream_t st, HbError* err) {
   unsigned grid = grid_for(tcap, kGravWarps), blk = kGravWarps * 32;
   size_t sm = gt.rows * sizeof(float4);
-  if (gt.kind == GT_SOFT) k_gravity<GT_SOFT><<<grid, blk, sm, st>>>(d, table, gt, ntd);
-  else if (gt.kind == GT_T) k_gravity<GT_T><<<grid, blk, sm, st>>>(d, table, gt, ntd);
-  else k_gravity<GT_R><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+  if (gt.kind == GT_SOFT && gt.jbits == 5)
+    k_gravity<GT_SOFT, 5><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+  else if (gt.kind == GT_SOFT)
+    k_gravity<GT_SOFT, 4><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+  else if (gt.kind == GT_T)
+    k_gravity<GT_T, 0><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+  else
+    k_gravity<GT_R, 0><<<grid, blk, sm, st>>>(d, table, gt, ntd);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
@@ -907,7 +914,13 @@ static double tab_fn(double u, const double* p) {
 int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_out, GravTab* gt) {
   gt->kind = kind;
   if (kind == GT_SOFT) {
-    const int sh = 23 - kGravSoftBits;
+    static int jb = 0;
+    if (!jb) {  // HB_GRAV_JBITS: 4 (default) or 5 intervals-per-octave bits
+      const char* e = getenv("HB_GRAV_JBITS");
+      jb = (e && atoi(e) == 5) ? 5 : kGravSoftBitsDefault;
+    }
+    gt->jbits = jb;
+    const int sh = 23 - jb;
     float scut = (float)(r_cut * r_cut + eps * eps);
     // lowest row: eps^2, floored so the table spans <= kGravSoftOctaves octaves
     // (soft below the floor -- only r < 2^-20 r_cut at eps = 0 -- reads zero)
@@ -923,7 +936,7 @@ int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_o
       int e = 0;
       frexp((double)f0, &e);
       double prm[5] = {r_s, eps, (double)f0, (double)GT_SOFT, ldexp(1.0, e - 1)};
-      host_out[k] = cheb_cubic(0.0, ldexp(1.0, -kGravSoftBits), tab_fn, prm);
+      host_out[k] = cheb_cubic(0.0, ldexp(1.0, -jb), tab_fn, prm);
       if (!(isfinite(host_out[k].x) && isfinite(host_out[k].y) && isfinite(host_out[k].z) &&
             isfinite(host_out[k].w)))
         return -1;
@@ -938,7 +951,7 @@ int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_o
     host_out[k] = cheb_cubic(-0.5, 0.5, tab_fn, prm);
   }
   host_out[kGravTableN + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-  gt->base = 0; gt->last = kGravTableN + 1; gt->rows = kGravTableN + 2;
+  gt->base = 0; gt->last = kGravTableN + 1; gt->rows = kGravTableN + 2; gt->jbits = 0;
   gt->scale = (float)(kGravTableN / r_cut);
   return gt->rows;
 }

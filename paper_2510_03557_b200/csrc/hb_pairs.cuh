@@ -272,16 +272,18 @@ int kid_selects_gas(int kid);
 // resident fast gravity: table of S(r/r_s), 128 cubic intervals over [0, r_cut]
 constexpr int kGravTableN = 128;            // GT_R / GT_T intervals over [0, r_cut]
 constexpr int kGravTableRMax = kGravTableN + 2;
-constexpr int kGravSoftBits = 5;            // GT_SOFT: 2^5 intervals per octave of soft
+constexpr int kGravSoftBitsMax = 5;         // GT_SOFT: 2^jbits intervals per octave of soft
+constexpr int kGravSoftBitsDefault = 4;
 constexpr int kGravSoftOctaves = 40;
-constexpr int kGravTableMax = (kGravSoftOctaves + 1) * (1 << kGravSoftBits) + 2;
+constexpr int kGravTableMax = (kGravSoftOctaves + 1) * (1 << kGravSoftBitsMax) + 2;
 constexpr bool kGravitySoftTable = true;    // gravity_mode 0/1/4 use GT_SOFT
 enum { GT_R = 0, GT_T = 1, GT_SOFT = 2 };
 struct GravTab {
   int kind, rows;  // rows to stage in shared memory (the last one is zero)
   float scale;     // GT_R / GT_T: intervals per unit r (or t)
-  unsigned base;   // GT_SOFT: (bits of the lowest soft) >> (23 - kGravSoftBits)
+  unsigned base;   // GT_SOFT: (bits of the lowest soft) >> (23 - jbits)
   unsigned last;   // zero row index
+  int jbits;       // GT_SOFT: log2(intervals per octave), 4 or 5
 };
 // host: fill host_out (kGravTableMax rows) and gt; returns rows or -1 (unrepresentable)
 int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_out, GravTab* gt);
