@@ -221,7 +221,6 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   int32_t* st_code = ws.take<int32_t>(nbins * 27 + 1);
   int64_t* ntd = ws.take<int64_t>(1);
   float4* P0 = ws.take<float4>(g.n + 1);
-  float4* tab = ws.take<float4>(kGravTableMax);
   if (ws.dry) {
     Arena s = ws;
     build_tiling(T, nbins, nullptr, nullptr, nullptr, nullptr, 0.0, 0, nullptr, s, st, err);
@@ -242,14 +241,11 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   int rc = pack_records(KID_GRAVITY, T, ntd, g.state, g.pshift, nullptr, 0, g.L, P0, nullptr,
                         nullptr, st, err);
   if (rc) return rc;
-  static float4 host_tab[kGravTableMax];
   GravTab gt;
   // k_gravity2 only has the r / t tables
   int kind = g.half_warp ? (g.eps <= 0.05 * g.r_s ? GT_T : GT_R) : g.table_kind;
-  if (gravity_table(g.r_s, g.r_cut, g.eps, kind, host_tab, &gt) < 0)
-    return set_err(err, HB_CONTRACT, "gravity table: r_cut / softening not representable");
-  HB_CUDA_TRY(cudaMemcpyAsync(tab, host_tab, gt.rows * sizeof(float4), cudaMemcpyHostToDevice,
-                              st));
+  const float4* tab = gravity_table_device(g.r_s, g.r_cut, g.eps, kind, &gt, st, err);
+  if (!tab) return err ? err->status : HB_CUDA;
   if (!g.half_warp) {
     k_stride_ptr<<<grid_for(nbins + 1, 256), 256, 0, st>>>(nbins, 27, st_ptr);
     HB_LAUNCH_CHECK();

@@ -17,6 +17,8 @@
 //   * integer outputs (counting, neighbour counts, pairs_in_reach) decide the
 //     reach / 4h^2 predicates in float64 with the reference's exact expression
 //     whenever the FP32 r^2 falls within 2^-12 of the threshold.
+#include <mutex>
+
 #include "hb_pairs.cuh"
 
 namespace hb {
@@ -257,15 +259,14 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     base += __popc(b);
   }
   __syncwarp();
+  constexpr int J = kTileWarpCap / 32;  // members per lane in the split loop
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-  double v[kTileWarpCapBlock / 32][3];
-  int nloc = 0;
-  for (int k = lane; k < m_sel; k += 32, ++nloc) {
+  for (int k = lane; k < m_sel; k += 32) {
     int64_t r = row[k];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      v[nloc][d] = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
-      mn[d] = fmin(mn[d], v[nloc][d]); mx[d] = fmax(mx[d], v[nloc][d]);
+      double v = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+      mn[d] = fmin(mn[d], v); mx[d] = fmax(mx[d], v);
     }
   }
   double org[3];
@@ -279,16 +280,28 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     org[d] = 0.5 * (mn[d] + mx[d]);
   }
   if (lane < 3) T.origin[3 * leaf + lane] = org[lane];
-  nloc = 0;
-  for (int k = lane; k < m_sel; k += 32, ++nloc)
+  for (int k = lane; k < m_sel; k += 32) {  // second pass (L1-hot): leaf-frame FP32
+    int64_t r = row[k];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) cc[d][k] = (float)(v[nloc][d] - org[d]);
+    for (int d = 0; d < 3; ++d)
+      cc[d][k] = (float)(bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L) -
+                         org[d]);
+  }
   __syncwarp();
-  // proportional median splits into ceil(m/32) tiles (DFS left-first)
+  // proportional median splits into ceil(m/32) tiles (DFS left-first).  The
+  // coordinates stay put; each split permutes the member order `ord` (kept in
+  // the row buffer's twin) with a stable median partition: the `left` smallest
+  // (key, position) members go first, in position order.  K = the left-th
+  // smallest key by radix descent (32 warp-reduced counting passes over
+  // register-held keys), ties at K by position: O(m) per level.
+  int32_t* ord = tmp;
+  for (int k = lane; k < m_sel; k += 32) ord[k] = k;
+  __syncwarp();
   int stk_a[24], stk_m[24], stk_k[24];  // warp-uniform stack
   int sp = 1, tile_j = 0;
   stk_a[0] = 0; stk_m[0] = m_sel; stk_k[0] = tiles_for(m_sel, T.tile_max, T.even);
   int64_t tbase = T.tile_ptr[leaf], so = T.sel_off[leaf];
+  unsigned lt = lanemask_lt();
   while (sp) {
     --sp;
     int a0 = stk_a[sp], m = stk_m[sp], kk = stk_k[sp];
@@ -302,13 +315,20 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
       ++tile_j;
       continue;
     }
+    int id[J];
     float lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int k = lane; k < m; k += 32)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        float x = cc[d][a0 + k];
-        lo3[d] = fminf(lo3[d], x); hi3[d] = fmaxf(hi3[d], x);
-      }
+    for (int jj = 0; jj < J; ++jj) {
+      int k = 32 * jj + lane;
+      id[jj] = k < m ? ord[a0 + k] : 0;
+      if (32 * jj >= m) continue;
+      if (k < m)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          float x = cc[d][id[jj]];
+          lo3[d] = fminf(lo3[d], x); hi3[d] = fmaxf(hi3[d], x);
+        }
+    }
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
@@ -319,39 +339,57 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     float ex0 = hi3[0] - lo3[0], ex1 = hi3[1] - lo3[1], ex2 = hi3[2] - lo3[2];
     int axis = ex1 > ex0 ? 1 : 0;
     if (ex2 > (axis ? ex1 : ex0)) axis = 2;
-    for (int k = lane; k < m; k += 32) {
-      float x = cc[axis][a0 + k];
-      int rank = 0;
-      for (int q = 0; q < m; ++q) {
-        float y = cc[axis][a0 + q];
-        rank += (y < x) || (y == x && q < k);
-      }
-      tmp[a0 + rank] = a0 + k;
-    }
-    __syncwarp();
-    int32_t rr[kTileWarpCapBlock / 32];
-    float c3[kTileWarpCapBlock / 32][3];
-    nloc = 0;
-    for (int k = lane; k < m; k += 32, ++nloc) {
-      int src = tmp[a0 + k];
-      rr[nloc] = row[src];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) c3[nloc][d] = cc[d][src];
-    }
-    __syncwarp();
-    nloc = 0;
-    for (int k = lane; k < m; k += 32, ++nloc) {
-      row[a0 + k] = rr[nloc];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) cc[d][a0 + k] = c3[nloc][d];
-    }
-    __syncwarp();
     int k1 = (kk + 1) / 2, k2 = kk - k1;
     int left = (int)(((int64_t)m * k1 + kk - 1) / kk);
+    const int nj = (m + 31) >> 5;  // warp-uniform: slots in use
+    unsigned key[J];
+    unsigned kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      bool v = 32 * jj + lane < m;
+      key[jj] = v ? sortable_key(cc[axis][id[jj]]) : 0xffffffffu;
+      if (v) { kmin = min(kmin, key[jj]); kmax = max(kmax, key[jj]); }
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    // bits above the highest one where kmin and kmax differ are common to all
+    int top = 31 - __clz(kmin ^ kmax | 1u);
+    unsigned K = top >= 31 ? 0u : (kmin >> (top + 1)) << (top + 1);
+    for (int b = top; b >= 0; --b) {
+      unsigned cand = K | (1u << b);
+      int c = 0;
+#pragma unroll
+      for (int jj = 0; jj < J; ++jj)
+        if (jj < nj) c += key[jj] < cand ? 1 : 0;  // padding keys are 0xffffffff
+      if (__reduce_add_sync(0xffffffffu, c) < left) K = cand;
+    }
+    int c_lt = 0;
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj)
+      if (jj < nj) c_lt += key[jj] < K ? 1 : 0;
+    int need_eq = left - __reduce_add_sync(0xffffffffu, c_lt);
+    int eq_seen = 0, nl_run = 0, nr_run = 0;
+    __syncwarp();
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      if (jj < nj) {
+        bool valid = 32 * jj + lane < m;
+        bool eq = valid && key[jj] == K;
+        unsigned be = __ballot_sync(0xffffffffu, eq);
+        bool isl = valid && (key[jj] < K || (eq && eq_seen + __popc(be & lt) < need_eq));
+        eq_seen += __popc(be);
+        unsigned bl = __ballot_sync(0xffffffffu, isl), bv = __ballot_sync(0xffffffffu, valid);
+        if (isl) ord[a0 + nl_run + __popc(bl & lt)] = id[jj];
+        else if (valid) ord[a0 + left + nr_run + __popc(bv & ~bl & lt)] = id[jj];
+        nl_run += __popc(bl);
+        nr_run += __popc(bv & ~bl);
+      }
+    }
+    __syncwarp();
     stk_a[sp] = a0 + left; stk_m[sp] = m - left; stk_k[sp] = k2; ++sp;   // right (popped last)
     stk_a[sp] = a0; stk_m[sp] = left; stk_k[sp] = k1; ++sp;              // left first
   }
-  for (int k = lane; k < m_sel; k += 32) T.tperm[so + k] = row[k];
+  for (int k = lane; k < m_sel; k += 32) T.tperm[so + k] = row[ord[k]];
 }
 
 // tile boxes (FP32, leaf frame) and hmax, one warp per tile
@@ -954,6 +992,53 @@ int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_o
   gt->base = 0; gt->last = kGravTableN + 1; gt->rows = kGravTableN + 2; gt->jbits = 0;
   gt->scale = (float)(kGravTableN / r_cut);
   return gt->rows;
+}
+
+// Device copy of the table, cached per device and re-uploaded only when the
+// parameters change.  A per-step upload from pageable host memory would be
+// host-synchronous (and on the legacy stream wait for all device work),
+// which serialised the gravity chain behind the concurrent SPH chain.
+const float4* gravity_table_device(double r_s, double r_cut, double eps, int kind, GravTab* gt,
+                                   cudaStream_t st, HbError* err) {
+  struct Slot {
+    bool ok = false;
+    double r_s, r_cut, eps;
+    int kind;
+    GravTab gt;
+    float4* dev = nullptr;
+    float4* host = nullptr;
+  };
+  static Slot slots[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    set_err(err, HB_CUDA, "no CUDA device for the gravity table");
+    return nullptr;
+  }
+  Slot& sl = slots[dev];
+  if (sl.ok && sl.r_s == r_s && sl.r_cut == r_cut && sl.eps == eps && sl.kind == kind) {
+    *gt = sl.gt;
+    return sl.dev;
+  }
+  if (!sl.dev && (cudaMalloc(&sl.dev, kGravTableMax * sizeof(float4)) != cudaSuccess ||
+                  cudaMallocHost(&sl.host, kGravTableMax * sizeof(float4)) != cudaSuccess)) {
+    set_err(err, HB_CUDA, "gravity table allocation failed");
+    return nullptr;
+  }
+  if (gravity_table(r_s, r_cut, eps, kind, sl.host, gt) < 0) {
+    set_err(err, HB_CONTRACT, "gravity table: r_cut / softening not representable");
+    return nullptr;
+  }
+  // the pinned staging buffer is reused on the next parameter change: finish the copy
+  if (cudaMemcpyAsync(sl.dev, sl.host, gt->rows * sizeof(float4), cudaMemcpyHostToDevice, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_err(err, HB_CUDA, "gravity table upload failed");
+    return nullptr;
+  }
+  sl.ok = true; sl.r_s = r_s; sl.r_cut = r_cut; sl.eps = eps; sl.kind = kind; sl.gt = *gt;
+  return sl.dev;
 }
 
 int gravity_kind(int gravity_mode, double eps, double r_s) {

@@ -288,6 +288,9 @@ struct GravTab {
 // host: fill host_out (kGravTableMax rows) and gt; returns rows or -1 (unrepresentable)
 int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_out, GravTab* gt);
 int gravity_kind(int gravity_mode, double eps, double r_s);
+// cached device copy (library-owned, per device); nullptr + err on failure
+const float4* gravity_table_device(double r_s, double r_cut, double eps, int kind, GravTab* gt,
+                                   cudaStream_t st, HbError* err);
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
                         const int64_t* ntd, cudaStream_t st, HbError* err);
 

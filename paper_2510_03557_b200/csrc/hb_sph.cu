@@ -129,16 +129,20 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
 // per-lane in-support bitmask over the stage, stored word-major in shared
 // memory (mask[w][lane], conflict-free); threshold on r^2 per lane (and per
 // source h_j for hydro's 2 max(h_i, h_j) support)
+// The last word is padded with far sources (r^2 ~ 3e36 beyond any threshold)
+// so every word is a fully unrolled 32-source sweep with constant shifts.
 template <int NP, bool HYDRO>
-__device__ __forceinline__ void build_masks(const float4 (*stage)[NP], int cnt, float4 ti0,
+__device__ __forceinline__ void build_masks(float4 (*stage)[NP], int cnt, float4 ti0,
                                             float hi, float thr_i, float reach2c,
                                             unsigned (*mask)[32]) {
   int lane = threadIdx.x & 31;
   int nw = (cnt + 31) >> 5;
+  if (cnt + lane < nw * 32) stage[cnt + lane][0] = make_float4(1e18f, 1e18f, 1e18f, 0.0f);
+  __syncwarp();
   for (int w = 0; w < nw; ++w) {
     unsigned bits = 0u;
-    int qmax = min(32, cnt - w * 32);
-    for (int b = 0; b < qmax; ++b) {
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
       float4 s = stage[w * 32 + b][0];
       float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
@@ -155,7 +159,7 @@ __device__ __forceinline__ void build_masks(const float4 (*stage)[NP], int cnt, 
 }
 
 // ---------------------------------------------------------------- pass A
-__global__ void __launch_bounds__(kSphWarps * 32)
+__global__ void __launch_bounds__(kSphWarps * 32, 6)
 k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   __shared__ float4 s_stage[kSphWarps][kStageA][1];
   __shared__ int2 s_meta[kSphWarps][kStageA];
@@ -204,7 +208,7 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
       }
       if (in) {
         count += c4 ? 1u : 0u;
-        float qq = sqrtf(r2) * hinv;
+        float qq = r2 * rsqrt_ftz(fmaxf(r2, 1e-30f)) * hinv;  // MUFU.RSQ, no IEEE sqrt fix-up
         rho = fmaf(s.w, w_body(qq), rho);
       }
     });

@@ -101,7 +101,6 @@ struct StepWs {
   float4 *P0, *P1, *P2;
   unsigned long long* err_key;
   int64_t* inv;
-  float4* gtab;
   uint8_t* no_ghost;
   int64_t *seg_s, *seg_e, *st_ptr;
   int32_t *st_src, *st_code;
@@ -123,7 +122,6 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
   w.P0 = ws.take<float4>(n + 1); w.P1 = ws.take<float4>(n + 1); w.P2 = ws.take<float4>(n + 1);
   w.err_key = ws.take<unsigned long long>(1);
   w.inv = ws.take<int64_t>(n + 1);
-  w.gtab = ws.take<float4>(kGravTableMax);
   w.no_ghost = ws.take<uint8_t>(cap + 1);
   w.seg_s = ws.take<int64_t>(nbins + 1); w.seg_e = ws.take<int64_t>(nbins + 1);
   w.st_ptr = ws.take<int64_t>(nbins + 1);
@@ -343,34 +341,38 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   }
   if (a->sph_done_event) HB_CUDA_TRY(cudaEventRecord((cudaEvent_t)a->sph_done_event, st));
   tm.mark(5);
-  // 7. short-range gravity (hb/kernels.py:152-163): bin segments with half-warp
-  // tiles (hb_grav2.cu) unless a bin outgrows the block tiler, then leaf tiles
-  if (a->passes & HB_PASS_GRAVITY) {
+  // 7. short-range gravity (hb/kernels.py:152-163): bin segments (hb_grav2.cu)
+  // unless a bin outgrows the block tiler, then leaf tiles.  (Running it on a
+  // second stream concurrently with the SPH chain was measured: the two
+  // throughput-bound grids time-slice the SMs -- whichever has dispatch
+  // priority starves the other -- so the step time did not change.)
+  bool bin_gravity = (a->passes & HB_PASS_GRAVITY) && !use_leaf_gravity;
+  if (bin_gravity) {
     HB_CUDA_TRY(cudaMemsetAsync(a->grav, 0, n * 3 * sizeof(double), st));
-    if (!use_leaf_gravity) {
-      GravBinArgs gb;
-      gb.n = n; gb.nbins = nbins; gb.bin_ptr = w.bin_ptr; gb.leaf_start = w.leaf_start;
-      gb.leaf_end = w.leaf_end; gb.geom = ld.g; gb.state = w.state; gb.pshift = a->image_shift;
-      gb.L = a->side_length; gb.r_s = a->r_s; gb.r_cut = a->r_cut; gb.eps = a->softening;
-      gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
-      gb.half_warp = a->gravity_mode == 2;
-      gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
-      Arena s = ws;
-      rc = gravity_bins(gb, s, st, err);
-      if (rc) return rc;
-    } else {
+    GravBinArgs gb;
+    gb.n = n; gb.nbins = nbins; gb.bin_ptr = w.bin_ptr; gb.leaf_start = w.leaf_start;
+    gb.leaf_end = w.leaf_end; gb.geom = ld.g; gb.state = w.state; gb.pshift = a->image_shift;
+    gb.L = a->side_length; gb.r_s = a->r_s; gb.r_cut = a->r_cut; gb.eps = a->softening;
+    gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
+    gb.half_warp = a->gravity_mode == 2;
+    gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
+    Arena s = ws;
+    rc = gravity_bins(gb, s, st, err);
+    if (rc) return rc;
+  }
+  if ((a->passes & HB_PASS_GRAVITY) && !bin_gravity) {
+    HB_CUDA_TRY(cudaMemsetAsync(a->grav, 0, n * 3 * sizeof(double), st));
+    {
       rc = pack_records(KID_GRAVITY, w.Ta, w.nta, w.state, a->image_shift, nullptr, 0,
                         a->side_length, w.P0, w.P1, w.P2, st, err);
       if (rc) return rc;
       setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
-      static float4 host_tab[kGravTableMax];
       GravTab gt;
-      if (gravity_table(a->r_s, a->r_cut, a->softening,
-                        gravity_kind(a->gravity_mode, a->softening, a->r_s), host_tab, &gt) < 0)
-        return set_err(err, HB_CONTRACT, "gravity table: r_cut / softening not representable");
-      HB_CUDA_TRY(cudaMemcpyAsync(w.gtab, host_tab, gt.rows * sizeof(float4),
-                                  cudaMemcpyHostToDevice, st));
-      rc = launch_gravity_fast(d, w.gtab, gt, w.Ta.n_tiles_cap, w.nta, st, err);
+      const float4* gtab = gravity_table_device(
+          a->r_s, a->r_cut, a->softening, gravity_kind(a->gravity_mode, a->softening, a->r_s), &gt,
+          st, err);
+      if (!gtab) return err ? err->status : HB_CUDA;
+      rc = launch_gravity_fast(d, gtab, gt, w.Ta.n_tiles_cap, w.nta, st, err);
       if (rc) return rc;
     }
   }
