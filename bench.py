@@ -310,9 +310,10 @@ def run_gpu_arm(args):
     value = n_total / (ms_step * 1e-3)
     ph = {k: float(np.mean([x[k] for x in phases])) for k in phases[0]}
     if dist:
-        t = torch.tensor([ph["gravity"]], device="cuda")
+        t = torch.tensor([ph["gravity"], ph["k_gravity"]], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ph["gravity_max_over_ranks"] = float(t.item())
+        ph["gravity_max_over_ranks"] = float(t[0].item())
+        ph["k_gravity_max_over_ranks"] = float(t[1].item())
 
     # ---- e2e: pinned host inputs -> device -> step (exchange incl.) -> results to host;
     # each call's copies overlap only that call's own compute (HostStepper)
@@ -379,7 +380,7 @@ def run_gpu_arm(args):
         if dist:
             dist.destroy_process_group()
         return 0
-    # ---- roofline of the dominant kernel (gravity phase, timed live above)
+    # ---- roofline of the dominant kernel (k_gravity, event-timed live above)
     if n_total > 40_000_000:
         # exact counting pass too large to run untimed next to the rank data:
         # per-particle in-support counts measured at c2 (same sigma/d statistics)
@@ -393,13 +394,13 @@ def run_gpu_arm(args):
         counts = pair_counts(p, cfg)
     peak, peak_src = peaks()
     alg_flops = counts["gravity"] * OPCOST["gravity"]
-    t_grav = ph.get("gravity_max_over_ranks", ph["gravity"]) * 1e-3
+    t_grav = ph.get("k_gravity_max_over_ranks", ph["k_gravity"]) * 1e-3
     achieved = alg_flops / t_grav / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get("gravity_dram_bytes_per_launch")
-    roof = {"bound": "fp32", "kernel": "k_gravity (gravity phase incl. record pack)",
+    roof = {"bound": "fp32", "kernel": "k_gravity (single launch, CUDA events on its stream)",
             "achieved": achieved, "peak": peak * world, "unit": "TFLOP/s",
             "frac": achieved / (peak * world), "traffic": traffic, "peak_source": peak_src,
             "algorithmic_flops_per_launch": alg_flops, "in_support_pairs": counts["gravity"],

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 1
+#define HB_ABI_VERSION 2
 
 /* status codes; map onto hb/errors.py */
 enum HbStatus {
@@ -261,6 +261,9 @@ typedef struct HbStepArgs {
   int64_t n_leaves, n_entries, list_capacity_needed;
   float ms_phase[8];    /* build, list, tiling, sph A (count+density+eos),
                            sph B (crk+hydro+solve), gravity, tail, total */
+  float ms_kernel[4];   /* timing=1: event-timed single-kernel spans on the step
+                           stream: gravity pair kernel, SPH pass A kernel, SPH
+                           pass B kernel, 0 (reserved) -- roofline inputs     */
 } HbStepArgs;
 
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,

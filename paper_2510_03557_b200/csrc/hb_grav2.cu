@@ -256,7 +256,10 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     e.cull_reach = (float)(g.r_cut * (1.0 + 1e-4)) + 1e-30f;
     e.nchan = 3; e.out_flt = g.out; e.write_out = 1; e.err_key = g.err_key;
     e.skip_leaf = nullptr;
-    return launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err);
+    if (g.t0) HB_CUDA_TRY(cudaEventRecord(g.t0, st));
+    int rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err);
+    if (g.t1) HB_CUDA_TRY(cudaEventRecord(g.t1, st));
+    return rc2;
   }
   G2Dev d;
   d.T = T; d.st_src = st_src; d.st_code = st_code; d.P0 = P0; d.L = g.L;
@@ -265,9 +268,11 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   d.tab_scale = gt.scale; d.tab_last = (int)gt.last;
   d.out = g.out; d.err_key = g.err_key;
   unsigned grid = grid_for((T.n_tiles_cap + 1) / 2, kG2Warps);
+  if (g.t0) HB_CUDA_TRY(cudaEventRecord(g.t0, st));
   if (kind == GT_T) k_gravity2<true><<<grid, kG2Warps * 32, 0, st>>>(d, tab, ntd);
   else k_gravity2<false><<<grid, kG2Warps * 32, 0, st>>>(d, tab, ntd);
   HB_LAUNCH_CHECK();
+  if (g.t1) HB_CUDA_TRY(cudaEventRecord(g.t1, st));
   if (g.overflow_host) {
     int ovf = 0;
     HB_CUDA_TRY(cudaMemcpyAsync(&ovf, T.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -61,6 +61,7 @@ struct GravBinArgs {
   int* overflow_host;
   bool half_warp;
   int table_kind;  // GT_* for k_gravity (hb_pairs.cuh)
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // optional: recorded around the pair kernel
 };
 int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);
 // bins as segments: row range per bin and the 27-bin stencil as a receiver CSR

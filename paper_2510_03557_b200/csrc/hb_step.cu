@@ -134,12 +134,22 @@ struct PhaseTimer {
   bool on;
   cudaStream_t st;
   cudaEvent_t ev[9];
+  cudaEvent_t kv[6];  // start/stop of gravity, SPH pass A, SPH pass B kernels
   int k = 0;
   PhaseTimer(bool on_, cudaStream_t s) : on(on_), st(s) {
-    if (on) for (int i = 0; i < 9; ++i) cudaEventCreate(&ev[i]);
+    if (on) {
+      for (int i = 0; i < 9; ++i) cudaEventCreate(&ev[i]);
+      for (int i = 0; i < 6; ++i) cudaEventCreate(&kv[i]);
+    }
   }
-  ~PhaseTimer() { if (on) for (int i = 0; i < 9; ++i) cudaEventDestroy(ev[i]); }
+  ~PhaseTimer() {
+    if (on) {
+      for (int i = 0; i < 9; ++i) cudaEventDestroy(ev[i]);
+      for (int i = 0; i < 6; ++i) cudaEventDestroy(kv[i]);
+    }
+  }
   void mark(int i) { if (on) cudaEventRecord(ev[i], st); }
+  void kmark(int i) { if (on) cudaEventRecord(kv[i], st); }
 };
 
 int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
@@ -309,7 +319,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, 0, st,
                   err);
     if (rc) return rc;
+    tm.kmark(2);
     rc = launch_sph(0, sa, st, err);
+    tm.kmark(3);
     if (rc) return rc;
   }
   if (a->passes & HB_PASS_DENSITY) {
@@ -333,7 +345,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, 1, st,
                   err);
     if (rc) return rc;
+    tm.kmark(4);
     rc = launch_sph(1, sa, st, err);
+    tm.kmark(5);
     if (rc) return rc;
     rc = hb_crk_solve(n, a->crk_moments, 10, a->species, 1e8, a->crk_A, a->crk_B,
                       a->crk_fallback, st, err);
@@ -356,6 +370,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
     gb.half_warp = a->gravity_mode == 2;
     gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
+    gb.t0 = tm.on ? tm.kv[0] : nullptr;
+    gb.t1 = tm.on ? tm.kv[1] : nullptr;
     Arena s = ws;
     rc = gravity_bins(gb, s, st, err);
     if (rc) return rc;
@@ -372,7 +388,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
           a->r_s, a->r_cut, a->softening, gravity_kind(a->gravity_mode, a->softening, a->r_s), &gt,
           st, err);
       if (!gtab) return err ? err->status : HB_CUDA;
+      tm.kmark(0);
       rc = launch_gravity_fast(d, gtab, gt, w.Ta.n_tiles_cap, w.nta, st, err);
+      tm.kmark(1);
       if (rc) return rc;
     }
   }
@@ -396,6 +414,12 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (tm.on) {
     for (int i = 0; i < 7; ++i) cudaEventElapsedTime(&a->ms_phase[i], tm.ev[i], tm.ev[i + 1]);
     cudaEventElapsedTime(&a->ms_phase[7], tm.ev[0], tm.ev[7]);
+    for (int i = 0; i < 4; ++i) a->ms_kernel[i] = 0.f;
+    if (a->passes & HB_PASS_GRAVITY) cudaEventElapsedTime(&a->ms_kernel[0], tm.kv[0], tm.kv[1]);
+    if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY))
+      cudaEventElapsedTime(&a->ms_kernel[1], tm.kv[2], tm.kv[3]);
+    if (a->passes & (HB_PASS_CRK | HB_PASS_HYDRO))
+      cudaEventElapsedTime(&a->ms_kernel[2], tm.kv[4], tm.kv[5]);
   }
   if (ovf || ovf2) return set_err(err, HB_CONTRACT, "leaf exceeds the tiling capacity (2048 members)");
   if (ek != ~0ull) {

@@ -28,6 +28,7 @@ from .particles import FIELD_SPECS, ParticleSet
 PASS_NCOUNT, PASS_DENSITY, PASS_CRK, PASS_GRAVITY, PASS_HYDRO = 1, 2, 4, 8, 16
 PASS_ALL = 31
 PHASES = ("build", "list", "tiling", "sph_density", "sph_force", "gravity", "tail", "total")
+KERNELS = ("k_gravity", "k_sph_density", "k_sph_force")  # single-kernel spans (ms_kernel)
 
 STEP_FIELDS = ("pos", "vel", "mass", "smoothing", "internal_energy", "density", "species",
                "ghost", "image_shift", "global_id", "ghost_src")
@@ -52,7 +53,7 @@ class HbStepArgs(C.Structure):
                    ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
                    ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
-                   ("ms_phase", C.c_float * 8)])
+                   ("ms_phase", C.c_float * 8), ("ms_kernel", C.c_float * 4)])
 
 
 def _bind(lib):
@@ -213,7 +214,9 @@ class ResidentRank:
             break
         self.cur = 1 - self.cur
         self.last = {"n_leaves": int(a.n_leaves), "n_entries": int(a.n_entries),
-                     "ms_phase": dict(zip(PHASES, list(a.ms_phase))) if timing else None}
+                     "ms_phase": ({**dict(zip(PHASES, list(a.ms_phase))),
+                                   **dict(zip(KERNELS, list(a.ms_kernel)[:3]))}
+                                  if timing else None)}
         return self.out
 
 
