@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 2
+#define HB_ABI_VERSION 3
 
 /* status codes; map onto hb/errors.py */
 enum HbStatus {
@@ -240,6 +240,11 @@ typedef struct HbStepArgs {
                             ghost rows near the rank face get fresh rho, P, c_s
                             (multi-rank; fixes SURVEY.md finding 4); gravity,
                             CRK and hydro still skip ghost-only receivers     */
+  int32_t owned_targets; /* 1: gravity and pass B (CRK + hydro) skip target
+                            tiles without an owned row (ghost == 0); rows of
+                            skipped tiles read 0.  For rank sets whose ghost
+                            outputs are discarded (multi-rank).  Pass A still
+                            serves every row (ghost densities).             */
   int64_t list_capacity; /* entries the workspace was sized for              */
   /* optional cudaEvent_t handles (void*, NULL = unused) for overlapping host
      copies with the step: the step waits on fields_ready before it first reads

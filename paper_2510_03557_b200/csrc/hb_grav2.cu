@@ -235,7 +235,8 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   HB_LAUNCH_CHECK();
   {
     Arena s = ws;
-    int rc = build_tiling(T, nbins, seg_s, seg_e, g.state, g.pshift, g.L, 0, ntd, s, st, err);
+    int rc = build_tiling(T, nbins, seg_s, seg_e, g.state, g.pshift, g.L, 0, ntd, s, st, err,
+                          g.ghost);
     if (rc) return rc;
   }
   int rc = pack_records(KID_GRAVITY, T, ntd, g.state, g.pshift, nullptr, 0, g.L, P0, nullptr,
@@ -256,6 +257,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     e.cull_reach = (float)(g.r_cut * (1.0 + 1e-4)) + 1e-30f;
     e.nchan = 3; e.out_flt = g.out; e.write_out = 1; e.err_key = g.err_key;
     e.skip_leaf = nullptr;
+    e.skip_tiles = g.ghost ? 1 : 0;
     if (g.t0) HB_CUDA_TRY(cudaEventRecord(g.t0, st));
     int rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err);
     if (g.t1) HB_CUDA_TRY(cudaEventRecord(g.t1, st));

@@ -42,6 +42,7 @@ struct SphArgs {
   double *ncount, *rho, *moments, *hydro;
   unsigned long long* err_key;
   const uint8_t* skip_leaf;
+  int skip_tiles;  // pass B: skip tiles without an owned member
 };
 int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
              double L, float4* P0, float4* P1, float4* P2, int layout, cudaStream_t st,
@@ -61,6 +62,7 @@ struct GravBinArgs {
   int* overflow_host;
   bool half_warp;
   int table_kind;  // GT_* for k_gravity (hb_pairs.cuh)
+  const uint8_t* ghost = nullptr;  // owned_targets: skip tiles without an owned row
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // optional: recorded around the pair kernel
 };
 int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);

@@ -394,7 +394,8 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
 
 // tile boxes (FP32, leaf frame) and hmax, one warp per tile
 __global__ void k_tile_boxes(int64_t n_tiles, const int64_t* n_tiles_dev, Tiling T,
-                             const double* state, const int8_t* pshift, double L) {
+                             const double* state, const int8_t* pshift, double L,
+                             const uint8_t* ghost) {
   int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (t >= *n_tiles_dev) return;
@@ -422,9 +423,13 @@ __global__ void k_tile_boxes(int64_t n_tiles, const int64_t* n_tiles_dev, Tiling
     }
     hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
   }
+  // owned-target skip flag (only when built with a ghost array)
+  bool own = lane < n && ghost && ghost[T.tperm[ks + lane]] == 0;
+  unsigned ob = __ballot_sync(0xffffffffu, own);
   if (lane == 0) {
     T.tile_lo[t] = make_float4(lo[0], lo[1], lo[2], hm);
     T.tile_hi[t] = make_float4(hi[0], hi[1], hi[2], 0.0f);
+    T.tile_skip[t] = (ghost && ob == 0u) ? 1 : 0;
   }
 }
 
@@ -780,6 +785,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   const Tiling& T = a.T;
   int A = T.tile_leaf[t];
   if (a.skip_leaf && a.skip_leaf[A]) return;
+  if (a.skip_tiles && T.tile_skip[t]) return;  // owned_targets: no owned member
   int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
   if (e0 == e1) return;
   int n_t = T.tile_n[t];
@@ -1062,6 +1068,7 @@ void carve_tiling(Arena& ws, int64_t n, int64_t nl, Tiling& T, int tile_max, int
   T.tile_lo = ws.take<float4>(tc); T.tile_hi = ws.take<float4>(tc);
   T.origin = ws.take<double>(3 * nl + 3);
   T.overflow = ws.take<int>(1);
+  T.tile_skip = ws.take<uint8_t>(tc);
 }
 
 int kid_selects_gas(int kid) {
@@ -1071,7 +1078,8 @@ int kid_selects_gas(int kid) {
 
 int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t* leaf_end,
                  const double* state, const int8_t* pshift, double L, int sel,
-                 int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err) {
+                 int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err,
+                 const uint8_t* ghost) {
   if (ws.dry) {
     Arena s = ws;
     exclusive_scan_i64(nullptr, nullptr, nl, nullptr, s, st, err);
@@ -1099,7 +1107,8 @@ int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t
                                                          L, sel);
   HB_LAUNCH_CHECK();
   int64_t tcap = T.n_tiles_cap;
-  k_tile_boxes<<<grid_for(tcap * 32, 256), 256, 0, st>>>(tcap, n_tiles_dev, T, state, pshift, L);
+  k_tile_boxes<<<grid_for(tcap * 32, 256), 256, 0, st>>>(tcap, n_tiles_dev, T, state, pshift, L,
+                                                       ghost);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
@@ -1241,7 +1250,7 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                                                               a->leaf_start, a->leaf_end, a->W2,
                                                               w.dev_cnt);
   HB_LAUNCH_CHECK();
-  EvalDev d;
+  EvalDev d = {};
   d.T = T; d.ent_ptr = w.ent_ptr; d.ent_src = w.s_src; d.ent_code = w.s_code;
   d.P0 = w.P0; d.P1 = w.P1; d.P2 = w.P2; d.state = a->state; d.pshift = a->pshift;
   d.L = a->side_length; d.reach = a->reach;

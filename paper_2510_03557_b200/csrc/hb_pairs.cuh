@@ -227,6 +227,7 @@ struct Tiling {
   float4* tile_hi;
   double* origin;       // (n_leaves,3)
   int* overflow;        // device flag: a leaf exceeded kTileBuildCap
+  uint8_t* tile_skip;   // (cap) 1: no owned member (set when built with a ghost array)
 };
 
 // Everything one pair-kernel launch reads.
@@ -248,6 +249,7 @@ struct EvalDev {
   int64_t* out_int;
   int write_out;
   const uint8_t* skip_leaf;  // receivers to skip (ghost-only leaves), or null
+  int skip_tiles;            // 1: skip tiles with T.tile_skip set (owned_targets)
   unsigned long long* in_count;
   unsigned long long* err_key;  // min (entry*4 + kind)
 };
@@ -261,7 +263,8 @@ __host__ __device__ inline int tiles_for(int m, int tile_max, int even) {
 }
 int build_tiling(Tiling& T, int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
                  const double* state, const int8_t* pshift, double L, int sel,
-                 int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err);
+                 int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err,
+                 const uint8_t* ghost = nullptr);
 int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, const double* state,
                  const int8_t* pshift, const double* aux, int naux, double L, float4* P0,
                  float4* P1, float4* P2, cudaStream_t st, HbError* err);

@@ -36,6 +36,7 @@ struct SphDev {
   double *ncount, *rho, *moments, *hydro;
   unsigned long long* err_key;
   const uint8_t* skip_leaf;  // pass B: ghost-only receivers to skip (or null)
+  int skip_tiles;            // pass B: skip tiles without an owned member
 };
 
 __device__ __forceinline__ double exact_r2_rows(const double* st, const int8_t* ps, double L,
@@ -236,6 +237,7 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   const Tiling& T = a.T;
   int A = T.tile_leaf[t];
   if (a.skip_leaf && a.skip_leaf[A]) return;
+  if (a.skip_tiles && T.tile_skip[t]) return;
   int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
   if (e0 == e1) return;
   int n_t = T.tile_n[t];
@@ -368,6 +370,7 @@ int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   a.ncount = s.ncount; a.rho = s.rho; a.moments = s.moments; a.hydro = s.hydro;
   a.err_key = s.err_key;
   a.skip_leaf = s.skip_leaf;
+  a.skip_tiles = s.skip_tiles;
   unsigned grid = grid_for(s.T->n_tiles_cap, kSphWarps);
   if (pass == 0) k_sph_density<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   else k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);

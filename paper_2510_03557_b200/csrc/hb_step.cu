@@ -265,7 +265,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   {
     Arena s = ws;
     int rc = build_tiling(w.Tg, n_seg, seg_s, seg_e, w.state, a->image_shift, a->side_length, 1,
-                          w.ntg, s, st, err);
+                          w.ntg, s, st, err, a->owned_targets ? a->ghost : nullptr);
     if (rc) return rc;
     if ((a->passes & HB_PASS_GRAVITY) && use_leaf_gravity) {
       Arena s2 = ws;
@@ -311,6 +311,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   sa.alpha = a->visc_alpha; sa.beta = a->visc_beta; sa.err_key = w.err_key;
   sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = a->crk_moments; sa.hydro = a->hydro;
   sa.skip_leaf = (a->ghost_density && !sph_bins) ? w.ghost_only : nullptr;
+  sa.skip_tiles = a->owned_targets ? 1 : 0;
   d.skip_leaf = a->ghost_density ? w.ghost_only : nullptr;
   // 4. pass A: neighbour count + density (hb/hydro.py:223-227, 60-84), EOS (48-57)
   if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY)) {
@@ -370,6 +371,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
     gb.half_warp = a->gravity_mode == 2;
     gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
+    gb.ghost = a->owned_targets ? a->ghost : nullptr;
     gb.t0 = tm.on ? tm.kv[0] : nullptr;
     gb.t1 = tm.on ? tm.kv[1] : nullptr;
     Arena s = ws;

@@ -294,7 +294,7 @@ class DistributedRank:
         self.n_owned = n_owned
         if self.engine is None:
             self.engine = ResidentRank(None, self.cfg, fields=new, ghost_density=self.world > 1,
-                                       h_range=self.h_range)
+                                       h_range=self.h_range, owned_targets=self.world > 1)
         else:
             self.engine.set_fields(new, self.h_range)
         return new

@@ -47,7 +47,7 @@ class HbStepArgs(C.Structure):
                    ("r_cut", C.c_double), ("softening", C.c_double), ("eos_gamma", C.c_double),
                    ("visc_alpha", C.c_double), ("visc_beta", C.c_double), ("passes", C.c_int32),
                    ("timing", C.c_int32), ("gravity_mode", C.c_int32),
-                   ("ghost_density", C.c_int32),
+                   ("ghost_density", C.c_int32), ("owned_targets", C.c_int32),
                    ("list_capacity", C.c_int64), ("fields_ready_event", P),
                    ("sph_done_event", P),
                    ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
@@ -87,12 +87,16 @@ class ResidentRank:
     """One rank's working set on the current CUDA device."""
 
     def __init__(self, particles: ParticleSet | None, cfg: StepConfig, fields: dict | None = None,
-                 ghost_density: bool = False, h_range: tuple | None = None):
+                 ghost_density: bool = False, h_range: tuple | None = None,
+                 owned_targets: bool = False):
         """Either host ``particles`` or device ``fields`` (dict of STEP_FIELDS
-        tensors).  ``h_range`` = (h_min_gas, h_max) when given as fields."""
+        tensors).  ``h_range`` = (h_min_gas, h_max) when given as fields.
+        ``owned_targets``: gravity / CRK / hydro outputs are needed for owned
+        rows only (ghost rows read 0 in tiles without an owned row)."""
         torch = N.torch_cuda()
         self.cfg = cfg
         self.ghost_density = ghost_density
+        self.owned_targets = owned_targets
         lo, hi, nb, width, periodic = mesh_geometry(cfg.box, cfg.bin_width, cfg.bounds_lo,
                                                     cfg.bounds_hi)
         self.lo, self.nb, self.width, self.periodic = lo, nb, width, periodic
@@ -191,6 +195,7 @@ class ResidentRank:
         a.passes = int(passes)
         a.timing = 1 if timing else 0
         a.ghost_density = 1 if self.ghost_density else 0
+        a.owned_targets = 1 if self.owned_targets else 0
         a.gravity_mode = int(os.environ.get("HB_GRAVITY_MODE", "0"))
         a.fields_ready_event = P(fields_ready.cuda_event) if fields_ready is not None else P(0)
         a.sph_done_event = P(sph_done.cuda_event) if sph_done is not None else P(0)

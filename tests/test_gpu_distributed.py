@@ -72,7 +72,8 @@ def test_emulated_ranks_match_single_domain(world, periodic_unsplit, oracle):
                                           rs.global_id[own_ref])
         from paper_2510_03557_b200.resident import ResidentRank
         eng = ResidentRank(None, rk.cfg, fields=new, ghost_density=world > 1 or not periodic_unsplit,
-                           h_range=(h_min, h_max))
+                           h_range=(h_min, h_max),
+                           owned_targets=world > 1 or not periodic_unsplit)
         out = eng.step()
         flds = eng.fields()
         gid = flds["global_id"].cpu().numpy()
