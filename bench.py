@@ -320,7 +320,8 @@ def run_gpu_arm(args):
     if world == 1:
         src_fields = {f: getattr(p, f) for f in STEP_FIELDS}
     else:
-        src_fields = {f: rr.owned_fields[f].cpu().numpy() for f in STEP_FIELDS}
+        own = rr.owned_fields["ghost"] == 0  # the rank set's owned rows are the host inputs
+        src_fields = {f: rr.owned_fields[f][own].cpu().numpy() for f in STEP_FIELDS}
     pinned_in = {f: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
                  for f, a in src_fields.items()}
     eng = rr if world == 1 else rr.engine

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 3
+#define HB_ABI_VERSION 4
 
 /* status codes; map onto hb/errors.py */
 enum HbStatus {
@@ -311,6 +311,32 @@ int hb_halo_unpack(int64_t m, const void* recs, int32_t key_bits, int64_t row0, 
                    void* stream, HbError* err);
 int hb_halo_resolve_sources(int64_t n_owned, int64_t m, const int64_t* global_id,
                             int64_t* ghost_src, void* stream, HbError* err);
+/* Fused exchange halves (one C call each; the per-call host round trips, not
+ * the data, dominate the exchange at 1-4 M rows per rank).  HbFieldSet: the
+ * SoA rank fields (all device pointers).
+ * hb_halo_pack_all: select (count) -> counts to counts_host (one stream sync)
+ * -> device scan -> select (emit) -> pack.  The source may hold ghost rows
+ * (only ghost == 0 rows are sources).  Returns HB_OVERFLOW, with counts_host
+ * filled, when the records exceed cap (caller grows rows/slots/send, retries).
+ * hb_halo_unpack_keep: dst rows [0, n_stay) = the stay-flagged src rows in
+ * row order, then the m received records from row n_stay as hb_halo_unpack. */
+typedef struct HbFieldSet {
+  double *pos, *vel, *mass, *smoothing, *internal_energy, *density;
+  uint8_t *species, *ghost;
+  int8_t* image_shift;
+  int64_t *global_id, *ghost_src;
+} HbFieldSet;
+size_t hb_halo_pack_all_workspace(int32_t n_ranks);
+int hb_halo_pack_all(int64_t n, const HbFieldSet* src, const int32_t g[3], double side_length,
+                     double overload_width, int32_t self, int32_t periodic_unsplit,
+                     uint64_t* counts, uint64_t* counts_host, uint8_t* stay, int64_t cap,
+                     int64_t* rows, int32_t* slots, void* send, void* ws, size_t ws_bytes,
+                     void* stream, HbError* err);
+size_t hb_halo_unpack_keep_workspace(int64_t n_src, int64_t m);
+int hb_halo_unpack_keep(int64_t m, const void* recs, int32_t key_bits, int64_t n_src,
+                        const HbFieldSet* src, const uint8_t* stay, int64_t n_stay,
+                        const HbFieldSet* dst, void* ws, size_t ws_bytes, void* stream,
+                        HbError* err);
 /* Row indices of the nonzero flags in row order (a device compaction whose
  * size the caller already knows -- no host sync). */
 size_t hb_flag_indices_workspace(int64_t n);

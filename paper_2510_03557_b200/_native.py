@@ -23,6 +23,22 @@ _lib = None
 _lock = threading.Lock()
 
 
+FIELDSET_ORDER = ("pos", "vel", "mass", "smoothing", "internal_energy", "density", "species",
+                  "ghost", "image_shift", "global_id", "ghost_src")
+
+
+class HbFieldSet(C.Structure):
+    """include/hb.h HbFieldSet: SoA rank fields (device pointers)."""
+    _fields_ = [(f, C.c_void_p) for f in FIELDSET_ORDER]
+
+
+def fieldset(fields: dict) -> "HbFieldSet":
+    fs = HbFieldSet()
+    for f in FIELDSET_ORDER:
+        setattr(fs, f, ptr(fields[f]))
+    return fs
+
+
 class HbError(C.Structure):
     _fields_ = [("status", C.c_int32), ("cuda_err", C.c_int32), ("leaf_a", C.c_int64),
                 ("leaf_b", C.c_int64), ("msg", C.c_char * 224)]
@@ -97,6 +113,16 @@ def lib():
             lb.hb_flag_indices_workspace.argtypes = [C.c_int64]
             lb.hb_flag_indices.argtypes = [C.c_int64, P, P, P, C.c_size_t, P, P]
             lb.hb_crk_solve.argtypes = [C.c_int64, P, C.c_int64, P, C.c_double, P, P, P, P, P]
+            lb.hb_halo_pack_all_workspace.restype = C.c_size_t
+            lb.hb_halo_pack_all_workspace.argtypes = [C.c_int32]
+            lb.hb_halo_pack_all.argtypes = [C.c_int64, C.POINTER(HbFieldSet), C.c_int32 * 3,
+                                            C.c_double, C.c_double, C.c_int32, C.c_int32, P, P,
+                                            P, C.c_int64, P, P, P, P, C.c_size_t, P, P]
+            lb.hb_halo_unpack_keep_workspace.restype = C.c_size_t
+            lb.hb_halo_unpack_keep_workspace.argtypes = [C.c_int64, C.c_int64]
+            lb.hb_halo_unpack_keep.argtypes = [C.c_int64, P, C.c_int32, C.c_int64,
+                                               C.POINTER(HbFieldSet), P, C.c_int64,
+                                               C.POINTER(HbFieldSet), P, C.c_size_t, P, P]
             _lib = lb
         return _lib
 
@@ -107,8 +133,9 @@ EXPORTS = ("hb_abi_version", "hb_launch_count", "hb_device_query", "hb_build_mes
            "hb_assemble_lists_workspace", "hb_assemble_lists", "hb_eval_pairs_workspace",
            "hb_eval_pairs", "hb_crk_solve", "hb_force_step_workspace", "hb_force_step",
            "hb_halo_record_bytes", "hb_halo_select", "hb_halo_pack", "hb_halo_unpack_workspace",
-           "hb_halo_unpack", "hb_halo_resolve_sources", "hb_flag_indices_workspace",
-           "hb_flag_indices")
+           "hb_halo_unpack", "hb_halo_resolve_sources", "hb_halo_pack_all_workspace",
+           "hb_halo_pack_all", "hb_halo_unpack_keep_workspace", "hb_halo_unpack_keep",
+           "hb_flag_indices_workspace", "hb_flag_indices")
 
 
 def torch_cuda():

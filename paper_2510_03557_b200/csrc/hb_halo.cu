@@ -235,6 +235,23 @@ __global__ void k_flags_to_i64(int64_t n, const uint8_t* flags, int64_t* out) {
   if (i < n) out[i] = flags[i] ? 1 : 0;
 }
 
+// kept rows: dst[pos[i]] = src[i] for every flagged row, all fields in one pass
+__global__ void k_keep_gather(int64_t n, const uint8_t* flags, const int64_t* pos, HbFieldSet s,
+                              HbFieldSet d) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !flags[i]) return;
+  int64_t o = pos[i];
+  for (int c = 0; c < 3; ++c) {
+    d.pos[3 * o + c] = s.pos[3 * i + c];
+    d.vel[3 * o + c] = s.vel[3 * i + c];
+    d.image_shift[3 * o + c] = s.image_shift[3 * i + c];
+  }
+  d.mass[o] = s.mass[i]; d.smoothing[o] = s.smoothing[i];
+  d.internal_energy[o] = s.internal_energy[i]; d.density[o] = s.density[i];
+  d.species[o] = s.species[i]; d.ghost[o] = s.ghost[i];
+  d.global_id[o] = s.global_id[i]; d.ghost_src[o] = s.ghost_src[i];
+}
+
 }  // namespace hb
 
 using namespace hb;
@@ -351,4 +368,102 @@ extern "C" int hb_halo_resolve_sources(int64_t n_owned, int64_t m, const int64_t
                                                                         ghost_src);
   HB_LAUNCH_CHECK();
   return HB_OK;
+}
+
+extern "C" size_t hb_halo_pack_all_workspace(int32_t n_ranks) {
+  Arena ws;
+  ws.dry = true;
+  int64_t nslot = (int64_t)n_ranks * 28;
+  ws.take<int64_t>(nslot + 1);
+  exclusive_scan_i64(nullptr, nullptr, nslot, nullptr, ws, nullptr, nullptr);
+  return ws.used + 1024;
+}
+
+extern "C" int hb_halo_pack_all(int64_t n, const HbFieldSet* src, const int32_t g[3],
+                                double side_length, double overload_width, int32_t self,
+                                int32_t periodic_unsplit, uint64_t* counts, uint64_t* counts_host,
+                                uint8_t* stay, int64_t cap, int64_t* rows, int32_t* slots,
+                                void* send, void* wsp, size_t ws_bytes, void* stream,
+                                HbError* err) {
+  if (err) *err = HbError{};
+  cudaStream_t st = (cudaStream_t)stream;
+  DomGrid G;
+  for (int d = 0; d < 3; ++d) G.g[d] = g[d];
+  G.L = side_length;
+  G.w = overload_width;
+  int64_t nslot = (int64_t)g[0] * g[1] * g[2] * 28;
+  Arena ws;
+  ws.base = (char*)wsp; ws.cap = ws_bytes;
+  int64_t* fill = ws.take<int64_t>(nslot + 1);
+  if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (halo pack)");
+  int* drift = (int*)(counts + nslot);
+  HB_CUDA_TRY(cudaMemsetAsync(counts, 0, (nslot + 2) * sizeof(uint64_t), st));
+  if (n > 0) {
+    k_halo_select<<<grid_for(n, 128), 128, 0, st>>>(
+        n, src->pos, src->ghost, G, self, periodic_unsplit, 0, (unsigned long long*)counts,
+        nullptr, nullptr, nullptr, drift, stay);
+    HB_LAUNCH_CHECK();
+  }
+  HB_CUDA_TRY(cudaMemcpyAsync(counts_host, counts, (nslot + 2) * sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, st));
+  HB_CUDA_TRY(cudaStreamSynchronize(st));
+  int64_t m = 0;
+  for (int64_t s = 0; s < nslot; ++s) m += (int64_t)counts_host[s];
+  if ((counts_host[nslot] & 0xFFFFFFFFull) != 0) return HB_OK;  // drift: caller raises
+  if (m > cap) return set_err(err, HB_OVERFLOW, "halo records exceed the buffer capacity");
+  if (m == 0) return HB_OK;
+  {
+    Arena s2 = ws;
+    int rc = exclusive_scan_i64((const int64_t*)counts, fill, nslot, nullptr, s2, st, err);
+    if (rc) return rc;
+  }
+  k_halo_select<<<grid_for(n, 128), 128, 0, st>>>(
+      n, src->pos, src->ghost, G, self, periodic_unsplit, 1, (unsigned long long*)counts,
+      (unsigned long long*)fill, rows, slots, drift, stay);
+  HB_LAUNCH_CHECK();
+  G.w = 0.0;
+  k_halo_pack<<<grid_for(m, 256), 256, 0, st>>>(m, rows, slots, src->pos, src->vel, src->mass,
+                                                src->smoothing, src->internal_energy,
+                                                src->density, src->species, src->global_id, G,
+                                                self, (HaloRec*)send);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
+
+extern "C" size_t hb_halo_unpack_keep_workspace(int64_t n_src, int64_t m) {
+  Arena ws;
+  ws.dry = true;
+  ws.take<int64_t>(n_src + 1);
+  exclusive_scan_i64(nullptr, nullptr, n_src, nullptr, ws, nullptr, nullptr);
+  size_t a = ws.used;
+  Arena w2;
+  w2.dry = true;
+  w2.take<uint64_t>(m + 1);
+  w2.take<uint32_t>(m + 1);
+  radix_sort_u64_u32(nullptr, nullptr, m, 64, w2, nullptr, nullptr);
+  return (a > w2.used ? a : w2.used) + 1024;
+}
+
+extern "C" int hb_halo_unpack_keep(int64_t m, const void* recs, int32_t key_bits, int64_t n_src,
+                                   const HbFieldSet* src, const uint8_t* stay, int64_t n_stay,
+                                   const HbFieldSet* dst, void* wsp, size_t ws_bytes,
+                                   void* stream, HbError* err) {
+  if (err) *err = HbError{};
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_stay > 0 && n_src > 0) {
+    Arena ws;
+    ws.base = (char*)wsp; ws.cap = ws_bytes;
+    int64_t* pos = ws.take<int64_t>(n_src + 1);
+    if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (halo keep)");
+    k_flags_to_i64<<<grid_for(n_src, 256), 256, 0, st>>>(n_src, stay, pos);
+    HB_LAUNCH_CHECK();
+    int rc = exclusive_scan_i64(pos, pos, n_src, nullptr, ws, st, err);
+    if (rc) return rc;
+    k_keep_gather<<<grid_for(n_src, 256), 256, 0, st>>>(n_src, stay, pos, *src, *dst);
+    HB_LAUNCH_CHECK();
+  }
+  return hb_halo_unpack(m, recs, key_bits, n_stay, dst->pos, dst->vel, dst->mass, dst->smoothing,
+                        dst->internal_energy, dst->density, dst->species, dst->ghost,
+                        dst->image_shift, dst->global_id, dst->ghost_src, wsp, ws_bytes, stream,
+                        err);
 }

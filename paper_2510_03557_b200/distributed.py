@@ -138,46 +138,53 @@ class HaloExchange:
         rank mesh and at most 2 ranks along every split axis."""
         return self.periodic_unsplit and all(g <= 2 for g in self.grid)
 
+    def _full(self, name, n, dtype, shape=()):
+        """Whole capacity-backed buffer (>= n rows) and its capacity."""
+        self._buf(name, n, dtype, shape)
+        b = self._bufs[name]
+        return b, int(b.shape[0])
+
     def pack(self, fields: dict):
-        """Select + pack.  Returns (send bytes, slot counts (world, 28) numpy,
-        stay flags or None, number of staying rows).  One host sync (counts)."""
+        """Select + pack in one C call (hb_halo_pack_all: one host sync for the
+        counts).  `fields` may be the whole previous rank set: only its owned
+        rows (ghost == 0) are sources.  Returns (send bytes, slot counts
+        (world, 28) numpy, stay flags or None, number of staying rows)."""
         import torch
         n = int(fields["pos"].shape[0])
         nslot = self.world * 28
         g = (C.c_int32 * 3)(*self.grid)
         counts = self._buf("counts", nslot + 2, torch.int64)
-        counts.zero_()
-        drift = counts[nslot:nslot + 1].view(torch.int32)[:1]
+        if getattr(self, "_counts_host", None) is None or self._counts_host.numel() < nslot + 2:
+            self._counts_host = torch.zeros(nslot + 2, dtype=torch.int64).pin_memory()
+        ch_t = self._counts_host
         stay = self._buf("stay", max(n, 1), torch.uint8) if self.fast else None
-        err = N.HbError()
-        st = N.stream_ptr()
+        ws = self._buf("pack_ws", int(self.lib.hb_halo_pack_all_workspace(self.world)), torch.uint8)
+        fs = N.fieldset(fields)
         pu = 1 if self.periodic_unsplit else 0
-        N.check(self.lib.hb_halo_select(n, N.ptr(fields["pos"]), N.ptr(fields["ghost"]), g,
-                                        float(self.box.side_length), self.w, self.rank, pu, 0,
-                                        N.ptr(counts), N.ptr(counts), None, None, N.ptr(drift),
-                                        N.ptr(stay), st, C.byref(err)), err)
-        ch_all = counts.cpu().numpy()
+        cap = getattr(self, "_rec_cap", max(1024, n // 2))
+        while True:
+            rows, cap_r = self._full("rows", cap, torch.int64)
+            slots, cap_s = self._full("slots", cap, torch.int32)
+            send, cap_b = self._full("send", cap * self.rec, torch.uint8)
+            cap = min(cap_r, cap_s, cap_b // self.rec)
+            err = N.HbError()
+            st = self.lib.hb_halo_pack_all(
+                n, C.byref(fs), g, float(self.box.side_length), self.w, self.rank, pu,
+                N.ptr(counts), N.ptr(ch_t), N.ptr(stay), cap, N.ptr(rows), N.ptr(slots),
+                N.ptr(send), N.ptr(ws), C.c_size_t(ws.numel()), N.stream_ptr(), C.byref(err))
+            if st == N.HB_OVERFLOW:
+                cap = int(int(ch_t[:nslot].sum()) * 1.25) + 1024
+                continue
+            N.check(st, err, "halo pack")
+            break
+        self._rec_cap = cap
+        ch_all = ch_t.numpy().copy()
         ch = ch_all[:nslot]
         if int(ch_all[nslot]) & 0xFFFFFFFF:
             raise DriftError("particle crossed more than one domain in one PM step")
         n_stay = int(ch_all[nslot + 1])
-        offs = np.concatenate([[0], np.cumsum(ch)]).astype(np.int64)
-        m = int(offs[-1])
-        rows = self._buf("rows", max(m, 1), torch.int64)
-        slots = self._buf("slots", max(m, 1), torch.int32)
-        fill = self._buf("fill", nslot, torch.int64)
-        fill.copy_(torch.from_numpy(offs[:-1].copy()), non_blocking=False)
-        N.check(self.lib.hb_halo_select(n, N.ptr(fields["pos"]), N.ptr(fields["ghost"]), g,
-                                        float(self.box.side_length), self.w, self.rank, pu, 1,
-                                        N.ptr(counts), N.ptr(fill), N.ptr(rows), N.ptr(slots),
-                                        N.ptr(drift), N.ptr(stay), st, C.byref(err)), err)
-        send = self._buf("send", max(m, 1) * self.rec, torch.uint8)
-        N.check(self.lib.hb_halo_pack(m, N.ptr(rows), N.ptr(slots), N.ptr(fields["pos"]),
-                                      N.ptr(fields["vel"]), N.ptr(fields["mass"]),
-                                      N.ptr(fields["smoothing"]), N.ptr(fields["internal_energy"]),
-                                      N.ptr(fields["density"]), N.ptr(fields["species"]),
-                                      N.ptr(fields["global_id"]), g, float(self.box.side_length),
-                                      self.rank, N.ptr(send), st, C.byref(err)), err)
+        m = int(ch.sum())
+        self._counts_dev = counts[:nslot]
         return (send[:m * self.rec], ch.reshape(self.world, 28),
                 stay[:n] if stay is not None else None, n_stay)
 
@@ -202,18 +209,23 @@ class HaloExchange:
         m = int(recv.numel()) // self.rec
         n0 = int(keep[2]) if keep is not None else 0
         out = self._field_set(max(n0 + m, 1))
-        if keep is not None:  # staying owned rows, current order
-            src, stay, n_stay = keep
-            idx = self.flag_indices(stay, n_stay, "keep_idx")
-            for f in out:
-                torch.index_select(src[f], 0, idx, out=out[f][:n0])
-        ws = self._buf("unpack_ws", int(self.lib.hb_halo_unpack_workspace(m)), torch.uint8)
         err = N.HbError()
         st = N.stream_ptr()
-        N.check(self.lib.hb_halo_unpack(m, N.ptr(recv), self.key_bits, n0, *[N.ptr(out[f]) for f in (
-            "pos", "vel", "mass", "smoothing", "internal_energy", "density", "species", "ghost",
-            "image_shift", "global_id", "ghost_src")], N.ptr(ws), C.c_size_t(ws.numel()), st,
-            C.byref(err)), err)
+        if keep is not None:  # staying owned rows (current order), then arrivals: one C call
+            src, stay, n_stay = keep
+            n_src = int(src["pos"].shape[0])
+            ws = self._buf("unpack_ws", int(self.lib.hb_halo_unpack_keep_workspace(n_src, m)),
+                           torch.uint8)
+            fs_src, fs_dst = N.fieldset(src), N.fieldset(out)
+            N.check(self.lib.hb_halo_unpack_keep(m, N.ptr(recv), self.key_bits, n_src,
+                                                 C.byref(fs_src), N.ptr(stay), n0,
+                                                 C.byref(fs_dst), N.ptr(ws),
+                                                 C.c_size_t(ws.numel()), st, C.byref(err)), err)
+        else:
+            ws = self._buf("unpack_ws", int(self.lib.hb_halo_unpack_workspace(m)), torch.uint8)
+            N.check(self.lib.hb_halo_unpack(m, N.ptr(recv), self.key_bits, n0, *[
+                N.ptr(out[f]) for f in N.FIELDSET_ORDER], N.ptr(ws), C.c_size_t(ws.numel()), st,
+                C.byref(err)), err)
         out = {k: v[:n0 + m] for k, v in out.items()}
         if n_owned is None:
             n_owned = int((out["ghost"] == 0).sum().item())
@@ -230,8 +242,11 @@ class HaloExchange:
         import torch.distributed as dist
         if self.world == 1:
             return send, slot_counts
-        sc = torch.from_numpy(np.ascontiguousarray(slot_counts.reshape(-1))).cuda()
-        rc = torch.empty_like(sc)
+        sc = getattr(self, "_counts_dev", None)  # pack's device counts: no H2D copy
+        if sc is None or sc.numel() != slot_counts.size:
+            sc = torch.from_numpy(np.ascontiguousarray(slot_counts.reshape(-1))).cuda()
+        self._counts_dev = None
+        rc = self._buf("recv_counts", sc.numel(), torch.int64)
         dist.all_to_all_single(rc, sc, group=self.group)
         recv_slots = rc.cpu().numpy().reshape(self.world, 28)
         send_bytes = [int(x) * self.rec for x in slot_counts.sum(axis=1)]
@@ -314,14 +329,6 @@ class DistributedRank:
             torch.cuda.synchronize()
             self.engine.last["ms_phase"]["exchange"] = e0.elapsed_time(e1)
         fields = self.engine.fields()
-        # keep only owned rows (leaf order) as next step's owned set
-        n_own = self.n_owned
-        own_flags = (fields["ghost"] == 0).to(torch.uint8)
-        idx = self.halo.flag_indices(own_flags, n_own, "own_idx")
-        store = getattr(self, "_owned_store", None)
-        if store is None or store["pos"].shape[0] < n_own:
-            store = empty_fields(int(n_own * 1.2) + 1024)
-            self._owned_store = store
-        self.owned_fields = {k: torch.index_select(v, 0, idx, out=store[k][:n_own])
-                             for k, v in fields.items()}
+        # next exchange reads the whole rank set: only its owned rows are sources
+        self.owned_fields = fields
         return out, fields
