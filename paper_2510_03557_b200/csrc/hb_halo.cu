@@ -128,6 +128,21 @@ __global__ void k_halo_select(int64_t n, const double* pos, const uint8_t* ghost
     }
   }
   int oc[3] = {own / (G.g[1] * G.g[2]), (own / G.g[2]) % G.g[1], own % G.g[2]};
+  {  // interior rows (farther than w, with margin, from every face of the owner
+     // cell on the axes that can have images) have no ghost copies: skip the
+     // FP64 enumeration.  The margin (1e-9 L) dwarfs its rounding, so the
+     // enumeration below could not have found a candidate either.
+    bool interior = true;
+    double margin = G.w + 1e-9 * G.L;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (periodic_unsplit && G.g[d] == 1) continue;
+      double lo = (G.L * (double)oc[d]) / (double)G.g[d];
+      double hi = (G.L * (double)(oc[d] + 1)) / (double)G.g[d];
+      interior = interior && (p[d] - lo > margin) && (hi - p[d] > margin);
+    }
+    if (interior) return;
+  }
   int cand_c[3][6], cand_s[3][6], nc[3];
   for (int d = 0; d < 3; ++d) {
     nc[d] = 0;
