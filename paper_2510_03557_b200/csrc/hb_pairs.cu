@@ -496,8 +496,11 @@ __global__ void k_expand(int64_t n_pairs, int mirror, const int64_t* pa, const i
   int sx = ps[3 * i], sy = ps[3 * i + 1], sz = ps[3 * i + 2];
   int code = (sx + 1) * 9 + (sy + 1) * 3 + (sz + 1);
   keys[i] = (uint64_t)a; vals[i] = (uint32_t)i;
-  e_src[i] = (int32_t)b; e_code[i] = code | (1 << 8); e_orig[i] = (int32_t)i;
-  if (mirror && (a != b || code != 13)) {
+  // mirror 2 (deterministic): no reversed entries; partners of a != b or
+  // shifted entries receive the mirrored quanta by scatter (bit 9)
+  int scat = (mirror == 2 && (a != b || code != 13)) ? (1 << 9) : 0;
+  e_src[i] = (int32_t)b; e_code[i] = code | (1 << 8) | scat; e_orig[i] = (int32_t)i;
+  if (mirror == 1 && (a != b || code != 13)) {
     int64_t j = n_pairs + rev_off[i];
     keys[j] = (uint64_t)b; vals[j] = (uint32_t)j;
     e_src[j] = (int32_t)a; e_code[j] = 26 - code; e_orig[j] = (int32_t)i;
@@ -630,27 +633,52 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
         in = exact_r2(a, row_i, row_j, meta.y & 31) <= reach2_64;
       }
       if (!LEAN && !a.include_self && meta.x == k_i && (meta.y & 31) == 13) in = false;
-      if (!in) continue;
-      if (!LEAN && live && (meta.y >> 8)) nin += 1;
-      float phi[NC];
-      if (KID == KID_NEIGHBOR_COUNT) {
-        bool c4 = r2 <= thr_n;
-        if (live && fabsf(r2 - thr_n) <= thr_n * 2.44140625e-4f) {
-          if (row_j < 0) row_j = T.tperm[meta.x];
-          c4 = exact_r2(a, row_i, row_j, meta.y & 31) <= thr_n64;
-        }
-        phi[0] = c4 ? 1.0f : 0.0f;
-      } else {
-        P::pair(ti, rec, dx, dy, dz, r2, a.pp, phi);
-      }
+      long long qv[DET ? NC : 1];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (DET) {
-          float v = phi[c] * a.scale[c];
-          if (!(fabsf(v) <= 7.2057594e16f)) bad |= (v == v && fabsf(v) != INFINITY) ? 2 : 1;
-          else iacc[c] += __float2ll_rn(v);
+      for (int c = 0; c < (DET ? NC : 1); ++c) qv[c] = 0;
+      if (in) {
+        if (!LEAN && live && ((meta.y >> 8) & 1)) nin += 1;
+        float phi[NC];
+        if (KID == KID_NEIGHBOR_COUNT) {
+          bool c4 = r2 <= thr_n;
+          if (live && fabsf(r2 - thr_n) <= thr_n * 2.44140625e-4f) {
+            if (row_j < 0) row_j = T.tperm[meta.x];
+            c4 = exact_r2(a, row_i, row_j, meta.y & 31) <= thr_n64;
+          }
+          phi[0] = c4 ? 1.0f : 0.0f;
         } else {
-          acc[c] += phi[c];
+          P::pair(ti, rec, dx, dy, dz, r2, a.pp, phi);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (DET) {
+            float v = phi[c] * a.scale[c];
+            if (!(fabsf(v) <= 7.2057594e16f)) bad |= (v == v && fabsf(v) != INFINITY) ? 2 : 1;
+            else qv[c] = __float2ll_rn(v);
+            iacc[c] += qv[c];
+          } else {
+            acc[c] += phi[c];
+          }
+        }
+      }
+      // deterministic mirror: the partner row gets chan_sign * q[mirror_map]
+      // summed over this warp's live targets, one integer atomic per channel
+      // (integer sums are order-independent: still run-to-run deterministic)
+      if (DET && !LEAN && a.scatter && ((meta.y >> 9) & 1)) {
+        int64_t prow = T.tperm[meta.x];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          long long m = 0;
+          if (live && c < a.nchan) {
+            int mc = a.mmap[c];
+#pragma unroll
+            for (int k = 0; k < NC; ++k)
+              if (k == mc) m = (long long)a.csign[c] * qv[k];
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+          if (lane == 0 && m != 0 && c < a.nchan && a.write_out)
+            atomicAdd((unsigned long long*)&a.out_int[prow * a.nchan + c], (unsigned long long)m);
         }
       }
     }
@@ -736,7 +764,13 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
     }
   }
   if (live && a.write_out) {
-    if (DET) {
+    if (DET && !LEAN && a.scatter) {  // partners' scatter lands in these rows concurrently
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c < a.nchan && iacc[c] != 0)
+          atomicAdd((unsigned long long*)&a.out_int[row_i * a.nchan + c],
+                    (unsigned long long)iacc[c]);
+    } else if (DET) {
 #pragma unroll
       for (int c = 0; c < NC; ++c)
         if (c < a.nchan) a.out_int[row_i * a.nchan + c] += iacc[c];
@@ -1203,7 +1237,12 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   int64_t nl = a->n_leaves;
   // receiver CSR (stable: deterministic accumulation order)
   int64_t n_rev = 0;
-  if (a->mirror) {
+  // mirror: relaxed -> receiver expansion (every ordered pair gathered on its
+  // receiver, fixed order); deterministic -> each listed pair evaluated once and
+  // the partner gets chan_sign * q[mirror_map] by integer scatter, so the two
+  // sides' quanta cancel exactly as in hb/kernels.py:378-382
+  int mm = a->mirror ? (a->deterministic ? 2 : 1) : 0;
+  if (mm == 1) {
     k_rev_flags<<<grid_for(a->n_pairs, 256), 256, 0, st>>>(a->n_pairs, a->pair_a, a->pair_b,
                                                            a->pair_shift, w.rev_flag);
     HB_LAUNCH_CHECK();
@@ -1214,7 +1253,7 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     HB_CUDA_TRY(cudaStreamSynchronize(st));
   }
   int64_t En = a->n_pairs + n_rev;
-  k_expand<<<grid_for(a->n_pairs, 256), 256, 0, st>>>(a->n_pairs, a->mirror, a->pair_a, a->pair_b,
+  k_expand<<<grid_for(a->n_pairs, 256), 256, 0, st>>>(a->n_pairs, mm, a->pair_a, a->pair_b,
                                                       a->pair_shift, w.rev_off, w.keys, w.vals,
                                                       w.e_src, w.e_code, w.e_orig);
   HB_LAUNCH_CHECK();
@@ -1260,6 +1299,11 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   d.cull_reach = (float)(a->reach * (1.0 + 1e-4)) + 1e-30f;
   d.include_self = a->include_self; d.nchan = a->nchan;
   for (int c = 0; c < 10; ++c) d.scale[c] = (float)a->scales[c];
+  d.scatter = mm == 2;
+  for (int c = 0; c < 10; ++c) {
+    d.csign[c] = (int)a->chan_sign[c];
+    d.mmap[c] = (a->mirror_map[c] >= 0 && a->mirror_map[c] < 10) ? (int)a->mirror_map[c] : c;
+  }
   d.out_flt = a->out_flt; d.out_int = a->out_int; d.write_out = 1; d.skip_leaf = nullptr;
   d.in_count = w.dev_cnt + 2; d.err_key = w.dev_cnt + 3;
   int rc = launch_pairs(a->kid, a->deterministic != 0, false, d, tcap, w.n_tiles_dev, st, err);

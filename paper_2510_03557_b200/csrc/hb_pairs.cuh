@@ -235,7 +235,7 @@ struct EvalDev {
   Tiling T;
   const int64_t* ent_ptr;  // (n_leaves+1)
   const int32_t* ent_src;
-  const int32_t* ent_code;  // shift code | fwd << 8
+  const int32_t* ent_code;  // shift code | fwd << 8 | scatter-eligible << 9
   const float4 *P0, *P1, *P2;
   const double* state;
   const int8_t* pshift;
@@ -245,6 +245,8 @@ struct EvalDev {
   int include_self;
   int nchan;
   float scale[10];
+  int scatter;               // deterministic mirror: scatter chan_sign * q[mirror_map] to partners
+  int csign[10], mmap[10];
   double* out_flt;
   int64_t* out_int;
   int write_out;

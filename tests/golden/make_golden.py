@@ -35,7 +35,8 @@ from hydrobox.kernels import (counting_kernel, crk_interp_kernel,  # noqa: E402
                               gravity_potential_kernel, hydro_force_kernel,
                               neighbor_count_kernel)
 from hydrobox.lane import EvalMode, eval_interaction_list, reference_pair_sum  # noqa: E402
-from hydrobox.stepper import unordered_due_pairs  # noqa: E402
+from hydrobox.hydro import assign_timestep_levels  # noqa: E402
+from hydrobox.stepper import ShortRangeContext, subcycle_pm_step, unordered_due_pairs  # noqa: E402
 
 REL, DET = EvalMode.RELAXED, EvalMode.DETERMINISTIC
 
@@ -258,10 +259,68 @@ def adapt_fixture():
     return out
 
 
+def subcycle_fixture():
+    """One PM interval of the hierarchical subcycle (hb/stepper.py:103-192) on a
+    bare periodic 2x8^3 box (no overload shell, so no same-rank alias ghosts:
+    SURVEY.md finding 3 cannot trigger), levels from assign_timestep_levels
+    (hb/hydro.py:277-317) with synthetic DM accelerations; run in deterministic
+    and relaxed mode from identical inputs."""
+    box = BoxGeometry(1.0)
+    npd = 8
+    p = make_lattice_ic(npd, box, 0.1 / npd, seed=77)
+    rng = np.random.default_rng(5)
+    p.vel = rng.normal(0, 0.05, p.pos.shape)
+    gas = p.species == 1
+    p.internal_energy[gas] = rng.uniform(0.5e-2, 2e-2, int(gas.sum()))
+    p.accel = rng.normal(0, 1, p.pos.shape) * np.exp(rng.uniform(-2, 3, p.n))[:, None]
+    split = ForceSplit(r_s=0.03, r_cut=0.15)
+    eps = 1.0 / p.n ** (1 / 3) / 50
+    reach = max(split.r_cut, 2 * p.smoothing.max())
+    bw = reach * (1 + 1e-9)
+    mesh = build_mesh_and_leaves(p, box, bw, 16)
+    out = {}
+    # dt_pm such that the deepest leaf sits at level 2 (n_fine = 4, 5 boundaries)
+    probe = p.copy()
+    dt_pm = 1e-3
+    for _ in range(60):
+        h = assign_timestep_levels(probe, mesh, dt_pm, 0.25, 4, eps, 5 / 3)
+        if h.max_level >= 2:
+            break
+        dt_pm *= 1.5
+    hier = assign_timestep_levels(p, mesh, dt_pm, 0.25, 4, eps, 5 / 3)
+    out.update(particle_arrays(p, "in_"))
+    out["in_accel"] = p.accel.copy()
+    out.update(mesh_arrays(mesh))
+    out["dt_pm"], out["max_level"], out["n_levels"] = (np.float64(dt_pm), np.int64(hier.max_level),
+                                                       np.int64(hier.n_levels))
+    out["reach"], out["r_s"], out["r_cut"], out["eps"] = (np.float64(reach), np.float64(split.r_s),
+                                                          np.float64(split.r_cut), np.float64(eps))
+    for tag, mode in (("det", DET), ("rel", REL)):
+        q = p.copy()
+        m = build_mesh_and_leaves(q, box, bw, 16)
+        m.leaf_level[:] = mesh.leaf_level
+        ctx = ShortRangeContext(particles=q, mesh=m, box=box, eos_gamma=5 / 3, reach=reach,
+                                mode=mode, gravity_kernel=short_range_gravity_kernel(split, eps),
+                                hydro_enabled=True)
+        audit = subcycle_pm_step(ctx, hier)
+        for k in ("pos", "vel", "internal_energy", "density", "accel"):
+            out[f"{tag}_{k}"] = getattr(q, k).copy()
+        out[f"{tag}_leaf_lo"], out[f"{tag}_leaf_hi"] = m.leaf_lo.copy(), m.leaf_hi.copy()
+        out[f"{tag}_max_quanta"] = np.int64(audit.max_momentum_quanta)
+        log = [(r.s, r.depth, lv, n) for r in audit.boundary_log
+               for lv, n in sorted(r.pairs_per_level.items())]
+        out[f"{tag}_pairs_log"] = np.array(log, dtype=np.int64).reshape(-1, 4)
+    return out
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
+    only = set(sys.argv[1:])
     for name, fn in (("lane", lane_fixture), ("mesh", mesh_fixture),
-                     ("step", step_fixture), ("adapt", adapt_fixture)):
+                     ("step", step_fixture), ("adapt", adapt_fixture),
+                     ("subcycle", subcycle_fixture)):
+        if only and name not in only:
+            continue
         data = fn()
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **data)
