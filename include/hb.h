@@ -337,6 +337,24 @@ int hb_halo_unpack_keep(int64_t m, const void* recs, int32_t key_bits, int64_t n
                         const HbFieldSet* src, const uint8_t* stay, int64_t n_stay,
                         const HbFieldSet* dst, void* ws, size_t ws_bytes, void* stream,
                         HbError* err);
+/* ---------------------------------------------------------------------------
+ * Particle-mesh long-range gravity (hb/gravity.py:58-245).
+ * Grids are float64 row-major (n, n, n); spectra half-complex (n, n, n/2+1)
+ * interleaved (re, im) float64, as cuFFT / torch.fft produce them.
+ * hb_pm_deposit: CIC mass deposition onto cell centres (periodic), then divided
+ *   by cell_volume (pass spacing ** 3 as the caller computes it).
+ * hb_pm_spectral: phi_k = -four_pi_g rho_k D(k) (phi_0 = 0) and the three
+ *   force spectra -i k_d phi_k; phi_k may be NULL.
+ * hb_pm_interp: CIC gather of n_fields (1..3) grids at the positions into
+ *   out (np, n_fields). */
+int hb_pm_deposit(int64_t np, const double* pos, const double* mass, int64_t grid_n,
+                  double spacing, double cell_volume, double* rho, void* stream, HbError* err);
+int hb_pm_spectral(int64_t grid_n, double side_length, double four_pi_g, const void* rho_k,
+                   const double* influence, void* fx_k, void* fy_k, void* fz_k, void* phi_k,
+                   void* stream, HbError* err);
+int hb_pm_interp(int64_t np, const double* pos, int32_t n_fields, const double* f0,
+                 const double* f1, const double* f2, int64_t grid_n, double spacing,
+                 double* out, void* stream, HbError* err);
 /* Row indices of the nonzero flags in row order (a device compaction whose
  * size the caller already knows -- no host sync). */
 size_t hb_flag_indices_workspace(int64_t n);

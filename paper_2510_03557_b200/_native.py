@@ -113,6 +113,12 @@ def lib():
             lb.hb_flag_indices_workspace.argtypes = [C.c_int64]
             lb.hb_flag_indices.argtypes = [C.c_int64, P, P, P, C.c_size_t, P, P]
             lb.hb_crk_solve.argtypes = [C.c_int64, P, C.c_int64, P, C.c_double, P, P, P, P, P]
+            lb.hb_pm_deposit.argtypes = [C.c_int64, P, P, C.c_int64, C.c_double, C.c_double, P,
+                                         P, P]
+            lb.hb_pm_spectral.argtypes = [C.c_int64, C.c_double, C.c_double, P, P, P, P, P, P,
+                                          P, P]
+            lb.hb_pm_interp.argtypes = [C.c_int64, P, C.c_int32, P, P, P, C.c_int64, C.c_double,
+                                        P, P, P]
             lb.hb_halo_pack_all_workspace.restype = C.c_size_t
             lb.hb_halo_pack_all_workspace.argtypes = [C.c_int32]
             lb.hb_halo_pack_all.argtypes = [C.c_int64, C.POINTER(HbFieldSet), C.c_int32 * 3,
@@ -135,7 +141,8 @@ EXPORTS = ("hb_abi_version", "hb_launch_count", "hb_device_query", "hb_build_mes
            "hb_halo_record_bytes", "hb_halo_select", "hb_halo_pack", "hb_halo_unpack_workspace",
            "hb_halo_unpack", "hb_halo_resolve_sources", "hb_halo_pack_all_workspace",
            "hb_halo_pack_all", "hb_halo_unpack_keep_workspace", "hb_halo_unpack_keep",
-           "hb_flag_indices_workspace", "hb_flag_indices")
+           "hb_flag_indices_workspace", "hb_flag_indices", "hb_pm_deposit", "hb_pm_spectral",
+           "hb_pm_interp")
 
 
 def torch_cuda():

@@ -25,7 +25,9 @@ from hydrobox.cmtree import (InteractionList, assemble_interaction_lists,  # noq
                              build_mesh_and_leaves)
 from hydrobox.config import SimConfig  # noqa: E402
 from hydrobox.domain import build_overload, decompose  # noqa: E402
-from hydrobox.gravity import ForceSplit, short_range_gravity_kernel  # noqa: E402
+from hydrobox.gravity import (ForceSplit, _optimal_influence, deposit_cic,  # noqa: E402
+                              interpolate_force, long_range_potential_energy,
+                              short_range_gravity_kernel, solve_long_range)
 from hydrobox.hydro import (adapt_smoothing_length, compute_crk_coefficients,  # noqa: E402
                             compute_density, compute_hydro_accel,
                             corrected_interpolate, refresh_eos_columns)
@@ -313,12 +315,36 @@ def subcycle_fixture():
     return out
 
 
+def pm_fixture():
+    """Long-range PM pipeline (hb/gravity.py:58-245): CIC deposit, alias-optimal
+    and naive influence, filtered spectral solve with potential, CIC gather and
+    the long-range potential energy, on a jittered 2x8^3 lattice, 16^3 grid."""
+    box = BoxGeometry(1.0)
+    p = make_lattice_ic(8, box, 0.2 / 8, seed=404)
+    rng = np.random.default_rng(3)
+    p.mass = p.mass * rng.uniform(0.5, 1.5, p.n)  # unequal masses exercise the weights
+    n = 16
+    split = ForceSplit.for_grid(box, n)
+    out = {"pos": p.pos.copy(), "mass": p.mass.copy(), "grid_n": np.int64(n),
+           "r_s": np.float64(split.r_s), "r_cut": np.float64(split.r_cut)}
+    rho = deposit_cic(p, n, box)
+    out["rho"] = rho.values.copy()
+    out["d_opt"] = _optimal_influence(n, box, split.r_s).copy()
+    for tag in ("optimal", "naive"):
+        fields, pot = solve_long_range(rho, split, box, want_potential=True, influence=tag)
+        out[f"{tag}_fields"] = np.stack([f.values for f in fields])
+        out[f"{tag}_pot"] = pot.values.copy()
+        out[f"{tag}_acc"] = interpolate_force(fields, p)
+        out[f"{tag}_energy"] = np.float64(long_range_potential_energy(pot, p))
+    return out
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
     only = set(sys.argv[1:])
     for name, fn in (("lane", lane_fixture), ("mesh", mesh_fixture),
                      ("step", step_fixture), ("adapt", adapt_fixture),
-                     ("subcycle", subcycle_fixture)):
+                     ("subcycle", subcycle_fixture), ("pm", pm_fixture)):
         if only and name not in only:
             continue
         data = fn()

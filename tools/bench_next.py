@@ -1,0 +1,120 @@
+"""Measurements of the §8(f) rows built on top of the force path (1 GPU):
+
+  pm        long-range kick at the c2 workload: 2x128^3 particles on the
+            pm_grid_n = 2 npd = 256^3 grid (CIC deposit, cuFFT R2C, spectral
+            multiply, 3 C2R, CIC gather), CUDA events, median of --reps
+  subcycle  one PM interval of the hierarchical integrator (SubcycleEngine) on
+            a 2 x npd^3 Zel'dovich box with leaf levels from
+            assign_timestep_levels (dt_pm chosen for a 3-level hierarchy)
+
+    python tools/bench_next.py [--npd 128] [--sub-npd 64] [--reps 5]
+Prints one JSON line per measurement."""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def bench_pm(npd, reps):
+    import numpy as np
+    import torch
+    from bench import make_workload
+    from paper_2510_03557_b200 import gravity as G
+    p, cfg, meta = make_workload("c2" if npd == 128 else "c1")
+    box = cfg.box
+    n = 2 * npd
+    split = G.ForceSplit.for_grid(box, n)
+    solver = G.LongRangeSolver(n, split, box)
+    pos = torch.from_numpy(np.ascontiguousarray(p.pos)).cuda()
+    mass = torch.from_numpy(np.ascontiguousarray(p.mass)).cuda()
+    t0 = time.perf_counter()
+    G.optimal_influence_device(n, box, split.r_s)
+    torch.cuda.synchronize()
+    t_infl = time.perf_counter() - t0
+    stages = {"deposit": [], "solve": [], "gather": [], "total": []}
+    for _ in range(reps + 2):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        rho = G.deposit_cic_device(pos, mass, n, box)
+        ev[1].record()
+        fields, pot = G.solve_long_range_device(rho, split, box, False)
+        ev[2].record()
+        acc = G.interpolate_device(fields, pos, box.side_length / n)
+        ev[3].record()
+        torch.cuda.synchronize()
+        for k, (a, b) in zip(stages, ((0, 1), (1, 2), (2, 3), (0, 3))):
+            stages[k].append(ev[a].elapsed_time(ev[b]))
+    med = {k: float(np.median(v[2:])) for k, v in stages.items()}
+    mom = float((acc * mass[:, None]).sum(dim=0).abs().max() /
+                (acc.abs() * mass[:, None]).sum())
+    return {"measurement": "pm_long_range_kick", "n_particles": int(p.n), "grid": n,
+            "ms": med, "particles_per_s": p.n / (med["total"] * 1e-3),
+            "influence_setup_s": t_infl, "momentum_residual_rel": mom,
+            "note": "float64 throughout; FFTs are cuFFT (torch.fft); influence cached per grid"}
+
+
+def bench_subcycle(npd, reps):
+    import numpy as np
+    import torch
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.cmtree import build_mesh_and_leaves
+    from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
+    from paper_2510_03557_b200.hydro import assign_timestep_levels
+    from paper_2510_03557_b200.ic import make_zeldovich_ic
+    from paper_2510_03557_b200.lane import EvalMode
+    from paper_2510_03557_b200.stepper import ShortRangeContext, SubcycleEngine
+    box = BoxGeometry(1.0)
+    p = make_zeldovich_ic(npd, box, 0.05)
+    rng = np.random.default_rng(1)
+    p.internal_energy[p.species == 1] = 1e-2
+    p.accel = rng.normal(0, 1, p.pos.shape) * np.exp(rng.uniform(-2, 3, p.n))[:, None]
+    split = ForceSplit.for_grid(box, 2 * npd)
+    eps = 1.0 / p.n ** (1 / 3) / 50
+    reach = max(split.r_cut, 2 * float(p.smoothing.max()))
+    mesh = build_mesh_and_leaves(p, box, reach * (1 + 1e-9), 256)
+    dt_pm = 1e-3
+    for _ in range(80):
+        hier = assign_timestep_levels(p.copy(), mesh, dt_pm, 0.25, 4, eps, 5 / 3)
+        if hier.max_level >= 2:
+            break
+        dt_pm *= 1.5
+    hier = assign_timestep_levels(p, mesh, dt_pm, 0.25, 4, eps, 5 / 3)
+    out = {}
+    for mode in (EvalMode.DETERMINISTIC, EvalMode.RELAXED):
+        ctx = ShortRangeContext(particles=p, mesh=mesh, box=box, eos_gamma=5 / 3, reach=reach,
+                                mode=mode, gravity_kernel=short_range_gravity_kernel(split, eps))
+        times = []
+        for _ in range(reps):
+            eng = SubcycleEngine(ctx)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            audit = eng.run(hier)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        out[mode] = {"s_per_interval": float(np.median(times)),
+                     "boundaries": audit.n_boundaries, "max_momentum_quanta":
+                     audit.max_momentum_quanta,
+                     "pairs_per_boundary": [sum(r.pairs_per_level.values())
+                                            for r in audit.boundary_log]}
+    levels = np.bincount(mesh.leaf_level, minlength=hier.max_level + 1).tolist()
+    return {"measurement": "subcycle_interval", "n_particles": int(p.n), "n_fine": hier.n_fine,
+            "leaf_levels": levels, "modes": out,
+            "note": "wall time of SubcycleEngine.run (device-resident), compat pair engine "
+                    "(hb_eval_pairs) per level"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--npd", type=int, default=128)
+    ap.add_argument("--sub-npd", type=int, default=64)
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    print(json.dumps(bench_pm(args.npd, args.reps)))
+    print(json.dumps(bench_subcycle(args.sub_npd, max(1, args.reps // 2))))
+
+
+if __name__ == "__main__":
+    main()
