@@ -355,6 +355,27 @@ int hb_pm_spectral(int64_t grid_n, double side_length, double four_pi_g, const v
 int hb_pm_interp(int64_t np, const double* pos, int32_t n_fields, const double* f0,
                  const double* f1, const double* f2, int64_t grid_n, double spacing,
                  double* out, void* stream, HbError* err);
+/* ---------------------------------------------------------------------------
+ * In-situ cluster finding (hb/insitu.py:25-142).
+ * hb_fof_scan: radius-wide cell grid (lo, inv_w, ncell as _grid_geometry),
+ *   27-stencil sweep over binpos (n,3) with the reference's float64 edge test
+ *   from the lower row's side.  mode 0: FOF union into parent (init arange,
+ *   flattened on return: root = smallest row of the component); 1: counts[i]
+ *   += neighbours within r (self included); 2: union of core-core edges;
+ *   3: border_key[i] = min(border_key[i], core_label[j]) over core neighbours
+ *   j of non-core i.  Unused arrays may be NULL.
+ * hb_uf_union_edges: union of the m edges (a[k], b[k]) into parent (n) and
+ *   flatten (global-id stitching of rank components).
+ * hb_crc32c: CRC32C (Castagnoli) of a HOST buffer, running value in/out. */
+size_t hb_fof_workspace(int64_t n, const int64_t ncell[3]);
+int hb_fof_scan(int64_t n, const double* binpos, const double lo[3], const double inv_w[3],
+                const int64_t ncell[3], double side_length, int32_t periodic, double r2max,
+                int32_t mode, int64_t* parent, const uint8_t* core, int64_t* counts,
+                int64_t* border_key, const int64_t* core_label, void* ws, size_t ws_bytes,
+                void* stream, HbError* err);
+int hb_uf_union_edges(int64_t m, const int64_t* a, const int64_t* b, int64_t n, int64_t* parent,
+                      void* stream, HbError* err);
+uint32_t hb_crc32c(const void* data, size_t nbytes, uint32_t value);
 /* Row indices of the nonzero flags in row order (a device compaction whose
  * size the caller already knows -- no host sync). */
 size_t hb_flag_indices_workspace(int64_t n);

@@ -38,6 +38,8 @@ from hydrobox.kernels import (counting_kernel, crk_interp_kernel,  # noqa: E402
                               neighbor_count_kernel)
 from hydrobox.lane import EvalMode, eval_interaction_list, reference_pair_sum  # noqa: E402
 from hydrobox.hydro import assign_timestep_levels  # noqa: E402
+from hydrobox.insitu import (dbscan_find, encode_halo_catalog, fof_find,  # noqa: E402
+                             power_spectrum)
 from hydrobox.stepper import ShortRangeContext, subcycle_pm_step, unordered_due_pairs  # noqa: E402
 
 REL, DET = EvalMode.RELAXED, EvalMode.DETERMINISTIC
@@ -339,12 +341,58 @@ def pm_fixture():
     return out
 
 
+def _groups_arrays(groups, tag):
+    ids = [g.member_ids for g in groups]
+    return {f"{tag}_halo_id": np.array([g.halo_id for g in groups], dtype=np.int64),
+            f"{tag}_count": np.array([g.count for g in groups], dtype=np.int64),
+            f"{tag}_mass": np.array([g.total_mass for g in groups]),
+            f"{tag}_center": np.array([g.center for g in groups]).reshape(-1, 3),
+            f"{tag}_radius": np.array([g.radius for g in groups]),
+            f"{tag}_members": np.concatenate(ids) if ids else np.zeros(0, dtype=np.int64),
+            f"{tag}_offsets": np.cumsum([0] + [len(i) for i in ids]).astype(np.int64)}
+
+
+def fof_fixture():
+    """Friends-of-friends and DBSCAN (hb/insitu.py:244-368) on a clustered box,
+    single periodic set and (2,2,1) overloaded rank sets (global-id stitching);
+    halo catalog bytes (CRC32C footer) and P(k) of its CIC density."""
+    box = BoxGeometry(1.0)
+    p = make_clustered_ic(16, box, seed=11)
+    out = {"pos": p.pos.copy(), "mass": p.mass.copy(), "global_id": p.global_id.copy(),
+           "species": p.species.copy()}
+    ll = 0.2 / 16
+    out["ll"] = np.float64(ll)
+    out.update(_groups_arrays(fof_find(p, box, ll, min_members=5), "fof1"))
+    w = 2.5 * ll
+    doms = decompose(box, (2, 2, 1), w)
+    sets = build_overload(p, doms, box, (2, 2, 1))[0]
+    for r, rs in enumerate(sets):
+        out.update(particle_arrays(rs, f"rank{r}_"))
+    out["w"] = np.float64(w)
+    out.update(_groups_arrays(fof_find(sets, box, ll, min_members=5, overload_width=w), "fof4"))
+    eps = 0.25 / 16
+    out["eps"] = np.float64(eps)
+    g1, noise1 = dbscan_find(p, box, eps, 6)
+    out.update(_groups_arrays(g1, "db1"))
+    out["db1_noise"] = noise1
+    g4, noise4 = dbscan_find(sets, box, eps, 6, overload_width=w)
+    out.update(_groups_arrays(g4, "db4"))
+    out["db4_noise"] = noise4
+    groups = fof_find(p, box, ll, min_members=5)
+    out["catalog"] = np.frombuffer(encode_halo_catalog(groups, 7), dtype=np.uint8).copy()
+    rho = deposit_cic(p, 32, box)
+    k, pk, cnt = power_spectrum(rho.values, box)
+    out["pk_rho"], out["pk_k"], out["pk"], out["pk_counts"] = rho.values, k, pk, cnt
+    return out
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
     only = set(sys.argv[1:])
     for name, fn in (("lane", lane_fixture), ("mesh", mesh_fixture),
                      ("step", step_fixture), ("adapt", adapt_fixture),
-                     ("subcycle", subcycle_fixture), ("pm", pm_fixture)):
+                     ("subcycle", subcycle_fixture), ("pm", pm_fixture),
+                     ("fof", fof_fixture)):
         if only and name not in only:
             continue
         data = fn()

@@ -110,3 +110,16 @@ def test_unordered_pairs_match_golden(golden):
         np.testing.assert_array_equal(a, g[k + "ua"])
         np.testing.assert_array_equal(b, g[k + "ub"])
         np.testing.assert_array_equal(s, g[k + "us"])
+
+
+def test_crc32c_and_catalog_codec_vs_reference(golden):
+    """hb_crc32c (host, slice-by-8) against the reference's halo catalog bytes
+    (CRC32C footer, hb/insitu.py:371-404) and the CRC32C check value."""
+    import struct
+    from paper_2510_03557_b200.insitu import crc32c, decode_halo_catalog
+    assert crc32c(b"123456789") == 0xE3069283  # CRC-32C check value
+    blob = golden("fof")["catalog"].tobytes()
+    assert struct.unpack("<I", blob[-4:])[0] == crc32c(blob[:-4])
+    assert crc32c(blob[10:], crc32c(blob[:10])) == crc32c(blob)  # running value
+    rec = decode_halo_catalog(blob)
+    assert rec.shape[0] == 25 and int(rec["step"][0]) == 7

@@ -6,6 +6,8 @@
   subcycle  one PM interval of the hierarchical integrator (SubcycleEngine) on
             a 2 x npd^3 Zel'dovich box with leaf levels from
             assign_timestep_levels (dt_pm chosen for a 3-level hierarchy)
+  fof       FOF (ll = 0.2 d, >= 10 members) and DBSCAN on a 2 x npd^3
+            clustered box (device sweeps + host group statistics)
 
     python tools/bench_next.py [--npd 128] [--sub-npd 64] [--reps 5]
 Prints one JSON line per measurement."""
@@ -106,6 +108,33 @@ def bench_subcycle(npd, reps):
                     "(hb_eval_pairs) per level"}
 
 
+def bench_fof(npd, reps):
+    import numpy as np
+    import torch
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.ic import make_clustered_ic
+    from paper_2510_03557_b200.insitu import dbscan_find, fof_find
+    box = BoxGeometry(1.0)
+    p = make_clustered_ic(npd, box, seed=11)  # Gaussian clumps over a floor (hb/ic.py:137)
+    ll = 0.2 / npd
+    res = {}
+    for name, fn in (("fof", lambda: fof_find(p, box, ll, min_members=10)),
+                     ("dbscan", lambda: dbscan_find(p, box, ll, 8))):
+        fn()
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        groups = out[0] if isinstance(out, tuple) else out
+        res[name] = {"s": float(np.median(ts)), "groups": len(groups)}
+    return {"measurement": "insitu_cluster_finding", "n_particles": int(p.n),
+            "linking_length": "0.2 d", "results": res,
+            "note": "wall time incl. host group statistics and H2D of positions"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--npd", type=int, default=128)
@@ -114,6 +143,7 @@ def main():
     args = ap.parse_args()
     print(json.dumps(bench_pm(args.npd, args.reps)))
     print(json.dumps(bench_subcycle(args.sub_npd, max(1, args.reps // 2))))
+    print(json.dumps(bench_fof(args.npd, max(1, args.reps // 2))))
 
 
 if __name__ == "__main__":
