@@ -376,6 +376,12 @@ int hb_fof_scan(int64_t n, const double* binpos, const double lo[3], const doubl
 int hb_uf_union_edges(int64_t m, const int64_t* a, const int64_t* b, int64_t n, int64_t* parent,
                       void* stream, HbError* err);
 uint32_t hb_crc32c(const void* data, size_t nbytes, uint32_t value);
+/* CRC32C of a DEVICE buffer (HCKP checkpoint codec, hb/tiered_io.py:80-142):
+ * parallel per-chunk CRCs folded with GF(2) zero-shift operators; writes the
+ * standard CRC32C to *out_host and synchronises the stream. */
+size_t hb_crc32c_device_workspace(int64_t nbytes);
+int hb_crc32c_device(const void* data, int64_t nbytes, uint32_t* out_host, void* ws,
+                     size_t ws_bytes, void* stream, HbError* err);
 /* Row indices of the nonzero flags in row order (a device compaction whose
  * size the caller already knows -- no host sync). */
 size_t hb_flag_indices_workspace(int64_t n);

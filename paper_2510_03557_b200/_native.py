@@ -125,6 +125,9 @@ def lib():
                                        C.c_int64 * 3, C.c_double, C.c_int32, C.c_double,
                                        C.c_int32, P, P, P, P, P, P, C.c_size_t, P, P]
             lb.hb_uf_union_edges.argtypes = [C.c_int64, P, P, C.c_int64, P, P, P]
+            lb.hb_crc32c_device_workspace.restype = C.c_size_t
+            lb.hb_crc32c_device_workspace.argtypes = [C.c_int64]
+            lb.hb_crc32c_device.argtypes = [P, C.c_int64, P, P, C.c_size_t, P, P]
             lb.hb_crc32c.restype = C.c_uint32
             lb.hb_crc32c.argtypes = [P, C.c_size_t, C.c_uint32]
             lb.hb_halo_pack_all_workspace.restype = C.c_size_t
@@ -150,7 +153,8 @@ EXPORTS = ("hb_abi_version", "hb_launch_count", "hb_device_query", "hb_build_mes
            "hb_halo_unpack", "hb_halo_resolve_sources", "hb_halo_pack_all_workspace",
            "hb_halo_pack_all", "hb_halo_unpack_keep_workspace", "hb_halo_unpack_keep",
            "hb_flag_indices_workspace", "hb_flag_indices", "hb_pm_deposit", "hb_pm_spectral",
-           "hb_pm_interp", "hb_fof_workspace", "hb_fof_scan", "hb_uf_union_edges", "hb_crc32c")
+           "hb_pm_interp", "hb_fof_workspace", "hb_fof_scan", "hb_uf_union_edges", "hb_crc32c",
+           "hb_crc32c_device_workspace", "hb_crc32c_device")
 
 
 def torch_cuda():

@@ -40,6 +40,7 @@ from hydrobox.lane import EvalMode, eval_interaction_list, reference_pair_sum  #
 from hydrobox.hydro import assign_timestep_levels  # noqa: E402
 from hydrobox.insitu import (dbscan_find, encode_halo_catalog, fof_find,  # noqa: E402
                              power_spectrum)
+from hydrobox.tiered_io import encode_rank_checkpoint  # noqa: E402
 from hydrobox.stepper import ShortRangeContext, subcycle_pm_step, unordered_due_pairs  # noqa: E402
 
 REL, DET = EvalMode.RELAXED, EvalMode.DETERMINISTIC
@@ -386,13 +387,31 @@ def fof_fixture():
     return out
 
 
+def ckpt_fixture():
+    """HCKP rank checkpoint blob (hb/tiered_io.py:80-96) of one overloaded rank
+    set of a 2x8^3 box (ghosts, image shifts, alias sources, timestep levels)."""
+    box = BoxGeometry(1.0)
+    p = make_lattice_ic(8, box, 0.1 / 8, seed=9)
+    rng = np.random.default_rng(4)
+    p.vel = rng.normal(0, 0.05, p.pos.shape)
+    p.accel = rng.normal(0, 1, p.pos.shape)
+    p.timestep_level[:] = rng.integers(0, 4, p.n)
+    w = 0.2
+    doms = decompose(box, (1, 1, 1), w)
+    rs = build_overload(p, doms, box, (1, 1, 1))[0][0]
+    out = particle_arrays(rs, "in_")
+    out["in_accel"] = rs.accel.copy()
+    out["blob"] = np.frombuffer(encode_rank_checkpoint(rs, 12, 3), dtype=np.uint8).copy()
+    return out
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
     only = set(sys.argv[1:])
     for name, fn in (("lane", lane_fixture), ("mesh", mesh_fixture),
                      ("step", step_fixture), ("adapt", adapt_fixture),
                      ("subcycle", subcycle_fixture), ("pm", pm_fixture),
-                     ("fof", fof_fixture)):
+                     ("fof", fof_fixture), ("ckpt", ckpt_fixture)):
         if only and name not in only:
             continue
         data = fn()

@@ -123,3 +123,13 @@ def test_crc32c_and_catalog_codec_vs_reference(golden):
     assert crc32c(blob[10:], crc32c(blob[:10])) == crc32c(blob)  # running value
     rec = decode_halo_catalog(blob)
     assert rec.shape[0] == 25 and int(rec["step"][0]) == 7
+
+
+def test_checkpoint_decode_reference_blob(golden):
+    """The reference's HCKP blob decodes through the host path (CRCs checked)."""
+    from paper_2510_03557_b200.checkpoint import decode_rank_checkpoint
+    g = golden("ckpt")
+    p, step, rank = decode_rank_checkpoint(g["blob"].tobytes())
+    assert (step, rank) == (12, 3)
+    for k in ("pos", "vel", "global_id", "ghost_src", "image_shift", "timestep_level"):
+        np.testing.assert_array_equal(getattr(p, k), g["in_" + k])

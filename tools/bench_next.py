@@ -8,6 +8,8 @@
             assign_timestep_levels (dt_pm chosen for a 3-level hierarchy)
   fof       FOF (ll = 0.2 d, >= 10 members) and DBSCAN on a 2 x npd^3
             clustered box (device sweeps + host group statistics)
+  ckpt      HCKP encode of the c2 rank state from device fields; device CRC32C
+            bandwidth over 512 MiB
 
     python tools/bench_next.py [--npd 128] [--sub-npd 64] [--reps 5]
 Prints one JSON line per measurement."""
@@ -135,6 +137,39 @@ def bench_fof(npd, reps):
             "note": "wall time incl. host group statistics and H2D of positions"}
 
 
+def bench_ckpt(npd, reps):
+    import numpy as np
+    import torch
+    from bench import make_workload
+    from paper_2510_03557_b200 import _native as N
+    from paper_2510_03557_b200.checkpoint import crc32c_device, encode_rank_checkpoint_device
+    p, cfg, meta = make_workload("c2" if npd == 128 else "c1")
+    fields = {k: N.dev(np.ascontiguousarray(getattr(p, k))) for k in (
+        "pos", "vel", "mass", "smoothing", "internal_energy", "density", "species", "ghost",
+        "image_shift", "global_id", "ghost_src", "timestep_level", "accel")}
+    big = torch.empty(512 << 20, dtype=torch.uint8, device="cuda").random_(0, 255)
+    crc32c_device(big)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(reps):
+        crc32c_device(big)
+    ev1.record()
+    torch.cuda.synchronize()
+    crc_gbs = big.numel() * reps / (ev0.elapsed_time(ev1) * 1e-3) / 1e9
+    blob = encode_rank_checkpoint_device(fields, 1, 0)
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        blob = encode_rank_checkpoint_device(fields, 1, 0)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.median(ts))
+    return {"measurement": "hckp_encode", "n_particles": int(p.n), "blob_bytes": len(blob),
+            "encode_s": t, "encode_gbs": len(blob) / t / 1e9, "device_crc32c_gbs": crc_gbs,
+            "note": "encode = device column conversion + 22 device CRCs + assembly + one "
+                    "D2H into pinned memory (PCIe-bound)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--npd", type=int, default=128)
@@ -144,6 +179,7 @@ def main():
     print(json.dumps(bench_pm(args.npd, args.reps)))
     print(json.dumps(bench_subcycle(args.sub_npd, max(1, args.reps // 2))))
     print(json.dumps(bench_fof(args.npd, max(1, args.reps // 2))))
+    print(json.dumps(bench_ckpt(args.npd, args.reps)))
 
 
 if __name__ == "__main__":
