@@ -16,6 +16,16 @@
 namespace hb {
 
 constexpr int kG2Warps = 8;
+// within-tile k-d levels for the bin-gravity tiles (2: 4 groups of <= 8 lanes);
+// HB_GRAV_TILE_LEVELS overrides (0 disables) for A/B measurement
+static int tile_order_levels() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HB_GRAV_TILE_LEVELS");
+    v = e ? atoi(e) : 2;
+  }
+  return v;
+}
 constexpr int kG2Stage = 96;
 
 // rows of bin b: [leaf_start[first leaf], leaf_end[last leaf]) (leaves of a bin are contiguous)
@@ -188,6 +198,72 @@ k_gravity2(G2Dev a, const float4* __restrict__ table, const int64_t* n_tiles_dev
   }
 }
 
+// Warp per tile: reorder the tile's members (P0 and tperm together) into a
+// `levels`-deep median k-d order (each segment split on its longest axis,
+// stable by position; first part (sz + 1) / 2).  With 2 levels every 8-lane
+// phase of a warp holds a compact group of <= 8 targets, so the GT_SOFT rows
+// one phase gathers for a source are closer together.  Measured: k_gravity
+// 10.47 -> 10.25 ms at c2 (bank conflicts -4%: even a compact group spans
+// several octaves of soft for a near source).
+// Internal order only: it changes FP32 summation order, not the pairs.
+constexpr int kTOWarps = 8;
+__global__ void __launch_bounds__(kTOWarps * 32)
+k_tile_order(const int64_t* n_tiles_dev, Tiling T, float4* P0, int levels) {
+  __shared__ float4 s_p[kTOWarps][32];
+  __shared__ int s_r[kTOWarps][32];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = (int64_t)blockIdx.x * kTOWarps + wid;
+  if (t >= *n_tiles_dev) return;
+  int n = T.tile_n[t];
+  if (n <= 8) return;
+  int64_t s0 = T.tile_start[t];
+  bool live = lane < n;
+  float4* sp = s_p[wid];
+  int* sr = s_r[wid];
+  if (live) {
+    sp[lane] = P0[s0 + lane];
+    sr[lane] = T.tperm[s0 + lane];
+  }
+  __syncwarp();
+  for (int lvl = 0; lvl < levels; ++lvl) {
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    int r = 0, np = lane;
+    if (live) {
+      int off = 0, sz = n;
+      for (int l = 0; l < lvl; ++l) {
+        int h = (sz + 1) >> 1;
+        if (lane - off >= h) { off += h; sz -= h; } else { sz = h; }
+      }
+      float lx = INFINITY, ly = INFINITY, lz = INFINITY;
+      float hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
+      for (int j = off; j < off + sz; ++j) {
+        float4 q = sp[j];
+        lx = fminf(lx, q.x); ly = fminf(ly, q.y); lz = fminf(lz, q.z);
+        hx = fmaxf(hx, q.x); hy = fmaxf(hy, q.y); hz = fmaxf(hz, q.z);
+      }
+      float ex = hx - lx, ey = hy - ly, ez = hz - lz;
+      int ax = (ex >= ey && ex >= ez) ? 0 : (ey >= ez ? 1 : 2);
+      p = sp[lane];
+      r = sr[lane];
+      unsigned key = sortable_key(ax == 0 ? p.x : ax == 1 ? p.y : p.z);
+      int rank = 0;
+      for (int j = off; j < off + sz; ++j) {
+        float4 q = sp[j];
+        unsigned kj = sortable_key(ax == 0 ? q.x : ax == 1 ? q.y : q.z);
+        rank += (kj < key || (kj == key && j < lane)) ? 1 : 0;
+      }
+      np = off + rank;
+    }
+    __syncwarp();
+    if (live) { sp[np] = p; sr[np] = r; }
+    __syncwarp();
+  }
+  if (live) {
+    P0[s0 + lane] = sp[lane];
+    T.tperm[s0 + lane] = sr[lane];
+  }
+}
+
 __global__ void k_stride_ptr(int64_t n, int64_t stride, int64_t* ptr) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i <= n) ptr[i] = i * stride;
@@ -248,8 +324,15 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   const float4* tab = gravity_table_device(g.r_s, g.r_cut, g.eps, kind, &gt, st, err);
   if (!tab) return err ? err->status : HB_CUDA;
   if (!g.half_warp) {
+    if (tile_order_levels() > 0) {
+      k_tile_order<<<grid_for(T.n_tiles_cap, kTOWarps), kTOWarps * 32, 0, st>>>(
+          ntd, T, P0, tile_order_levels());
+      HB_LAUNCH_CHECK();
+    }
     k_stride_ptr<<<grid_for(nbins + 1, 256), 256, 0, st>>>(nbins, 27, st_ptr);
     HB_LAUNCH_CHECK();
+  }
+  if (!g.half_warp) {
     EvalDev e = {};
     e.T = T; e.ent_ptr = st_ptr; e.ent_src = st_src; e.ent_code = st_code; e.P0 = P0;
     e.L = g.L; e.reach = g.r_cut;
