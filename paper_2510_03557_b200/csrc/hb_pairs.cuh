@@ -23,14 +23,19 @@ constexpr float kSigma = 0.318309886183790671f;  // 1/pi (hb/kernels.py:63)
 
 // walk this lane's set bits across all words; body(q) per in-support source.
 // The warp loops max-over-lanes(total bits) times: balanced over the stage.
+// nz = this lane's bitmask of non-empty words (from the mask build), so moving
+// to the next word is one predicated step (ffs), never a divergent scan.
 template <class Body>
-__device__ __forceinline__ void walk_masks(const unsigned (*mask)[32], int cnt, Body body) {
+__device__ __forceinline__ void walk_masks(const unsigned (*mask)[32], unsigned nz, Body body) {
   int lane = threadIdx.x & 31;
-  int nw = (cnt + 31) >> 5;
   int wi = 0;
-  unsigned m = nw > 0 ? mask[0][lane] : 0u;
+  unsigned m = 0u;
   while (true) {
-    while (m == 0u && ++wi < nw) m = mask[wi][lane];
+    if (m == 0u && nz != 0u) {
+      wi = __ffs(nz) - 1;
+      nz &= nz - 1;
+      m = mask[wi][lane];
+    }
     bool has = m != 0u;
     if (!__any_sync(0xffffffffu, has)) break;
     if (has) {

@@ -133,13 +133,14 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
 // The last word is padded with far sources (r^2 ~ 3e36 beyond any threshold)
 // so every word is a fully unrolled 32-source sweep with constant shifts.
 template <int NP, bool HYDRO>
-__device__ __forceinline__ void build_masks(float4 (*stage)[NP], int cnt, float4 ti0,
-                                            float hi, float thr_i, float reach2c,
-                                            unsigned (*mask)[32]) {
+__device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, float4 ti0,
+                                                float hi, float thr_i, float reach2c,
+                                                unsigned (*mask)[32]) {
   int lane = threadIdx.x & 31;
   int nw = (cnt + 31) >> 5;
   if (cnt + lane < nw * 32) stage[cnt + lane][0] = make_float4(1e18f, 1e18f, 1e18f, 0.0f);
   __syncwarp();
+  unsigned nz = 0u;  // non-empty words of this lane
   for (int w = 0; w < nw; ++w) {
     unsigned bits = 0u;
 #pragma unroll
@@ -155,8 +156,10 @@ __device__ __forceinline__ void build_masks(float4 (*stage)[NP], int cnt, float4
       bits |= (r2 <= thr ? 1u : 0u) << b;
     }
     mask[w][lane] = bits;
+    nz |= (bits != 0u ? 1u : 0u) << w;
   }
   __syncwarp();
+  return nz;
 }
 
 // ---------------------------------------------------------------- pass A
@@ -193,8 +196,8 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   unsigned(*mask)[32] = s_mask[wid];
   auto consume = [&]() {
     __syncwarp();
-    build_masks<1, false>(stage, cnt, ti0, h, live ? thr_mask : -1.0f, 0.0f, mask);
-    walk_masks(mask, cnt, [&](int q) {
+    unsigned nz = build_masks<1, false>(stage, cnt, ti0, h, live ? thr_mask : -1.0f, 0.0f, mask);
+    walk_masks(mask, nz, [&](int q) {
       float4 s = stage[q][0];
       float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
@@ -259,8 +262,9 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   unsigned(*mask)[32] = s_mask[wid];
   auto consume = [&]() {
     __syncwarp();
-    build_masks<3, true>(stage, cnt, ti0, live ? hi : -1.0f, 0.0f, live ? reach2c : -1.0f, mask);
-    walk_masks(mask, cnt, [&](int q) {
+    unsigned nz =
+        build_masks<3, true>(stage, cnt, ti0, live ? hi : -1.0f, 0.0f, live ? reach2c : -1.0f, mask);
+    walk_masks(mask, nz, [&](int q) {
       float4 s0 = stage[q][0], s1 = stage[q][1], s2 = stage[q][2];
       float dx = ti0.x - s0.x, dy = ti0.y - s0.y, dz = ti0.z - s0.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
