@@ -342,12 +342,20 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     int k1 = (kk + 1) / 2, k2 = kk - k1;
     int left = (int)(((int64_t)m * k1 + kk - 1) / kk);
     const int nj = (m + 31) >> 5;  // warp-uniform: slots in use
+    // 16-bit keys: the coordinate along the split axis quantised over the
+    // segment's extent (monotone; ties -- also merged neighbours -- are split
+    // by position, so the left part still holds exactly `left` members):
+    // at most 16 descent passes instead of 32 for sign-straddling floats
+    float qlo = axis == 0 ? lo3[0] : axis == 1 ? lo3[1] : lo3[2];
+    float qex = axis == 0 ? ex0 : axis == 1 ? ex1 : ex2;
+    float qsc = qex > 0.0f ? 65535.0f / qex : 0.0f;
     unsigned key[J];
     unsigned kmin = 0xffffffffu, kmax = 0u;
 #pragma unroll
     for (int jj = 0; jj < J; ++jj) {
       bool v = 32 * jj + lane < m;
-      key[jj] = v ? sortable_key(cc[axis][id[jj]]) : 0xffffffffu;
+      float qv = fminf(fmaxf((cc[axis][id[jj]] - qlo) * qsc, 0.0f), 65535.0f);
+      key[jj] = v ? (qv == qv ? (unsigned)qv : 65535u) : 0xffffffffu;
       if (v) { kmin = min(kmin, key[jj]); kmax = max(kmax, key[jj]); }
     }
     kmin = __reduce_min_sync(0xffffffffu, kmin);
