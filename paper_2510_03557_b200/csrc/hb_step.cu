@@ -11,22 +11,6 @@
 
 namespace hb {
 
-__global__ void k_state_matrix(int64_t n, const double* pos, const double* vel, const double* mass,
-                               const double* h, const double* u, const double* rho,
-                               const uint8_t* species, double gamma, double* st) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double* s = st + i * NCOL;
-  s[C_X] = pos[3 * i]; s[C_Y] = pos[3 * i + 1]; s[C_Z] = pos[3 * i + 2];
-  s[C_VX] = vel[3 * i]; s[C_VY] = vel[3 * i + 1]; s[C_VZ] = vel[3 * i + 2];
-  s[C_M] = mass[i];
-  s[C_H] = h[i];
-  double gm1 = gamma - 1.0;
-  s[C_RHO] = rho[i];
-  s[C_P] = gm1 * rho[i] * u[i];
-  s[C_CS] = sqrt(fmax(gamma * gm1 * u[i], 0.0));
-  s[C_SP] = (double)species[i];
-}
 
 // density write-back for gas rows of active leaves (hb/hydro.py:73-80), then
 // EOS columns for every row (hb/hydro.py:48-57)
@@ -78,12 +62,44 @@ __global__ void k_ghost_src(int64_t n, const int64_t* perm, const int64_t* inv,
   src_out[k] = g >= 0 ? inv[g] : -1;
 }
 
-template <class T>
-__global__ void k_gather(int64_t n, int w, const int64_t* perm, const T* in, T* out) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * w) return;
-  int64_t r = t / w, c = t - r * w;
-  out[t] = in[perm[r] * w + c];
+
+// mesh order <- input order for every field and the (n,12) float64 state
+// matrix (hb/particles.py:135-154) in one pass: each row reads its source row
+// once (10 fields) and writes the gathered fields and its state row
+struct FieldIn {
+  const double *pos, *vel, *mass, *h, *u, *rho;
+  const uint8_t *species, *ghost;
+  const int8_t* shift;
+  const int64_t* gid;
+};
+struct FieldOut {
+  double *pos, *vel, *mass, *h, *u, *rho;
+  uint8_t *species, *ghost;
+  int8_t* shift;
+  int64_t* gid;
+};
+__global__ void k_gather_state(int64_t n, const int64_t* perm, FieldIn in, FieldOut out,
+                               double gamma, double* st) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int64_t r = perm[k];
+  double* s = st + k * NCOL;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double x = in.pos[3 * r + d], v = in.vel[3 * r + d];
+    out.pos[3 * k + d] = x; out.vel[3 * k + d] = v;
+    s[C_X + d] = x; s[C_VX + d] = v;
+    out.shift[3 * k + d] = in.shift[3 * r + d];
+  }
+  double m = in.mass[r], h = in.h[r], u = in.u[r], rho = in.rho[r];
+  uint8_t sp = in.species[r];
+  out.mass[k] = m; out.h[k] = h; out.u[k] = u; out.rho[k] = rho;
+  out.species[k] = sp; out.ghost[k] = in.ghost[r]; out.gid[k] = in.gid[r];
+  double gm1 = gamma - 1.0;
+  s[C_M] = m; s[C_H] = h; s[C_RHO] = rho;
+  s[C_P] = gm1 * rho * u;
+  s[C_CS] = sqrt(fmax(gamma * gm1 * u, 0.0));
+  s[C_SP] = (double)sp;
 }
 
 struct StepWs {
@@ -201,23 +217,17 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->fields_ready_event)
     HB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a->fields_ready_event, 0));
   {
-    unsigned g3 = grid_for(n * 3, 256), g1 = grid_for(n, 256);
-    k_gather<double><<<g3, 256, 0, st>>>(n, 3, a->perm, a->pos_in, a->pos);
-    k_gather<double><<<g3, 256, 0, st>>>(n, 3, a->perm, a->vel_in, a->vel);
-    k_gather<double><<<g1, 256, 0, st>>>(n, 1, a->perm, a->mass_in, a->mass);
-    k_gather<double><<<g1, 256, 0, st>>>(n, 1, a->perm, a->smoothing_in, a->smoothing);
-    k_gather<double><<<g1, 256, 0, st>>>(n, 1, a->perm, a->internal_energy_in, a->internal_energy);
-    k_gather<double><<<g1, 256, 0, st>>>(n, 1, a->perm, a->density_in, a->density);
-    k_gather<uint8_t><<<g1, 256, 0, st>>>(n, 1, a->perm, a->species_in, a->species);
-    k_gather<uint8_t><<<g1, 256, 0, st>>>(n, 1, a->perm, a->ghost_in, a->ghost);
-    k_gather<int8_t><<<g3, 256, 0, st>>>(n, 3, a->perm, a->image_shift_in, a->image_shift);
-    k_gather<int64_t><<<g1, 256, 0, st>>>(n, 1, a->perm, a->global_id_in, a->global_id);
+    unsigned g1 = grid_for(n, 256);
+    FieldIn fi = {a->pos_in, a->vel_in, a->mass_in, a->smoothing_in, a->internal_energy_in,
+                  a->density_in, a->species_in, a->ghost_in, a->image_shift_in, a->global_id_in};
+    FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
+                   a->species, a->ghost, a->image_shift, a->global_id};
+    k_gather_state<<<g1, 256, 0, st>>>(n, a->perm, fi, fo, a->eos_gamma, w.state);
     if (a->ghost_src_in && a->ghost_src) {
       k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
       k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
       HB_COUNT_LAUNCH(2);
     }
-    HB_COUNT_LAUNCH(9);
     HB_LAUNCH_CHECK();
   }
   tm.mark(1);
@@ -239,11 +249,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     if (rc) return rc;
   }
   tm.mark(2);
-  // 3. state matrix, tilings
-  k_state_matrix<<<grid_for(n, 256), 256, 0, st>>>(n, a->pos, a->vel, a->mass, a->smoothing,
-                                                   a->internal_energy, a->density, a->species,
-                                                   a->eos_gamma, w.state);
-  HB_LAUNCH_CHECK();
+  // 3. tilings (the state matrix was written by the gather)
   w.Tg.n_leaves = nl; w.Ta.n_leaves = nl;
   // gravity over bin segments (half-warp tiles) or leaf tiles; bins beyond the
   // block tiler's capacity force the leaf path
