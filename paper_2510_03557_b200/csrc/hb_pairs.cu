@@ -471,9 +471,13 @@ __global__ void k_pack(int kid, int64_t n_tiles_cap, const int64_t* n_tiles_dev,
       P1[k] = make_float4((float)h, (float)norm3, (float)hinv, 0.0f);
       break;
     case KID_CRK_MOMENTS:
+    case KID_CRK_GRAD1:
+    case KID_CRK_GRAD2: {
+      double n5 = h > 0 ? sig / (h * h * h * h * h) : 0.0;
       P0[k] = make_float4(c[0], c[1], c[2], (float)vol);
-      P1[k] = make_float4((float)h, (float)norm3, (float)hinv, 0.0f);
+      P1[k] = make_float4((float)h, (float)norm3, (float)hinv, (float)n5);
       break;
+    }
     case KID_HYDRO_FORCE: {
       double fpart = rho > 0 ? st[C_P] / (rho * rho) : 0.0;
       double norm5 = h > 0 ? sig / (h * h * h * h * h) : 0.0;
@@ -1115,7 +1119,8 @@ void carve_tiling(Arena& ws, int64_t n, int64_t nl, Tiling& T, int tile_max, int
 
 int kid_selects_gas(int kid) {
   return kid == KID_DENSITY || kid == KID_NEIGHBOR_COUNT || kid == KID_CRK_MOMENTS ||
-         kid == KID_HYDRO_FORCE || kid == KID_CRK_INTERP;
+         kid == KID_HYDRO_FORCE || kid == KID_CRK_INTERP || kid == KID_CRK_GRAD1 ||
+         kid == KID_CRK_GRAD2;
 }
 
 int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t* leaf_end,
@@ -1190,6 +1195,8 @@ int launch_pairs(int kid, bool det, bool lean, const EvalDev& d, int64_t tcap,
     case KID_NEIGHBOR_COUNT: launch_kid<KID_NEIGHBOR_COUNT>(d, tcap, ntd, det, lean, st); break;
     case KID_STUB_ZERO: launch_kid<KID_STUB_ZERO>(d, tcap, ntd, det, lean, st); break;
     case KID_CRK_INTERP: launch_kid<KID_CRK_INTERP>(d, tcap, ntd, det, lean, st); break;
+    case KID_CRK_GRAD1: launch_kid<KID_CRK_GRAD1>(d, tcap, ntd, det, lean, st); break;
+    case KID_CRK_GRAD2: launch_kid<KID_CRK_GRAD2>(d, tcap, ntd, det, lean, st); break;
     default: return set_err(err, HB_CONTRACT, "unknown kernel id");
   }
   HB_LAUNCH_CHECK();

@@ -15,7 +15,8 @@ namespace hb {
 
 enum {
   KID_COUNTING = 0, KID_GRAVITY = 1, KID_GRAV_POT = 2, KID_DENSITY = 3, KID_CRK_MOMENTS = 4,
-  KID_HYDRO_FORCE = 5, KID_NEIGHBOR_COUNT = 6, KID_STUB_ZERO = 7, KID_CRK_INTERP = 8
+  KID_HYDRO_FORCE = 5, KID_NEIGHBOR_COUNT = 6, KID_STUB_ZERO = 7, KID_CRK_INTERP = 8,
+  KID_CRK_GRAD1 = 9, KID_CRK_GRAD2 = 10
 };
 enum { C_X = 0, C_Y, C_Z, C_VX, C_VY, C_VZ, C_M, C_H, C_RHO, C_P, C_CS, C_SP, NCOL };
 
@@ -154,6 +155,36 @@ template <> struct Pol<KID_CRK_MOMENTS> {
     float wx = w * dx, wy = w * dy;
     phi[4] = wx * dx; phi[5] = wx * dy; phi[6] = wx * dz;
     phi[7] = wy * dy; phi[8] = wy * dz; phi[9] = (w * dz) * dz;
+  }
+};
+// CRK gradient moments (north star's gradA / gradB; not in the reference):
+// G = V_j (dW/dr)/r (h_i) = V_j sigma/h_i^5 gradw(q); dr = x_i - x_j.
+// GRAD1: sum G dr (3), sum G dr dr (xx xy xz yy yz zz);  GRAD2: sum G dr dr dr
+// (xxx xxy xxz xyy xyz xzz yyy yyz yzz zzz).  P1.w = sigma/h^5 of the target.
+template <> struct Pol<KID_CRK_GRAD1> {
+  static constexpr int NP = 2, NC = 9, SEL = 1;
+  static constexpr bool HVAR = true;
+  __device__ static void pair(const float4* ti, const float4* sj, float dx, float dy, float dz,
+                              float r2, const PairParams&, float* phi) {
+    float q = sqrtf(r2) * ti[1].z;
+    float g = sj[0].w * (ti[1].w * gradw_body(q));
+    float gx = g * dx, gy = g * dy, gz = g * dz;
+    phi[0] = gx; phi[1] = gy; phi[2] = gz;
+    phi[3] = gx * dx; phi[4] = gx * dy; phi[5] = gx * dz;
+    phi[6] = gy * dy; phi[7] = gy * dz; phi[8] = gz * dz;
+  }
+};
+template <> struct Pol<KID_CRK_GRAD2> {
+  static constexpr int NP = 2, NC = 10, SEL = 1;
+  static constexpr bool HVAR = true;
+  __device__ static void pair(const float4* ti, const float4* sj, float dx, float dy, float dz,
+                              float r2, const PairParams&, float* phi) {
+    float q = sqrtf(r2) * ti[1].z;
+    float g = sj[0].w * (ti[1].w * gradw_body(q));
+    float gxx = g * dx * dx, gyy = g * dy * dy, gzz = g * dz * dz, gxy = g * dx * dy;
+    phi[0] = gxx * dx; phi[1] = gxx * dy; phi[2] = gxx * dz;
+    phi[3] = gyy * dx; phi[4] = gxy * dz; phi[5] = gzz * dx;
+    phi[6] = gyy * dy; phi[7] = gyy * dz; phi[8] = gzz * dy; phi[9] = gzz * dz;
   }
 };
 // hydro: P0 = (x,y,z,m), P1 = (vx,vy,vz,h), P2 = (P/rho^2, c_s, rho, sigma/h^5)

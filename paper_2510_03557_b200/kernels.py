@@ -18,6 +18,8 @@ KID_HYDRO_FORCE = 5
 KID_NEIGHBOR_COUNT = 6
 KID_STUB_ZERO = 7
 KID_CRK_INTERP = 8
+KID_CRK_GRAD1 = 9   # CRK gradient moments (north star; not in the reference)
+KID_CRK_GRAD2 = 10
 
 GAS = 1.0
 
@@ -126,6 +128,24 @@ def crk_moments_kernel(reach: float) -> PairKernel:
               ("smoothing",), ("mass", "density"), Symmetry.NONE, True, reach, [0.0],
               np.ones(10, dtype=np.int64), (52,) * 10, OpCost(adds=10, muls=18, special=1),
               mirrorable=False)
+
+
+def crk_gradient_kernels(reach: float) -> tuple:
+    """Gradient moments for gradA / gradB (the north star's CRK gradients; the
+    reference has none): with G = V_j (dW/dr)/r at h_i and dr = x_i - x_j,
+    GRAD1 = [sum G dr (3), sum G dr dr (xx xy xz yy yz zz)],
+    GRAD2 = sum G dr dr dr (xxx xxy xxz xyy xyz xzz yyy yyz yzz zzz)."""
+    g1 = _k("crk_grad1", KID_CRK_GRAD1,
+            ("gx", "gy", "gz", "gxx", "gxy", "gxz", "gyy", "gyz", "gzz"),
+            ("smoothing",), ("mass", "density"), Symmetry.NONE, True, reach, [0.0],
+            np.ones(9, dtype=np.int64), (48,) * 9, OpCost(adds=9, muls=14, special=1),
+            mirrorable=False)
+    g2 = _k("crk_grad2", KID_CRK_GRAD2,
+            ("gxxx", "gxxy", "gxxz", "gxyy", "gxyz", "gxzz", "gyyy", "gyyz", "gyzz", "gzzz"),
+            ("smoothing",), ("mass", "density"), Symmetry.NONE, True, reach, [0.0],
+            np.ones(10, dtype=np.int64), (44,) * 10, OpCost(adds=10, muls=18, special=1),
+            mirrorable=False)
+    return g1, g2
 
 
 def crk_interp_kernel(reach: float) -> PairKernel:
