@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 4
+#define HB_ABI_VERSION 5
 
 /* status codes; map onto hb/errors.py */
 enum HbStatus {
@@ -266,6 +266,12 @@ typedef struct HbStepArgs {
   int64_t n_leaves, n_entries, list_capacity_needed;
   float ms_phase[8];    /* build, list, tiling, sph A (count+density+eos),
                            sph B (crk+hydro+solve), gravity, tail, total */
+  void* status_out;     /* optional pinned host uint64_t[3] (zeroed by the caller):
+                           when non-NULL (and timing == 0) the step does NOT
+                           synchronise at its end; the error key and overflow
+                           flags are copied there asynchronously and the
+                           caller decodes them with hb_force_step_check()
+                           once the stream has completed                      */
   float ms_kernel[4];   /* timing=1: event-timed single-kernel spans on the step
                            stream: gravity pair kernel, SPH pass A kernel, SPH
                            pass B kernel, 0 (reserved) -- roofline inputs     */
@@ -274,6 +280,9 @@ typedef struct HbStepArgs {
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,
                                int64_t list_capacity);
 int hb_force_step(HbStepArgs* args, void* ws, size_t ws_bytes, void* stream, HbError* err);
+/* Decode a deferred status (HbStepArgs.status_out) after the step's stream has
+ * completed: the status the synchronous call would have returned. */
+int hb_force_step_check(const void* status, HbError* err);
 
 /* ---------------------------------------------------------------------------
  * Overload-shell exchange (multi-GPU ranks).  Distributed build_overload /

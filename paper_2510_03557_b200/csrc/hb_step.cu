@@ -44,9 +44,9 @@ __global__ void k_zero_ghost_rows(int64_t n_leaves, const int64_t* leaf_start,
   if (leaf >= n_leaves || !ghost_only[leaf]) return;
   for (int64_t r = leaf_start[leaf] + lane; r < leaf_end[leaf]; r += 32) {
     if (ncount) ncount[r] = 0.0;
-    for (int c = 0; c < 10; ++c) moments[r * 10 + c] = 0.0;
-    for (int c = 0; c < 5; ++c) hydro[r * 5 + c] = 0.0;
-    for (int c = 0; c < 3; ++c) grav[r * 3 + c] = 0.0;
+    if (moments) for (int c = 0; c < 10; ++c) moments[r * 10 + c] = 0.0;
+    if (hydro) for (int c = 0; c < 5; ++c) hydro[r * 5 + c] = 0.0;
+    if (grav) for (int c = 0; c < 3; ++c) grav[r * 3 + c] = 0.0;
   }
 }
 
@@ -258,6 +258,16 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   // SPH passes over bin segments too (fuller gas tiles); the leaf list stays the
   // reference's product and the fallback when a bin outgrows the tiler
   bool sph_bins = a->gravity_mode != 1 && max_bin_count <= 2048;
+  // bin segments evaluate every row; the reference's receivers are the
+  // non-ghost-only leaves, so their ghost-only rows read zero (hb/cmtree.py:318)
+  bool zero_ghost = sph_bins || !use_leaf_gravity;
+  bool zero_ghost_sph = zero_ghost;
+  auto zero_rows = [&](double* nc, double* mo, double* hy, double* gr) -> int {
+    k_zero_ghost_rows<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, w.leaf_start, w.leaf_end,
+                                                               w.ghost_only, nc, mo, hy, gr);
+    HB_LAUNCH_CHECK();
+    return HB_OK;
+  };
   int64_t n_seg = sph_bins ? nbins : nl;
   const int64_t* seg_s = w.leaf_start;
   const int64_t* seg_e = w.leaf_end;
@@ -356,10 +366,20 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     rc = launch_sph(1, sa, st, err);
     tm.kmark(5);
     if (rc) return rc;
+    if (zero_ghost) {  // before the solve: zero moments give A = 1, B = 0 as in the reference
+      rc = zero_rows(a->ghost_density ? nullptr : a->ncount, a->crk_moments, a->hydro, nullptr);
+      if (rc) return rc;
+      zero_ghost_sph = false;
+    }
     rc = hb_crk_solve(n, a->crk_moments, 10, a->species, 1e8, a->crk_A, a->crk_B,
                       a->crk_fallback, st, err);
     if (rc) return rc;
   }
+  if (zero_ghost_sph && !a->ghost_density && (a->passes & HB_PASS_NCOUNT)) {
+    rc = zero_rows(a->ncount, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+  }
+  // the SPH outputs are final here (ghost rows included): copies may start
   if (a->sph_done_event) HB_CUDA_TRY(cudaEventRecord((cudaEvent_t)a->sph_done_event, st));
   tm.mark(5);
   // 7. short-range gravity (hb/kernels.py:152-163): bin segments (hb_grav2.cu)
@@ -403,15 +423,22 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     }
   }
   tm.mark(6);
-  if (sph_bins || !use_leaf_gravity) {
-    // bin segments evaluate every row; the reference's receivers are the
-    // non-ghost-only leaves, so their ghost-only rows read zero (hb/cmtree.py:318)
-    k_zero_ghost_rows<<<grid_for(nl * 32, 256), 256, 0, st>>>(
-        nl, w.leaf_start, w.leaf_end, w.ghost_only, a->ghost_density ? nullptr : a->ncount,
-        a->crk_moments, a->hydro, a->grav);
-    HB_LAUNCH_CHECK();
+  if (zero_ghost && (a->passes & HB_PASS_GRAVITY)) {
+    rc = zero_rows(nullptr, nullptr, nullptr, a->grav);
+    if (rc) return rc;
   }
   tm.mark(7);
+  if (a->status_out && !tm.on) {
+    // deferred status: the error key and overflow flags land in the caller's
+    // pinned words; no end-of-step sync, so the caller can queue its
+    // device-to-host copies behind sph_done_event / the step stream right away
+    uint64_t* so = (uint64_t*)a->status_out;
+    HB_CUDA_TRY(cudaMemcpyAsync(&so[0], w.err_key, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    HB_CUDA_TRY(cudaMemcpyAsync(&so[1], w.Tg.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (use_leaf_gravity)
+      HB_CUDA_TRY(cudaMemcpyAsync(&so[2], w.Ta.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+    return HB_OK;
+  }
   unsigned long long ek = 0;
   int ovf = 0, ovf2 = 0;
   HB_CUDA_TRY(cudaMemcpyAsync(&ek, w.err_key, sizeof(ek), cudaMemcpyDeviceToHost, st));
@@ -453,6 +480,20 @@ extern "C" size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_
   ws.dry = true;
   force_step(&a, ws, nullptr, nullptr);
   return ws.used + 4096;
+}
+
+extern "C" int hb_force_step_check(const void* status, HbError* err) {
+  if (err) *err = HbError{};
+  const uint64_t* so = (const uint64_t*)status;
+  if ((uint32_t)so[1] || (uint32_t)so[2])
+    return set_err(err, HB_CONTRACT, "leaf exceeds the tiling capacity (2048 members)");
+  uint64_t ek = so[0];
+  if (ek != ~0ull) {
+    if (err) { err->leaf_a = -1; err->leaf_b = -1; }
+    return set_err(err, (ek % 4) == 1 ? HB_NONFINITE : HB_OVERFLOW,
+                   (ek % 4) == 1 ? "non-finite partial" : "accumulator overflow");
+  }
+  return HB_OK;
 }
 
 extern "C" int hb_force_step(HbStepArgs* a, void* wsp, size_t ws_bytes, void* stream, HbError* err) {

@@ -53,7 +53,7 @@ class HbStepArgs(C.Structure):
                    ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
                    ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
-                   ("ms_phase", C.c_float * 8), ("ms_kernel", C.c_float * 4)])
+                   ("ms_phase", C.c_float * 8), ("status_out", P), ("ms_kernel", C.c_float * 4)])
 
 
 def _bind(lib):
@@ -62,7 +62,19 @@ def _bind(lib):
     lib.hb_force_step_workspace.restype = C.c_size_t
     lib.hb_force_step_workspace.argtypes = [C.c_int64, C.c_void_p, C.c_int64, C.c_int64]
     lib.hb_force_step.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+    lib.hb_force_step_check.argtypes = [C.c_void_p, C.c_void_p]
     lib._step_bound = True
+
+
+def _event_handle(ev):
+    """Raw cudaEvent_t of a torch.cuda.Event (NULL for None).  torch creates
+    the CUDA event lazily on its first record(), so an unrecorded event has no
+    handle yet: one passed to the step would silently never be recorded."""
+    if ev is None:
+        return P(0)
+    if not ev.cuda_event:
+        raise HydroboxError("step event has no CUDA event yet: record() it once first")
+    return P(ev.cuda_event)
 
 
 @dataclass
@@ -171,10 +183,13 @@ class ResidentRank:
         return self.buf[self.cur]
 
     def step(self, passes: int = PASS_ALL, timing: bool = False, fields_ready=None,
-             sph_done=None) -> dict:
+             sph_done=None, status=None) -> dict:
         """One force evaluation; returns the device outputs (leaf order).
         fields_ready / sph_done: optional torch.cuda.Event for copy overlap
-        (see HbStepArgs in include/hb.h)."""
+        (see HbStepArgs in include/hb.h).  status: optional zeroed pinned
+        int64[3] tensor; when given (and timing is off) the step returns
+        without its final synchronisation and the caller must synchronise the
+        stream and call check_status(status) before trusting the outputs."""
         cfg = self.cfg
         src, dst = self.buf[self.cur], self.buf[1 - self.cur]
         a = HbStepArgs()
@@ -197,8 +212,9 @@ class ResidentRank:
         a.ghost_density = 1 if self.ghost_density else 0
         a.owned_targets = 1 if self.owned_targets else 0
         a.gravity_mode = int(os.environ.get("HB_GRAVITY_MODE", "0"))
-        a.fields_ready_event = P(fields_ready.cuda_event) if fields_ready is not None else P(0)
-        a.sph_done_event = P(sph_done.cuda_event) if sph_done is not None else P(0)
+        a.fields_ready_event = _event_handle(fields_ready)
+        a.sph_done_event = _event_handle(sph_done)
+        a.status_out = P(status.data_ptr()) if status is not None and not timing else P(0)
         for k in ("perm", "ncount", "grav", "hydro", "crk_moments", "crk_A", "crk_B",
                   "crk_fallback"):
             setattr(a, k, N.ptr(self.out[k]))
@@ -224,6 +240,13 @@ class ResidentRank:
                                   if timing else None)}
         return self.out
 
+    def check_status(self, status) -> None:
+        """Raise the error a deferred step (status=...) recorded; call after
+        the step's stream has been synchronised."""
+        err = N.HbError()
+        N.check(self.lib.hb_force_step_check(P(status.data_ptr()), C.byref(err)), err,
+                "force_step")
+
 
 SPH_OUTPUTS = ("ncount", "crk_A", "crk_B", "hydro")
 
@@ -233,9 +256,12 @@ class HostStepper:
 
     Per call: H2D of the 11 input fields (positions/shift/ghost first, the
     rest on a second copy stream while the mesh build runs), the step, and
-    D2H of the results -- the SPH outputs while gravity is still running, the
-    gravity output, permutation and density after.  Copies of one call overlap
-    that call's own compute; nothing is carried between calls."""
+    D2H of the results -- the SPH outputs and density while gravity is still
+    running, the gravity output and permutation after.  The step runs with a
+    deferred status word, so all copies are enqueued before the host waits;
+    the call then synchronises, checks the status and returns host arrays.
+    Copies of one call overlap that call's own compute; nothing is carried
+    between calls."""
 
     FIRST = ("pos", "image_shift", "ghost")
 
@@ -248,6 +274,9 @@ class HostStepper:
         self.ev_fields = torch.cuda.Event()
         self.ev_sph = torch.cuda.Event()
         self.ev_done = torch.cuda.Event()
+        self.status = torch.zeros(3, dtype=torch.int64, pin_memory=True)
+        for ev in (self.ev_first, self.ev_fields, self.ev_sph, self.ev_done):
+            ev.record()   # materialise the CUDA events (torch creates them lazily)
 
     def __call__(self):
         torch = N.torch_cuda()
@@ -264,7 +293,9 @@ class HostStepper:
                     dst[f].copy_(self.pin_in[f], non_blocking=True)
             self.ev_fields.record(self.s_in)
         main.wait_event(self.ev_first)
-        out = rk.step(PASS_ALL, fields_ready=self.ev_fields, sph_done=self.ev_sph)
+        self.status.zero_()   # no copy into it is pending: every call ends synchronised
+        out = rk.step(PASS_ALL, fields_ready=self.ev_fields, sph_done=self.ev_sph,
+                      status=self.status)
         self.ev_done.record(main)
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_event(self.ev_sph)
@@ -275,6 +306,8 @@ class HostStepper:
             for k in ("grav", "perm"):
                 self.pin_out[k].copy_(out[k], non_blocking=True)
         main.wait_stream(self.s_out)
+        main.synchronize()
+        rk.check_status(self.status)
         return self.pin_out
 
 

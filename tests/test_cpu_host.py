@@ -33,6 +33,23 @@ def test_workspace_queries_are_host_only():
     assert lib.hb_eval_pairs_workspace(C.byref(a)) > 10_000 * 16
 
 
+def test_deferred_status_decoding():
+    """hb_force_step_check maps the deferred status words exactly as the
+    synchronous end of hb_force_step does (host-only)."""
+    import ctypes as C
+    from paper_2510_03557_b200 import _native as N
+    lib = N.lib()
+    lib.hb_force_step_check.argtypes = [C.c_void_p, C.c_void_p]
+    ok = 0xFFFFFFFFFFFFFFFF
+    cases = [((ok, 0, 0), N.HB_OK), ((ok, 1, 0), N.HB_CONTRACT), ((ok, 0, 1), N.HB_CONTRACT),
+             ((4 * 7 + 1, 0, 0), N.HB_NONFINITE), ((4 * 7 + 2, 0, 0), N.HB_OVERFLOW),
+             ((0, 0, 0), N.HB_OVERFLOW)]
+    for words, want in cases:
+        buf = (C.c_uint64 * 3)(*words)
+        err = N.HbError()
+        assert lib.hb_force_step_check(C.addressof(buf), C.byref(err)) == want, words
+
+
 def test_leaf_capacity_bounds_the_split():
     from paper_2510_03557_b200 import _native as N
     lib = N.lib()

@@ -218,6 +218,9 @@ def test_gpu_resident_force_step(golden, oracle):
     ok = gas & (g["crk_m0"] > 0)
     relA = np.abs(out["crk_A"] - g["crk_A"])[ok] / np.abs(g["crk_A"][ok])
     assert np.median(relA) <= 1e-6 and np.quantile(relA, 0.999) <= 1e-5, relA.max()
+    z = g["crk_m0"] == 0   # non-gas and ghost-only rows: the reference's A = 1, B = 0
+    np.testing.assert_array_equal(out["crk_A"][z], g["crk_A"][z])
+    np.testing.assert_array_equal(out["crk_B"][z], g["crk_B"][z])
     own = p.ghost == 0
     st = g["state_eos"]
     ms = MeshView(g, "mesh_")
@@ -291,3 +294,34 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma):
     hy, _, _, _ = oracle.eval_pairs(hk, *args, mode="relaxed", workers=8)
     habs = oracle.eval_abs_sums(hk, *args)
     assert_fp32_close(out["hydro"], hy, habs, what="hydro")
+
+
+def test_gpu_host_stepper_matches_sync_step(golden):
+    """The e2e path (HostStepper: pinned H2D, step with deferred status, D2H
+    queued before the host waits) returns what the synchronous step returns."""
+    import torch
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.resident import STEP_FIELDS, HostStepper, ResidentRank, StepConfig
+    g = golden("step")
+    cfg = StepConfig(box=BoxGeometry(1.0), bin_width=float(g["bin_width"]), max_leaf_size=256,
+                     r_s=float(g["r_s"]), r_cut=float(g["r_cut"]), softening=float(g["eps"]),
+                     bounds_lo=g["bounds_lo"], bounds_hi=g["bounds_hi"])
+    p = particle_set(g, "in_")
+    ref = ResidentRank(p.copy(), cfg)
+    ref_out = {k: v.cpu().numpy() for k, v in ref.step().items()}
+    ref_density = ref.fields()["density"].cpu().numpy()
+    rk = ResidentRank(p.copy(), cfg)
+    pin_in = {f: torch.from_numpy(np.ascontiguousarray(getattr(p, f))).pin_memory()
+              for f in STEP_FIELDS}
+    names = ("grav", "hydro", "ncount", "crk_A", "crk_B", "perm")
+    pin_out = {k: torch.empty(rk.out[k].shape, dtype=rk.out[k].dtype).pin_memory() for k in names}
+    pin_out["density"] = torch.empty(rk.n, dtype=torch.float64).pin_memory()
+    hs = HostStepper(rk, pin_in, pin_out)
+    for _ in range(2):   # the second call reuses the buffers and the status word
+        got = {k: v.numpy().copy() for k, v in hs().items()}
+        np.testing.assert_array_equal(got["perm"][:p.n], ref_out["perm"][:p.n])
+        np.testing.assert_array_equal(got["ncount"][:p.n], ref_out["ncount"][:p.n])
+        for k in ("grav", "hydro", "crk_A", "crk_B"):
+            np.testing.assert_allclose(got[k][:p.n], ref_out[k][:p.n], rtol=1e-6, atol=1e-12,
+                                       err_msg=k)
+        np.testing.assert_allclose(got["density"], ref_density, rtol=1e-6)
