@@ -39,8 +39,15 @@ CONFIGS = {
     "c1": (32, 0.05, "both", "2x32^3 particles (DM + baryon), one short-range gravity + CRK-SPH step"),
     "c2": (128, 0.05, "both", "2x128^3 particles, z=10 near-uniform Zel'dovich ICs, single B200"),
     "c3": (256, 2.0, "both", "2x256^3 particles, z=0 strongly clustered (neighbour-count imbalance)"),
-    "c4": (512, 0.05, "both", "2x512^3 particles, spatial decomposition"),
+    "c4": (512, 0.05, "both", "2x512^3 particles, spatial decomposition with ghost exchange "
+                              "at 2/4/8 B200"),
 }
+# default workload per GPU count: configs[1] at N = 1 (the metric's single-GPU
+# config), configs[3] -- the config BASELINE.json names for 2/4/8 GPUs and its
+# strong-scaling target -- at N > 1
+DEFAULT_CONFIG = {1: "c2"}
+DEFAULT_CONFIG_MULTI = "c4"
+SUBBOX_ABOVE = 40_000_000   # CPU samples above this size use an interior sub-box
 
 
 def peaks():
@@ -56,14 +63,41 @@ def peaks():
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
-        self.gpu = gpu
+        self.gpu = int(gpu)
         self.proc = None
         self.lines = []
+        self.window = None
+
+    def start(self):
+        """Begin sampling (before warm-up, so nvidia-smi is running when the
+        timed window opens); mark the window with begin() / end()."""
+        return self.__enter__()
+
+    def begin(self):
+        self.window = [time.time(), None]
+
+    def end(self):
+        self.window[1] = time.time()
+        # wait (<= 5 s) for a sample stamped after the window: it bounds the
+        # window from above and flushes the pipe's buffered lines
+        t_stop = time.time() + 5.0
+        while time.time() < t_stop and not any(
+                (self._stamp(ln) or 0) > self.window[1] for ln in self.lines[-3:]):
+            time.sleep(0.05)
+        self.__exit__()
+
+    @staticmethod
+    def _stamp(ln):
+        try:
+            from datetime import datetime
+            return datetime.strptime(ln.split(",")[0].strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except Exception:
+            return None
 
     def __enter__(self):
         try:
@@ -92,8 +126,19 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
+        lines = self.lines
+        if self.window is not None and self.window[1] is not None:
+            # samples inside the timed window, plus the nearest one on each side
+            # (a window shorter than the 100 ms period may hold none)
+            t0, t1 = self.window
+            st = [(self._stamp(ln), ln) for ln in self.lines]
+            st = [(t, ln) for t, ln in st if t is not None]
+            inside = [ln for t, ln in st if t0 <= t <= t1]
+            before = [ln for t, ln in st if t < t0][-1:]
+            after = [ln for t, ln in st if t > t1][:1]
+            lines = before + inside + after
+        for ln in lines:
+            parts = [x.strip() for x in ln.split(",")][1:]
             if len(parts) < 6:
                 continue
             try:
@@ -108,25 +153,36 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_workload(cfg_name: str, rank: int = 0, world: int = 1):
+def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = False):
+    """Synthetic workload; local=True (world > 1) materialises only the rows
+    rank `rank` owns (identical to selecting them from the full set), so the
+    host never holds world copies of a 2x512^3 set."""
     from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.distributed import rank_grid_for
+    from paper_2510_03557_b200.domain import owner_ranks
     from paper_2510_03557_b200.ic import make_zeldovich_ic
     from paper_2510_03557_b200.resident import StepConfig
     npd, sigma, species, desc = CONFIGS[cfg_name]
     box = BoxGeometry(1.0)
-    p = make_zeldovich_ic(npd, box, sigma, species=species)
+    select = None
+    if local and world > 1:
+        grid = rank_grid_for(world)
+        select = lambda pos: owner_ranks(pos, box, grid) == rank  # noqa: E731
+    p = make_zeldovich_ic(npd, box, sigma, species=species, select=select)
     d = 1.0 / npd
     pm_grid = 2 * npd                       # SURVEY.md 8: pm_grid_n = 2 npd
     pm_cell = 1.0 / pm_grid
     r_s = 2.0 * pm_cell                     # hb/config.py:87-90
     r_cut = 5.0 * r_s                       # hb/config.py:91-93
-    eps = (1.0 / p.n ** (1.0 / 3.0)) / 50.0  # hb/config.py:95-99
-    h_max = float(p.smoothing.max())
+    n_all = (2 if species == "both" else 1) * npd ** 3
+    eps = (1.0 / n_all ** (1.0 / 3.0)) / 50.0  # hb/config.py:95-99
+    h_max = 1.3 * d if species == "both" else 0.0   # gas smoothing of the IC
     reach = max(r_cut, 2.0 * h_max)
     bin_width = max(4.0 * pm_cell, reach * (1 + 1e-9))  # hb/driver.py:147-150
     cfg = StepConfig(box=box, bin_width=bin_width, max_leaf_size=256, r_s=r_s, r_cut=r_cut,
                      softening=eps)
-    meta = {"workload": desc, "config": cfg_name, "n_particles": int(p.n),
+    meta = {"workload": desc, "config": cfg_name, "n_particles": n_all,
+            "n_gas": npd ** 3 if species == "both" else 0,
             "n_per_dim": npd, "sigma_psi_spacings": sigma, "smoothing": "h = 1.3 d (unadapted)",
             "r_s": "d", "r_cut": "5 d", "softening": "L/N^(1/3)/50", "max_leaf_size": 256,
             "mesh": "bare periodic box, bin width max(4 PM cells, reach)",
@@ -158,12 +214,36 @@ def pair_counts(p, cfg):
             "gravity_scheduled_leafpairs": int(g.counters["pairs_scheduled"])}
 
 
-def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None):
+def subbox_sample(p, cfg, n_target: int = 2 * 128 ** 3):
+    """Interior cube of the workload holding ~n_target owned particles plus its
+    overload shell (width = reach) as ghosts, on a bounded mesh -- the domain
+    one rank of a spatial decomposition sees.  Returns (ParticleSet, bounds_lo,
+    bounds_hi).  Per-particle work matches the full box (same lattice
+    statistics), so owned / time is the full workload's rate."""
+    L = cfg.box.side_length
+    side = L * min(1.0, (n_target / p.n) ** (1.0 / 3.0))
+    a = 0.5 * (L - side)
+    reach = max(cfg.r_cut, 2 * float(p.smoothing.max()))
+    x = p.pos
+    inner = np.all((x >= a) & (x < a + side), axis=1)
+    shell = np.all((x >= a - reach) & (x < a + side + reach), axis=1) & ~inner
+    idx = np.concatenate([np.nonzero(inner)[0], np.nonzero(shell)[0]])
+    q = p.select(idx)
+    q.ghost[:] = 0
+    q.ghost[int(inner.sum()):] = 1
+    q.image_shift[:] = 0
+    lo = np.full(3, a - reach)
+    hi = np.full(3, a + side + reach)
+    return q, lo, hi
+
+
+def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None, bounds=None):
     """The reference algorithm (oracle/ C restatement, bitwise-pinned to the
     reference) on the host cores: full build + lists, a contiguous 1/32 slice
     of each kernel's list scaled up (fixed per-call cost measured separately),
     full CRK solve.  Gravity and hydro use the reference driver's mirror mode
-    over unordered pairs (half the pair work)."""
+    over unordered pairs (half the pair work).  bounds: (lo, hi) of a bounded
+    (rank-domain) mesh, else the periodic box."""
     from oracle import oracle as O
     from paper_2510_03557_b200.kernels import (crk_moments_kernel, density_kernel,
                                                hydro_force_kernel, neighbor_count_kernel)
@@ -172,7 +252,9 @@ def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None):
     O.set_threads(threads)
     L = cfg.box.side_length
     t0 = time.perf_counter()
-    m = O.build_mesh(p.pos, p.image_shift, p.ghost, L, cfg.bin_width, cfg.max_leaf_size)
+    blo, bhi = bounds if bounds is not None else (None, None)
+    m = O.build_mesh(p.pos, p.image_shift, p.ghost, L, cfg.bin_width, cfg.max_leaf_size,
+                     bounds_lo=blo, bounds_hi=bhi)
     t_build = time.perf_counter() - t0
     h_max = float(p.smoothing.max())
     reach = max(cfg.r_cut, 2 * h_max)
@@ -224,12 +306,18 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     p, cfg, meta = make_workload(args.config)
+    bounds, where = None, ""
+    if p.n > SUBBOX_ABOVE:
+        p, lo, hi = subbox_sample(p, cfg)
+        bounds = (lo, hi)
+        where = (f"interior sub-box of {int(np.count_nonzero(p.ghost == 0))} owned + "
+                 f"{int(np.count_nonzero(p.ghost))} overload-shell particles (bounded mesh); ")
     vals = []
     base = None
     for _ in range(args.warmup):
-        cpu_baseline(p, cfg, frac=args.cpu_frac / 4)
+        cpu_baseline(p, cfg, frac=args.cpu_frac / 4, bounds=bounds)
     for _ in range(args.steps):
-        base = cpu_baseline(p, cfg, frac=args.cpu_frac)
+        base = cpu_baseline(p, cfg, frac=args.cpu_frac, bounds=bounds)
         vals.append(base["value"])
     v = float(np.median(vals))
     n_owned = meta["n_particles"]
@@ -238,25 +326,26 @@ def run_reference_arm(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": meta,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "port",
-                             "sample": base["sample"]},
+                             "sample": where + base["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def _make_rank(args, p, cfg, rank, world, group=None):
-    """N = 1: the bare periodic mesh; N > 1: cuboid rank + overload exchange."""
+def _make_rank(args, p, cfg, rank, world, meta, group=None, local=False):
+    """N = 1: the bare periodic mesh; N > 1: cuboid rank + overload exchange.
+    local: p already holds only this rank's rows."""
     from paper_2510_03557_b200.distributed import DistributedRank, rank_grid_for
     from paper_2510_03557_b200.domain import owner_ranks
     from paper_2510_03557_b200.resident import ResidentRank
     if world == 1:
         return ResidentRank(p, cfg)
-    owner = owner_ranks(p.pos, cfg.box, rank_grid_for(world))
-    gas = p.species == 1
-    return DistributedRank(p.select(np.nonzero(owner == rank)[0]), cfg.box, rank, world,
-                           cfg.r_s, cfg.r_cut, cfg.softening, float(p.smoothing.max()),
-                           float(p.smoothing[gas].min()), cfg.max_leaf_size, group=group,
-                           n_global=p.n)
+    if not local:
+        owner = owner_ranks(p.pos, cfg.box, rank_grid_for(world))
+        p = p.select(np.nonzero(owner == rank)[0])
+    h = 1.3 * (1.0 / CONFIGS[meta["config"]][0])   # IC gas smoothing (ic.py), every rank
+    return DistributedRank(p, cfg.box, rank, world, cfg.r_s, cfg.r_cut, cfg.softening, h, h,
+                           cfg.max_leaf_size, group=group, n_global=meta["n_particles"])
 
 
 def run_gpu_arm(args):
@@ -271,9 +360,10 @@ def run_gpu_arm(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    p, cfg, meta = make_workload(args.config, rank, world)
-    n_total = int(p.n)
-    rr = _make_rank(args, p, cfg, rank, world)
+    rank_rows = world > 1 and CONFIGS[args.config][0] ** 3 * 2 > SUBBOX_ABOVE
+    p, cfg, meta = make_workload(args.config, rank, world, local=rank_rows)
+    n_total = meta["n_particles"]
+    rr = _make_rank(args, p, cfg, rank, world, meta, local=rank_rows)
     engine = rr if world == 1 else None
     lib = N.lib()
     stream = torch.cuda.current_stream()
@@ -285,6 +375,7 @@ def run_gpu_arm(args):
         rr.step(timing=timing)
         return rr.engine.last
 
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -293,13 +384,14 @@ def run_gpu_arm(args):
     l0 = lib.hb_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     phases = []
-    with ClockSampler(local) as clocks:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            phases.append(step(timing=True)["ms_phase"])
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    clocks.begin()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        phases.append(step(timing=True)["ms_phase"])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks.end()
     launches = lib.hb_launch_count() - l0
     ms_total = ev0.elapsed_time(ev1)
     if dist:
@@ -386,7 +478,7 @@ def run_gpu_arm(args):
         # exact counting pass too large to run untimed next to the rank data:
         # per-particle in-support counts measured at c2 (same sigma/d statistics)
         per = {"gravity": 1047.0503, "sph": 81.0037}
-        n_gas = int(np.count_nonzero(p.species == 1))
+        n_gas = meta["n_gas"]
         sph = int(per["sph"] * n_gas)
         counts = {"gravity": int(per["gravity"] * n_total), "density": sph, "ncount": sph,
                   "crk": sph, "hydro": sph - n_gas,
@@ -439,11 +531,15 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="workload (default: c2 at 1 GPU, c4 at more)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-frac", type=float, default=1 / 32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.config is None:
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        args.config = DEFAULT_CONFIG.get(world, DEFAULT_CONFIG_MULTI)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_gpu_arm(args)

@@ -258,7 +258,10 @@ typedef struct HbStepArgs {
   double* ncount;       /* (n)                                                */
   double* grav;         /* (n,3) m_i a_i short-range gravity                  */
   double* hydro;        /* (n,5) fx fy fz m du/dt (edot_i) edot_j             */
-  double* crk_moments;  /* (n,10)                                             */
+  double* crk_moments;  /* (n,10), or NULL: the moments then live inside the
+                           workspace (over scratch that is dead by pass B) and
+                           crk_moments_out says where; valid until the
+                           workspace is reused                               */
   double* crk_A;        /* (n)                                                */
   double* crk_B;        /* (n,3)                                              */
   uint8_t* crk_fallback;/* (n)                                                */
@@ -275,6 +278,7 @@ typedef struct HbStepArgs {
   float ms_kernel[4];   /* timing=1: event-timed single-kernel spans on the step
                            stream: gravity pair kernel, SPH pass A kernel, SPH
                            pass B kernel, 0 (reserved) -- roofline inputs     */
+  double* crk_moments_out; /* out: where the (n,10) moments were written     */
 } HbStepArgs;
 
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,

@@ -174,7 +174,26 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   int64_t cap = hb_leaf_capacity(n, nbins, a->max_leaf_size);
   StepWs w;
   carve_step(ws, n, nbins, cap, a->list_capacity, w);
-  // nested arenas (mesh build, list csr, tilings) reuse the space after the carve
+  // nested arenas (mesh build, list csr, tilings) reuse the space after the carve.
+  // With crk_moments == NULL the moments live there too, past the scratch the
+  // bin gravity needs after pass B; only scratch that is dead before pass B
+  // (mesh build, list csr, SPH tiling) overlaps them.  Saves 48 of the 80 B
+  // per row the caller's buffer would cost (2x512^3 then fits one GPU).
+  size_t mom_end = 0;
+  double* mom = a->crk_moments;
+  {
+    Arena g = ws;
+    g.dry = true;
+    GravBinArgs gd = {};
+    gd.n = n; gd.nbins = nbins; gd.half_warp = true;  // the larger tiling of the two
+    gravity_bins(gd, g, st, err);
+    Arena mm = ws;
+    mm.used = g.used;
+    double* p = mm.take<double>(n * 10 + 1);
+    mom_end = mm.used;
+    if (!mom) mom = p;
+  }
+  a->crk_moments_out = mom;
   HbMeshArgs m = {};
   m.n = n; m.pos = a->pos_in; m.image_shift = a->image_shift_in; m.ghost = a->ghost_in;
   m.side_length = a->side_length;
@@ -199,10 +218,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     GravBinArgs gb = {};
     gb.n = n; gb.nbins = nbins; gb.half_warp = true;
     Arena s4 = ws; gravity_bins(gb, s4, st, err); if (s4.used > mx) mx = s4.used;
+    if (mom_end > mx) mx = mom_end;
     ws.used = mx;
     return HB_OK;
   }
-  if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (step)");
+  if (!ws.ok() || mom_end > ws.cap) return set_err(err, HB_CONTRACT, "workspace too small (step)");
   if (n <= 0) return HB_OK;
   if (n >= (1LL << 31)) return set_err(err, HB_CONTRACT, "too many rows for one rank");
   PhaseTimer tm(a->timing != 0, st);
@@ -325,7 +345,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   sa.P0 = w.P0; sa.P1 = w.P1; sa.P2 = w.P2; sa.state = w.state;
   sa.pshift = a->image_shift; sa.L = a->side_length; sa.reach = sph_reach; sa.band = band;
   sa.alpha = a->visc_alpha; sa.beta = a->visc_beta; sa.err_key = w.err_key;
-  sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = a->crk_moments; sa.hydro = a->hydro;
+  sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = mom; sa.hydro = a->hydro;
   sa.skip_leaf = (a->ghost_density && !sph_bins) ? w.ghost_only : nullptr;
   sa.skip_tiles = a->owned_targets ? 1 : 0;
   d.skip_leaf = a->ghost_density ? w.ghost_only : nullptr;
@@ -357,7 +377,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   tm.mark(4);
   // 5. pass B: CRK moments (+ 3x3 solve, hb/hydro.py:99-150) + hydro force (hb/kernels.py:222-258)
   if (a->passes & (HB_PASS_CRK | HB_PASS_HYDRO)) {
-    HB_CUDA_TRY(cudaMemsetAsync(a->crk_moments, 0, n * 10 * sizeof(double), st));
+    HB_CUDA_TRY(cudaMemsetAsync(mom, 0, n * 10 * sizeof(double), st));
     HB_CUDA_TRY(cudaMemsetAsync(a->hydro, 0, n * 5 * sizeof(double), st));
     rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, 1, st,
                   err);
@@ -367,11 +387,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     tm.kmark(5);
     if (rc) return rc;
     if (zero_ghost) {  // before the solve: zero moments give A = 1, B = 0 as in the reference
-      rc = zero_rows(a->ghost_density ? nullptr : a->ncount, a->crk_moments, a->hydro, nullptr);
+      rc = zero_rows(a->ghost_density ? nullptr : a->ncount, mom, a->hydro, nullptr);
       if (rc) return rc;
       zero_ghost_sph = false;
     }
-    rc = hb_crk_solve(n, a->crk_moments, 10, a->species, 1e8, a->crk_A, a->crk_B,
+    rc = hb_crk_solve(n, mom, 10, a->species, 1e8, a->crk_A, a->crk_B,
                       a->crk_fallback, st, err);
     if (rc) return rc;
   }

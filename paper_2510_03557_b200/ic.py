@@ -81,13 +81,20 @@ def zeldovich_displacement(n_per_dim: int, box: BoxGeometry, sigma_psi: float,
 
 def make_zeldovich_ic(n_per_dim: int, box: BoxGeometry, sigma_psi_cells: float,
                       seed: int = ZELDOVICH_SEED, velocity_factor: float = 0.1,
-                      gas_internal_energy: float = 1e-4, species: str = "both") -> ParticleSet:
+                      gas_internal_energy: float = 1e-4, species: str = "both",
+                      select=None) -> ParticleSet:
     """Two interleaved lattices displaced by the same psi.
 
     sigma_psi_cells: rms displacement in lattice spacings (0.05 ~ z=10,
-    2 ~ z=0).  species='dm' gives the single-species gravity-only set."""
+    2 ~ z=0).  species='dm' gives the single-species gravity-only set.
+    select: optional callable(pos (m,3)) -> bool mask; only the selected
+    particles are materialised (e.g. one rank's domain), with the values and
+    global ids they have in the full set, in the same order."""
     spacing = box.side_length / n_per_dim
     psi = zeldovich_displacement(n_per_dim, box, sigma_psi_cells * spacing, seed)
+    if select is not None:
+        return _zeldovich_subset(n_per_dim, box, psi, velocity_factor, gas_internal_energy,
+                                 species, select)
     vel = velocity_factor * psi
     if species == "dm":
         n3 = n_per_dim ** 3
@@ -102,6 +109,38 @@ def make_zeldovich_ic(n_per_dim: int, box: BoxGeometry, sigma_psi_cells: float,
     gas = _lattice(n_per_dim, spacing, 0.75 * spacing) + psi
     p = _two_species(n_per_dim, box, dm, gas, gas_internal_energy)
     p.vel = np.vstack([vel, vel])
+    return p
+
+
+def _zeldovich_subset(n_per_dim, box, psi, velocity_factor, gas_internal_energy, species,
+                      select) -> ParticleSet:
+    """Selected rows of make_zeldovich_ic's set, built species by species so
+    the full particle arrays never exist at once."""
+    n3 = n_per_dim ** 3
+    spacing = box.side_length / n_per_dim
+    lattices = ([(Species.DARK_MATTER, 0.5, 0)] if species == "dm"
+                else [(Species.DARK_MATTER, 0.25, 0), (Species.GAS, 0.75, n3)])
+    n_all = n3 * len(lattices)
+    parts = []
+    for sp, origin, id0 in lattices:
+        pos = wrap_position(_lattice(n_per_dim, spacing, origin * spacing) + psi, box)
+        idx = np.nonzero(select(pos))[0]
+        parts.append((sp, idx, pos[idx], id0))
+        del pos
+    p = ParticleSet(sum(len(x[1]) for x in parts))
+    o = 0
+    for sp, idx, pos, id0 in parts:
+        k = len(idx)
+        sl = slice(o, o + k)
+        p.pos[sl] = pos
+        p.vel[sl] = velocity_factor * psi[idx]
+        p.mass[sl] = box.volume / n_all
+        p.species[sl] = sp
+        if sp == Species.GAS:
+            p.smoothing[sl] = 1.3 * spacing
+            p.internal_energy[sl] = gas_internal_energy
+        p.global_id[sl] = idx + id0
+        o += k
     return p
 
 

@@ -53,7 +53,8 @@ class HbStepArgs(C.Structure):
                    ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
                    ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
-                   ("ms_phase", C.c_float * 8), ("status_out", P), ("ms_kernel", C.c_float * 4)])
+                   ("ms_phase", C.c_float * 8), ("status_out", P), ("ms_kernel", C.c_float * 4),
+                   ("crk_moments_out", P)])
 
 
 def _bind(lib):
@@ -120,6 +121,9 @@ class ResidentRank:
         self.last = None
         self.out = {}
         self.buf = [None, None]
+        # capacity slack for row counts that change between steps (distributed
+        # engine); a host-loaded rank keeps its n, so exact capacity
+        self._slack = 1.0 if particles is not None else 1.1
         if particles is not None:
             gas = particles.species == 1
             h_range = ((float(particles.smoothing[gas].min()), float(particles.smoothing.max()))
@@ -136,7 +140,7 @@ class ResidentRank:
         m = max(n, 1)
         cap = getattr(self, "_cap", 0)
         if m > cap:
-            cap = int(m * 1.1) + 1024
+            cap = int(m * self._slack) + 1024
             f64 = torch.float64
             self._buf1_store = {k: torch.empty((cap,) + tuple(v.shape[1:]), dtype=v.dtype,
                                                device="cuda") for k, v in fields.items()}
@@ -145,7 +149,6 @@ class ResidentRank:
                 "ncount": torch.zeros(cap, dtype=f64, device="cuda"),
                 "grav": torch.zeros((cap, 3), dtype=f64, device="cuda"),
                 "hydro": torch.zeros((cap, 5), dtype=f64, device="cuda"),
-                "crk_moments": torch.zeros((cap, 10), dtype=f64, device="cuda"),
                 "crk_A": torch.zeros(cap, dtype=f64, device="cuda"),
                 "crk_B": torch.zeros((cap, 3), dtype=f64, device="cuda"),
                 "crk_fallback": torch.zeros(cap, dtype=torch.uint8, device="cuda"),
@@ -215,9 +218,9 @@ class ResidentRank:
         a.fields_ready_event = _event_handle(fields_ready)
         a.sph_done_event = _event_handle(sph_done)
         a.status_out = P(status.data_ptr()) if status is not None and not timing else P(0)
-        for k in ("perm", "ncount", "grav", "hydro", "crk_moments", "crk_A", "crk_B",
-                  "crk_fallback"):
+        for k in ("perm", "ncount", "grav", "hydro", "crk_A", "crk_B", "crk_fallback"):
             setattr(a, k, N.ptr(self.out[k]))
+        a.crk_moments = P(0)   # moments live in the workspace (include/hb.h)
         for d in range(3):
             if a.reach > self.width[d] and self.nb[d] > 3:
                 raise HydroboxError(f"reach {a.reach:.4g} exceeds bin width "
@@ -234,6 +237,11 @@ class ResidentRank:
             N.check(st, err, "force_step")
             break
         self.cur = 1 - self.cur
+        off = int(a.crk_moments_out or 0) - ws.data_ptr()
+        if not 0 <= off <= ws.numel() - self.n * 80:
+            raise HydroboxError("force_step placed the CRK moments outside its workspace")
+        torch = N.torch_cuda()
+        self.out["crk_moments"] = ws[off:off + self.n * 80].view(torch.float64).view(self.n, 10)
         self.last = {"n_leaves": int(a.n_leaves), "n_entries": int(a.n_entries),
                      "ms_phase": ({**dict(zip(PHASES, list(a.ms_phase))),
                                    **dict(zip(KERNELS, list(a.ms_kernel)[:3]))}

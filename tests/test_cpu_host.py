@@ -50,6 +50,28 @@ def test_deferred_status_decoding():
         assert lib.hb_force_step_check(C.addressof(buf), C.byref(err)) == want, words
 
 
+def test_rank_local_ic_equals_selection():
+    """make_zeldovich_ic(select=...) (bench.py's rank-local workload at N > 1)
+    yields exactly the rows a rank would select from the full set."""
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.distributed import rank_grid_for
+    from paper_2510_03557_b200.domain import owner_ranks
+    from paper_2510_03557_b200.ic import make_zeldovich_ic
+    box = BoxGeometry(1.0)
+    grid = rank_grid_for(4)
+    for sp in ("both", "dm"):
+        full = make_zeldovich_ic(16, box, 0.05, species=sp)
+        own = owner_ranks(full.pos, box, grid)
+        for r in range(4):
+            sub = make_zeldovich_ic(16, box, 0.05, species=sp,
+                                    select=lambda pos: owner_ranks(pos, box, grid) == r)
+            ref = full.select(np.nonzero(own == r)[0])
+            for f in ("pos", "vel", "mass", "smoothing", "internal_energy", "density", "species",
+                      "ghost", "image_shift", "global_id", "ghost_src", "timestep_level"):
+                a, b = getattr(sub, f), getattr(ref, f)
+                assert a.dtype == b.dtype and np.array_equal(a, b), (sp, r, f)
+
+
 def test_leaf_capacity_bounds_the_split():
     from paper_2510_03557_b200 import _native as N
     lib = N.lib()

@@ -16,7 +16,7 @@ def main():
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
     p, cfg, meta = make_workload(sys.argv[1] if len(sys.argv) > 1 else "c2")
-    rr = _make_rank(None, p, cfg, rank, world)
+    rr = _make_rank(None, p, cfg, rank, world, meta)
     for _ in range(3):
         rr.step()
     torch.cuda.synchronize()
