@@ -250,9 +250,13 @@ typedef struct HbStepArgs {
      copies with the step: the step waits on fields_ready before it first reads
      any input field other than pos / image_shift / ghost (the mesh build only
      needs those), and records sph_done once ncount, density, CRK and hydro
-     outputs are final (gravity still running) */
+     outputs are final (gravity still running).  With late_fields set as well,
+     fields_ready covers only mass / smoothing / density / species; vel,
+     internal_energy, global_id and ghost_src are first read after the step
+     waits on late_fields, which happens after SPH pass A and before the EOS */
   void* fields_ready_event;
   void* sph_done_event;
+  void* late_fields_event;
   /* outputs (device, leaf order) */
   int64_t* perm;        /* (n) row k = input row perm[k]                    */
   double* ncount;       /* (n)                                                */

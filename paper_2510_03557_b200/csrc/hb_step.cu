@@ -78,6 +78,27 @@ struct FieldOut {
   int8_t* shift;
   int64_t* gid;
 };
+// late half of a split gather (HbStepArgs.late_fields_event): the fields SPH
+// pass A does not read, plus the state columns built from them
+__global__ void k_gather_late(int64_t n, const int64_t* perm, FieldIn in, FieldOut out,
+                              double* st) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int64_t r = perm[k];
+  double* s = st + k * NCOL;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double v = in.vel[3 * r + d];
+    out.vel[3 * k + d] = v;
+    s[C_VX + d] = v;
+  }
+  out.u[k] = in.u[r];
+  out.gid[k] = in.gid[r];
+}
+
+// LATE = true: skip the late fields (and P, c_s, which need u; k_eos writes
+// them after pass A, which reads neither)
+template <bool LATE>
 __global__ void k_gather_state(int64_t n, const int64_t* perm, FieldIn in, FieldOut out,
                                double gamma, double* st) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -86,20 +107,30 @@ __global__ void k_gather_state(int64_t n, const int64_t* perm, FieldIn in, Field
   double* s = st + k * NCOL;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    double x = in.pos[3 * r + d], v = in.vel[3 * r + d];
-    out.pos[3 * k + d] = x; out.vel[3 * k + d] = v;
-    s[C_X + d] = x; s[C_VX + d] = v;
+    double x = in.pos[3 * r + d];
+    out.pos[3 * k + d] = x;
+    s[C_X + d] = x;
+    if (!LATE) {
+      double v = in.vel[3 * r + d];
+      out.vel[3 * k + d] = v;
+      s[C_VX + d] = v;
+    }
     out.shift[3 * k + d] = in.shift[3 * r + d];
   }
-  double m = in.mass[r], h = in.h[r], u = in.u[r], rho = in.rho[r];
+  double m = in.mass[r], h = in.h[r], rho = in.rho[r];
   uint8_t sp = in.species[r];
-  out.mass[k] = m; out.h[k] = h; out.u[k] = u; out.rho[k] = rho;
-  out.species[k] = sp; out.ghost[k] = in.ghost[r]; out.gid[k] = in.gid[r];
-  double gm1 = gamma - 1.0;
+  out.mass[k] = m; out.h[k] = h; out.rho[k] = rho;
+  out.species[k] = sp; out.ghost[k] = in.ghost[r];
   s[C_M] = m; s[C_H] = h; s[C_RHO] = rho;
-  s[C_P] = gm1 * rho * u;
-  s[C_CS] = sqrt(fmax(gamma * gm1 * u, 0.0));
   s[C_SP] = (double)sp;
+  if (!LATE) {
+    double u = in.u[r];
+    out.u[k] = u;
+    out.gid[k] = in.gid[r];
+    double gm1 = gamma - 1.0;
+    s[C_P] = gm1 * rho * u;
+    s[C_CS] = sqrt(fmax(gamma * gm1 * u, 0.0));
+  }
 }
 
 struct StepWs {
@@ -236,20 +267,44 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   a->n_leaves = nl;
   if (a->fields_ready_event)
     HB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a->fields_ready_event, 0));
+  bool late_split = a->late_fields_event != nullptr;
   {
     unsigned g1 = grid_for(n, 256);
     FieldIn fi = {a->pos_in, a->vel_in, a->mass_in, a->smoothing_in, a->internal_energy_in,
                   a->density_in, a->species_in, a->ghost_in, a->image_shift_in, a->global_id_in};
     FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
                    a->species, a->ghost, a->image_shift, a->global_id};
-    k_gather_state<<<g1, 256, 0, st>>>(n, a->perm, fi, fo, a->eos_gamma, w.state);
+    if (late_split) {
+      k_gather_state<true><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, a->eos_gamma, w.state);
+    } else {
+      k_gather_state<false><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, a->eos_gamma, w.state);
+      if (a->ghost_src_in && a->ghost_src) {
+        k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
+        k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
+        HB_COUNT_LAUNCH(2);
+      }
+    }
+    HB_LAUNCH_CHECK();
+  }
+  // the late fields (split gather): waited for and gathered after pass A
+  auto gather_late = [&]() -> int {
+    if (!late_split) return HB_OK;
+    late_split = false;
+    HB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a->late_fields_event, 0));
+    unsigned g1 = grid_for(n, 256);
+    FieldIn fi = {a->pos_in, a->vel_in, a->mass_in, a->smoothing_in, a->internal_energy_in,
+                  a->density_in, a->species_in, a->ghost_in, a->image_shift_in, a->global_id_in};
+    FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
+                   a->species, a->ghost, a->image_shift, a->global_id};
+    k_gather_late<<<g1, 256, 0, st>>>(n, a->perm, fi, fo, w.state);
     if (a->ghost_src_in && a->ghost_src) {
       k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
       k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
       HB_COUNT_LAUNCH(2);
     }
     HB_LAUNCH_CHECK();
-  }
+    return HB_OK;
+  };
   tm.mark(1);
   // 2. ordered list as a receiver CSR
   ld.n_leaves = nl; ld.leaf_bin = w.leaf_bin; ld.leaf_level = nullptr; ld.bin_ptr = w.bin_ptr;
@@ -361,6 +416,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     tm.kmark(3);
     if (rc) return rc;
   }
+  rc = gather_late();  // before the EOS and the ghost alias sync read them
+  if (rc) return rc;
   if (a->passes & HB_PASS_DENSITY) {
     k_density_update<<<grid_for(nl * 32, 256), 256, 0, st>>>(
         nl, w.leaf_start, w.leaf_end, a->ghost_density ? w.no_ghost : w.ghost_only, a->species,

@@ -49,7 +49,7 @@ class HbStepArgs(C.Structure):
                    ("timing", C.c_int32), ("gravity_mode", C.c_int32),
                    ("ghost_density", C.c_int32), ("owned_targets", C.c_int32),
                    ("list_capacity", C.c_int64), ("fields_ready_event", P),
-                   ("sph_done_event", P),
+                   ("sph_done_event", P), ("late_fields_event", P),
                    ("perm", P), ("ncount", P), ("grav", P), ("hydro", P), ("crk_moments", P),
                    ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
@@ -186,10 +186,12 @@ class ResidentRank:
         return self.buf[self.cur]
 
     def step(self, passes: int = PASS_ALL, timing: bool = False, fields_ready=None,
-             sph_done=None, status=None) -> dict:
+             sph_done=None, status=None, late_fields=None) -> dict:
         """One force evaluation; returns the device outputs (leaf order).
         fields_ready / sph_done: optional torch.cuda.Event for copy overlap
-        (see HbStepArgs in include/hb.h).  status: optional zeroed pinned
+        (see HbStepArgs in include/hb.h); late_fields: event after which vel,
+        internal_energy, global_id and ghost_src are ready (read only from
+        the EOS on; fields_ready then covers the rest).  status: optional zeroed pinned
         int64[3] tensor; when given (and timing is off) the step returns
         without its final synchronisation and the caller must synchronise the
         stream and call check_status(status) before trusting the outputs."""
@@ -217,6 +219,7 @@ class ResidentRank:
         a.gravity_mode = int(os.environ.get("HB_GRAVITY_MODE", "0"))
         a.fields_ready_event = _event_handle(fields_ready)
         a.sph_done_event = _event_handle(sph_done)
+        a.late_fields_event = _event_handle(late_fields)
         a.status_out = P(status.data_ptr()) if status is not None and not timing else P(0)
         for k in ("perm", "ncount", "grav", "hydro", "crk_A", "crk_B", "crk_fallback"):
             setattr(a, k, N.ptr(self.out[k]))
@@ -262,19 +265,24 @@ SPH_OUTPUTS = ("ncount", "crk_A", "crk_B", "hydro")
 class HostStepper:
     """End-to-end force evaluation from pinned host arrays (the e2e path).
 
-    Per call: H2D of the 11 input fields (positions/shift/ghost first, the
-    rest on a second copy stream while the mesh build runs), the step, and
-    D2H of the results -- the SPH outputs and density while gravity is still
-    running, the gravity output and permutation after.  The step runs with a
+    Per call: H2D of the 11 input fields in three groups on a copy stream --
+    positions/shift/ghost (the mesh build waits only for these), then the
+    fields SPH pass A reads, then those first read at the EOS (vel,
+    internal_energy, ids) -- the step, and D2H of the results: the SPH
+    outputs, density and permutation while gravity is still running, the
+    gravity output after.  The step runs with a
     deferred status word, so all copies are enqueued before the host waits;
     the call then synchronises, checks the status and returns host arrays.
     Copies of one call overlap that call's own compute; nothing is carried
     between calls."""
 
-    FIRST = ("pos", "image_shift", "ghost")
+    FIRST = ("pos", "image_shift", "ghost")                  # the mesh build
+    EARLY = ("mass", "smoothing", "density", "species")         # + SPH pass A
+    LATE = ("vel", "internal_energy", "global_id", "ghost_src")  # from the EOS on
 
     def __init__(self, rank: "ResidentRank", pinned_in: dict, pinned_out: dict):
         torch = N.torch_cuda()
+        assert sorted(self.FIRST + self.EARLY + self.LATE) == sorted(STEP_FIELDS)
         self.rank, self.pin_in, self.pin_out = rank, pinned_in, pinned_out
         self.s_in = torch.cuda.Stream()
         self.s_out = torch.cuda.Stream()
@@ -282,8 +290,9 @@ class HostStepper:
         self.ev_fields = torch.cuda.Event()
         self.ev_sph = torch.cuda.Event()
         self.ev_done = torch.cuda.Event()
+        self.ev_late = torch.cuda.Event()
         self.status = torch.zeros(3, dtype=torch.int64, pin_memory=True)
-        for ev in (self.ev_first, self.ev_fields, self.ev_sph, self.ev_done):
+        for ev in (self.ev_first, self.ev_fields, self.ev_sph, self.ev_done, self.ev_late):
             ev.record()   # materialise the CUDA events (torch creates them lazily)
 
     def __call__(self):
@@ -296,23 +305,24 @@ class HostStepper:
             for f in self.FIRST:
                 dst[f].copy_(self.pin_in[f], non_blocking=True)
             self.ev_first.record(self.s_in)
-            for f in STEP_FIELDS:
-                if f not in self.FIRST:
-                    dst[f].copy_(self.pin_in[f], non_blocking=True)
+            for f in self.EARLY:
+                dst[f].copy_(self.pin_in[f], non_blocking=True)
             self.ev_fields.record(self.s_in)
+            for f in self.LATE:
+                dst[f].copy_(self.pin_in[f], non_blocking=True)
+            self.ev_late.record(self.s_in)
         main.wait_event(self.ev_first)
         self.status.zero_()   # no copy into it is pending: every call ends synchronised
         out = rk.step(PASS_ALL, fields_ready=self.ev_fields, sph_done=self.ev_sph,
-                      status=self.status)
+                      status=self.status, late_fields=self.ev_late)
         self.ev_done.record(main)
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_event(self.ev_sph)
-            for k in SPH_OUTPUTS:
+            for k in SPH_OUTPUTS + ("perm",):
                 self.pin_out[k].copy_(out[k], non_blocking=True)
             self.pin_out["density"].copy_(rk.fields()["density"], non_blocking=True)
             self.s_out.wait_event(self.ev_done)
-            for k in ("grav", "perm"):
-                self.pin_out[k].copy_(out[k], non_blocking=True)
+            self.pin_out["grav"].copy_(out["grav"], non_blocking=True)
         main.wait_stream(self.s_out)
         main.synchronize()
         rk.check_status(self.status)

@@ -310,6 +310,7 @@ def test_gpu_host_stepper_matches_sync_step(golden):
     ref = ResidentRank(p.copy(), cfg)
     ref_out = {k: v.cpu().numpy() for k, v in ref.step().items()}
     ref_density = ref.fields()["density"].cpu().numpy()
+    ref_fields = {f: v.cpu().numpy() for f, v in ref.fields().items()}
     rk = ResidentRank(p.copy(), cfg)
     pin_in = {f: torch.from_numpy(np.ascontiguousarray(getattr(p, f))).pin_memory()
               for f in STEP_FIELDS}
@@ -325,3 +326,5 @@ def test_gpu_host_stepper_matches_sync_step(golden):
             np.testing.assert_allclose(got[k][:p.n], ref_out[k][:p.n], rtol=1e-6, atol=1e-12,
                                        err_msg=k)
         np.testing.assert_allclose(got["density"], ref_density, rtol=1e-6)
+        for f, v in rk.fields().items():   # the split (early / late) gather
+            np.testing.assert_array_equal(v.cpu().numpy(), ref_fields[f], err_msg=f)
