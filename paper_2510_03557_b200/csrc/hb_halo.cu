@@ -174,6 +174,157 @@ __global__ void k_halo_select(int64_t n, const double* pos, const uint8_t* ghost
       }
 }
 
+// ---- block-aggregated select (hb_halo_pack_all) -------------------------------
+// Same selection as k_halo_select, restructured for throughput (it was
+// load-latency bound at ~320 GB/s): a block owns kSelRows consecutive rows and
+// prefetches the next row's position and ghost flag before working on the
+// current one; domain edges come precomputed (identical FP64 expression, no
+// division in the kernel); counts go to a shared-memory slot histogram with one
+// global atomic per (block, slot).  mode 1 re-walks the block's rows (L1/L2
+// resident) after reserving each slot's range with one atomic.
+constexpr int kSelBlock = 256;
+constexpr int kSelRows = 2048;
+constexpr int kSelMaxSlots = 1024;
+
+struct DomEdges {
+  double e[3][9];  // e[d][c] = (L * c) / g[d], c = 0..g[d]  (g[d] <= 8)
+};
+
+__device__ __forceinline__ int owner_edges(const DomGrid& G, const DomEdges& E, const double* p) {
+  int c[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    int k = 0;
+    for (int e = 1; e < G.g[d]; ++e)
+      if (p[d] >= E.e[d][e]) k = e;
+    c[d] = k;
+  }
+  return (c[0] * G.g[1] + c[1]) * G.g[2] + c[2];
+}
+
+// every ghost-copy slot of an owned row at p (owner cell oc), as k_halo_select
+template <class F>
+__device__ __forceinline__ void for_each_ghost_slot(const DomGrid& G, const DomEdges& E,
+                                                    int periodic_unsplit, const double* p,
+                                                    const int* oc, F&& f) {
+  bool interior = true;
+  double margin = G.w + 1e-9 * G.L;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (periodic_unsplit && G.g[d] == 1) continue;
+    double lo = E.e[d][oc[d]], hi = E.e[d][oc[d] + 1];
+    interior = interior && (p[d] - lo > margin) && (hi - p[d] > margin);
+  }
+  if (interior) return;
+  int cand_c[3][6], cand_s[3][6], nc[3];
+  for (int d = 0; d < 3; ++d) {
+    nc[d] = 0;
+    if (periodic_unsplit && G.g[d] == 1) {
+      cand_c[d][0] = 0; cand_s[d][0] = 0; nc[d] = 1;
+      continue;
+    }
+    for (int c = 0; c < G.g[d] && nc[d] < 6; ++c) {
+      double lo = E.e[d][c], hi = E.e[d][c + 1];
+      for (int sv = -1; sv <= 1; ++sv) {
+        double x = __dadd_rn(p[d], __dmul_rn((double)sv, G.L));
+        if (x > __dsub_rn(lo, G.w) && x < __dadd_rn(hi, G.w) && nc[d] < 6) {
+          cand_c[d][nc[d]] = c; cand_s[d][nc[d]] = sv; ++nc[d];
+        }
+      }
+    }
+  }
+  for (int a0 = 0; a0 < nc[0]; ++a0)
+    for (int a1 = 0; a1 < nc[1]; ++a1)
+      for (int a2 = 0; a2 < nc[2]; ++a2) {
+        int c0 = cand_c[0][a0], c1 = cand_c[1][a1], c2 = cand_c[2][a2];
+        int s0 = cand_s[0][a0], s1 = cand_s[1][a1], s2 = cand_s[2][a2];
+        if (s0 == 0 && s1 == 0 && s2 == 0 && c0 == oc[0] && c1 == oc[1] && c2 == oc[2]) continue;
+        int r = (c0 * G.g[1] + c1) * G.g[2] + c2;
+        f(r * 28 + (s0 + 1) * 9 + (s1 + 1) * 3 + (s2 + 1));
+      }
+}
+
+__global__ void __launch_bounds__(kSelBlock)
+k_halo_select_blk(int64_t n, const double* __restrict__ pos, const uint8_t* __restrict__ ghost,
+                  DomGrid G, DomEdges E, int self, int periodic_unsplit, int mode, int nslot,
+                  unsigned long long* counts, unsigned long long* fill, int64_t* out_row,
+                  int32_t* out_slot, int* drift, uint8_t* stay) {
+  __shared__ unsigned int hist[kSelMaxSlots];
+  __shared__ unsigned long long base[kSelMaxSlots];
+  __shared__ unsigned int s_stay;
+  for (int t = threadIdx.x; t < nslot; t += blockDim.x) hist[t] = 0;
+  if (threadIdx.x == 0) s_stay = 0;
+  __syncthreads();
+  int64_t r0 = (int64_t)blockIdx.x * kSelRows;
+  int64_t r1 = min(n, r0 + (int64_t)kSelRows);
+  unsigned my_stay = 0;
+  for (int sweep = 0; sweep < (mode == 0 ? 1 : 2); ++sweep) {
+    if (sweep == 1) {  // reserve this block's range of every slot
+      __syncthreads();
+      for (int t = threadIdx.x; t < nslot; t += blockDim.x) {
+        unsigned c = hist[t];
+        base[t] = c ? atomicAdd(&fill[t], (unsigned long long)c) : 0ull;
+        hist[t] = 0;
+      }
+      __syncthreads();
+    }
+    auto emit = [&](int slot, int64_t i) {
+      unsigned k = atomicAdd(&hist[slot], 1u);
+      if (sweep == 1) {
+        unsigned long long o = base[slot] + k;
+        out_row[o] = i;
+        out_slot[o] = slot;
+      }
+    };
+    int64_t i = r0 + threadIdx.x;
+    double px = 0.0, py = 0.0, pz = 0.0;
+    uint8_t gh = 1;
+    if (i < r1) { px = pos[3 * i]; py = pos[3 * i + 1]; pz = pos[3 * i + 2]; gh = ghost[i]; }
+    for (; i < r1; i += kSelBlock) {
+      int64_t in = i + kSelBlock;
+      double nx = 0.0, ny = 0.0, nz = 0.0;
+      uint8_t ng = 1;
+      if (in < r1) { nx = pos[3 * in]; ny = pos[3 * in + 1]; nz = pos[3 * in + 2]; ng = ghost[in]; }
+      bool st = false;
+      if (!gh) {
+        double p[3] = {px, py, pz};
+        int own = owner_edges(G, E, p);
+        st = stay && own == self;
+        if (!st) emit(own * 28 + 27, i);  // owned copy: migrant (or every row without stay)
+        int oc[3] = {own / (G.g[1] * G.g[2]), (own / G.g[2]) % G.g[1], own % G.g[2]};
+        if (mode == 0 && own != self) {  // DriftError: more than one domain hop
+          int b[3] = {self / (G.g[1] * G.g[2]), (self / G.g[2]) % G.g[1], self % G.g[2]};
+          for (int d = 0; d < 3; ++d) {
+            int hop = abs(oc[d] - b[d]);
+            hop = min(hop, G.g[d] - hop);
+            if (hop > 1) atomicExch(drift, 1);
+          }
+        }
+        for_each_ghost_slot(G, E, periodic_unsplit, p, oc, [&](int slot) { emit(slot, i); });
+      }
+      if (mode == 0 && stay) {
+        stay[i] = st ? 1 : 0;
+        my_stay += st ? 1u : 0u;
+      }
+      px = nx; py = ny; pz = nz; gh = ng;
+    }
+  }
+  if (mode != 0) return;
+  my_stay = __reduce_add_sync(0xffffffffu, my_stay);
+  if ((threadIdx.x & 31) == 0 && my_stay) atomicAdd(&s_stay, my_stay);
+  __syncthreads();
+  for (int t = threadIdx.x; t < nslot; t += blockDim.x)
+    if (hist[t]) atomicAdd(&counts[t], (unsigned long long)hist[t]);
+  if (threadIdx.x == 0 && s_stay) atomicAdd(&counts[nslot + 1], (unsigned long long)s_stay);
+}
+
+static DomEdges dom_edges(const DomGrid& G) {
+  DomEdges E;
+  for (int d = 0; d < 3; ++d)
+    for (int c = 0; c < 9; ++c) E.e[d][c] = c <= G.g[d] ? (G.L * (double)c) / (double)G.g[d] : 0.0;
+  return E;
+}
+
 __global__ void k_halo_pack(int64_t m, const int64_t* rows, const int32_t* slots,
                             const double* pos, const double* vel, const double* mass,
                             const double* h, const double* u, const double* rho,
@@ -413,10 +564,18 @@ extern "C" int hb_halo_pack_all(int64_t n, const HbFieldSet* src, const int32_t 
   if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (halo pack)");
   int* drift = (int*)(counts + nslot);
   HB_CUDA_TRY(cudaMemsetAsync(counts, 0, (nslot + 2) * sizeof(uint64_t), st));
+  bool blk = nslot <= kSelMaxSlots && g[0] <= 8 && g[1] <= 8 && g[2] <= 8;
+  DomEdges E = dom_edges(G);
+  unsigned sel_grid = (unsigned)((n + kSelRows - 1) / kSelRows);
   if (n > 0) {
-    k_halo_select<<<grid_for(n, 128), 128, 0, st>>>(
-        n, src->pos, src->ghost, G, self, periodic_unsplit, 0, (unsigned long long*)counts,
-        nullptr, nullptr, nullptr, drift, stay);
+    if (blk)
+      k_halo_select_blk<<<sel_grid, kSelBlock, 0, st>>>(
+          n, src->pos, src->ghost, G, E, self, periodic_unsplit, 0, (int)nslot,
+          (unsigned long long*)counts, nullptr, nullptr, nullptr, drift, stay);
+    else
+      k_halo_select<<<grid_for(n, 128), 128, 0, st>>>(
+          n, src->pos, src->ghost, G, self, periodic_unsplit, 0, (unsigned long long*)counts,
+          nullptr, nullptr, nullptr, drift, stay);
     HB_LAUNCH_CHECK();
   }
   HB_CUDA_TRY(cudaMemcpyAsync(counts_host, counts, (nslot + 2) * sizeof(uint64_t),
@@ -432,9 +591,14 @@ extern "C" int hb_halo_pack_all(int64_t n, const HbFieldSet* src, const int32_t 
     int rc = exclusive_scan_i64((const int64_t*)counts, fill, nslot, nullptr, s2, st, err);
     if (rc) return rc;
   }
-  k_halo_select<<<grid_for(n, 128), 128, 0, st>>>(
-      n, src->pos, src->ghost, G, self, periodic_unsplit, 1, (unsigned long long*)counts,
-      (unsigned long long*)fill, rows, slots, drift, stay);
+  if (blk)
+    k_halo_select_blk<<<sel_grid, kSelBlock, 0, st>>>(
+        n, src->pos, src->ghost, G, E, self, periodic_unsplit, 1, (int)nslot,
+        (unsigned long long*)counts, (unsigned long long*)fill, rows, slots, drift, stay);
+  else
+    k_halo_select<<<grid_for(n, 128), 128, 0, st>>>(
+        n, src->pos, src->ghost, G, self, periodic_unsplit, 1, (unsigned long long*)counts,
+        (unsigned long long*)fill, rows, slots, drift, stay);
   HB_LAUNCH_CHECK();
   G.w = 0.0;
   k_halo_pack<<<grid_for(m, 256), 256, 0, st>>>(m, rows, slots, src->pos, src->vel, src->mass,
