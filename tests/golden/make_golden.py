@@ -264,6 +264,23 @@ def adapt_fixture():
     return out
 
 
+def adapt_periodic_fixture():
+    """adapt_smoothing_length on a jittered two-species lattice in a bare
+    periodic box (no overload shell, so no alias ghosts): the case the
+    device-resident iteration serves."""
+    box = BoxGeometry(1.0)
+    p = make_lattice_ic(12, box, 0.2 / 12, seed=22)
+    bw = 0.25
+    mesh = build_mesh_and_leaves(p, box, bw, 64)
+    out = {}
+    out.update(particle_arrays(p, "in_"))
+    out.update(mesh_arrays(mesh))
+    out["bin_width"] = np.float64(bw)
+    h = adapt_smoothing_length(p, mesh, lambda: p.state_matrix(5 / 3), 40, bw, mode=DET)
+    out["h_out"] = h.copy()
+    return out
+
+
 def subcycle_fixture():
     """One PM interval of the hierarchical subcycle (hb/stepper.py:103-192) on a
     bare periodic 2x8^3 box (no overload shell, so no same-rank alias ghosts:
@@ -410,6 +427,7 @@ def main():
     only = set(sys.argv[1:])
     for name, fn in (("lane", lane_fixture), ("mesh", mesh_fixture),
                      ("step", step_fixture), ("adapt", adapt_fixture),
+                     ("adapt_periodic", adapt_periodic_fixture),
                      ("subcycle", subcycle_fixture), ("pm", pm_fixture),
                      ("fof", fof_fixture), ("ckpt", ckpt_fixture)):
         if only and name not in only:

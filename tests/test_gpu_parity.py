@@ -179,6 +179,30 @@ def test_gpu_adapt_smoothing_bitwise(golden):
     np.testing.assert_array_equal(h, g["h_out"])
 
 
+def test_gpu_adapt_smoothing_resident_bitwise(golden):
+    """No alias ghosts: adapt_smoothing_length iterates on the device (test on
+    the device, numpy update of the moving rows) and still returns the
+    reference's h bit for bit."""
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.cmtree import ChainingMesh
+    from paper_2510_03557_b200.hydro import adapt_smoothing_length
+    from paper_2510_03557_b200.lane import EvalMode
+    g = golden("adapt_periodic")
+    p = particle_set(g, "in_")
+    assert not np.any(p.ghost_src >= 0)
+    mv = MeshView(g, "mesh_")
+    mesh = ChainingMesh(box=BoxGeometry(1.0), bounds_lo=None, bounds_hi=None,
+                        bin_count=mv.bin_count, bin_width=mv.bin_width,
+                        periodic_axis=mv.periodic_axis, n_particles=p.n,
+                        leaf_start=mv.leaf_start, leaf_end=mv.leaf_end, leaf_lo=mv.leaf_lo,
+                        leaf_hi=mv.leaf_hi, leaf_level=mv.leaf_level.copy(),
+                        leaf_ghost_only=mv.leaf_ghost_only, leaf_bin=mv.leaf_bin,
+                        _bin_ptr=mv._bin_ptr, _bin_ids=mv._bin_ids)
+    h = adapt_smoothing_length(p, mesh, lambda: p.state_matrix(5 / 3), 40, float(g["bin_width"]),
+                               mode=EvalMode.DETERMINISTIC)
+    np.testing.assert_array_equal(h, g["h_out"])
+
+
 def test_gpu_nonfinite_raises(golden):
     from paper_2510_03557_b200.cmtree import InteractionList
     from paper_2510_03557_b200.errors import KernelEvalError

@@ -10,6 +10,7 @@
             clustered box (device sweeps + host group statistics)
   ckpt      HCKP encode of the c2 rank state from device fields; device CRC32C
             bandwidth over 512 MiB
+  adapt     adapt_smoothing_length to 64 neighbours from h = 1.3 d at c1 and c2
 
     python tools/bench_next.py [--npd 128] [--sub-npd 64] [--reps 5]
 Prints one JSON line per measurement."""
@@ -170,16 +171,67 @@ def bench_ckpt(npd, reps):
                     "D2H into pinned memory (PCIe-bound)"}
 
 
+def bench_adapt(npd, reps):
+    """adapt_smoothing_length (hb/hydro.py:199-248; the reference's largest
+    CPU cost, 47-48 s at 2x32^3 on 8 threads) to 64 neighbours from h = 1.3 d:
+    iterations and wall time, counts on the GPU (deterministic mode)."""
+    import numpy as np
+    import torch
+    from bench import make_workload
+    from paper_2510_03557_b200.cmtree import build_mesh_and_leaves
+    from paper_2510_03557_b200.hydro import adapt_smoothing_length
+    from paper_2510_03557_b200.lane import EvalMode
+    out = {}
+    for name in ("c1", "c2" if npd == 128 else "c1"):
+        p0, cfg, meta = make_workload(name)
+        ts, iters = [], None
+        for _ in range(max(1, reps)):
+            p = p0.copy()
+            mesh = build_mesh_and_leaves(p, cfg.box, cfg.bin_width, cfg.max_leaf_size)
+            from paper_2510_03557_b200 import lane as LN
+            calls = {"n": 0}
+            inner = LN.eval_on_device
+
+            def counting(*a, **k):   # one count evaluation per iteration
+                calls["n"] += 1
+                return inner(*a, **k)
+            LN.eval_on_device = counting
+            try:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                h = adapt_smoothing_length(p, mesh, lambda: p.state_matrix(cfg.eos_gamma), 64,
+                                           cfg.bin_width, mode=EvalMode.DETERMINISTIC)
+                torch.cuda.synchronize()
+                ts.append(time.perf_counter() - t0)
+            finally:
+                LN.eval_on_device = inner
+            iters = calls["n"]
+        gas = p.species == 1
+        out[name] = {"n_particles": int(p.n), "s": float(np.median(ts)), "iterations": iters,
+                     "h_over_d_median": float(np.median(h[gas]) * meta["n_per_dim"])}
+        if name == "c2":
+            break
+    return {"measurement": "adapt_smoothing_length", "target_neighbours": 64, "results": out,
+            "note": "state, list and leaf ranges resident on the GPU; per iteration the h "
+                    "column is refreshed, counts read back, and h updated in numpy as the "
+                    "reference does (bit-identical); reference CPU: 47-48 s at c1, 8 threads"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--npd", type=int, default=128)
     ap.add_argument("--sub-npd", type=int, default=64)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--only", default=None, help="one of pm, subcycle, fof, ckpt, adapt")
     args = ap.parse_args()
+    if args.only == "adapt":
+        print(json.dumps(bench_adapt(args.npd, max(1, args.reps // 2))))
+        return
     print(json.dumps(bench_pm(args.npd, args.reps)))
     print(json.dumps(bench_subcycle(args.sub_npd, max(1, args.reps // 2))))
     print(json.dumps(bench_fof(args.npd, max(1, args.reps // 2))))
     print(json.dumps(bench_ckpt(args.npd, args.reps)))
+    print(json.dumps(bench_adapt(args.npd, max(1, args.reps // 2))))
 
 
 if __name__ == "__main__":
