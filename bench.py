@@ -432,6 +432,15 @@ def run_gpu_arm(args):
     if world == 1:
         from paper_2510_03557_b200.resident import HostStepper
         host_stepper = HostStepper(rr, pinned_in, pinned_out)
+    else:
+        # rank set: the exchange reads every input field, so the H2D copies
+        # precede it; the SPH outputs, density and permutation drain while
+        # gravity runs (sph_done), the gravity output after; deferred status
+        s_out = torch.cuda.Stream()
+        ev_sph, ev_done = torch.cuda.Event(), torch.cuda.Event()
+        ev_sph.record()
+        ev_done.record()
+        status = torch.zeros(3, dtype=torch.int64, pin_memory=True)
 
     def e2e_step():
         if host_stepper is not None:
@@ -440,13 +449,26 @@ def run_gpu_arm(args):
         dst = rr.owned_fields = e2e_dev
         for f in STEP_FIELDS:
             dst[f].copy_(pinned_in[f], non_blocking=True)
-        step()
-        e = rr if world == 1 else rr.engine
-        for k in out_names:
-            if e.out[k].shape == pinned_out[k].shape:
-                pinned_out[k].copy_(e.out[k], non_blocking=True)
-        if e.fields()["density"].shape == pinned_out["density"].shape:
-            pinned_out["density"].copy_(e.fields()["density"], non_blocking=True)
+        status.zero_()
+        rr.step(sph_done=ev_sph, status=status)
+        main = torch.cuda.current_stream()
+        ev_done.record(main)
+        e = rr.engine
+        late = ("grav",)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_sph)
+            for k in out_names:
+                if k not in late and e.out[k].shape == pinned_out[k].shape:
+                    pinned_out[k].copy_(e.out[k], non_blocking=True)
+            if e.fields()["density"].shape == pinned_out["density"].shape:
+                pinned_out["density"].copy_(e.fields()["density"], non_blocking=True)
+            s_out.wait_event(ev_done)
+            for k in late:
+                if e.out[k].shape == pinned_out[k].shape:
+                    pinned_out[k].copy_(e.out[k], non_blocking=True)
+        main.wait_stream(s_out)
+        main.synchronize()
+        e.check_status(status)
 
     for _ in range(max(1, args.warmup // 2)):
         e2e_step()

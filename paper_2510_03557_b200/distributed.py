@@ -314,9 +314,11 @@ class DistributedRank:
             self.engine.set_fields(new, self.h_range)
         return new
 
-    def step(self, timing: bool = False):
+    def step(self, timing: bool = False, sph_done=None, status=None):
         """Exchange + force evaluation; returns device outputs (leaf order of
-        the rank set) and the reordered fields."""
+        the rank set) and the reordered fields.  sph_done / status: as
+        ResidentRank.step (copy overlap; deferred status, checked with
+        self.engine.check_status after the caller's sync)."""
         import torch
         if timing:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -324,7 +326,7 @@ class DistributedRank:
         self.exchange()
         if timing:
             e1.record()
-        out = self.engine.step(timing=timing)
+        out = self.engine.step(timing=timing, sph_done=sph_done, status=status)
         if timing:
             torch.cuda.synchronize()
             self.engine.last["ms_phase"]["exchange"] = e0.elapsed_time(e1)
