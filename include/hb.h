@@ -251,7 +251,7 @@ typedef struct HbStepArgs {
      any input field other than pos / image_shift / ghost (the mesh build only
      needs those), and records sph_done once ncount, density, CRK and hydro
      outputs are final (gravity still running).  With late_fields set as well,
-     fields_ready covers only mass / smoothing / density / species; vel,
+     fields_ready covers only mass / smoothing / species; vel, density,
      internal_energy, global_id and ghost_src are first read after the step
      waits on late_fields, which happens after SPH pass A and before the EOS */
   void* fields_ready_event;

@@ -94,10 +94,13 @@ __global__ void k_gather_late(int64_t n, const int64_t* perm, FieldIn in, FieldO
   }
   out.u[k] = in.u[r];
   out.gid[k] = in.gid[r];
+  double rho = in.rho[r];   // only non-gas rows keep it; gas rows get pass A's
+  out.rho[k] = rho;
+  s[C_RHO] = rho;
 }
 
-// LATE = true: skip the late fields (and P, c_s, which need u; k_eos writes
-// them after pass A, which reads neither)
+// LATE = true: skip the late fields (vel, u, density, ids) and P, c_s, which
+// need u and rho; k_eos writes them after pass A, which reads none of them
 template <bool LATE>
 __global__ void k_gather_state(int64_t n, const int64_t* perm, FieldIn in, FieldOut out,
                                double gamma, double* st) {
@@ -117,13 +120,16 @@ __global__ void k_gather_state(int64_t n, const int64_t* perm, FieldIn in, Field
     }
     out.shift[3 * k + d] = in.shift[3 * r + d];
   }
-  double m = in.mass[r], h = in.h[r], rho = in.rho[r];
+  double m = in.mass[r], h = in.h[r];
   uint8_t sp = in.species[r];
-  out.mass[k] = m; out.h[k] = h; out.rho[k] = rho;
+  out.mass[k] = m; out.h[k] = h;
   out.species[k] = sp; out.ghost[k] = in.ghost[r];
-  s[C_M] = m; s[C_H] = h; s[C_RHO] = rho;
+  s[C_M] = m; s[C_H] = h;
   s[C_SP] = (double)sp;
   if (!LATE) {
+    double rho = in.rho[r];
+    out.rho[k] = rho;
+    s[C_RHO] = rho;
     double u = in.u[r];
     out.u[k] = u;
     out.gid[k] = in.gid[r];

@@ -190,7 +190,7 @@ class ResidentRank:
         """One force evaluation; returns the device outputs (leaf order).
         fields_ready / sph_done: optional torch.cuda.Event for copy overlap
         (see HbStepArgs in include/hb.h); late_fields: event after which vel,
-        internal_energy, global_id and ghost_src are ready (read only from
+        internal_energy, density, global_id and ghost_src are ready (read only from
         the EOS on; fields_ready then covers the rest).  status: optional zeroed pinned
         int64[3] tensor; when given (and timing is off) the step returns
         without its final synchronisation and the caller must synchronise the
@@ -277,8 +277,8 @@ class HostStepper:
     between calls."""
 
     FIRST = ("pos", "image_shift", "ghost")                  # the mesh build
-    EARLY = ("mass", "smoothing", "density", "species")         # + SPH pass A
-    LATE = ("vel", "internal_energy", "global_id", "ghost_src")  # from the EOS on
+    EARLY = ("mass", "smoothing", "species")                     # + SPH pass A
+    LATE = ("vel", "internal_energy", "density", "global_id", "ghost_src")  # EOS on
 
     def __init__(self, rank: "ResidentRank", pinned_in: dict, pinned_out: dict):
         torch = N.torch_cuda()

@@ -1,4 +1,4 @@
-"""Lane-slot efficiency of the gravity tile schemes (CPU simulation, c1-like
+"""Lane-slot efficiency of the gravity (and SPH: argv[2] = sph) tile schemes (CPU simulation, c1-like
 geometry: 2 x npd^3 Zel'dovich, r_cut = 5 d, bins of >= r_cut, proportional
 median tiles of <= 32, 2-level k-d order inside a tile).
 
@@ -15,11 +15,14 @@ from paper_2510_03557_b200.box import BoxGeometry
 from paper_2510_03557_b200.ic import make_zeldovich_ic
 
 npd = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+mode = sys.argv[2] if len(sys.argv) > 2 else "gravity"   # or "sph": gas tiles, reach 2h
 p = make_zeldovich_ic(npd, BoxGeometry(1.0), 0.05)
-x = p.pos % 1.0
 d = 1.0 / npd
-rc = 5 * d
-nb = int(np.floor(1.0 / rc))
+if mode == "sph":
+    p = p.select(np.nonzero(p.species == 1)[0])
+x = p.pos % 1.0
+rc = 5 * d if mode == "gravity" else 2 * 1.3 * d
+nb = int(np.floor(1.0 / (5 * d)))   # bins of >= r_cut in both modes
 w = 1.0 / nb
 b3 = np.minimum((x / w).astype(int), nb - 1)
 bid = (b3[:, 0] * nb + b3[:, 1]) * nb + b3[:, 2]
