@@ -1,5 +1,5 @@
 """Write profiles/ summaries from ncu outputs (run here, no GPU needed):
-  python tools/ncu_digest.py launches <launches.csv> <out.md>
+  python tools/ncu_digest.py launches <launches.csv> <out.md> ["<command / note>"]
   python tools/ncu_digest.py kernels <report.ncu-rep> <out.md>"""
 import collections
 import csv
@@ -26,7 +26,7 @@ KEYS = [
 ]
 
 
-def launches(path, out):
+def launches(path, out, what="`tools/profile_step.py --steps 2` (2x128^3, c2)"):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr, data = rows[hi], rows[hi + 1:]
@@ -45,7 +45,7 @@ def launches(path, out):
     T = sum(tot.values())
     with open(out, "w") as f:
         f.write(f"# ncu launch list: {path}\n\n`ncu --metrics gpu__time_duration.sum "
-                "--clock-control none` over `tools/profile_step.py --steps 2` (2x128^3, c2); "
+                f"--clock-control none` over {what}; "
                 "cold-cache serialised launches: compare shares.\n\n")
         f.write(f"Total {T / 1e6:.3f} ms over {len(data)} launches.\n\n")
         f.write("| kernel | launches | total ms | share |\n|---|---|---|---|\n")
@@ -71,4 +71,4 @@ def kernels(path, out):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "kernels": kernels}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "kernels": kernels}[sys.argv[1]](*sys.argv[2:])
