@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 constexpr int kGravWarps = 8;
 constexpr int kGravStage = 128;
 
-template <int KIND, int JB>
+template <int KIND, int JB, int REP, int kGravBatch>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -846,8 +846,37 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   int cnt = 0;
   auto flush = [&]() {
     __syncwarp();
+    int q0 = 0;
+    if (KIND == GT_SOFT && kGravBatch > 1) {
+      // batches of kGravBatch sources: every table row is requested before the
+      // first one is used, so the gathers' latency overlaps within the warp
+      // (the unrolled per-pair loop stalled on each row: short scoreboard).
+      // Accumulation order is unchanged.
+      for (; q0 + kGravBatch <= cnt; q0 += kGravBatch) {
+        float bx[kGravBatch], by[kGravBatch], bz[kGravBatch], bu[kGravBatch], bm[kGravBatch];
+        float4 bc[kGravBatch];
+#pragma unroll
+        for (int b = 0; b < kGravBatch; ++b) {
+          float4 s = stage[q0 + b];
+          bx[b] = ti.x - s.x; by[b] = ti.y - s.y; bz[b] = ti.z - s.z; bm[b] = s.w;
+          float soft = fmaf(bz[b], bz[b], fmaf(by[b], by[b], fmaf(bx[b], bx[b], eps2)));
+          unsigned bits = __float_as_uint(soft);
+          unsigned kk = min((bits >> (23 - JB)) - gt.base, gt.last);
+          bu[b] = __uint_as_float((bits & ((1u << (23 - JB)) - 1u)) | 0x3F800000u) - 1.0f;
+          bc[b] = s_tab[kk * REP];
+        }
+#pragma unroll
+        for (int b = 0; b < kGravBatch; ++b) {
+          float4 c = bc[b];
+          float w = fmaf(fmaf(fmaf(c.w, bu[b], c.z), bu[b], c.y), bu[b], c.x) * bm[b];
+          ax = fmaf(w, bx[b], ax);
+          ay = fmaf(w, by[b], ay);
+          az = fmaf(w, bz[b], az);
+        }
+      }
+    }
 #pragma unroll 4
-    for (int q = 0; q < cnt; ++q) {
+    for (int q = q0; q < cnt; ++q) {
       float4 s = stage[q];
       float dx = ti.x - s.x, dy = ti.y - s.y, dz = ti.z - s.z;
       float w;
@@ -856,7 +885,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
         unsigned bits = __float_as_uint(soft);
         unsigned k = min((bits >> (23 - JB)) - gt.base, gt.last);
         float u = __uint_as_float((bits & ((1u << (23 - JB)) - 1u)) | 0x3F800000u) - 1.0f;
-        float4 c = s_tab[k];
+        float4 c = s_tab[k * REP];
         w = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x) * s.w;
       } else {
         float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
@@ -866,7 +895,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
         float fm = fmaf(rr, gt.scale, 12582912.0f);
         int k = min(__float_as_int(fm) - 0x4B400000, (int)gt.last);
         float u = fmaf(rr, gt.scale, 12582912.0f - fm);
-        float4 c = s_tab[k];
+        float4 c = s_tab[k * REP];
         float S = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x);
         w = (S * (ri * ri)) * (ri * s.w);
       }
@@ -932,30 +961,78 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   }
 }
 
-template <int KIND, int JB>
+// REP = 8: the table is held as 8 interleaved copies (row r of copy j at
+// float4 index 8 r + j) and lane l reads copy l & 7.  A 16-B gather is served
+// in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
+// a phase owns one 16-B bank group whatever row it reads, so the gather takes
+// the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
+template <int KIND, int JB, int REP, int NB>
 __global__ void __launch_bounds__(kGravWarps * 32, 4)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev) {
-  extern __shared__ float4 s_tab[];  // gt.rows
+  extern __shared__ float4 s_tab[];  // gt.rows * REP
   __shared__ float4 s_src[kGravWarps][kGravStage];
-  for (int k = threadIdx.x; k < gt.rows; k += blockDim.x) s_tab[k] = table[k];
+  for (int k = threadIdx.x; k < gt.rows * REP; k += blockDim.x) s_tab[k] = table[k / REP];
   __syncthreads();
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * kGravWarps + wid;
-  if (t < *n_tiles_dev) grav_tile<KIND, JB>(a, s_tab, gt, s_src[wid], t, lane);
+  if (t < *n_tiles_dev)
+    grav_tile<KIND, JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
+                                 t, lane);
+}
+
+// HB_GRAV_BATCH: sources per pipelined batch (1, 2, 4, 8).  c2 k_gravity:
+// 10.31 / 10.17 / 10.15 / 10.04 ms -> 8
+static int gravity_batch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HB_GRAV_BATCH");
+    int x = e ? atoi(e) : 8;
+    v = (x == 1 || x == 2 || x == 4) ? x : 8;
+  }
+  return v;
+}
+
+template <int KIND, int JB, int NB>
+static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
+                               unsigned grid, unsigned blk, const int64_t* ntd, cudaStream_t st,
+                               HbError* err) {
+  constexpr int REP = 8;
+  size_t sm = (size_t)gt.rows * REP * sizeof(float4);
+  // static staging + dynamic table may pass the 48 KB default: raise the
+  // per-kernel limit whenever the table grows (per device and instantiation)
+  static std::mutex mu;
+  static size_t set_for[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<KIND, JB, REP, NB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      set_for[dev] = sm;
+    }
+  }
+  k_gravity<KIND, JB, REP, NB><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+  return HB_OK;
 }
 
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
                         const int64_t* ntd, cudaStream_t st, HbError* err) {
   unsigned grid = grid_for(tcap, kGravWarps), blk = kGravWarps * 32;
-  size_t sm = gt.rows * sizeof(float4);
+  int nb = gravity_batch();
+  int rc;
   if (gt.kind == GT_SOFT && gt.jbits == 5)
-    k_gravity<GT_SOFT, 5><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+    rc = launch_gravity_kind<GT_SOFT, 5, 8>(d, table, gt, grid, blk, ntd, st, err);
   else if (gt.kind == GT_SOFT)
-    k_gravity<GT_SOFT, 4><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+    rc = nb == 1   ? launch_gravity_kind<GT_SOFT, 4, 1>(d, table, gt, grid, blk, ntd, st, err)
+         : nb == 2 ? launch_gravity_kind<GT_SOFT, 4, 2>(d, table, gt, grid, blk, ntd, st, err)
+         : nb == 8 ? launch_gravity_kind<GT_SOFT, 4, 8>(d, table, gt, grid, blk, ntd, st, err)
+                   : launch_gravity_kind<GT_SOFT, 4, 4>(d, table, gt, grid, blk, ntd, st, err);
   else if (gt.kind == GT_T)
-    k_gravity<GT_T, 0><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+    rc = launch_gravity_kind<GT_T, 0, 1>(d, table, gt, grid, blk, ntd, st, err);
   else
-    k_gravity<GT_R, 0><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+    rc = launch_gravity_kind<GT_R, 0, 1>(d, table, gt, grid, blk, ntd, st, err);
+  if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
