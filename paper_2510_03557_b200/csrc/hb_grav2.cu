@@ -16,13 +16,16 @@
 namespace hb {
 
 constexpr int kG2Warps = 8;
-// within-tile k-d levels for the bin-gravity tiles (2: 4 groups of <= 8 lanes);
-// HB_GRAV_TILE_LEVELS overrides (0 disables) for A/B measurement
+// within-tile k-d levels for the bin-gravity tiles (2: 4 groups of <= 8 lanes).
+// It only served the table gather's bank conflicts; with the conflict-free
+// 8-copy table (hb_pairs.cu) k_gravity runs the same without it (10.036 ms
+// both at c2) and the step saves the 0.21 ms pass, so the default is 0.
+// HB_GRAV_TILE_LEVELS overrides for A/B measurement.
 static int tile_order_levels() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HB_GRAV_TILE_LEVELS");
-    v = e ? atoi(e) : 2;
+    v = e ? atoi(e) : 0;
   }
   return v;
 }
