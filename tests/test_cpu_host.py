@@ -172,3 +172,36 @@ def test_checkpoint_decode_reference_blob(golden):
     assert (step, rank) == (12, 3)
     for k in ("pos", "vel", "global_id", "ghost_src", "image_shift", "timestep_level"):
         np.testing.assert_array_equal(getattr(p, k), g["in_" + k])
+
+
+def test_clock_sampler_window():
+    """bench.ClockSampler keeps the samples stamped inside the timed window plus
+    the nearest one on each side, and reports throttle reasons seen there."""
+    import bench
+    c = bench.ClockSampler(0)
+    rows = [("12:00:00.000", 1965, "Not Active"), ("12:00:00.100", 1900, "Active"),
+            ("12:00:00.200", 1950, "Not Active"), ("12:00:05.000", 500, "Not Active")]
+    c.lines = [f"2026/10/18 {t}, {mhz}, 1965, Not Active, Not Active, Not Active, {pc}"
+               for t, mhz, pc in rows]
+    t = bench.ClockSampler._stamp(c.lines[1])
+    c.window = [t - 0.01, t + 0.01]
+    s = c.summary()
+    assert s["samples"] == 3 and s["sm_mhz"] == 1950.0 and s["reasons"] == ["sw_power_cap"]
+    c.window = None   # no window: every sample
+    assert c.summary()["samples"] == 4
+
+
+def test_subbox_sample_is_a_rank_domain():
+    """bench.subbox_sample: owned rows are exactly the interior cube, ghosts the
+    r_cut shell around it, all unshifted, on bounds that enclose both."""
+    import bench
+    p, cfg, meta = bench.make_workload("c1")
+    q, lo, hi = bench.subbox_sample(p, cfg, n_target=4096)
+    own = q.ghost == 0
+    side = (hi - lo) - 2 * max(cfg.r_cut, 2 * float(p.smoothing.max()))
+    a = lo + (hi - lo - side) / 2
+    inside = np.all((p.pos >= a) & (p.pos < a + side), axis=1)
+    assert own.sum() == inside.sum() and 0 < own.sum() < p.n
+    np.testing.assert_array_equal(np.sort(q.global_id[own]), np.sort(p.global_id[inside]))
+    assert np.all((q.pos >= lo) & (q.pos < hi)) and not np.any(q.image_shift)
+    assert q.ghost[~own].min() == 1 and (~own).sum() > 0
