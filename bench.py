@@ -41,7 +41,10 @@ CONFIGS = {
     "c3": (256, 2.0, "both", "2x256^3 particles, z=0 strongly clustered (neighbour-count imbalance)"),
     "c4": (512, 0.05, "both", "2x512^3 particles, spatial decomposition with ghost exchange "
                               "at 2/4/8 B200"),
+    "c5": (1024, 0.05, "dm", "gravity-only 1024^3 dark-matter particles, short-range PP kernel "
+                             "sweep (>= 4 B200)"),
 }
+DEVICE_IC_ABOVE = 1 << 29   # particles: displacement field built on the GPU (numpy: ~60 GB/rank)
 # default workload per GPU count: configs[1] at N = 1 (the metric's single-GPU
 # config), configs[3] -- the config BASELINE.json names for 2/4/8 GPUs and its
 # strong-scaling target -- at N > 1
@@ -153,28 +156,47 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = False):
+def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = False,
+                  region=None):
     """Synthetic workload; local=True (world > 1) materialises only the rows
     rank `rank` owns (identical to selecting them from the full set), so the
-    host never holds world copies of a 2x512^3 set."""
+    host never holds world copies of a 2x512^3 set; region = (lo, hi) keeps
+    only the particles inside that cube (the reference arm's sub-box sample).
+    Above DEVICE_IC_ABOVE particles the displacement field is built on the
+    GPU (ic.make_zeldovich_ic_device) and a selection is required."""
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.distributed import rank_grid_for
-    from paper_2510_03557_b200.domain import owner_ranks
-    from paper_2510_03557_b200.ic import make_zeldovich_ic
+    from paper_2510_03557_b200.domain import owner_ranks, owner_ranks_torch
+    from paper_2510_03557_b200.ic import make_zeldovich_ic, make_zeldovich_ic_device
     from paper_2510_03557_b200.resident import StepConfig
     npd, sigma, species, desc = CONFIGS[cfg_name]
     box = BoxGeometry(1.0)
+    n_all = (2 if species == "both" else 1) * npd ** 3
+    on_device = n_all > DEVICE_IC_ABOVE
     select = None
-    if local and world > 1:
+    if region is not None:
+        rlo, rhi = (float(v) for v in region)
+        if on_device:
+            select = lambda pos: ((pos >= rlo) & (pos < rhi)).all(dim=1)  # noqa: E731
+        else:
+            select = lambda pos: np.all((pos >= rlo) & (pos < rhi), axis=1)  # noqa: E731
+    elif local and world > 1:
         grid = rank_grid_for(world)
-        select = lambda pos: owner_ranks(pos, box, grid) == rank  # noqa: E731
-    p = make_zeldovich_ic(npd, box, sigma, species=species, select=select)
+        if on_device:
+            select = lambda pos: owner_ranks_torch(pos, box, grid) == rank  # noqa: E731
+        else:
+            select = lambda pos: owner_ranks(pos, box, grid) == rank  # noqa: E731
+    if on_device:
+        if select is None:
+            raise ValueError(f"{cfg_name} is built per rank or per region only (--gpus >= 4)")
+        p = make_zeldovich_ic_device(npd, box, sigma, select, species=species)
+    else:
+        p = make_zeldovich_ic(npd, box, sigma, species=species, select=select)
     d = 1.0 / npd
     pm_grid = 2 * npd                       # SURVEY.md 8: pm_grid_n = 2 npd
     pm_cell = 1.0 / pm_grid
     r_s = 2.0 * pm_cell                     # hb/config.py:87-90
     r_cut = 5.0 * r_s                       # hb/config.py:91-93
-    n_all = (2 if species == "both" else 1) * npd ** 3
     eps = (1.0 / n_all ** (1.0 / 3.0)) / 50.0  # hb/config.py:95-99
     h_max = 1.3 * d if species == "both" else 0.0   # gas smoothing of the IC
     reach = max(r_cut, 2.0 * h_max)
@@ -183,7 +205,10 @@ def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = Fa
                      softening=eps)
     meta = {"workload": desc, "config": cfg_name, "n_particles": n_all,
             "n_gas": npd ** 3 if species == "both" else 0,
-            "n_per_dim": npd, "sigma_psi_spacings": sigma, "smoothing": "h = 1.3 d (unadapted)",
+            "n_per_dim": npd, "sigma_psi_spacings": sigma,
+            "smoothing": "h = 1.3 d (unadapted)" if species == "both" else "none (gravity only)",
+            "passes": "all" if species == "both" else "gravity",
+            "ic_fft": "cuFFT (GPU)" if on_device else "numpy",
             "r_s": "d", "r_cut": "5 d", "softening": "L/N^(1/3)/50", "max_leaf_size": 256,
             "mesh": "bare periodic box, bin width max(4 PM cells, reach)",
             "bins_per_axis": int(np.floor(1.0 / bin_width)),
@@ -214,16 +239,23 @@ def pair_counts(p, cfg):
             "gravity_scheduled_leafpairs": int(g.counters["pairs_scheduled"])}
 
 
-def subbox_sample(p, cfg, n_target: int = 2 * 128 ** 3):
+def subbox_region(L: float, r_cut: float, n_all: int, h_max: float,
+                  n_target: int = 2 * 128 ** 3):
+    """(a, side, reach) of the interior sample cube [a, a + side)^3 holding
+    ~n_target of n_all particles; its shell reaches `reach` further out."""
+    side = L * min(1.0, (n_target / n_all) ** (1.0 / 3.0))
+    return 0.5 * (L - side), side, max(r_cut, 2 * h_max)
+
+
+def subbox_sample(p, cfg, n_target: int = 2 * 128 ** 3, n_all: int | None = None):
     """Interior cube of the workload holding ~n_target owned particles plus its
     overload shell (width = reach) as ghosts, on a bounded mesh -- the domain
     one rank of a spatial decomposition sees.  Returns (ParticleSet, bounds_lo,
     bounds_hi).  Per-particle work matches the full box (same lattice
-    statistics), so owned / time is the full workload's rate."""
-    L = cfg.box.side_length
-    side = L * min(1.0, (n_target / p.n) ** (1.0 / 3.0))
-    a = 0.5 * (L - side)
-    reach = max(cfg.r_cut, 2 * float(p.smoothing.max()))
+    statistics), so owned / time is the full workload's rate.  p may already
+    be restricted to the shell's outer cube (then pass the full n_all)."""
+    a, side, reach = subbox_region(cfg.box.side_length, cfg.r_cut, n_all or p.n,
+                                   float(p.smoothing.max()), n_target)
     x = p.pos
     inner = np.all((x >= a) & (x < a + side), axis=1)
     shell = np.all((x >= a - reach) & (x < a + side + reach), axis=1) & ~inner
@@ -237,7 +269,8 @@ def subbox_sample(p, cfg, n_target: int = 2 * 128 ** 3):
     return q, lo, hi
 
 
-def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None, bounds=None):
+def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None, bounds=None,
+                 gravity_only: bool = False):
     """The reference algorithm (oracle/ C restatement, bitwise-pinned to the
     reference) on the host cores: full build + lists, a contiguous 1/32 slice
     of each kernel's list scaled up (fixed per-call cost measured separately),
@@ -271,6 +304,8 @@ def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None, bound
             ("crk", crk_moments_kernel(2 * h_max), False),
             ("gravity", gk, True),
             ("hydro", hydro_force_kernel(2 * h_max), True)]
+    if gravity_only:   # the gravity-only configs' step: build + lists + gravity
+        jobs = [j for j in jobs if j[0] == "gravity"]
     times = {}
     for name, ker, mirror in jobs:
         A, B, S = (ua, ub, us) if mirror else (la, lb, ls)
@@ -285,12 +320,13 @@ def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None, bound
                      workers=threads, mirror=mirror)
         t_s = time.perf_counter() - t0
         times[name] = t_fixed + max(t_s - t_fixed, 0.0) * len(A) / k
-    t0 = time.perf_counter()
-    vals = np.zeros((p.n, 10))
-    vals[:, 0] = 1.0
-    vals[:, 4] = vals[:, 7] = vals[:, 9] = 1.0
-    O.crk_solve(vals, p.species[perm] == 1)
-    times["crk_solve"] = time.perf_counter() - t0
+    if not gravity_only:
+        t0 = time.perf_counter()
+        vals = np.zeros((p.n, 10))
+        vals[:, 0] = 1.0
+        vals[:, 4] = vals[:, 7] = vals[:, 9] = 1.0
+        O.crk_solve(vals, p.species[perm] == 1)
+        times["crk_solve"] = time.perf_counter() - t0
     total = t_build + t_list + sum(times.values())
     n_owned = int(np.count_nonzero(p.ghost == 0))
     return {"value": n_owned / total, "unit": UNIT, "cores": threads, "kind": "port",
@@ -305,19 +341,26 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    p, cfg, meta = make_workload(args.config)
+    npd, _, species, _ = CONFIGS[args.config]
+    n_all = (2 if species == "both" else 1) * npd ** 3
     bounds, where = None, ""
-    if p.n > SUBBOX_ABOVE:
-        p, lo, hi = subbox_sample(p, cfg)
+    if n_all > SUBBOX_ABOVE:   # build only the sample cube and its shell
+        h = 1.3 * (1.0 / npd) if species == "both" else 0.0
+        a, side, reach = subbox_region(1.0, 5.0 / npd, n_all, h)   # r_cut = 5 d (make_workload)
+        p, cfg, meta = make_workload(args.config, region=(a - reach, a + side + reach))
+        p, lo, hi = subbox_sample(p, cfg, n_all=n_all)
         bounds = (lo, hi)
         where = (f"interior sub-box of {int(np.count_nonzero(p.ghost == 0))} owned + "
                  f"{int(np.count_nonzero(p.ghost))} overload-shell particles (bounded mesh); ")
+    else:
+        p, cfg, meta = make_workload(args.config)
     vals = []
     base = None
+    gonly = species == "dm"
     for _ in range(args.warmup):
-        cpu_baseline(p, cfg, frac=args.cpu_frac / 4, bounds=bounds)
+        cpu_baseline(p, cfg, frac=args.cpu_frac / 4, bounds=bounds, gravity_only=gonly)
     for _ in range(args.steps):
-        base = cpu_baseline(p, cfg, frac=args.cpu_frac, bounds=bounds)
+        base = cpu_baseline(p, cfg, frac=args.cpu_frac, bounds=bounds, gravity_only=gonly)
         vals.append(base["value"])
     v = float(np.median(vals))
     n_owned = meta["n_particles"]
@@ -337,21 +380,23 @@ def _make_rank(args, p, cfg, rank, world, meta, group=None, local=False):
     local: p already holds only this rank's rows."""
     from paper_2510_03557_b200.distributed import DistributedRank, rank_grid_for
     from paper_2510_03557_b200.domain import owner_ranks
-    from paper_2510_03557_b200.resident import ResidentRank
+    from paper_2510_03557_b200.resident import PASS_ALL, PASS_GRAVITY, ResidentRank
     if world == 1:
-        return ResidentRank(p, cfg)
+        return ResidentRank(p, cfg, gravity_only=meta["n_gas"] == 0)
     if not local:
         owner = owner_ranks(p.pos, cfg.box, rank_grid_for(world))
         p = p.select(np.nonzero(owner == rank)[0])
-    h = 1.3 * (1.0 / CONFIGS[meta["config"]][0])   # IC gas smoothing (ic.py), every rank
+    gas = meta["n_gas"] > 0
+    h = 1.3 * (1.0 / CONFIGS[meta["config"]][0]) if gas else 0.0   # IC gas smoothing (ic.py)
     return DistributedRank(p, cfg.box, rank, world, cfg.r_s, cfg.r_cut, cfg.softening, h, h,
-                           cfg.max_leaf_size, group=group, n_global=meta["n_particles"])
+                           cfg.max_leaf_size, group=group, n_global=meta["n_particles"],
+                           passes=PASS_ALL if gas else PASS_GRAVITY)
 
 
 def run_gpu_arm(args):
     import torch
     from paper_2510_03557_b200 import _native as N
-    from paper_2510_03557_b200.resident import PASS_ALL, STEP_FIELDS
+    from paper_2510_03557_b200.resident import PASS_ALL, PASS_GRAVITY, STEP_FIELDS
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -360,7 +405,9 @@ def run_gpu_arm(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rank_rows = world > 1 and CONFIGS[args.config][0] ** 3 * 2 > SUBBOX_ABOVE
+    npd_c, _, species_c, _ = CONFIGS[args.config]
+    passes = PASS_ALL if species_c == "both" else PASS_GRAVITY
+    rank_rows = world > 1 and npd_c ** 3 * (2 if species_c == "both" else 1) > SUBBOX_ABOVE
     p, cfg, meta = make_workload(args.config, rank, world, local=rank_rows)
     n_total = meta["n_particles"]
     rr = _make_rank(args, p, cfg, rank, world, meta, local=rank_rows)
@@ -370,7 +417,7 @@ def run_gpu_arm(args):
 
     def step(timing=False):
         if world == 1:
-            rr.step(PASS_ALL, timing=timing)
+            rr.step(passes, timing=timing)
             return rr.last
         rr.step(timing=timing)
         return rr.engine.last
@@ -417,10 +464,12 @@ def run_gpu_arm(args):
     pinned_in = {f: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
                  for f, a in src_fields.items()}
     eng = rr if world == 1 else rr.engine
-    out_names = ("grav", "hydro", "ncount", "crk_A", "crk_B", "perm")
+    out_names = (("grav", "hydro", "ncount", "crk_A", "crk_B", "perm") if passes == PASS_ALL
+                 else ("grav", "perm"))
     pinned_out = {k: torch.empty(eng.out[k].shape, dtype=eng.out[k].dtype).pin_memory()
                   for k in out_names}
-    pinned_out["density"] = torch.empty(eng.n, dtype=torch.float64).pin_memory()
+    if passes == PASS_ALL:
+        pinned_out["density"] = torch.empty(eng.n, dtype=torch.float64).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in pinned_in.values())
     d2h = sum(t.numel() * t.element_size() for t in pinned_out.values())
 
@@ -431,7 +480,7 @@ def run_gpu_arm(args):
     host_stepper = None
     if world == 1:
         from paper_2510_03557_b200.resident import HostStepper
-        host_stepper = HostStepper(rr, pinned_in, pinned_out)
+        host_stepper = HostStepper(rr, pinned_in, pinned_out, passes)
     else:
         # rank set: the exchange reads every input field, so the H2D copies
         # precede it; the SPH outputs, density and permutation drain while
@@ -460,7 +509,8 @@ def run_gpu_arm(args):
             for k in out_names:
                 if k not in late and e.out[k].shape == pinned_out[k].shape:
                     pinned_out[k].copy_(e.out[k], non_blocking=True)
-            if e.fields()["density"].shape == pinned_out["density"].shape:
+            if "density" in pinned_out and \
+                    e.fields()["density"].shape == pinned_out["density"].shape:
                 pinned_out["density"].copy_(e.fields()["density"], non_blocking=True)
             s_out.wait_event(ev_done)
             for k in late:
@@ -499,12 +549,16 @@ def run_gpu_arm(args):
     if n_total > 40_000_000:
         # exact counting pass too large to run untimed next to the rank data:
         # per-particle in-support counts measured at c2 (same sigma/d statistics)
+        # (gravity: neighbours within r_cut = 5 d at 2 particles per d^3; a
+        # single-species set has half the number density)
         per = {"gravity": 1047.0503, "sph": 81.0037}
         n_gas = meta["n_gas"]
         sph = int(per["sph"] * n_gas)
-        counts = {"gravity": int(per["gravity"] * n_total), "density": sph, "ncount": sph,
-                  "crk": sph, "hydro": sph - n_gas,
-                  "estimated": "per-particle counts measured exactly at c2 (2x128^3)"}
+        g_per = per["gravity"] * (1.0 if species_c == "both" else 0.5)
+        counts = {"gravity": int(g_per * n_total), "density": sph, "ncount": sph,
+                  "crk": sph, "hydro": max(sph - n_gas, 0),
+                  "estimated": "per-particle counts measured exactly at c2 (2x128^3), "
+                               "halved for gravity in single-species sets"}
     else:
         counts = pair_counts(p, cfg)
     peak, peak_src = peaks()
@@ -526,14 +580,15 @@ def run_gpu_arm(args):
     roof["kflop_per_update"] = step_flops / n_total / 1e3
     base = None
     if world == 1 and not args.no_cpu_baseline:
-        base = cpu_baseline(p, cfg, frac=args.cpu_frac)
+        base = cpu_baseline(p, cfg, frac=args.cpu_frac, gravity_only=passes != PASS_ALL)
     meta = dict(meta)
     if world > 1:
         meta["parallelism"] = f"spatial cuboids {rr.grid}, overload width {rr.w:.4g}, NCCL all-to-all shell exchange per step"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (Zel'dovich-displaced two-species lattice)",
+            "data": ("synthetic (Zel'dovich-displaced two-species lattice)" if passes == PASS_ALL
+                     else "synthetic (Zel'dovich-displaced dark-matter lattice)"),
             "config": meta, "phases_ms": ph,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e},

@@ -32,7 +32,7 @@ from . import _native as N
 from .box import BoxGeometry
 from .errors import DriftError, HydroboxError
 from .particles import ParticleSet
-from .resident import STEP_FIELDS, ResidentRank, StepConfig
+from .resident import PASS_ALL, PASS_GRAVITY, STEP_FIELDS, ResidentRank, StepConfig
 
 RANK_GRIDS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
 
@@ -273,8 +273,9 @@ class DistributedRank:
                  r_cut: float, softening: float, h_max: float, h_min: float,
                  max_leaf_size: int = 256, cm_bin_width: float = 0.0, group=None,
                  transport=None, eos_gamma: float = 5.0 / 3.0, periodic_unsplit: bool = True,
-                 n_global: int | None = None):
+                 n_global: int | None = None, passes: int = PASS_ALL):
         import torch
+        self.passes = int(passes)
         self.box, self.rank, self.world = box, rank, world
         self.grid = rank_grid_for(world)
         self.w = overload_width(r_cut, h_max)
@@ -309,7 +310,8 @@ class DistributedRank:
         self.n_owned = n_owned
         if self.engine is None:
             self.engine = ResidentRank(None, self.cfg, fields=new, ghost_density=self.world > 1,
-                                       h_range=self.h_range, owned_targets=self.world > 1)
+                                       h_range=self.h_range, owned_targets=self.world > 1,
+                                       gravity_only=self.passes == PASS_GRAVITY)
         else:
             self.engine.set_fields(new, self.h_range)
         return new
@@ -326,7 +328,7 @@ class DistributedRank:
         self.exchange()
         if timing:
             e1.record()
-        out = self.engine.step(timing=timing, sph_done=sph_done, status=status)
+        out = self.engine.step(self.passes, timing=timing, sph_done=sph_done, status=status)
         if timing:
             torch.cuda.synchronize()
             self.engine.last["ms_phase"]["exchange"] = e0.elapsed_time(e1)

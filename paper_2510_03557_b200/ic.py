@@ -144,6 +144,77 @@ def _zeldovich_subset(n_per_dim, box, psi, velocity_factor, gas_internal_energy,
     return p
 
 
+def make_zeldovich_ic_device(n_per_dim: int, box: BoxGeometry, sigma_psi_cells: float,
+                             select, seed: int = ZELDOVICH_SEED, velocity_factor: float = 0.1,
+                             gas_internal_energy: float = 1e-4,
+                             species: str = "both") -> ParticleSet:
+    """make_zeldovich_ic(select=...) with the displacement field built on the
+    GPU (cuFFT), for sizes whose numpy field does not fit the host per rank
+    (1024^3: ~60 GB).  The white noise is numpy's (same seed, same values); the
+    FFTs are cuFFT's, so positions agree with the numpy set to rounding, not
+    bitwise.  select: callable(pos torch (m,3) float64 CUDA) -> bool mask."""
+    import torch
+    n = n_per_dim
+    L = box.side_length
+    d = L / n
+    dev = torch.device("cuda")
+    white = torch.from_numpy(np.random.default_rng(seed).standard_normal((n, n, n))).to(dev)
+    dk = torch.fft.rfftn(white)
+    del white
+    k1 = 2 * np.pi * torch.fft.fftfreq(n, d=d, dtype=torch.float64, device=dev)
+    kz = 2 * np.pi * torch.fft.rfftfreq(n, d=d, dtype=torch.float64, device=dev)
+    k2 = k1[:, None, None] ** 2 + k1[None, :, None] ** 2 + kz[None, None, :] ** 2
+    k2[0, 0, 0] = 1.0
+    amp = torch.sqrt(torch.exp(-k2 * d * d) / k2)
+    amp[0, 0, 0] = 0.0
+    dk *= amp
+    del amp
+    psi = torch.empty((3, n, n, n), dtype=torch.float64, device=dev)
+    for comp, K in enumerate((k1[:, None, None], k1[None, :, None], kz[None, None, :])):
+        psi[comp] = torch.fft.irfftn(1j * K / k2 * dk, s=(n, n, n))
+    del dk, k2
+    rms = torch.sqrt(torch.mean(torch.sum(psi ** 2, dim=0)))
+    if float(rms) > 0:
+        psi *= sigma_psi_cells * d / rms
+    psi = psi.reshape(3, -1)
+    lattices = ([(Species.DARK_MATTER, 0.5, 0)] if species == "dm"
+                else [(Species.DARK_MATTER, 0.25, 0), (Species.GAS, 0.75, n ** 3)])
+    n_all = n ** 3 * len(lattices)
+    ax = torch.arange(n, dtype=torch.float64, device=dev)
+    parts = []
+    for sp, origin, id0 in lattices:
+        axis = origin * d + d * ax
+        pos = torch.stack([axis[:, None, None].expand(n, n, n).reshape(-1),
+                           axis[None, :, None].expand(n, n, n).reshape(-1),
+                           axis[None, None, :].expand(n, n, n).reshape(-1)], dim=1)
+        pos += psi.T
+        if not bool(torch.isfinite(pos).all()):
+            raise ConfigError("non-finite position component")
+        pos = pos - L * torch.floor(pos / L)      # wrap_position (box.py)
+        pos[pos >= L] -= L
+        pos[pos < 0.0] = 0.0
+        idx = torch.nonzero(select(pos)).squeeze(1)
+        parts.append((sp, idx.cpu().numpy(), pos[idx].cpu().numpy(),
+                      (velocity_factor * psi[:, idx]).T.cpu().numpy(), id0))
+        del pos
+    del psi
+    torch.cuda.empty_cache()
+    p = ParticleSet(sum(len(x[1]) for x in parts))
+    o = 0
+    for sp, idx, pos, vel, id0 in parts:
+        sl = slice(o, o + len(idx))
+        p.pos[sl] = pos
+        p.vel[sl] = vel
+        p.mass[sl] = box.volume / n_all
+        p.species[sl] = sp
+        if sp == Species.GAS:
+            p.smoothing[sl] = 1.3 * d
+            p.internal_energy[sl] = gas_internal_energy
+        p.global_id[sl] = idx + id0
+        o += len(idx)
+    return p
+
+
 def make_clustered_ic(n_per_dim: int, box: BoxGeometry, seed: int = 0, n_clumps: int = 8,
                       clumped_fraction: float = 0.7,
                       gas_internal_energy: float = 1e-4) -> ParticleSet:

@@ -101,7 +101,7 @@ class ResidentRank:
 
     def __init__(self, particles: ParticleSet | None, cfg: StepConfig, fields: dict | None = None,
                  ghost_density: bool = False, h_range: tuple | None = None,
-                 owned_targets: bool = False):
+                 owned_targets: bool = False, gravity_only: bool = False):
         """Either host ``particles`` or device ``fields`` (dict of STEP_FIELDS
         tensors).  ``h_range`` = (h_min_gas, h_max) when given as fields.
         ``owned_targets``: gravity / CRK / hydro outputs are needed for owned
@@ -124,6 +124,9 @@ class ResidentRank:
         # capacity slack for row counts that change between steps (distributed
         # engine); a host-loaded rank keeps its n, so exact capacity
         self._slack = 1.0 if particles is not None else 1.1
+        # gravity-only ranks (PASS_GRAVITY, e.g. the dark-matter configs) keep
+        # no SPH output buffers
+        self.gravity_only = gravity_only
         if particles is not None:
             gas = particles.species == 1
             h_range = ((float(particles.smoothing[gas].min()), float(particles.smoothing.max()))
@@ -144,15 +147,19 @@ class ResidentRank:
             f64 = torch.float64
             self._buf1_store = {k: torch.empty((cap,) + tuple(v.shape[1:]), dtype=v.dtype,
                                                device="cuda") for k, v in fields.items()}
+            sph = not self.gravity_only
             self._out_store = {
                 "perm": torch.empty(cap, dtype=torch.int64, device="cuda"),
-                "ncount": torch.zeros(cap, dtype=f64, device="cuda"),
                 "grav": torch.zeros((cap, 3), dtype=f64, device="cuda"),
-                "hydro": torch.zeros((cap, 5), dtype=f64, device="cuda"),
-                "crk_A": torch.zeros(cap, dtype=f64, device="cuda"),
-                "crk_B": torch.zeros((cap, 3), dtype=f64, device="cuda"),
-                "crk_fallback": torch.zeros(cap, dtype=torch.uint8, device="cuda"),
             }
+            if sph:
+                self._out_store.update({
+                    "ncount": torch.zeros(cap, dtype=f64, device="cuda"),
+                    "hydro": torch.zeros((cap, 5), dtype=f64, device="cuda"),
+                    "crk_A": torch.zeros(cap, dtype=f64, device="cuda"),
+                    "crk_B": torch.zeros((cap, 3), dtype=f64, device="cuda"),
+                    "crk_fallback": torch.zeros(cap, dtype=torch.uint8, device="cuda"),
+                })
             self._cap = cap
         self.buf[0] = fields
         self.buf[1] = {k: v[:n] for k, v in self._buf1_store.items()}
@@ -221,8 +228,10 @@ class ResidentRank:
         a.sph_done_event = _event_handle(sph_done)
         a.late_fields_event = _event_handle(late_fields)
         a.status_out = P(status.data_ptr()) if status is not None and not timing else P(0)
+        if self.gravity_only and passes & ~PASS_GRAVITY:
+            raise HydroboxError("gravity-only rank: SPH passes requested")
         for k in ("perm", "ncount", "grav", "hydro", "crk_A", "crk_B", "crk_fallback"):
-            setattr(a, k, N.ptr(self.out[k]))
+            setattr(a, k, N.ptr(self.out[k]) if k in self.out else P(0))
         a.crk_moments = P(0)   # moments live in the workspace (include/hb.h)
         for d in range(3):
             if a.reach > self.width[d] and self.nb[d] > 3:
@@ -240,11 +249,13 @@ class ResidentRank:
             N.check(st, err, "force_step")
             break
         self.cur = 1 - self.cur
-        off = int(a.crk_moments_out or 0) - ws.data_ptr()
-        if not 0 <= off <= ws.numel() - self.n * 80:
-            raise HydroboxError("force_step placed the CRK moments outside its workspace")
-        torch = N.torch_cuda()
-        self.out["crk_moments"] = ws[off:off + self.n * 80].view(torch.float64).view(self.n, 10)
+        if not self.gravity_only:
+            off = int(a.crk_moments_out or 0) - ws.data_ptr()
+            if not 0 <= off <= ws.numel() - self.n * 80:
+                raise HydroboxError("force_step placed the CRK moments outside its workspace")
+            torch = N.torch_cuda()
+            self.out["crk_moments"] = ws[off:off + self.n * 80].view(torch.float64).view(
+                self.n, 10)
         self.last = {"n_leaves": int(a.n_leaves), "n_entries": int(a.n_entries),
                      "ms_phase": ({**dict(zip(PHASES, list(a.ms_phase))),
                                    **dict(zip(KERNELS, list(a.ms_kernel)[:3]))}
@@ -280,8 +291,10 @@ class HostStepper:
     EARLY = ("mass", "smoothing", "species")                     # + SPH pass A
     LATE = ("vel", "internal_energy", "density", "global_id", "ghost_src")  # EOS on
 
-    def __init__(self, rank: "ResidentRank", pinned_in: dict, pinned_out: dict):
+    def __init__(self, rank: "ResidentRank", pinned_in: dict, pinned_out: dict,
+                 passes: int = PASS_ALL):
         torch = N.torch_cuda()
+        self.passes = int(passes)
         assert sorted(self.FIRST + self.EARLY + self.LATE) == sorted(STEP_FIELDS)
         self.rank, self.pin_in, self.pin_out = rank, pinned_in, pinned_out
         self.s_in = torch.cuda.Stream()
@@ -313,14 +326,16 @@ class HostStepper:
             self.ev_late.record(self.s_in)
         main.wait_event(self.ev_first)
         self.status.zero_()   # no copy into it is pending: every call ends synchronised
-        out = rk.step(PASS_ALL, fields_ready=self.ev_fields, sph_done=self.ev_sph,
+        out = rk.step(self.passes, fields_ready=self.ev_fields, sph_done=self.ev_sph,
                       status=self.status, late_fields=self.ev_late)
         self.ev_done.record(main)
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_event(self.ev_sph)
             for k in SPH_OUTPUTS + ("perm",):
-                self.pin_out[k].copy_(out[k], non_blocking=True)
-            self.pin_out["density"].copy_(rk.fields()["density"], non_blocking=True)
+                if k in self.pin_out:
+                    self.pin_out[k].copy_(out[k], non_blocking=True)
+            if "density" in self.pin_out:
+                self.pin_out["density"].copy_(rk.fields()["density"], non_blocking=True)
             self.s_out.wait_event(self.ev_done)
             self.pin_out["grav"].copy_(out["grav"], non_blocking=True)
         main.wait_stream(self.s_out)
