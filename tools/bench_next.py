@@ -11,6 +11,8 @@
   ckpt      HCKP encode of the c2 rank state from device fields; device CRC32C
             bandwidth over 512 MiB
   adapt     adapt_smoothing_length to 64 neighbours from h = 1.3 d at c1 and c2
+  c5rank    (--only c5rank) configs[4]'s per-rank gravity sweep of the 8-GPU
+            decomposition on one GPU
 
     python tools/bench_next.py [--npd 128] [--sub-npd 64] [--reps 5]
 Prints one JSON line per measurement."""
@@ -217,6 +219,53 @@ def bench_adapt(npd, reps):
                     "reference does (bit-identical); reference CPU: 47-48 s at c1, 8 threads"}
 
 
+def bench_c5_rank(reps):
+    """configs[4] (gravity-only 1024^3 DM) per-rank work of its 8-GPU
+    decomposition, on one GPU: an interior cube of 1/8 of the volume (134 M
+    owned particles, the size of one rank of 2x2x2) plus its r_cut shell as
+    ghosts on a bounded mesh, PASS_GRAVITY, ghost-only tiles skipped.  The full
+    c5 run needs >= 8 GPUs (about 193 GB per rank at 4)."""
+    import numpy as np
+    import torch
+    from bench import (CONFIGS, OPCOST, make_workload, peaks, subbox_region, subbox_sample)
+    from paper_2510_03557_b200.resident import PASS_GRAVITY, ResidentRank, StepConfig
+    npd = CONFIGS["c5"][0]
+    n_all = npd ** 3
+    a, side, reach = subbox_region(1.0, 5.0 / npd, n_all, 0.0, n_target=n_all // 8)
+    t0 = time.perf_counter()
+    p, cfg, meta = make_workload("c5", region=(a - reach, a + side + reach))
+    q, lo, hi = subbox_sample(p, cfg, n_target=n_all // 8, n_all=n_all)
+    del p
+    t_ic = time.perf_counter() - t0
+    n_own = int(np.count_nonzero(q.ghost == 0))
+    rcfg = StepConfig(box=cfg.box, bin_width=cfg.bin_width, max_leaf_size=256, r_s=cfg.r_s,
+                      r_cut=cfg.r_cut, softening=cfg.softening, bounds_lo=lo, bounds_hi=hi)
+    rk = ResidentRank(q, rcfg, gravity_only=True, owned_targets=True)
+    for _ in range(2):
+        rk.step(PASS_GRAVITY)
+    torch.cuda.synchronize()
+    ms, kg = [], []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rk.step(PASS_GRAVITY, timing=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        kg.append(rk.last["ms_phase"]["k_gravity"])
+    t = float(np.median(ms))
+    t_k = float(np.median(kg))
+    pairs = 1047.0503 / 2 * n_own          # per-particle in-support count (bench.py)
+    peak, _ = peaks()
+    return {"measurement": "c5_rank_gravity_sweep", "n_owned": n_own, "n_rows": int(q.n),
+            "ms_per_step": t, "updates_per_s_per_gpu": n_own / (t * 1e-3),
+            "k_gravity_ms": t_k,
+            "k_gravity_fp32_frac": pairs * OPCOST["gravity"] / (t_k * 1e-3) / 1e12 / peak,
+            "ic_s": t_ic,
+            "note": "one rank's domain of the 2x2x2 decomposition (interior cube, no exchange); "
+                    "8 such ranks = the full 1.07 G step minus the shell exchange"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--npd", type=int, default=128)
@@ -226,6 +275,9 @@ def main():
     args = ap.parse_args()
     if args.only == "adapt":
         print(json.dumps(bench_adapt(args.npd, max(1, args.reps // 2))))
+        return
+    if args.only == "c5rank":
+        print(json.dumps(bench_c5_rank(args.reps)))
         return
     print(json.dumps(bench_pm(args.npd, args.reps)))
     print(json.dumps(bench_subcycle(args.sub_npd, max(1, args.reps // 2))))
