@@ -473,9 +473,11 @@ def run_gpu_arm(args):
     h2d = sum(t.numel() * t.element_size() for t in pinned_in.values())
     d2h = sum(t.numel() * t.element_size() for t in pinned_out.values())
 
+    # N > 1: the owned rows land in the engine's reorder buffer, free between
+    # steps (the exchange reads them into the rank set before the step
+    # overwrites it) -- no second copy of the rank's fields on the device
     e2e_dev = None if world == 1 else {
-        f: torch.empty(pinned_in[f].shape, dtype=pinned_in[f].dtype, device="cuda")
-        for f in STEP_FIELDS}
+        f: rr.engine._buf1_store[f][:pinned_in[f].shape[0]] for f in STEP_FIELDS}
 
     host_stepper = None
     if world == 1:

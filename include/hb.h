@@ -287,6 +287,10 @@ typedef struct HbStepArgs {
 
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,
                                int64_t list_capacity);
+/* The same for steps restricted to `passes` (e.g. HB_PASS_GRAVITY: no room
+ * for workspace-resident CRK moments). */
+size_t hb_force_step_workspace_passes(int64_t n, const int64_t nb[3], int64_t max_leaf_size,
+                                      int64_t list_capacity, int32_t passes);
 int hb_force_step(HbStepArgs* args, void* ws, size_t ws_bytes, void* stream, HbError* err);
 /* Decode a deferred status (HbStepArgs.status_out) after the step's stream has
  * completed: the status the synchronous call would have returned. */

@@ -148,7 +148,7 @@ def lib():
 EXPORTS = ("hb_abi_version", "hb_launch_count", "hb_device_query", "hb_build_mesh_workspace", "hb_leaf_capacity",
            "hb_build_mesh", "hb_permute_rows", "hb_remap_through_inverse", "hb_grow_aabbs",
            "hb_assemble_lists_workspace", "hb_assemble_lists", "hb_eval_pairs_workspace",
-           "hb_eval_pairs", "hb_crk_solve", "hb_force_step_workspace", "hb_force_step", "hb_force_step_check",
+           "hb_eval_pairs", "hb_crk_solve", "hb_force_step_workspace", "hb_force_step", "hb_force_step_check", "hb_force_step_workspace_passes",
            "hb_halo_record_bytes", "hb_halo_select", "hb_halo_pack", "hb_halo_unpack_workspace",
            "hb_halo_unpack", "hb_halo_resolve_sources", "hb_halo_pack_all_workspace",
            "hb_halo_pack_all", "hb_halo_unpack_keep_workspace", "hb_halo_unpack_keep",

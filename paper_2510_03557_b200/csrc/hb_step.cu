@@ -218,7 +218,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   // per row the caller's buffer would cost (2x512^3 then fits one GPU).
   size_t mom_end = 0;
   double* mom = a->crk_moments;
-  {
+  a->crk_moments_out = nullptr;
+  if (a->passes & (HB_PASS_CRK | HB_PASS_HYDRO)) {  // gravity-only steps keep no moments
     Arena g = ws;
     g.dry = true;
     GravBinArgs gd = {};
@@ -555,9 +556,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
 
 using namespace hb;
 
-extern "C" size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,
-                                          int64_t list_capacity) {
+extern "C" size_t hb_force_step_workspace_passes(int64_t n, const int64_t nb[3],
+                                                 int64_t max_leaf_size, int64_t list_capacity,
+                                                 int32_t passes) {
   HbStepArgs a = {};
+  a.passes = passes;
   a.n = n;
   for (int d = 0; d < 3; ++d) a.nb[d] = nb[d];
   a.max_leaf_size = max_leaf_size;
@@ -566,6 +569,11 @@ extern "C" size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_
   ws.dry = true;
   force_step(&a, ws, nullptr, nullptr);
   return ws.used + 4096;
+}
+
+extern "C" size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,
+                                          int64_t list_capacity) {
+  return hb_force_step_workspace_passes(n, nb, max_leaf_size, list_capacity, HB_PASS_ALL);
 }
 
 extern "C" int hb_force_step_check(const void* status, HbError* err) {

@@ -121,13 +121,21 @@ class HaloExchange:
             self._bufs[name] = b
         return b[:n]
 
-    def _field_set(self, n):
-        """One of two alternating capacity-backed rank field sets."""
-        k = self._which
-        self._which ^= 1
+    def _field_set(self, n, avoid=None):
+        """A capacity-backed rank field set that does not share storage with
+        `avoid` (the set being read).  In the step loop the source is the
+        engine's own reorder buffer, so one set serves every exchange; the
+        second is allocated only if the source is the first (an exchange
+        without a step in between)."""
+        def alias(cur):
+            return (avoid is not None and cur is not None and
+                    cur["pos"].untyped_storage().data_ptr() ==
+                    avoid["pos"].untyped_storage().data_ptr())
+        k = 1 if alias(self._sets[0]) else 0
         cur = self._sets[k]
         if cur is None or cur["pos"].shape[0] < n:
-            cur = empty_fields(int(n * 1.2) + 1024)
+            self._sets[k] = None   # release before allocating the larger set
+            cur = empty_fields(int(n * 1.1) + 1024)
             self._sets[k] = cur
         return cur
 
@@ -161,7 +169,10 @@ class HaloExchange:
         ws = self._buf("pack_ws", int(self.lib.hb_halo_pack_all_workspace(self.world)), torch.uint8)
         fs = N.fieldset(fields)
         pu = 1 if self.periodic_unsplit else 0
-        cap = getattr(self, "_rec_cap", max(1024, n // 2))
+        # first call: shell records ~ 6 w / extent of the rows (+ migrants);
+        # 8 w / extent, capped at n / 2, avoids a 2x512^3-scale n / 2 buffer
+        ext = self.box.side_length / max(self.grid)
+        cap = getattr(self, "_rec_cap", max(1024, int(n * min(0.5, 8.0 * self.w / ext))))
         while True:
             rows, cap_r = self._full("rows", cap, torch.int64)
             slots, cap_s = self._full("slots", cap, torch.int32)
@@ -208,7 +219,7 @@ class HaloExchange:
         import torch
         m = int(recv.numel()) // self.rec
         n0 = int(keep[2]) if keep is not None else 0
-        out = self._field_set(max(n0 + m, 1))
+        out = self._field_set(max(n0 + m, 1), avoid=keep[0] if keep is not None else None)
         err = N.HbError()
         st = N.stream_ptr()
         if keep is not None:  # staying owned rows (current order), then arrivals: one C call
@@ -308,6 +319,7 @@ class DistributedRank:
     def exchange(self):
         new, n_owned = self.halo.exchange(self.owned_fields)
         self.n_owned = n_owned
+        self.owned_fields = new   # the rank set holds the owned rows: release the source
         if self.engine is None:
             self.engine = ResidentRank(None, self.cfg, fields=new, ghost_density=self.world > 1,
                                        h_range=self.h_range, owned_targets=self.world > 1,

@@ -64,6 +64,9 @@ def _bind(lib):
     lib.hb_force_step_workspace.argtypes = [C.c_int64, C.c_void_p, C.c_int64, C.c_int64]
     lib.hb_force_step.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
     lib.hb_force_step_check.argtypes = [C.c_void_p, C.c_void_p]
+    lib.hb_force_step_workspace_passes.restype = C.c_size_t
+    lib.hb_force_step_workspace_passes.argtypes = [C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                                                   C.c_int32]
     lib._step_bound = True
 
 
@@ -180,8 +183,9 @@ class ResidentRank:
         key = (self._cap, self.list_capacity)
         if self._ws is None or self._ws_key != key:
             nb3 = (C.c_int64 * 3)(*[int(v) for v in self.nb])
-            sz = self.lib.hb_force_step_workspace(self._cap, nb3, self.cfg.max_leaf_size,
-                                                  self.list_capacity)
+            sz = self.lib.hb_force_step_workspace_passes(
+                self._cap, nb3, self.cfg.max_leaf_size, self.list_capacity,
+                PASS_GRAVITY if self.gravity_only else PASS_ALL)
             if self._ws is None or self._ws.numel() < sz:
                 self._ws = None
                 self._ws = N.workspace(sz)
@@ -249,7 +253,7 @@ class ResidentRank:
             N.check(st, err, "force_step")
             break
         self.cur = 1 - self.cur
-        if not self.gravity_only:
+        if passes & (PASS_CRK | PASS_HYDRO):
             off = int(a.crk_moments_out or 0) - ws.data_ptr()
             if not 0 <= off <= ws.numel() - self.n * 80:
                 raise HydroboxError("force_step placed the CRK moments outside its workspace")
