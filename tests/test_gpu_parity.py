@@ -352,3 +352,29 @@ def test_gpu_host_stepper_matches_sync_step(golden):
         np.testing.assert_allclose(got["density"], ref_density, rtol=1e-6)
         for f, v in rk.fields().items():   # the split (early / late) gather
             np.testing.assert_array_equal(v.cpu().numpy(), ref_fields[f], err_msg=f)
+
+
+def test_gpu_resident_nonfinite_raises_sync_and_deferred(golden):
+    """A non-finite partial stops the resident step with the reference's error
+    (KernelEvalError), both from the synchronous call and from HostStepper's
+    deferred status check."""
+    import torch
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.errors import HydroboxError
+    from paper_2510_03557_b200.resident import STEP_FIELDS, HostStepper, ResidentRank, StepConfig
+    g = golden("step")
+    cfg = StepConfig(box=BoxGeometry(1.0), bin_width=float(g["bin_width"]), max_leaf_size=256,
+                     r_s=float(g["r_s"]), r_cut=float(g["r_cut"]), softening=float(g["eps"]),
+                     bounds_lo=g["bounds_lo"], bounds_hi=g["bounds_hi"])
+    p = particle_set(g, "in_")
+    p.mass[np.nonzero(p.ghost == 0)[0][7]] = np.inf
+    with pytest.raises(HydroboxError):
+        ResidentRank(p.copy(), cfg).step()
+    rk = ResidentRank(p.copy(), cfg)
+    pin_in = {f: torch.from_numpy(np.ascontiguousarray(getattr(p, f))).pin_memory()
+              for f in STEP_FIELDS}
+    names = ("grav", "hydro", "ncount", "crk_A", "crk_B", "perm")
+    pin_out = {k: torch.empty(rk.out[k].shape, dtype=rk.out[k].dtype).pin_memory() for k in names}
+    pin_out["density"] = torch.empty(rk.n, dtype=torch.float64).pin_memory()
+    with pytest.raises(HydroboxError):
+        HostStepper(rk, pin_in, pin_out)()
