@@ -283,6 +283,13 @@ typedef struct HbStepArgs {
                            stream: gravity pair kernel, SPH pass A kernel, SPH
                            pass B kernel, 0 (reserved) -- roofline inputs     */
   double* crk_moments_out; /* out: where the (n,10) moments were written     */
+  void* grav_half_event;   /* optional cudaEvent_t: bin gravity runs in two
+                              launches split at bin nb/2 and records this
+                              event between them; rows [0, grav_split_row)
+                              of `grav` are final from then on (the rest at
+                              the end of the step), so their copy-out can
+                              overlap the second half                         */
+  int64_t grav_split_row;  /* out (host, set before the call returns)         */
 } HbStepArgs;
 
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,

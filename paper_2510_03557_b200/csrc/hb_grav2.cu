@@ -345,7 +345,20 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     e.skip_leaf = nullptr;
     e.skip_tiles = g.ghost ? 1 : 0;
     if (g.t0) HB_CUDA_TRY(cudaEventRecord(g.t0, st));
-    int rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err);
+    int rc2;
+    if (g.split_event) {  // tiles of bins < nbins/2, then the rest (tile_ptr is per bin)
+      const int64_t* mid = T.tile_ptr + nbins / 2;
+      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, mid, st, err);
+      if (rc2) return rc2;
+      if (g.between) {
+        rc2 = g.between(g.between_ctx);
+        if (rc2) return rc2;
+      }
+      HB_CUDA_TRY(cudaEventRecord(g.split_event, st));
+      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err, mid);
+    } else {
+      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err);
+    }
     if (g.t1) HB_CUDA_TRY(cudaEventRecord(g.t1, st));
     return rc2;
   }

@@ -64,6 +64,12 @@ struct GravBinArgs {
   int table_kind;  // GT_* for k_gravity (hb_pairs.cuh)
   const uint8_t* ghost = nullptr;  // owned_targets: skip tiles without an owned row
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // optional: recorded around the pair kernel
+  // optional: run the pair kernel in two launches split at bin nbins / 2 and
+  // record split_event between them (rows of bins < nbins / 2 are then final
+  // up to the caller's ghost-row zeroing, done by `between` when set)
+  cudaEvent_t split_event = nullptr;
+  int (*between)(void* ctx) = nullptr;
+  void* between_ctx = nullptr;
 };
 int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);
 // bins as segments: row range per bin and the 27-bin stencil as a receiver CSR

@@ -968,13 +968,14 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
 template <int KIND, int JB, int REP, int NB>
 __global__ void __launch_bounds__(kGravWarps * 32, 4)
-k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev) {
+k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
+          const int64_t* t_begin_dev) {
   extern __shared__ float4 s_tab[];  // gt.rows * REP
   __shared__ float4 s_src[kGravWarps][kGravStage];
   for (int k = threadIdx.x; k < gt.rows * REP; k += blockDim.x) s_tab[k] = table[k / REP];
   __syncthreads();
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t t = (int64_t)blockIdx.x * kGravWarps + wid;
+  int64_t t = (int64_t)blockIdx.x * kGravWarps + wid + (t_begin_dev ? *t_begin_dev : 0);
   if (t < *n_tiles_dev)
     grav_tile<KIND, JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
                                  t, lane);
@@ -994,8 +995,8 @@ static int gravity_batch() {
 
 template <int KIND, int JB, int NB>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
-                               unsigned grid, unsigned blk, const int64_t* ntd, cudaStream_t st,
-                               HbError* err) {
+                               unsigned grid, unsigned blk, const int64_t* ntd,
+                               const int64_t* t_begin, cudaStream_t st, HbError* err) {
   constexpr int REP = 8;
   size_t sm = (size_t)gt.rows * REP * sizeof(float4);
   // static staging + dynamic table may pass the 48 KB default: raise the
@@ -1012,26 +1013,27 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
       set_for[dev] = sm;
     }
   }
-  k_gravity<KIND, JB, REP, NB><<<grid, blk, sm, st>>>(d, table, gt, ntd);
+  k_gravity<KIND, JB, REP, NB><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
   return HB_OK;
 }
 
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
-                        const int64_t* ntd, cudaStream_t st, HbError* err) {
+                        const int64_t* ntd, cudaStream_t st, HbError* err,
+                        const int64_t* t_begin) {
   unsigned grid = grid_for(tcap, kGravWarps), blk = kGravWarps * 32;
   int nb = gravity_batch();
   int rc;
   if (gt.kind == GT_SOFT && gt.jbits == 5)
-    rc = launch_gravity_kind<GT_SOFT, 5, 8>(d, table, gt, grid, blk, ntd, st, err);
+    rc = launch_gravity_kind<GT_SOFT, 5, 8>(d, table, gt, grid, blk, ntd, t_begin, st, err);
   else if (gt.kind == GT_SOFT)
-    rc = nb == 1   ? launch_gravity_kind<GT_SOFT, 4, 1>(d, table, gt, grid, blk, ntd, st, err)
-         : nb == 2 ? launch_gravity_kind<GT_SOFT, 4, 2>(d, table, gt, grid, blk, ntd, st, err)
-         : nb == 8 ? launch_gravity_kind<GT_SOFT, 4, 8>(d, table, gt, grid, blk, ntd, st, err)
-                   : launch_gravity_kind<GT_SOFT, 4, 4>(d, table, gt, grid, blk, ntd, st, err);
+    rc = nb == 1   ? launch_gravity_kind<GT_SOFT, 4, 1>(d, table, gt, grid, blk, ntd, t_begin, st, err)
+         : nb == 2 ? launch_gravity_kind<GT_SOFT, 4, 2>(d, table, gt, grid, blk, ntd, t_begin, st, err)
+         : nb == 8 ? launch_gravity_kind<GT_SOFT, 4, 8>(d, table, gt, grid, blk, ntd, t_begin, st, err)
+                   : launch_gravity_kind<GT_SOFT, 4, 4>(d, table, gt, grid, blk, ntd, t_begin, st, err);
   else if (gt.kind == GT_T)
-    rc = launch_gravity_kind<GT_T, 0, 1>(d, table, gt, grid, blk, ntd, st, err);
+    rc = launch_gravity_kind<GT_T, 0, 1>(d, table, gt, grid, blk, ntd, t_begin, st, err);
   else
-    rc = launch_gravity_kind<GT_R, 0, 1>(d, table, gt, grid, blk, ntd, st, err);
+    rc = launch_gravity_kind<GT_R, 0, 1>(d, table, gt, grid, blk, ntd, t_begin, st, err);
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;

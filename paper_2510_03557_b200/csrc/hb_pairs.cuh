@@ -332,7 +332,9 @@ int gravity_kind(int gravity_mode, double eps, double r_s);
 // cached device copy (library-owned, per device); nullptr + err on failure
 const float4* gravity_table_device(double r_s, double r_cut, double eps, int kind, GravTab* gt,
                                    cudaStream_t st, HbError* err);
+// tiles [*t_begin (0 if null), *ntd)
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
-                        const int64_t* ntd, cudaStream_t st, HbError* err);
+                        const int64_t* ntd, cudaStream_t st, HbError* err,
+                        const int64_t* t_begin = nullptr);
 
 }  // namespace hb

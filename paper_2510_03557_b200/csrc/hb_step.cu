@@ -183,6 +183,30 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
 
 constexpr bool kGravityBinsDefault = true;
 
+// rows of bins < half: leaf_start of the first leaf at or after bin `half`
+__global__ void k_split_row(const int64_t* bin_ptr, const int64_t* leaf_start, int64_t half,
+                            int64_t n_leaves, int64_t n, int64_t* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  int64_t l = bin_ptr[half];
+  *out = l < n_leaves ? leaf_start[l] : n;
+}
+
+struct GhostZeroCtx {  // zeroes the gravity rows of ghost-only leaves (between halves)
+  int64_t nl;
+  const int64_t *leaf_start, *leaf_end;
+  const uint8_t* ghost_only;
+  double* grav;
+  cudaStream_t st;
+};
+static int zero_grav_ghost_rows(void* p) {
+  GhostZeroCtx* c = (GhostZeroCtx*)p;
+  HbError* err = nullptr;
+  k_zero_ghost_rows<<<grid_for(c->nl * 32, 256), 256, 0, c->st>>>(
+      c->nl, c->leaf_start, c->leaf_end, c->ghost_only, nullptr, nullptr, nullptr, c->grav);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
+
 struct PhaseTimer {
   bool on;
   cudaStream_t st;
@@ -272,6 +296,16 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     if (rc) return rc;
   }
   a->n_leaves = nl;
+  a->grav_split_row = n;
+  if (a->grav_half_event) {  // rows of bins < nbins/2, final after the first gravity half
+    // scratch: the 256-B arena slot of err_key has room after its 8 bytes
+    int64_t* split_dev = (int64_t*)(w.err_key + 1);
+    k_split_row<<<1, 32, 0, st>>>(w.bin_ptr, w.leaf_start, nbins / 2, nl, n, split_dev);
+    HB_LAUNCH_CHECK();
+    HB_CUDA_TRY(cudaMemcpyAsync(&a->grav_split_row, split_dev, sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, st));
+    HB_CUDA_TRY(cudaStreamSynchronize(st));
+  }
   if (a->fields_ready_event)
     HB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a->fields_ready_event, 0));
   bool late_split = a->late_fields_event != nullptr;
@@ -487,6 +521,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     gb.ghost = a->owned_targets ? a->ghost : nullptr;
     gb.t0 = tm.on ? tm.kv[0] : nullptr;
     gb.t1 = tm.on ? tm.kv[1] : nullptr;
+    GhostZeroCtx zc = {nl, w.leaf_start, w.leaf_end, w.ghost_only, a->grav, st};
+    if (a->grav_half_event) {
+      gb.split_event = (cudaEvent_t)a->grav_half_event;
+      if (zero_ghost) { gb.between = zero_grav_ghost_rows; gb.between_ctx = &zc; }
+    }
     Arena s = ws;
     rc = gravity_bins(gb, s, st, err);
     if (rc) return rc;
@@ -510,6 +549,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     }
   }
   tm.mark(6);
+  if (a->grav_half_event && !bin_gravity) {   // no split: every row is final at the end
+    a->grav_split_row = 0;
+  }
   if (zero_ghost && (a->passes & HB_PASS_GRAVITY)) {
     rc = zero_rows(nullptr, nullptr, nullptr, a->grav);
     if (rc) return rc;

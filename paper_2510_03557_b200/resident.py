@@ -54,7 +54,8 @@ class HbStepArgs(C.Structure):
                    ("crk_A", P), ("crk_B", P), ("crk_fallback", P), ("n_leaves", C.c_int64),
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
                    ("ms_phase", C.c_float * 8), ("status_out", P), ("ms_kernel", C.c_float * 4),
-                   ("crk_moments_out", P)])
+                   ("crk_moments_out", P), ("grav_half_event", P),
+                   ("grav_split_row", C.c_int64)])
 
 
 def _bind(lib):
@@ -197,7 +198,7 @@ class ResidentRank:
         return self.buf[self.cur]
 
     def step(self, passes: int = PASS_ALL, timing: bool = False, fields_ready=None,
-             sph_done=None, status=None, late_fields=None) -> dict:
+             sph_done=None, status=None, late_fields=None, grav_half=None) -> dict:
         """One force evaluation; returns the device outputs (leaf order).
         fields_ready / sph_done: optional torch.cuda.Event for copy overlap
         (see HbStepArgs in include/hb.h); late_fields: event after which vel,
@@ -231,6 +232,7 @@ class ResidentRank:
         a.fields_ready_event = _event_handle(fields_ready)
         a.sph_done_event = _event_handle(sph_done)
         a.late_fields_event = _event_handle(late_fields)
+        a.grav_half_event = _event_handle(grav_half)
         a.status_out = P(status.data_ptr()) if status is not None and not timing else P(0)
         if self.gravity_only and passes & ~PASS_GRAVITY:
             raise HydroboxError("gravity-only rank: SPH passes requested")
@@ -261,6 +263,7 @@ class ResidentRank:
             self.out["crk_moments"] = ws[off:off + self.n * 80].view(torch.float64).view(
                 self.n, 10)
         self.last = {"n_leaves": int(a.n_leaves), "n_entries": int(a.n_entries),
+                     "grav_split_row": int(a.grav_split_row),
                      "ms_phase": ({**dict(zip(PHASES, list(a.ms_phase))),
                                    **dict(zip(KERNELS, list(a.ms_kernel)[:3]))}
                                   if timing else None)}
@@ -308,8 +311,10 @@ class HostStepper:
         self.ev_sph = torch.cuda.Event()
         self.ev_done = torch.cuda.Event()
         self.ev_late = torch.cuda.Event()
+        self.ev_ghalf = torch.cuda.Event()
         self.status = torch.zeros(3, dtype=torch.int64, pin_memory=True)
-        for ev in (self.ev_first, self.ev_fields, self.ev_sph, self.ev_done, self.ev_late):
+        for ev in (self.ev_first, self.ev_fields, self.ev_sph, self.ev_done, self.ev_late,
+                   self.ev_ghalf):
             ev.record()   # materialise the CUDA events (torch creates them lazily)
 
     def __call__(self):
@@ -331,7 +336,8 @@ class HostStepper:
         main.wait_event(self.ev_first)
         self.status.zero_()   # no copy into it is pending: every call ends synchronised
         out = rk.step(self.passes, fields_ready=self.ev_fields, sph_done=self.ev_sph,
-                      status=self.status, late_fields=self.ev_late)
+                      status=self.status, late_fields=self.ev_late, grav_half=self.ev_ghalf)
+        split = rk.last["grav_split_row"]
         self.ev_done.record(main)
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_event(self.ev_sph)
@@ -340,8 +346,11 @@ class HostStepper:
                     self.pin_out[k].copy_(out[k], non_blocking=True)
             if "density" in self.pin_out:
                 self.pin_out["density"].copy_(rk.fields()["density"], non_blocking=True)
+            self.s_out.wait_event(self.ev_ghalf)   # first gravity half: rows [0, split)
+            if split > 0:
+                self.pin_out["grav"][:split].copy_(out["grav"][:split], non_blocking=True)
             self.s_out.wait_event(self.ev_done)
-            self.pin_out["grav"].copy_(out["grav"], non_blocking=True)
+            self.pin_out["grav"][split:].copy_(out["grav"][split:], non_blocking=True)
         main.wait_stream(self.s_out)
         main.synchronize()
         rk.check_status(self.status)
