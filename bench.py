@@ -488,9 +488,9 @@ def run_gpu_arm(args):
         # precede it; the SPH outputs, density and permutation drain while
         # gravity runs (sph_done), the gravity output after; deferred status
         s_out = torch.cuda.Stream()
-        ev_sph, ev_done = torch.cuda.Event(), torch.cuda.Event()
-        ev_sph.record()
-        ev_done.record()
+        ev_sph, ev_done, ev_gh = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
+        for ev in (ev_sph, ev_done, ev_gh):
+            ev.record()
         status = torch.zeros(3, dtype=torch.int64, pin_memory=True)
 
     def e2e_step():
@@ -501,10 +501,11 @@ def run_gpu_arm(args):
         for f in STEP_FIELDS:
             dst[f].copy_(pinned_in[f], non_blocking=True)
         status.zero_()
-        rr.step(sph_done=ev_sph, status=status)
+        rr.step(sph_done=ev_sph, status=status, grav_half=ev_gh)
         main = torch.cuda.current_stream()
         ev_done.record(main)
         e = rr.engine
+        split = e.last["grav_split_row"]
         late = ("grav",)
         with torch.cuda.stream(s_out):
             s_out.wait_event(ev_sph)
@@ -514,10 +515,14 @@ def run_gpu_arm(args):
             if "density" in pinned_out and \
                     e.fields()["density"].shape == pinned_out["density"].shape:
                 pinned_out["density"].copy_(e.fields()["density"], non_blocking=True)
+            s_out.wait_event(ev_gh)   # gravity rows [0, split) are final
+            for k in late:
+                if split > 0 and e.out[k].shape == pinned_out[k].shape:
+                    pinned_out[k][:split].copy_(e.out[k][:split], non_blocking=True)
             s_out.wait_event(ev_done)
             for k in late:
                 if e.out[k].shape == pinned_out[k].shape:
-                    pinned_out[k].copy_(e.out[k], non_blocking=True)
+                    pinned_out[k][split:].copy_(e.out[k][split:], non_blocking=True)
         main.wait_stream(s_out)
         main.synchronize()
         e.check_status(status)

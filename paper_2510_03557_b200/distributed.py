@@ -328,7 +328,7 @@ class DistributedRank:
             self.engine.set_fields(new, self.h_range)
         return new
 
-    def step(self, timing: bool = False, sph_done=None, status=None):
+    def step(self, timing: bool = False, sph_done=None, status=None, grav_half=None):
         """Exchange + force evaluation; returns device outputs (leaf order of
         the rank set) and the reordered fields.  sph_done / status: as
         ResidentRank.step (copy overlap; deferred status, checked with
@@ -340,7 +340,8 @@ class DistributedRank:
         self.exchange()
         if timing:
             e1.record()
-        out = self.engine.step(self.passes, timing=timing, sph_done=sph_done, status=status)
+        out = self.engine.step(self.passes, timing=timing, sph_done=sph_done, status=status,
+                               grav_half=grav_half)
         if timing:
             torch.cuda.synchronize()
             self.engine.last["ms_phase"]["exchange"] = e0.elapsed_time(e1)
