@@ -7,5 +7,5 @@ timeout 900 python bench.py --impl reference > gpurun_out/final_c2_ref.json 2> g
 timeout 900 python bench.py --config c3 --no-cpu-baseline > gpurun_out/final_c3.json 2> gpurun_out/final_c3.err; echo "c3 rc=$?"; S gpurun_out/final_c3.json
 timeout 1200 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/final_c4_n1.json 2> gpurun_out/final_c4_n1.err; echo "c4 rc=$?"; S gpurun_out/final_c4_n1.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-file gpurun_out/final_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/final_launches.log 2>&1; echo "launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_gravity|k_sph_density|k_sph_force|k_tile_build_warp|k_gather_state|k_crk_solve" -c 6 -f -o gpurun_out/final_kernels python tools/profile_step.py --steps 1 > gpurun_out/final_kernels.log 2>&1; echo "full rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_gravity|k_sph_density|k_sph_force|k_tile_build_warp|k_gather_state|k_crk_solve" -c 7 -f -o gpurun_out/final_kernels python tools/profile_step.py --steps 1 > gpurun_out/final_kernels.log 2>&1; echo "full rc=$?"
 timeout 1500 python tools/bench_next.py > gpurun_out/final_next.jsonl 2> gpurun_out/final_next.err; echo "next rc=$?"; cut -c1-200 gpurun_out/final_next.jsonl
