@@ -92,7 +92,10 @@ __global__ void k_leaf_counts(int64_t nbins, const unsigned long long* bin_cnt, 
 
 // ------------------------------------------------------------------ k-d split
 constexpr int kKdBlock = 256;
-constexpr int kKdSmemCap = 1792;  // members held in shared memory; larger bins use global scratch
+// members held in shared memory (larger bins use global scratch).  768 (18 KB)
+// lets 8 CTAs share an SM; 1792 (43 KB, 5 CTAs) was 15% slower at c2
+// (k_kd_split 247 -> 215 us), bins there hold ~270 members
+constexpr int kKdSmemCap = 768;
 
 // stable merge sort of (key, idx)[0,m): after return data is in (key, idx)
 __device__ void block_stable_sort(double* key, uint32_t* idx, double* tk, uint32_t* ti, int m) {
