@@ -25,7 +25,7 @@ namespace hb {
 
 constexpr int kTileBuildBlock = 256;
 constexpr int kTileBuildCap = 2048;  // selected members per leaf held in shared memory
-constexpr int kTileWarpCapBlock = 512;  // leaves up to this many go to the warp kernel
+constexpr int kTileWarpCapBlock = 384;  // leaves up to this many go to the warp kernel
 constexpr int kEvalWarps = 4;
 constexpr int kStage = 64;           // staged sources per warp
 
@@ -229,7 +229,11 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
 // Same tiling as k_tile_build, one WARP per leaf (leaves with <= 256 selected
 // members -- the common case -- without block barriers); larger leaves are
 // left to k_tile_build (flagged by big != 0).
-constexpr int kTileWarpCap = 512;
+// members per warp-built segment (larger segments: the block kernel).  384:
+// 71 registers / 30 KB per 4-warp block; 512 (96 registers, 40 KB) took
+// 645 us for the two c2 tilings, 384 takes 554 us, and 320 is equal at c2 but
+// sends more of c3's clustered bins to the slower block kernel
+constexpr int kTileWarpCap = 384;
 constexpr int kTileWarps = 4;
 __global__ void __launch_bounds__(kTileWarps * 32)
 k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
