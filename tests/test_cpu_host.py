@@ -205,3 +205,23 @@ def test_subbox_sample_is_a_rank_domain():
     np.testing.assert_array_equal(np.sort(q.global_id[own]), np.sort(p.global_id[inside]))
     assert np.all((q.pos >= lo) & (q.pos < hi)) and not np.any(q.image_shift)
     assert q.ghost[~own].min() == 1 and (~own).sum() > 0
+
+
+def test_reference_arm_line_contract(capsys):
+    """`bench.py --impl reference` at c1 on the host: one JSON line with the
+    contract's keys (impl, value/unit, cpu_baseline kind/cores/sample, e2e with
+    zero copy bytes)."""
+    import argparse
+    import json
+    import bench
+    args = argparse.Namespace(gpus=1, steps=1, warmup=0, config="c1", impl="reference",
+                              cpu_frac=1 / 32, no_cpu_baseline=False)
+    assert bench.run_reference_arm(args) == 0
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["unit"] == bench.UNIT and line["metric"] == bench.METRIC
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == line["value"]
+    assert line["e2e"] == {"value": line["value"], "unit": bench.UNIT, "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    assert line["config"]["config"] == "c1"
