@@ -44,10 +44,23 @@ __device__ void jacobi_eig3(double a[3][3], double ev[3]) {
   ev[0] = a[0][0]; ev[1] = a[1][1]; ev[2] = a[2][2];
 }
 
-__global__ void k_crk_solve(int64_t n, const double* mom, int64_t stride, const uint8_t* species,
-                            double cond_limit, double* A, double* B, uint8_t* fallback) {
+// rows != nullptr: solve only rows[0, *n_rows) (the gas rows, so warps carry
+// no non-gas lanes: they idled ~half of each warp in the all-rows launch);
+// every other row was set to the non-gas result by k_crk_fill
+__global__ void k_crk_fill(int64_t n, double* A, double* B, uint8_t* fallback) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  A[i] = 1.0;
+  B[3 * i] = 0.0; B[3 * i + 1] = 0.0; B[3 * i + 2] = 0.0;
+  fallback[i] = 0;
+}
+
+__global__ void k_crk_solve(int64_t n, const double* mom, int64_t stride, const uint8_t* species,
+                            double cond_limit, double* A, double* B, uint8_t* fallback,
+                            const int32_t* rows, const int64_t* n_rows) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (rows ? *n_rows : n)) return;
+  int64_t i = rows ? (int64_t)rows[k] : k;
   const double* v = mom + i * stride;
   double m0 = v[0];
   double m1[3] = {v[1], v[2], v[3]};
@@ -119,7 +132,22 @@ extern "C" int hb_crk_solve(int64_t n, const double* moments, int64_t stride,
   if (err) *err = HbError{};
   if (n <= 0) return HB_OK;
   k_crk_solve<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(n, moments, stride, species,
-                                                                   cond_limit, A, B, fallback);
+                                                                   cond_limit, A, B, fallback,
+                                                                   nullptr, nullptr);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
+
+namespace hb {
+int crk_solve_rows(int64_t n, const double* moments, int64_t stride, const uint8_t* species,
+                   double cond_limit, double* A, double* B, uint8_t* fallback,
+                   const int32_t* rows, const int64_t* n_rows, cudaStream_t st, HbError* err) {
+  if (n <= 0) return HB_OK;
+  k_crk_fill<<<grid_for(n, 256), 256, 0, st>>>(n, A, B, fallback);
+  HB_LAUNCH_CHECK();
+  k_crk_solve<<<grid_for(n, 128), 128, 0, st>>>(n, moments, stride, species, cond_limit, A, B,
+                                                fallback, rows, n_rows);
+  HB_LAUNCH_CHECK();
+  return HB_OK;
+}
+}  // namespace hb

@@ -72,6 +72,11 @@ struct GravBinArgs {
   void* between_ctx = nullptr;
 };
 int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);
+// hb_crk_solve over a row list (rows[0, *n_rows), device count); other rows get
+// the non-gas result (A = 1, B = 0, no fallback)
+int crk_solve_rows(int64_t n, const double* moments, int64_t stride, const uint8_t* species,
+                   double cond_limit, double* A, double* B, uint8_t* fallback,
+                   const int32_t* rows, const int64_t* n_rows, cudaStream_t st, HbError* err);
 // bins as segments: row range per bin and the 27-bin stencil as a receiver CSR
 int bin_stencil_csr(int64_t nbins, const int64_t* bin_ptr, const int64_t* leaf_start,
                     const int64_t* leaf_end, const ListGeom& g, int64_t* seg_s, int64_t* seg_e,

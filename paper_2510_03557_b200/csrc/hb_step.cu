@@ -489,8 +489,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       if (rc) return rc;
       zero_ghost_sph = false;
     }
-    rc = hb_crk_solve(n, mom, 10, a->species, 1e8, a->crk_A, a->crk_B,
-                      a->crk_fallback, st, err);
+    // the SPH tiling lists every gas row once: tperm[0, sel_off[n_seg])
+    rc = crk_solve_rows(n, mom, 10, a->species, 1e8, a->crk_A, a->crk_B, a->crk_fallback,
+                        w.Tg.tperm, w.Tg.sel_off + n_seg, st, err);
     if (rc) return rc;
   }
   if (zero_ghost_sph && !a->ghost_density && (a->passes & HB_PASS_NCOUNT)) {
