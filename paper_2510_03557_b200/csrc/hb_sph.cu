@@ -219,7 +219,10 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
     __syncwarp();
     cnt = 0;
   };
-  sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, h, a.reach * 1.0001f, stage, meta, cnt,
+  // cull radius from the tile's largest h (k_tile_boxes: tile_lo.w), not this
+  // lane's: every lane culls sources for the whole tile
+  sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
+                               cnt,
                                consume);
   if (live) {
     float norm3 = h > 0.0f ? kSigma * hinv * hinv * hinv : 0.0f;
@@ -306,7 +309,8 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
     __syncwarp();
     cnt = 0;
   };
-  sph_sweep<3, true, kStageB>(a, A, e0, e1, tlo, thi, hi, a.reach * 1.0001f, stage, meta, cnt,
+  sph_sweep<3, true, kStageB>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
+                              cnt,
                               consume);
   bool bad = !(isfinite(fx) && isfinite(fy) && isfinite(fz) && isfinite(ei) && isfinite(mo[0]));
   if (__ballot_sync(0xffffffffu, live && bad)) {

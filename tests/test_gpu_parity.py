@@ -260,11 +260,13 @@ def test_gpu_resident_force_step(golden, oracle):
     assert_fp32_close(out["hydro"][own, :4], ref_h[own], absh[own, :4], what="resident hydro")
 
 
-@pytest.mark.parametrize("sigma", [0.05, 1.0, 2.5])
-def test_gpu_force_step_vs_oracle_c1(oracle, sigma):
+@pytest.mark.parametrize("sigma,h_jitter", [(0.05, 0.0), (1.0, 0.0), (2.5, 0.0), (1.0, 0.35)])
+def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter):
     """hb_force_step at 2x32^3 (config C1, near-uniform and shell-crossing
     Zel'dovich ICs) against the oracle's ordered evaluation of the same step:
-    leaf order and neighbour counts bit-exact, the rest within FP32 tolerance."""
+    leaf order and neighbour counts bit-exact, the rest within FP32 tolerance.
+    h_jitter > 0: gas smoothing lengths scattered by +-h_jitter (adapted h
+    varies between neighbours; the tile culls must use the tile's largest h)."""
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
     from paper_2510_03557_b200.ic import make_zeldovich_ic
@@ -274,6 +276,10 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma):
     npd = 32
     box = BoxGeometry(1.0)
     p0 = make_zeldovich_ic(npd, box, sigma)
+    if h_jitter > 0:
+        g0 = p0.species == 1
+        rng = np.random.default_rng(17)
+        p0.smoothing[g0] *= rng.uniform(1 - h_jitter, 1 + h_jitter, int(g0.sum()))
     pm = 1.0 / (2 * npd)
     r_s, r_cut = 2 * pm, 10 * pm
     eps = (1.0 / p0.n ** (1 / 3)) / 50
