@@ -260,13 +260,19 @@ def test_gpu_resident_force_step(golden, oracle):
     assert_fp32_close(out["hydro"][own, :4], ref_h[own], absh[own, :4], what="resident hydro")
 
 
-@pytest.mark.parametrize("sigma,h_jitter", [(0.05, 0.0), (1.0, 0.0), (2.5, 0.0), (1.0, 0.35)])
-def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter):
+@pytest.mark.parametrize("sigma,h_jitter,mode", [(0.05, 0.0, 0), (1.0, 0.0, 0), (2.5, 0.0, 0),
+                                                 (1.0, 0.35, 0), (1.0, 0.35, 1), (1.0, 0.35, 2),
+                                                 (1.0, 0.35, 3)])
+def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, monkeypatch):
     """hb_force_step at 2x32^3 (config C1, near-uniform and shell-crossing
     Zel'dovich ICs) against the oracle's ordered evaluation of the same step:
     leaf order and neighbour counts bit-exact, the rest within FP32 tolerance.
     h_jitter > 0: gas smoothing lengths scattered by +-h_jitter (adapted h
-    varies between neighbours; the tile culls must use the tile's largest h)."""
+    varies between neighbours; the tile culls must use the tile's largest h).
+    mode: HbStepArgs.gravity_mode -- 0 the default (bin tiles, soft table); 1
+    leaf tiles for gravity and SPH (the fallback when a bin outgrows the tiler);
+    2 half-warp bin gravity; 3 bin gravity with the r/t table."""
+    monkeypatch.setenv("HB_GRAVITY_MODE", str(mode))
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
     from paper_2510_03557_b200.ic import make_zeldovich_ic
