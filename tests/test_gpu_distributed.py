@@ -10,26 +10,31 @@ from tests.tolerances import assert_fp32_close
 pytestmark = pytest.mark.gpu
 
 
-def _setup(npd=32, sigma=0.3):
+def _setup(npd=32, sigma=0.3, h_jitter=0.0):
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.ic import make_zeldovich_ic
     box = BoxGeometry(1.0)
     p = make_zeldovich_ic(npd, box, sigma)
+    if h_jitter > 0:   # non-uniform smoothing lengths (as after h adaptation)
+        gas = p.species == 1
+        p.smoothing[gas] *= np.random.default_rng(23).uniform(1 - h_jitter, 1 + h_jitter,
+                                                              int(gas.sum()))
     pm = 1.0 / (2 * npd)
     r_s, r_cut = 2 * pm, 10 * pm
     eps = (1.0 / p.n ** (1 / 3)) / 50
     return box, p, r_s, r_cut, eps
 
 
-@pytest.mark.parametrize("world,periodic_unsplit", [(1, False), (2, False), (4, False),
-                                                    (8, False), (2, True), (4, True)])
-def test_emulated_ranks_match_single_domain(world, periodic_unsplit, oracle):
+@pytest.mark.parametrize("world,periodic_unsplit,h_jitter",
+                         [(1, False, 0.0), (2, False, 0.0), (4, False, 0.0), (8, False, 0.0),
+                          (2, True, 0.0), (4, True, 0.0), (4, False, 0.3)])
+def test_emulated_ranks_match_single_domain(world, periodic_unsplit, h_jitter, oracle):
     import torch
     from paper_2510_03557_b200.distributed import DistributedRank, rank_grid_for
     from paper_2510_03557_b200.domain import build_overload, decompose, owner_ranks
     from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
     from paper_2510_03557_b200.resident import StepConfig, force_step
-    box, p, r_s, r_cut, eps = _setup()
+    box, p, r_s, r_cut, eps = _setup(h_jitter=h_jitter)
     h_max = float(p.smoothing.max())
     h_min = float(p.smoothing[p.species == 1].min())
     reach = max(r_cut, 2 * h_max)
