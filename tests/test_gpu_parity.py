@@ -260,10 +260,11 @@ def test_gpu_resident_force_step(golden, oracle):
     assert_fp32_close(out["hydro"][own, :4], ref_h[own], absh[own, :4], what="resident hydro")
 
 
-@pytest.mark.parametrize("sigma,h_jitter,mode", [(0.05, 0.0, 0), (1.0, 0.0, 0), (2.5, 0.0, 0),
-                                                 (1.0, 0.35, 0), (1.0, 0.35, 1), (1.0, 0.35, 2),
-                                                 (1.0, 0.35, 3)])
-def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, monkeypatch):
+@pytest.mark.parametrize("sigma,h_jitter,mode,L", [(0.05, 0.0, 0, 1.0), (1.0, 0.0, 0, 1.0),
+                                                   (2.5, 0.0, 0, 1.0), (1.0, 0.35, 0, 1.0),
+                                                   (1.0, 0.35, 1, 1.0), (1.0, 0.35, 2, 1.0),
+                                                   (1.0, 0.35, 3, 1.0), (1.0, 0.35, 0, 3.0)])
+def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, monkeypatch):
     """hb_force_step at 2x32^3 (config C1, near-uniform and shell-crossing
     Zel'dovich ICs) against the oracle's ordered evaluation of the same step:
     leaf order and neighbour counts bit-exact, the rest within FP32 tolerance.
@@ -271,7 +272,8 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, monkeypatch)
     varies between neighbours; the tile culls must use the tile's largest h).
     mode: HbStepArgs.gravity_mode -- 0 the default (bin tiles, soft table); 1
     leaf tiles for gravity and SPH (the fallback when a bin outgrows the tiler);
-    2 half-warp bin gravity; 3 bin gravity with the r/t table."""
+    2 half-warp bin gravity; 3 bin gravity with the r/t table.  L: box side
+    (every length scales with it)."""
     monkeypatch.setenv("HB_GRAVITY_MODE", str(mode))
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
@@ -280,29 +282,28 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, monkeypatch)
                                                hydro_force_kernel, neighbor_count_kernel)
     from paper_2510_03557_b200.resident import StepConfig, force_step
     npd = 32
-    box = BoxGeometry(1.0)
+    box = BoxGeometry(L)
     p0 = make_zeldovich_ic(npd, box, sigma)
     if h_jitter > 0:
         g0 = p0.species == 1
         rng = np.random.default_rng(17)
         p0.smoothing[g0] *= rng.uniform(1 - h_jitter, 1 + h_jitter, int(g0.sum()))
-    pm = 1.0 / (2 * npd)
+    pm = L / (2 * npd)
     r_s, r_cut = 2 * pm, 10 * pm
-    eps = (1.0 / p0.n ** (1 / 3)) / 50
+    eps = (L / p0.n ** (1 / 3)) / 50
     h_max = float(p0.smoothing.max())
     reach = max(r_cut, 2 * h_max)
     bw = max(4 * pm, reach * (1 + 1e-9))
     cfg = StepConfig(box=box, bin_width=bw, max_leaf_size=256, r_s=r_s, r_cut=r_cut, softening=eps)
     p = p0.copy()
     out = force_step(p, cfg)
-    m = oracle.build_mesh(p0.pos, p0.image_shift, p0.ghost, 1.0, bw, 256)
+    m = oracle.build_mesh(p0.pos, p0.image_shift, p0.ghost, L, bw, 256)
     perm = m["perm"]
     np.testing.assert_array_equal(p.global_id, p0.global_id[perm])
-    la, lb, ls = oracle.assemble(m, 1.0, reach)
+    la, lb, ls = oracle.assemble(m, L, reach)
     assert out["n_entries"] == la.shape[0]
     q = p0.select(perm)
     st = q.state_matrix(5 / 3)
-    L = 1.0
     args = (la, lb, ls, st, m["leaf_start"], m["leaf_end"], L)
     nc, _, _, _ = oracle.eval_pairs(neighbor_count_kernel(2 * h_max), *args, mode="deterministic",
                                     workers=8)
