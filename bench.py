@@ -591,6 +591,18 @@ def run_gpu_arm(args):
     meta = dict(meta)
     if world > 1:
         meta["parallelism"] = f"spatial cuboids {rr.grid}, overload width {rr.w:.4g}, NCCL all-to-all shell exchange per step"
+        # N = 1 runs configs[1] (c2); for the strong-scaling ratio of THIS
+        # config, its own 1-GPU line (measured separately) is referenced here
+        ref1 = os.path.join(ROOT, "profiles", f"bench_r01_{args.config}_n1.json")
+        if os.path.exists(ref1):
+            try:
+                v1 = json.loads(open(ref1).read().strip().splitlines()[-1])["value"]
+                meta["same_config_n1"] = {
+                    "value": v1, "source": os.path.relpath(ref1, ROOT),
+                    "note": "the N=1 default bench line is c2; same-config strong-scaling "
+                            "efficiency = value / (n_gpus * this value)"}
+            except Exception:
+                pass
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
