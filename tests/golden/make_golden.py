@@ -335,17 +335,18 @@ def subcycle_fixture():
     return out
 
 
-def pm_fixture():
+def pm_fixture(L=1.0):
     """Long-range PM pipeline (hb/gravity.py:58-245): CIC deposit, alias-optimal
     and naive influence, filtered spectral solve with potential, CIC gather and
-    the long-range potential energy, on a jittered 2x8^3 lattice, 16^3 grid."""
-    box = BoxGeometry(1.0)
+    the long-range potential energy, on a jittered 2x8^3 lattice, 16^3 grid,
+    in a box of side L."""
+    box = BoxGeometry(L)
     p = make_lattice_ic(8, box, 0.2 / 8, seed=404)
     rng = np.random.default_rng(3)
     p.mass = p.mass * rng.uniform(0.5, 1.5, p.n)  # unequal masses exercise the weights
     n = 16
     split = ForceSplit.for_grid(box, n)
-    out = {"pos": p.pos.copy(), "mass": p.mass.copy(), "grid_n": np.int64(n),
+    out = {"pos": p.pos.copy(), "mass": p.mass.copy(), "grid_n": np.int64(n), "L": np.float64(L),
            "r_s": np.float64(split.r_s), "r_cut": np.float64(split.r_cut)}
     rho = deposit_cic(p, n, box)
     out["rho"] = rho.values.copy()
@@ -429,6 +430,7 @@ def main():
                      ("step", step_fixture), ("adapt", adapt_fixture),
                      ("adapt_periodic", adapt_periodic_fixture),
                      ("subcycle", subcycle_fixture), ("pm", pm_fixture),
+                     ("pm_L2", lambda: pm_fixture(2.0)),
                      ("fof", fof_fixture), ("ckpt", ckpt_fixture)):
         if only and name not in only:
             continue

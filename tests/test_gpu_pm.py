@@ -20,12 +20,14 @@ def _close(ours, ref, rel):
         float(np.max(np.abs(ours - ref))) / scale)
 
 
-def test_pm_matches_reference(golden):
+@pytest.mark.parametrize("fixture", ["pm", "pm_L2"])
+def test_pm_matches_reference(golden, fixture):
     from paper_2510_03557_b200 import gravity as G
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.particles import ParticleSet
-    g = golden("pm")
-    box = BoxGeometry(1.0)
+    g = golden(fixture)
+    L = float(g["L"]) if "L" in g else 1.0
+    box = BoxGeometry(L)
     p = ParticleSet(g["pos"].shape[0])
     p.pos[...] = g["pos"]
     p.mass[...] = g["mass"]
@@ -33,7 +35,7 @@ def test_pm_matches_reference(golden):
     split = G.ForceSplit(r_s=float(g["r_s"]), r_cut=float(g["r_cut"]))
     rho = G.deposit_cic(p, n, box)
     np.testing.assert_allclose(rho.values, g["rho"], rtol=1e-12, atol=1e-12 * g["rho"].max())
-    h3 = (1.0 / n) ** 3
+    h3 = (L / n) ** 3
     assert abs(rho.values.sum() * h3 - p.mass.sum()) <= 1e-12 * p.mass.sum()
     d = G.optimal_influence_device(n, box, split.r_s).cpu().numpy()
     np.testing.assert_allclose(d, g["d_opt"], rtol=1e-10, atol=1e-12 * np.abs(g["d_opt"]).max())
