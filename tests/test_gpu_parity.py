@@ -260,11 +260,11 @@ def test_gpu_resident_force_step(golden, oracle):
     assert_fp32_close(out["hydro"][own, :4], ref_h[own], absh[own, :4], what="resident hydro")
 
 
-@pytest.mark.parametrize("sigma,h_jitter,mode,L", [(0.05, 0.0, 0, 1.0), (1.0, 0.0, 0, 1.0),
-                                                   (2.5, 0.0, 0, 1.0), (1.0, 0.35, 0, 1.0),
-                                                   (1.0, 0.35, 1, 1.0), (1.0, 0.35, 2, 1.0),
-                                                   (1.0, 0.35, 3, 1.0), (1.0, 0.35, 0, 3.0)])
-def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, monkeypatch):
+@pytest.mark.parametrize("sigma,h_jitter,mode,L,phys", [
+    (0.05, 0.0, 0, 1.0, None), (1.0, 0.0, 0, 1.0, None), (2.5, 0.0, 0, 1.0, None),
+    (1.0, 0.35, 0, 1.0, None), (1.0, 0.35, 1, 1.0, None), (1.0, 0.35, 2, 1.0, None),
+    (1.0, 0.35, 3, 1.0, None), (1.0, 0.35, 0, 3.0, None), (1.0, 0.35, 0, 1.0, (1.4, 0.5, 1.0))])
+def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, phys, monkeypatch):
     """hb_force_step at 2x32^3 (config C1, near-uniform and shell-crossing
     Zel'dovich ICs) against the oracle's ordered evaluation of the same step:
     leaf order and neighbour counts bit-exact, the rest within FP32 tolerance.
@@ -273,7 +273,9 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, monkeypat
     mode: HbStepArgs.gravity_mode -- 0 the default (bin tiles, soft table); 1
     leaf tiles for gravity and SPH (the fallback when a bin outgrows the tiler);
     2 half-warp bin gravity; 3 bin gravity with the r/t table.  L: box side
-    (every length scales with it)."""
+    (every length scales with it).  phys: (eos_gamma, visc_alpha, visc_beta)
+    other than the defaults (5/3, 1, 2)."""
+    gamma, alpha, beta = phys if phys is not None else (5 / 3, 1.0, 2.0)
     monkeypatch.setenv("HB_GRAVITY_MODE", str(mode))
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
@@ -294,7 +296,8 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, monkeypat
     h_max = float(p0.smoothing.max())
     reach = max(r_cut, 2 * h_max)
     bw = max(4 * pm, reach * (1 + 1e-9))
-    cfg = StepConfig(box=box, bin_width=bw, max_leaf_size=256, r_s=r_s, r_cut=r_cut, softening=eps)
+    cfg = StepConfig(box=box, bin_width=bw, max_leaf_size=256, r_s=r_s, r_cut=r_cut, softening=eps,
+                     eos_gamma=gamma, visc_alpha=alpha, visc_beta=beta)
     p = p0.copy()
     out = force_step(p, cfg)
     m = oracle.build_mesh(p0.pos, p0.image_shift, p0.ghost, L, bw, 256)
@@ -303,7 +306,7 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, monkeypat
     la, lb, ls = oracle.assemble(m, L, reach)
     assert out["n_entries"] == la.shape[0]
     q = p0.select(perm)
-    st = q.state_matrix(5 / 3)
+    st = q.state_matrix(gamma)
     args = (la, lb, ls, st, m["leaf_start"], m["leaf_end"], L)
     nc, _, _, _ = oracle.eval_pairs(neighbor_count_kernel(2 * h_max), *args, mode="deterministic",
                                     workers=8)
@@ -314,7 +317,7 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, monkeypat
     rel = np.abs(p.density - rho[:, 0])[gas] / rho[gas, 0]
     assert np.median(rel) <= 1e-6 and np.quantile(rel, 0.999) <= 1e-5, rel.max()
     q.density[gas] = rho[gas, 0]
-    oracle.refresh_eos(st, q.density, q.internal_energy, 5 / 3)
+    oracle.refresh_eos(st, q.density, q.internal_energy, gamma)
     ck = crk_moments_kernel(2 * h_max)
     mom, _, _, _ = oracle.eval_pairs(ck, *args, mode="relaxed", workers=8)
     mabs = oracle.eval_abs_sums(ck, *args)
@@ -327,7 +330,7 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, monkeypat
     g, _, _, _ = oracle.eval_pairs(gk, *args, mode="relaxed", workers=8)
     gabs = oracle.eval_abs_sums(gk, *args)
     assert_fp32_close(out["grav"], g, gabs, what="gravity")
-    hk = hydro_force_kernel(2 * h_max)
+    hk = hydro_force_kernel(2 * h_max, alpha, beta)
     hy, _, _, _ = oracle.eval_pairs(hk, *args, mode="relaxed", workers=8)
     habs = oracle.eval_abs_sums(hk, *args)
     assert_fp32_close(out["hydro"], hy, habs, what="hydro")
