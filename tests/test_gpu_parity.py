@@ -263,7 +263,8 @@ def test_gpu_resident_force_step(golden, oracle):
 @pytest.mark.parametrize("sigma,h_jitter,mode,L,phys", [
     (0.05, 0.0, 0, 1.0, None), (1.0, 0.0, 0, 1.0, None), (2.5, 0.0, 0, 1.0, None),
     (1.0, 0.35, 0, 1.0, None), (1.0, 0.35, 1, 1.0, None), (1.0, 0.35, 2, 1.0, None),
-    (1.0, 0.35, 3, 1.0, None), (1.0, 0.35, 0, 3.0, None), (1.0, 0.35, 0, 1.0, (1.4, 0.5, 1.0))])
+    (1.0, 0.35, 3, 1.0, None), (1.0, 0.35, 0, 3.0, None), (1.0, 0.35, 0, 1.0, (1.4, 0.5, 1.0)),
+    (1.0, 0.35, 1, 1.0, "leaf64")])
 def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, phys, monkeypatch):
     """hb_force_step at 2x32^3 (config C1, near-uniform and shell-crossing
     Zel'dovich ICs) against the oracle's ordered evaluation of the same step:
@@ -275,7 +276,8 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, phys, mon
     2 half-warp bin gravity; 3 bin gravity with the r/t table.  L: box side
     (every length scales with it).  phys: (eos_gamma, visc_alpha, visc_beta)
     other than the defaults (5/3, 1, 2)."""
-    gamma, alpha, beta = phys if phys is not None else (5 / 3, 1.0, 2.0)
+    max_leaf = 64 if phys == "leaf64" else 256     # "leaf64": leaves of <= 64
+    gamma, alpha, beta = phys if isinstance(phys, tuple) else (5 / 3, 1.0, 2.0)
     monkeypatch.setenv("HB_GRAVITY_MODE", str(mode))
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
@@ -296,11 +298,11 @@ def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, phys, mon
     h_max = float(p0.smoothing.max())
     reach = max(r_cut, 2 * h_max)
     bw = max(4 * pm, reach * (1 + 1e-9))
-    cfg = StepConfig(box=box, bin_width=bw, max_leaf_size=256, r_s=r_s, r_cut=r_cut, softening=eps,
-                     eos_gamma=gamma, visc_alpha=alpha, visc_beta=beta)
+    cfg = StepConfig(box=box, bin_width=bw, max_leaf_size=max_leaf, r_s=r_s, r_cut=r_cut,
+                     softening=eps, eos_gamma=gamma, visc_alpha=alpha, visc_beta=beta)
     p = p0.copy()
     out = force_step(p, cfg)
-    m = oracle.build_mesh(p0.pos, p0.image_shift, p0.ghost, L, bw, 256)
+    m = oracle.build_mesh(p0.pos, p0.image_shift, p0.ghost, L, bw, max_leaf)
     perm = m["perm"]
     np.testing.assert_array_equal(p.global_id, p0.global_id[perm])
     la, lb, ls = oracle.assemble(m, L, reach)
