@@ -587,7 +587,10 @@ def run_gpu_arm(args):
     roof["kflop_per_update"] = step_flops / n_total / 1e3
     base = None
     if world == 1 and not args.no_cpu_baseline:
-        base = cpu_baseline(p, cfg, frac=args.cpu_frac, gravity_only=passes != PASS_ALL)
+        # one sample of ~10-30 s of host work: 4x the reference arm's per-step
+        # fraction (that arm repeats its sample K + W times)
+        base = cpu_baseline(p, cfg, frac=min(1.0, 4 * args.cpu_frac),
+                            gravity_only=passes != PASS_ALL)
     meta = dict(meta)
     if world > 1:
         meta["parallelism"] = f"spatial cuboids {rr.grid}, overload width {rr.w:.4g}, NCCL all-to-all shell exchange per step"
