@@ -106,16 +106,24 @@ def _component_groups(gids: np.ndarray, roots: np.ndarray, pos: np.ndarray, mass
     about the halo-id member; radius = max |minimage(x - centre)|."""
     if gids.size == 0:
         return []
-    order = np.lexsort((gids, roots))
-    g, r, x, m = gids[order], roots[order], pos[order], mass[order]
+    if gids.min() >= 0 and roots.min() >= 0 and max(gids.max(), roots.max()) < 2 ** 31:
+        # (root, gid) order by one device sort of root << 32 | gid: the same
+        # order as np.lexsort((gids, roots)) (gids are unique)
+        torch = N.torch_cuda()
+        key = torch.from_numpy((roots.astype(np.int64) << 32) | gids.astype(np.int64)).cuda()
+        order = torch.argsort(key).cpu().numpy()
+    else:
+        order = np.lexsort((gids, roots))
+    r = roots[order]
     starts = np.flatnonzero(np.r_[True, r[1:] != r[:-1]])
     sizes = np.diff(np.r_[starts, r.size])
+    keep = np.flatnonzero(sizes >= min_members)   # only these components become groups
     groups = []
-    for s0, sz in zip(starts, sizes):
-        if sz < min_members:
-            continue
-        members = g[s0:s0 + sz]
-        xm, mm = x[s0:s0 + sz], m[s0:s0 + sz]
+    for s0, sz in zip(starts[keep], sizes[keep]):
+        idx = order[s0:s0 + sz]
+        members = gids[idx]
+        g_x, g_m = pos[idx], mass[idx]
+        xm, mm = g_x, g_m
         ref = xm[0]  # members sorted by gid: the min gid (= halo id) comes first
         offs = minimum_image(xm - ref, box)
         total = float(mm.sum())
@@ -157,8 +165,8 @@ def fof_find(particles, box: BoxGeometry, linking_length: float, min_members: in
         eb.append(gid[roots])
     uniq, root = _stitch(ea, eb)
     gids, pos, mass = _owned_tables(rank_sets)
-    u, rt = uniq.cpu().numpy(), root.cpu().numpy()
-    roots = rt[np.searchsorted(u, gids)]
+    torch = N.torch_cuda()
+    roots = root[torch.searchsorted(uniq, torch.from_numpy(gids).cuda())].cpu().numpy()
     return _component_groups(gids, roots, pos, mass, min_members, box)
 
 

@@ -276,6 +276,9 @@ def main():
     if args.only == "adapt":
         print(json.dumps(bench_adapt(args.npd, max(1, args.reps // 2))))
         return
+    if args.only == "fof":
+        print(json.dumps(bench_fof(args.npd, max(1, args.reps // 2))))
+        return
     if args.only == "c5rank":
         print(json.dumps(bench_c5_rank(args.reps)))
         return
