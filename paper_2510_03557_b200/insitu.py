@@ -220,12 +220,13 @@ def dbscan_find(particles, box: BoxGeometry, eps: float, min_pts: int,
         bg.append(gd[sel])
         bl.append(border_key[sel])
     gids, pos, mass = _owned_tables(rank_sets)
-    roots = np.full(gids.size, -1, dtype=np.int64)
-    cg, cl = core_gids.cpu().numpy(), label.cpu().numpy()
-    idx = np.searchsorted(cg, gids)
-    is_core = (idx < cg.size) & (cg[np.minimum(idx, max(cg.size - 1, 0))] == gids) \
-        if cg.size else np.zeros(gids.size, dtype=bool)
-    roots[is_core] = cl[idx[is_core]]
+    # core rows take their cluster label (device lookup, same as searchsorted)
+    roots_d = torch.full((gids.size,), -1, dtype=torch.int64, device="cuda")
+    if core_gids.numel() and gids.size:
+        g_d = torch.from_numpy(gids).cuda()
+        pos_in = torch.searchsorted(core_gids, g_d).clamp(max=core_gids.numel() - 1)
+        roots_d = torch.where(core_gids[pos_in] == g_d, label[pos_in], roots_d)
+    roots = roots_d.cpu().numpy()
     if bg:
         b_g = torch.cat(bg).cpu().numpy()
         b_l = torch.cat(bl).cpu().numpy()
