@@ -1,6 +1,6 @@
-"""GPU, 2 processes over NCCL (skipped with fewer than 2 GPUs): the real
+"""GPU, 2 or 4 processes over NCCL (skipped with fewer GPUs): the real
 all-to-all overload exchange, which the emulated-rank tests route in-process.
-Two ranks step twice; their owned rows must equal one single-domain step of the
+The ranks step twice; their owned rows must equal one single-domain step of the
 same set (counts exactly, the rest to FP32 rounding)."""
 import os
 import socket
@@ -20,16 +20,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_nccl_two_ranks_match_single_domain(tmp_path):
+@pytest.mark.parametrize("world", [2, 4])
+def test_nccl_ranks_match_single_domain(tmp_path, world):
     import torch
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+           str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(HERE, "_nccl_worker.py"), str(tmp_path)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
-    got = [dict(np.load(tmp_path / f"rank{k}.npz")) for k in (0, 1)]
+    got = [dict(np.load(tmp_path / f"rank{k}.npz")) for k in range(world)]
     merged = {k: np.concatenate([g[k] for g in got]) for k in got[0]}
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.ic import make_zeldovich_ic
