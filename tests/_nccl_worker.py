@@ -8,7 +8,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def main(outdir):
+def main(outdir, move=False):
     import torch
     import torch.distributed as dist
     from paper_2510_03557_b200.box import BoxGeometry
@@ -26,12 +26,20 @@ def main(outdir):
     own = owner_ranks(p.pos, box, rank_grid_for(world)) == rank
     rr = DistributedRank(p.select(np.nonzero(own)[0]), box, rank, world, 2 * pm, 10 * pm,
                          (1.0 / p.n ** (1 / 3)) / 50, h, h, n_global=p.n)
-    for _ in range(2):
-        out, fields = rr.step()
+    out, fields = rr.step()
+    if move:   # drift every row by up to 0.3 w: migrants cross rank faces
+        g = torch.Generator(device="cuda").manual_seed(100 + rank)
+        d = (torch.rand(fields["pos"].shape, generator=g, device="cuda",
+                        dtype=torch.float64) - 0.5) * (0.6 * rr.w)
+        fields["pos"] += d
+        fields["pos"].remainder_(1.0)
+        fields["pos"][fields["pos"] >= 1.0] = 0.0
+    out, fields = rr.step()
     torch.cuda.synchronize()
     o = (fields["ghost"] == 0).cpu().numpy()
     res = {"gid": fields["global_id"].cpu().numpy()[o],
-           "density": fields["density"].cpu().numpy()[o]}
+           "density": fields["density"].cpu().numpy()[o],
+           "pos": fields["pos"].cpu().numpy()[o]}
     for k in ("grav", "hydro", "ncount", "crk_A"):
         res[k] = out[k].cpu().numpy()[:o.size][o]
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), **res)
@@ -39,4 +47,4 @@ def main(outdir):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], move=len(sys.argv) > 2 and sys.argv[2] == "move")

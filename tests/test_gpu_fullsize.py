@@ -104,7 +104,9 @@ def test_restep_after_motion_matches_fresh():
     gid_f = fresh.fields()["global_id"].cpu().numpy()
     a, b = np.argsort(gid2), np.argsort(gid_f)
     np.testing.assert_array_equal(out2["ncount"][a], out_f["ncount"][b])
-    for k in ("grav", "hydro", "crk_A"):
+    for k in ("grav", "hydro", "crk_A"):   # FP32 sums, possibly in another order
         x, y = out2[k][a], out_f[k][b]
         scale = np.abs(y).max()
-        assert np.abs(x - y).max() <= 1e-5 * scale, (k, np.abs(x - y).max() / scale)
+        err = np.abs(x - y).reshape(len(x), -1).max(axis=1)
+        assert err.max() <= 1e-4 * scale, (k, err.max() / scale)
+        assert np.median(err) <= 1e-6 * scale, (k, np.median(err) / scale)
