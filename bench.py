@@ -3,7 +3,11 @@
 evaluation (BASELINE.json metric), on synthetic Zel'dovich-displaced
 two-species lattices.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cX] [--impl ours|reference]
+
+Default workload: c2 (2x128^3, configs[1]) at N = 1; c4 (2x512^3, configs[3], the
+multi-GPU config BASELINE.json names) at N > 1.  c3 (clustered) and c5
+(gravity-only 1024^3 DM, >= 4 GPUs) run with --config.
 
 A step is one force evaluation at depth 0: bin sort + k-d leaf
 build + reorder, leaf-pair lists, one neighbour-count pass, density + EOS, CRK
