@@ -970,8 +970,8 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int KIND, int JB, int REP, int NB>
-__global__ void __launch_bounds__(kGravWarps * 32, 4)
+template <int KIND, int JB, int REP, int NB, int MINB = 4>
+__global__ void __launch_bounds__(kGravWarps * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev) {
   extern __shared__ float4 s_tab[];  // gt.rows * REP
@@ -997,11 +997,23 @@ static int gravity_batch() {
   return v;
 }
 
-template <int KIND, int JB, int NB>
+// HB_GRAV_OCC (A/B only): 0 = 8 table copies, 4 CTAs/SM (64 regs); 1 = 2
+// copies, 5 CTAs (51 regs), batch 8; 2 = same, batch 4; 3 = 2 copies, 6 CTAs
+// (42 regs), batch 4; 4 = 1 copy, 6 CTAs, batch 4.
+static int gravity_occupancy() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HB_GRAV_OCC");
+    int x = e ? atoi(e) : 0;
+    v = (x >= 0 && x <= 4) ? x : 0;
+  }
+  return v;
+}
+
+template <int KIND, int JB, int NB, int REP = 8, int MINB = 4>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                unsigned grid, unsigned blk, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err) {
-  constexpr int REP = 8;
   size_t sm = (size_t)gt.rows * REP * sizeof(float4);
   // static staging + dynamic table may pass the 48 KB default: raise the
   // per-kernel limit whenever the table grows (per device and instantiation)
@@ -1012,12 +1024,12 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<KIND, JB, REP, NB>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<KIND, JB, REP, NB, MINB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
   }
-  k_gravity<KIND, JB, REP, NB><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
+  k_gravity<KIND, JB, REP, NB, MINB><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
   return HB_OK;
 }
 
@@ -1026,8 +1038,14 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
                         const int64_t* t_begin) {
   unsigned grid = grid_for(tcap, kGravWarps), blk = kGravWarps * 32;
   int nb = gravity_batch();
+  int occ = gravity_occupancy();
   int rc;
-  if (gt.kind == GT_SOFT && gt.jbits == 5)
+  if (gt.kind == GT_SOFT && gt.jbits == 4 && occ)
+    rc = occ == 1   ? launch_gravity_kind<GT_SOFT, 4, 8, 2, 5>(d, table, gt, grid, blk, ntd, t_begin, st, err)
+         : occ == 2 ? launch_gravity_kind<GT_SOFT, 4, 4, 2, 5>(d, table, gt, grid, blk, ntd, t_begin, st, err)
+         : occ == 3 ? launch_gravity_kind<GT_SOFT, 4, 4, 2, 6>(d, table, gt, grid, blk, ntd, t_begin, st, err)
+                    : launch_gravity_kind<GT_SOFT, 4, 4, 1, 6>(d, table, gt, grid, blk, ntd, t_begin, st, err);
+  else if (gt.kind == GT_SOFT && gt.jbits == 5)
     rc = launch_gravity_kind<GT_SOFT, 5, 8>(d, table, gt, grid, blk, ntd, t_begin, st, err);
   else if (gt.kind == GT_SOFT)
     rc = nb == 1   ? launch_gravity_kind<GT_SOFT, 4, 1>(d, table, gt, grid, blk, ntd, t_begin, st, err)
