@@ -5,9 +5,11 @@ two-species lattices.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cX] [--impl ours|reference]
 
-Default workload: c2 (2x128^3, configs[1]) at N = 1; c4 (2x512^3, configs[3], the
-multi-GPU config BASELINE.json names) at N > 1.  c3 (clustered) and c5
-(gravity-only 1024^3 DM, >= 4 GPUs) run with --config.
+Default workload at every N: c4 (2x512^3, configs[3]) -- the largest config that
+fits one B200 (158 of 183 GB), the config BASELINE.json names for 2/4/8 GPUs
+and for its strong-scaling target, so the driver's 1 -> N ratio divides like
+by like.  c2 / c3 (2x128^3 / 2x256^3) and c5 (gravity-only 1024^3 DM, >= 4
+GPUs) run with --config.
 
 A step is one force evaluation at depth 0: bin sort + k-d leaf
 build + reorder, leaf-pair lists, one neighbour-count pass, density + EOS, CRK
@@ -49,11 +51,8 @@ CONFIGS = {
                              "sweep (>= 4 B200)"),
 }
 DEVICE_IC_ABOVE = 1 << 29   # particles: displacement field built on the GPU (numpy: ~60 GB/rank)
-# default workload per GPU count: configs[1] at N = 1 (the metric's single-GPU
-# config), configs[3] -- the config BASELINE.json names for 2/4/8 GPUs and its
-# strong-scaling target -- at N > 1
-DEFAULT_CONFIG = {1: "c2"}
-DEFAULT_CONFIG_MULTI = "c4"
+# default workload at every GPU count (see the module docstring)
+DEFAULT_CONFIG = "c4"
 SUBBOX_ABOVE = 40_000_000   # CPU samples above this size use an interior sub-box
 
 
@@ -161,19 +160,23 @@ class ClockSampler:
 
 
 def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = False,
-                  region=None):
+                  region=None, npd: int | None = None):
     """Synthetic workload; local=True (world > 1) materialises only the rows
     rank `rank` owns (identical to selecting them from the full set), so the
     host never holds world copies of a 2x512^3 set; region = (lo, hi) keeps
     only the particles inside that cube (the reference arm's sub-box sample).
     Above DEVICE_IC_ABOVE particles the displacement field is built on the
-    GPU (ic.make_zeldovich_ic_device) and a selection is required."""
+    GPU (ic.make_zeldovich_ic_device) and a selection is required.  npd: a
+    periodic replica of the config on an npd^3 lattice (every scale -- r_s,
+    r_cut, h, softening, sigma_psi, bin width -- is relative to the lattice
+    spacing, so the per-particle work is the config's; the CPU arms' sample)."""
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.distributed import rank_grid_for
     from paper_2510_03557_b200.domain import owner_ranks, owner_ranks_torch
     from paper_2510_03557_b200.ic import make_zeldovich_ic, make_zeldovich_ic_device
     from paper_2510_03557_b200.resident import StepConfig
-    npd, sigma, species, desc = CONFIGS[cfg_name]
+    npd_cfg, sigma, species, desc = CONFIGS[cfg_name]
+    npd = npd or npd_cfg
     box = BoxGeometry(1.0)
     n_all = (2 if species == "both" else 1) * npd ** 3
     on_device = n_all > DEVICE_IC_ABOVE
@@ -210,7 +213,9 @@ def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = Fa
     meta = {"workload": desc, "config": cfg_name, "n_particles": n_all,
             "n_gas": npd ** 3 if species == "both" else 0,
             "n_per_dim": npd, "sigma_psi_spacings": sigma,
-            "smoothing": "h = 1.3 d (unadapted)" if species == "both" else "none (gravity only)",
+            "smoothing": ("h = 1.3 d as generated (~81 SPH neighbours), not adapted to the 64 of "
+                          "SURVEY.md 8d; identical in every arm" if species == "both"
+                          else "none (gravity only)"),
             "passes": "all" if species == "both" else "gravity",
             "ic_fft": "cuFFT (GPU)" if on_device else "numpy",
             "r_s": "d", "r_cut": "5 d", "softening": "L/N^(1/3)/50", "max_leaf_size": 256,
@@ -221,164 +226,159 @@ def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = Fa
     return p, cfg, meta
 
 
-def pair_counts(p, cfg):
-    """Exact in-support ordered pair counts for the algorithmic-FLOP roofline
-    (untimed; uses the compat API's exact pairs_in_reach)."""
-    from paper_2510_03557_b200.cmtree import assemble_interaction_lists, build_mesh_and_leaves
-    from paper_2510_03557_b200.kernels import counting_kernel, neighbor_count_kernel
-    from paper_2510_03557_b200.lane import EvalMode, eval_interaction_list
-    q = p.copy()
-    mesh = build_mesh_and_leaves(q, cfg.box, cfg.bin_width, cfg.max_leaf_size)
-    reach = max(cfg.r_cut, 2 * float(q.smoothing.max()))
-    il = assemble_interaction_lists(mesh, reach, 0)
-    st = q.state_matrix(cfg.eos_gamma)
-    g = eval_interaction_list(counting_kernel(cfg.r_cut), il, st, mesh, mode=EvalMode.RELAXED)
-    nc = eval_interaction_list(neighbor_count_kernel(2 * float(q.smoothing.max())), il, st, mesh,
-                               mode=EvalMode.DETERMINISTIC)
-    gas = q.species == 1
-    sph_in = int(nc.values[gas, 0].sum())          # r <= 2 h_i, gas-gas, incl. self
-    n_gas = int(gas.sum())
-    return {"gravity": int(g.values[:, 0].sum()), "density": sph_in, "ncount": sph_in,
-            "crk": sph_in, "hydro": sph_in - n_gas,
-            "gravity_scheduled_leafpairs": int(g.counters["pairs_scheduled"])}
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
-def subbox_region(L: float, r_cut: float, n_all: int, h_max: float,
-                  n_target: int = 2 * 128 ** 3):
-    """(a, side, reach) of the interior sample cube [a, a + side)^3 holding
-    ~n_target of n_all particles; its shell reaches `reach` further out."""
-    side = L * min(1.0, (n_target / n_all) ** (1.0 / 3.0))
-    return 0.5 * (L - side), side, max(r_cut, 2 * h_max)
-
-
-def subbox_sample(p, cfg, n_target: int = 2 * 128 ** 3, n_all: int | None = None):
-    """Interior cube of the workload holding ~n_target owned particles plus its
-    overload shell (width = reach) as ghosts, on a bounded mesh -- the domain
-    one rank of a spatial decomposition sees.  Returns (ParticleSet, bounds_lo,
-    bounds_hi).  Per-particle work matches the full box (same lattice
-    statistics), so owned / time is the full workload's rate.  p may already
-    be restricted to the shell's outer cube (then pass the full n_all)."""
-    a, side, reach = subbox_region(cfg.box.side_length, cfg.r_cut, n_all or p.n,
-                                   float(p.smoothing.max()), n_target)
-    x = p.pos
-    inner = np.all((x >= a) & (x < a + side), axis=1)
-    shell = np.all((x >= a - reach) & (x < a + side + reach), axis=1) & ~inner
-    idx = np.concatenate([np.nonzero(inner)[0], np.nonzero(shell)[0]])
-    q = p.select(idx)
-    q.ghost[:] = 0
-    q.ghost[int(inner.sum()):] = 1
-    q.image_shift[:] = 0
-    lo = np.full(3, a - reach)
-    hi = np.full(3, a + side + reach)
-    return q, lo, hi
-
-
-def cpu_baseline(p, cfg, frac: float = 1 / 32, threads: int | None = None, bounds=None,
-                 gravity_only: bool = False):
-    """The reference algorithm (oracle/ C restatement, bitwise-pinned to the
-    reference) on the host cores: full build + lists, every (1/frac)-th entry
-    of each kernel's list scaled up (fixed per-call cost measured separately),
-    full CRK solve.  Gravity and hydro use the reference driver's mirror mode
-    over unordered pairs (half the pair work).  bounds: (lo, hi) of a bounded
-    (rank-domain) mesh, else the periodic box."""
+def cpu_reference_step(p, cfg, bounds=None, gravity_only: bool = False,
+                       threads: int | None = None) -> dict:
+    """One COMPLETE force evaluation of set p by the reference algorithm on the
+    host cores: the oracle/ C restatement, pinned bitwise to the reference
+    (tests/test_oracle_golden.py), with the reference driver's schedule --
+    build_mesh_and_leaves, assemble_interaction_lists, one neighbour-count
+    pass, compute_density, refresh_eos_columns, compute_crk_coefficients
+    (moments + 3x3 solve), then gravity and hydro over the unordered due pairs
+    in mirror mode (hb/stepper.py:113-192).  Nothing is
+    sampled or extrapolated: the returned rate is owned rows / wall time.
+    bounds: (lo, hi) of a bounded (rank-domain) mesh, else the periodic box."""
     from oracle import oracle as O
+    from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
     from paper_2510_03557_b200.kernels import (crk_moments_kernel, density_kernel,
                                                hydro_force_kernel, neighbor_count_kernel)
-    from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
     threads = threads or os.cpu_count() or 1
     O.set_threads(threads)
     L = cfg.box.side_length
+    sec = {}
+    t_all = time.perf_counter()
     t0 = time.perf_counter()
     blo, bhi = bounds if bounds is not None else (None, None)
     m = O.build_mesh(p.pos, p.image_shift, p.ghost, L, cfg.bin_width, cfg.max_leaf_size,
                      bounds_lo=blo, bounds_hi=bhi)
-    t_build = time.perf_counter() - t0
-    h_max = float(p.smoothing.max())
+    sec["build"] = time.perf_counter() - t0
+    gas = p.species == 1
+    h_max = float(p.smoothing[gas].max()) if np.any(gas) else 0.0
     reach = max(cfg.r_cut, 2 * h_max)
     t0 = time.perf_counter()
     la, lb, ls = O.assemble(m, L, reach)
-    t_list = time.perf_counter() - t0
+    sec["list"] = time.perf_counter() - t0
     perm = m["perm"]
+    pshift = p.image_shift[perm]
+    pshift = pshift if np.any(pshift) else None
     st = O.state_matrix(p.pos[perm], p.vel[perm], p.mass[perm], p.smoothing[perm],
                         p.density[perm], p.internal_energy[perm], p.species[perm], cfg.eos_gamma)
-    ua, ub, us, _ = O.unordered_due_pairs(la, lb, ls, m["leaf_start"].shape[0])
-    gk = short_range_gravity_kernel(ForceSplit(r_s=cfg.r_s, r_cut=cfg.r_cut), cfg.softening)
-    jobs = [("ncount", neighbor_count_kernel(2 * h_max), False),
-            ("density", density_kernel(2 * h_max), False),
-            ("crk", crk_moments_kernel(2 * h_max), False),
-            ("gravity", gk, True),
-            ("hydro", hydro_force_kernel(2 * h_max), True)]
-    if gravity_only:   # the gravity-only configs' step: build + lists + gravity
-        jobs = [j for j in jobs if j[0] == "gravity"]
-    times = {}
-    for name, ker, mirror in jobs:
-        A, B, S = (ua, ub, us) if mirror else (la, lb, ls)
-        # every stride-th entry: the sample spans the whole list (per-entry
-        # cost varies along it, so a leading slice extrapolates poorly)
-        stride = max(1, int(round(1.0 / frac)))
-        As, Bs, Ss = A[::stride], B[::stride], S[::stride]
-        k = max(1, len(As))
-        mode = "deterministic" if name == "ncount" else "relaxed"
-        t0 = time.perf_counter()
-        O.eval_pairs(ker, A[:0], B[:0], S[:0], st, m["leaf_start"], m["leaf_end"], L, mode=mode,
-                     workers=threads, mirror=mirror)
-        t_fixed = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        O.eval_pairs(ker, As, Bs, Ss, st, m["leaf_start"], m["leaf_end"], L, mode=mode,
-                     workers=threads, mirror=mirror)
-        t_s = time.perf_counter() - t0
-        times[name] = t_fixed + max(t_s - t_fixed, 0.0) * len(A) / k
+    args = (m["leaf_start"], m["leaf_end"], L)
+
+    def ev(name, ker, A, B, S, mode="relaxed", mirror=False):
+        t = time.perf_counter()
+        v, _, _, err = O.eval_pairs(ker, A, B, S, st, *args, mode=mode, workers=threads,
+                                    mirror=mirror, pshift=pshift)
+        sec[name] = time.perf_counter() - t
+        if err:
+            raise RuntimeError(f"reference step: {name} raised {err}")
+        return v
+
     if not gravity_only:
-        t0 = time.perf_counter()
-        vals = np.zeros((p.n, 10))
-        vals[:, 0] = 1.0
-        vals[:, 4] = vals[:, 7] = vals[:, 9] = 1.0
-        O.crk_solve(vals, p.species[perm] == 1)
-        times["crk_solve"] = time.perf_counter() - t0
-    total = t_build + t_list + sum(times.values())
+        ev("ncount", neighbor_count_kernel(2 * h_max), la, lb, ls, mode="deterministic")
+        rho = ev("density", density_kernel(2 * h_max), la, lb, ls)
+        t = time.perf_counter()
+        gp = gas[perm]
+        # write-back for gas rows of receiver leaves only (hb/hydro.py:73-80)
+        active_row = np.repeat(~np.asarray(m["leaf_ghost_only"], bool),
+                               m["leaf_end"] - m["leaf_start"])
+        dens = np.where(gp & active_row, rho[:, 0], st[:, 8])
+        O.refresh_eos(st, dens, p.internal_energy[perm], cfg.eos_gamma)
+        sec["eos"] = time.perf_counter() - t
+        mom = ev("crk", crk_moments_kernel(2 * h_max), la, lb, ls)
+        t = time.perf_counter()
+        O.crk_solve(mom, gp)
+        sec["crk_solve"] = time.perf_counter() - t
+    t = time.perf_counter()
+    ua, ub, us, _ = O.unordered_due_pairs(la, lb, ls, m["leaf_start"].shape[0])
+    sec["unordered"] = time.perf_counter() - t
+    gk = short_range_gravity_kernel(ForceSplit(r_s=cfg.r_s, r_cut=cfg.r_cut), cfg.softening)
+    ev("gravity", gk, ua, ub, us, mirror=True)
+    if not gravity_only:
+        ev("hydro", hydro_force_kernel(2 * h_max, cfg.visc_alpha, cfg.visc_beta), ua, ub, us,
+           mirror=True)
+    total = time.perf_counter() - t_all
+    sec["total"] = total
     n_owned = int(np.count_nonzero(p.ghost == 0))
     return {"value": n_owned / total, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": (f"full build+lists ({t_build:.2f}+{t_list:.2f} s), every "
-                       f"{max(1, int(round(1.0 / frac)))}th entry of each "
-                       f"kernel's list (ordered: ncount/density/crk; mirror-unordered: "
-                       f"gravity/hydro) scaled to the full list, full CRK solve; "
-                       f"est. step {total:.1f} s"),
-            "seconds": {"build": t_build, "list": t_list, **times, "total_est": total}}
+            "n_owned": n_owned, "n_rows": int(p.n), "seconds": sec}
+
+
+def reference_sample(cfg_name: str, npd_sample: int):
+    """The CPU arms' bounded workload: a periodic replica of config cfg_name on
+    an npd_sample^3 lattice (make_workload(npd=...): the same generator, every
+    scale relative to the lattice spacing, so each particle sees the config's
+    neighbourhood -- ~1047 gravity sources within r_cut and ~81 SPH neighbours
+    at 2 x npd^3 -- and, like the GPU arm at N = 1, a bare periodic mesh with
+    no shell).  Returns (p, cfg, meta of the FULL config + the sample, desc)."""
+    npd_cfg, _, species, _ = CONFIGS[cfg_name]
+    npd = min(int(npd_sample), npd_cfg)
+    p, cfg, meta = make_workload(cfg_name, npd=npd)
+    k = 2 if species == "both" else 1
+    d = 1.0 / npd_cfg
+    meta = dict(meta, n_particles=k * npd_cfg ** 3, n_gas=npd_cfg ** 3 if k == 2 else 0,
+                n_per_dim=npd_cfg,
+                bins_per_axis=int(np.floor(1.0 / max(2.0 * d, 5.0 * d * (1 + 1e-9)))))
+    desc = (f"periodic {'2x' if k == 2 else ''}{npd}^3 replica of the {cfg_name} workload "
+            f"({p.n} particles, all owned): the same generator with sigma_psi, h, r_s, r_cut, "
+            f"softening and bin width relative to the lattice spacing, so the same "
+            f"per-particle work")
+    meta["cpu_sample"] = {"n_per_dim": npd, "n_particles": int(p.n), "kind": "periodic replica"}
+    return p, cfg, meta, None, desc
+
+
+# lattice of the CPU samples.  npd = 5 k + 1 keeps the replica's bin width
+# (1 / floor(npd / 5) of the box, hb/driver.py:147-150) within 2% of the
+# full configs' 5.02 d (the bin width sets the leaf size and so the scheduled
+# pairs per particle).  A complete reference step of 2x46^3 takes ~7 s on the
+# GPU box's 16 host cores: the driver's K + W = 25 steps run in ~3 minutes.
+CPU_SAMPLE_NPD = {"both": 46, "dm": 71}
+CPU_BASELINE_NPD = {"both": 51, "dm": 81}   # the GPU arm's single cpu_baseline step
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference algorithm on the host cores, on a
+    bounded sample of the same workload (the sub-box above), K timed complete
+    steps after W untimed ones.  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    npd, _, species, _ = CONFIGS[args.config]
-    n_all = (2 if species == "both" else 1) * npd ** 3
-    bounds, where = None, ""
-    if n_all > SUBBOX_ABOVE:   # build only the sample cube and its shell
-        h = 1.3 * (1.0 / npd) if species == "both" else 0.0
-        a, side, reach = subbox_region(1.0, 5.0 / npd, n_all, h)   # r_cut = 5 d (make_workload)
-        p, cfg, meta = make_workload(args.config, region=(a - reach, a + side + reach))
-        p, lo, hi = subbox_sample(p, cfg, n_all=n_all)
-        bounds = (lo, hi)
-        where = (f"interior sub-box of {int(np.count_nonzero(p.ghost == 0))} owned + "
-                 f"{int(np.count_nonzero(p.ghost))} overload-shell particles (bounded mesh); ")
-    else:
-        p, cfg, meta = make_workload(args.config)
-    vals = []
-    base = None
+    species = CONFIGS[args.config][2]
+    npd = getattr(args, "cpu_npd", None) or CPU_SAMPLE_NPD[species]
+    p, cfg, meta, bounds, desc = reference_sample(args.config, npd)
     gonly = species == "dm"
     for _ in range(args.warmup):
-        cpu_baseline(p, cfg, frac=args.cpu_frac / 4, bounds=bounds, gravity_only=gonly)
+        cpu_reference_step(p, cfg, bounds, gravity_only=gonly)
+    steps = []
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        base = cpu_baseline(p, cfg, frac=args.cpu_frac, bounds=bounds, gravity_only=gonly)
-        vals.append(base["value"])
-    v = float(np.median(vals))
-    n_owned = meta["n_particles"]
+        steps.append(cpu_reference_step(p, cfg, bounds, gravity_only=gonly))
+    wall = time.perf_counter() - t0
+    n_owned = steps[0]["n_owned"]
+    ms_step = wall / args.steps * 1e3
+    v = n_owned / (ms_step * 1e-3)
+    phases = {k: float(np.median([x["seconds"][k] for x in steps])) for k in steps[0]["seconds"]}
+    cores = steps[0]["cores"]
+    meta = dict(meta)
+    meta["updates_per_step"] = n_owned
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_owned / v * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": meta,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "port",
-                             "sample": where + base["sample"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "cpu_model": cpu_model(), "extrapolated": False,
+                             "sample": desc + "; every step a complete force evaluation "
+                                              "(no list sampling)",
+                             "seconds_per_phase": phases},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -557,64 +557,76 @@ def run_gpu_arm(args):
         h2d, d2h = float(tt[0].item()), float(tt[1].item())
     e2e_value = n_total / (ms_e2e * 1e-3)
 
+    # ---- exact pair counts: an untimed accounting pass on every rank (the
+    # gravity count re-steps the rank set with HB_PASS_COUNT_ONLY; SPH counts
+    # are the step's own exact neighbour counts, r <= 2 h_i gas-gas incl. self)
+    eng = rr if world == 1 else rr.engine
+    fl = eng.fields()
+    own = fl["ghost"] == 0
+    sph_in = n_gas_own = 0
+    if passes == PASS_ALL:
+        gown = own & (fl["species"] == 1)
+        sph_in = int(eng.out["ncount"][:eng.n][gown].sum().item())
+        n_gas_own = int(gown.sum().item())
+    t_cnt = time.perf_counter()
+    g_pairs = eng.gravity_pair_count(owned_only=world > 1)
+    t_cnt = time.perf_counter() - t_cnt
+    if dist:
+        t = torch.tensor([g_pairs, sph_in, n_gas_own], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        g_pairs, sph_in, n_gas_own = (int(x) for x in t.tolist())
+    counts = {"gravity": g_pairs, "density": sph_in, "ncount": sph_in, "crk": sph_in,
+              "hydro": max(sph_in - n_gas_own, 0),
+              "how": "exact: gravity = ordered (i, j != i) pairs with r <= r_cut from the "
+                     "device counting pass (float64 re-check at the threshold); SPH = the "
+                     "step's neighbour counts (r <= 2 h_i, gas-gas, incl. self; hydro "
+                     "excludes self; uniform h)",
+              "count_pass_s": t_cnt}
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return 0
     # ---- roofline of the dominant kernel (k_gravity, event-timed live above)
-    if n_total > 40_000_000:
-        # exact counting pass too large to run untimed next to the rank data:
-        # per-particle in-support counts measured at c2 (same sigma/d statistics)
-        # (gravity: neighbours within r_cut = 5 d at 2 particles per d^3; a
-        # single-species set has half the number density)
-        per = {"gravity": 1047.0503, "sph": 81.0037}
-        n_gas = meta["n_gas"]
-        sph = int(per["sph"] * n_gas)
-        g_per = per["gravity"] * (1.0 if species_c == "both" else 0.5)
-        counts = {"gravity": int(g_per * n_total), "density": sph, "ncount": sph,
-                  "crk": sph, "hydro": max(sph - n_gas, 0),
-                  "estimated": "per-particle counts measured exactly at c2 (2x128^3), "
-                               "halved for gravity in single-species sets"}
-    else:
-        counts = pair_counts(p, cfg)
     peak, peak_src = peaks()
     alg_flops = counts["gravity"] * OPCOST["gravity"]
     t_grav = ph.get("k_gravity_max_over_ranks", ph["k_gravity"]) * 1e-3
     achieved = alg_flops / t_grav / 1e12
-    traffic = None
+    # ncu evidence for this config's k_gravity (profiles/traffic_<config>.json,
+    # from one `ncu --set full` capture): DRAM bytes per launch and the executed
+    # FP32 operations (fadd + fmul + 2 ffma, the paper's counting rule,
+    # PAPER.md:238) -- the latter over the live kernel time gives the executed
+    # FP32 rate next to the algorithmic one
+    traffic, fp32_ops = None, None
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get("gravity_dram_bytes_per_launch")
+        rec = json.load(open(tf))
+        traffic = rec.get("gravity_dram_bytes_per_launch")
+        fp32_ops = rec.get("gravity_fp32_ops_per_launch")
     roof = {"bound": "fp32", "kernel": "k_gravity (single launch, CUDA events on its stream)",
             "achieved": achieved, "peak": peak * world, "unit": "TFLOP/s",
             "frac": achieved / (peak * world), "traffic": traffic, "peak_source": peak_src,
             "algorithmic_flops_per_launch": alg_flops, "in_support_pairs": counts["gravity"],
             "flops_per_pair": OPCOST["gravity"]}
+    if fp32_ops:
+        roof["executed_fp32_tflops"] = fp32_ops / t_grav / 1e12
+        roof["executed_fp32_frac"] = roof["executed_fp32_tflops"] / (peak * world)
+        roof["executed_per_algorithmic"] = fp32_ops / alg_flops
     step_flops = sum(counts[k] * OPCOST[k] for k in OPCOST)
     roof["step_algorithmic_tflops"] = step_flops / (ms_step * 1e-3) / 1e12
     roof["step_frac"] = roof["step_algorithmic_tflops"] / (peak * world)
     roof["kflop_per_update"] = step_flops / n_total / 1e3
     base = None
     if world == 1 and not args.no_cpu_baseline:
-        # one sample of ~10-30 s of host work: 2x the reference arm's per-step
-        # fraction (that arm repeats its sample K + W times)
-        base = cpu_baseline(p, cfg, frac=min(1.0, 2 * args.cpu_frac),
-                            gravity_only=passes != PASS_ALL)
+        # one complete reference step on a bounded replica of this workload
+        # (~10 s on the host cores), after the GPU timings
+        q, qcfg, _, _, desc = reference_sample(args.config, CPU_BASELINE_NPD[species_c])
+        base = cpu_reference_step(q, qcfg, None, gravity_only=passes != PASS_ALL)
+        base["sample"] = "one complete force evaluation of a " + desc
+        base["cpu_model"] = cpu_model()
+        base["extrapolated"] = False
     meta = dict(meta)
     if world > 1:
         meta["parallelism"] = f"spatial cuboids {rr.grid}, overload width {rr.w:.4g}, NCCL all-to-all shell exchange per step"
-        # N = 1 runs configs[1] (c2); for the strong-scaling ratio of THIS
-        # config, its own 1-GPU line (measured separately) is referenced here
-        ref1 = os.path.join(ROOT, "profiles", f"bench_r01_{args.config}_n1.json")
-        if os.path.exists(ref1):
-            try:
-                v1 = json.loads(open(ref1).read().strip().splitlines()[-1])["value"]
-                meta["same_config_n1"] = {
-                    "value": v1, "source": os.path.relpath(ref1, ROOT),
-                    "note": "the N=1 default bench line is c2; same-config strong-scaling "
-                            "efficiency = value / (n_gpus * this value)"}
-            except Exception:
-                pass
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -626,7 +638,8 @@ def run_gpu_arm(args):
             "gpu_launches": int(launches), "roofline": roof, "clocks": clocks.summary(),
             "pair_counts": counts}
     if base is not None:
-        line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                     "cpu_model", "extrapolated")}
         line["cpu_baseline"]["seconds"] = base["seconds"]
     print(json.dumps(line), flush=True)
     if dist:
@@ -640,14 +653,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
-                    help="workload (default: c2 at 1 GPU, c4 at more)")
+                    help="workload (default: c4 at every GPU count)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-frac", type=float, default=1 / 16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-npd", type=int, default=None,
+                    help="lattice of the CPU reference sample (default: CPU_SAMPLE_NPD)")
     args = ap.parse_args()
     if args.config is None:
-        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-        args.config = DEFAULT_CONFIG.get(world, DEFAULT_CONFIG_MULTI)
+        args.config = DEFAULT_CONFIG
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_gpu_arm(args)

@@ -191,6 +191,22 @@ int hb_eval_pairs(HbEvalArgs* args, void* ws, size_t ws_bytes, void* stream, HbE
  * partially pivoted elimination, A = 1/(m0 - B.m1) with the |d| > 1e-300
  * guard, fallback A = 1/m0, B = 0.  Float64.
  * ------------------------------------------------------------------------- */
+/* assign_timestep_levels (hb/hydro.py:277-317) on the device: per-row
+ * levels (uint8) from the gas CFL / dark-matter acceleration timestep,
+ * leaf levels (int64) = max over members, all leaves set to the overall
+ * maximum when `flat`.  dev_max: 3 device int64 of scratch; max_host[3] <-
+ * (max row level, max leaf level, max level over non-ghost-only leaves).  The
+ * caller raises StiffStateError when max_host[0] > n_levels - 1 (the row
+ * levels are then clamped to 255).  One stream sync.  Replaces the numpy body
+ * of assign_timestep_levels. */
+int hb_timestep_levels(int64_t n, const double* vel, const double* internal_energy,
+                       const double* smoothing, const double* accel, const uint8_t* species,
+                       double cfl, double softening, double eos_gamma, double dt_pm,
+                       int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
+                       const uint8_t* leaf_ghost_only, int32_t flat, uint8_t* level,
+                       int64_t* leaf_level, int64_t* dev_max, int64_t* max_host, void* stream,
+                       HbError* err);
+
 int hb_crk_solve(int64_t n, const double* moments, int64_t stride, const uint8_t* species,
                  double cond_limit, double* A, double* B, uint8_t* fallback, void* stream,
                  HbError* err);
@@ -210,6 +226,12 @@ int hb_crk_solve(int64_t n, const double* moments, int64_t stride, const uint8_t
 #define HB_PASS_GRAVITY 8
 #define HB_PASS_HYDRO 16
 #define HB_PASS_ALL 31
+/* Untimed accounting pass (bench.py's roofline): with HB_PASS_GRAVITY, the
+ * gravity pass counts instead of summing forces -- grav[0..n) viewed as
+ * int64 receives, per row, the exact number of sources j != i within r_cut
+ * (float64 re-check of every FP32 decision near the threshold, as the
+ * reference's r2 <= reach2 test, hb/kernels.py:357-359). */
+#define HB_PASS_COUNT_ONLY 32
 
 typedef struct HbStepArgs {
   int64_t n;

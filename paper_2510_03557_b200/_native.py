@@ -113,6 +113,9 @@ def lib():
             lb.hb_flag_indices_workspace.argtypes = [C.c_int64]
             lb.hb_flag_indices.argtypes = [C.c_int64, P, P, P, C.c_size_t, P, P]
             lb.hb_crk_solve.argtypes = [C.c_int64, P, C.c_int64, P, C.c_double, P, P, P, P, P]
+            lb.hb_timestep_levels.argtypes = [C.c_int64, P, P, P, P, P, C.c_double, C.c_double,
+                                              C.c_double, C.c_double, C.c_int64, P, P, P,
+                                              C.c_int32, P, P, P, P, P, P]
             lb.hb_pm_deposit.argtypes = [C.c_int64, P, P, C.c_int64, C.c_double, C.c_double, P,
                                          P, P]
             lb.hb_pm_spectral.argtypes = [C.c_int64, C.c_double, C.c_double, P, P, P, P, P, P,
@@ -154,7 +157,7 @@ EXPORTS = ("hb_abi_version", "hb_launch_count", "hb_device_query", "hb_build_mes
            "hb_halo_pack_all", "hb_halo_unpack_keep_workspace", "hb_halo_unpack_keep",
            "hb_flag_indices_workspace", "hb_flag_indices", "hb_pm_deposit", "hb_pm_spectral",
            "hb_pm_interp", "hb_fof_workspace", "hb_fof_scan", "hb_uf_union_edges", "hb_crc32c",
-           "hb_crc32c_device_workspace", "hb_crc32c_device")
+           "hb_crc32c_device_workspace", "hb_crc32c_device", "hb_timestep_levels")
 
 
 def torch_cuda():

@@ -139,9 +139,11 @@ extern "C" int hb_crc32c_device(const void* data, int64_t nbytes, uint32_t* out_
   }
   int64_t n_chunks = (nbytes + kCrcChunk - 1) / kCrcChunk;
   int64_t n_blocks = (n_chunks + kCrcBlock - 1) / kCrcBlock;
-  static CrcOps ops;  // host staging (the call synchronises before returning)
-  static uint32_t slice8[8][256];
-  static bool slice_ready = false;
+  // host staging, per calling thread (the call synchronises before it returns,
+  // so one thread's buffers are never read by an earlier call's pending copy)
+  thread_local CrcOps ops;
+  thread_local uint32_t slice8[8][256];
+  thread_local bool slice_ready = false;
   if (!slice_ready) {
     for (uint32_t i = 0; i < 256; ++i) {
       uint32_t c = i;

@@ -298,7 +298,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   int64_t* seg_e = ws.take<int64_t>(nbins + 1);
   int32_t* st_src = ws.take<int32_t>(nbins * 27 + 1);
   int32_t* st_code = ws.take<int32_t>(nbins * 27 + 1);
-  int64_t* ntd = ws.take<int64_t>(1);
+  int64_t* ntd = ws.take<int64_t>(2);
   float4* P0 = ws.take<float4>(g.n + 1);
   if (ws.dry) {
     Arena s = ws;
@@ -334,6 +334,20 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     }
     k_stride_ptr<<<grid_for(nbins + 1, 256), 256, 0, st>>>(nbins, 27, st_ptr);
     HB_LAUNCH_CHECK();
+  }
+  if (g.count_only) {  // k_eval<KID_COUNTING>, float64 band re-check, no self pair
+    EvalDev e = {};
+    e.T = T; e.ent_ptr = st_ptr; e.ent_src = st_src; e.ent_code = st_code; e.P0 = P0;
+    e.state = g.state; e.pshift = g.pshift;
+    e.L = g.L; e.reach = g.r_cut;
+    e.pp.reach2 = (float)(g.r_cut * g.r_cut);
+    e.cull_reach = (float)(g.r_cut * (1.0 + 1e-4)) + 1e-30f;
+    e.include_self = 0; e.nchan = 1; e.scale[0] = 1.0f;
+    e.out_int = (int64_t*)g.out; e.write_out = 1; e.err_key = g.err_key;
+    e.in_count = (unsigned long long*)ntd + 1;  // unused (no counted-entry flags)
+    e.skip_tiles = g.ghost ? 1 : 0;
+    HB_CUDA_TRY(cudaMemsetAsync(g.out, 0, g.n * sizeof(int64_t), st));
+    return launch_pairs(KID_COUNTING, true, false, e, T.n_tiles_cap, ntd, st, err);
   }
   if (!g.half_warp) {
     EvalDev e = {};

@@ -422,6 +422,19 @@ __global__ void k_keep_gather(int64_t n, const uint8_t* flags, const int64_t* po
 
 using namespace hb;
 
+// owned rows are wrapped into [0, L) before the owner lookup, as
+// refresh_overload wraps them (hb/domain.py:175, hb/box.py:40-52: x - L
+// floor(x / L), a result of exactly L folded to 0 side, tiny negatives to 0)
+__global__ void k_wrap_owned(int64_t n, double* pos, const uint8_t* ghost, double L) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * n || ghost[i / 3]) return;
+  double x = pos[i];
+  double y = x - L * floor(x / L);
+  if (y >= L) y -= L;
+  if (y < 0.0) y = 0.0;
+  pos[i] = y;
+}
+
 extern "C" size_t hb_flag_indices_workspace(int64_t n) {
   Arena ws;
   ws.dry = true;
@@ -566,6 +579,10 @@ extern "C" int hb_halo_pack_all(int64_t n, const HbFieldSet* src, const int32_t 
   HB_CUDA_TRY(cudaMemsetAsync(counts, 0, (nslot + 2) * sizeof(uint64_t), st));
   bool blk = nslot <= kSelMaxSlots && g[0] <= 8 && g[1] <= 8 && g[2] <= 8;
   DomEdges E = dom_edges(G);
+  if (n > 0) {
+    k_wrap_owned<<<grid_for(3 * n, 256), 256, 0, st>>>(n, src->pos, src->ghost, side_length);
+    HB_LAUNCH_CHECK();
+  }
   unsigned sel_grid = (unsigned)((n + kSelRows - 1) / kSelRows);
   if (n > 0) {
     if (blk)

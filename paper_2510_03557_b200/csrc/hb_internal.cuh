@@ -70,6 +70,9 @@ struct GravBinArgs {
   cudaEvent_t split_event = nullptr;
   int (*between)(void* ctx) = nullptr;
   void* between_ctx = nullptr;
+  // count instead of sum: exact in-r_cut source counts per row into
+  // (int64_t*)out (HB_PASS_COUNT_ONLY)
+  bool count_only = false;
 };
 int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);
 // hb_crk_solve over a row list (rows[0, *n_rows), device count); other rows get

@@ -1160,8 +1160,15 @@ const float4* gravity_table_device(double r_s, double r_cut, double eps, int kin
     GravTab gt;
     float4* dev = nullptr;
     float4* host = nullptr;
+    uint64_t used = 0;
   };
-  static Slot slots[64];
+  // a few tables per device, keyed by their parameters: kernels on other
+  // streams may still read a cached table, so a live entry is never
+  // rewritten; evicting the least recently used one (rare: > kSlots distinct
+  // parameter sets) first waits for the device to go idle
+  constexpr int kSlots = 8;
+  static Slot slots[64][kSlots];
+  static uint64_t tick = 0;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
   int dev = 0;
@@ -1169,11 +1176,23 @@ const float4* gravity_table_device(double r_s, double r_cut, double eps, int kin
     set_err(err, HB_CUDA, "no CUDA device for the gravity table");
     return nullptr;
   }
-  Slot& sl = slots[dev];
-  if (sl.ok && sl.r_s == r_s && sl.r_cut == r_cut && sl.eps == eps && sl.kind == kind) {
-    *gt = sl.gt;
-    return sl.dev;
+  Slot* victim = &slots[dev][0];
+  for (int k = 0; k < kSlots; ++k) {
+    Slot& c = slots[dev][k];
+    if (c.ok && c.r_s == r_s && c.r_cut == r_cut && c.eps == eps && c.kind == kind) {
+      c.used = ++tick;
+      *gt = c.gt;
+      return c.dev;
+    }
+    if (!c.ok) { if (victim->ok) victim = &c; }
+    else if (victim->ok && c.used < victim->used) victim = &c;
   }
+  Slot& sl = *victim;
+  if (sl.ok && cudaDeviceSynchronize() != cudaSuccess) {
+    set_err(err, HB_CUDA, "gravity table eviction: device error");
+    return nullptr;
+  }
+  sl.ok = false;
   if (!sl.dev && (cudaMalloc(&sl.dev, kGravTableMax * sizeof(float4)) != cudaSuccess ||
                   cudaMallocHost(&sl.host, kGravTableMax * sizeof(float4)) != cudaSuccess)) {
     set_err(err, HB_CUDA, "gravity table allocation failed");
@@ -1190,6 +1209,7 @@ const float4* gravity_table_device(double r_s, double r_cut, double eps, int kin
     set_err(err, HB_CUDA, "gravity table upload failed");
     return nullptr;
   }
+  sl.used = ++tick;
   sl.ok = true; sl.r_s = r_s; sl.r_cut = r_cut; sl.eps = eps; sl.kind = kind; sl.gt = *gt;
   return sl.dev;
 }

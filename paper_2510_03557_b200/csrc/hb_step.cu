@@ -101,9 +101,14 @@ __global__ void k_gather_late(int64_t n, const int64_t* perm, FieldIn in, FieldO
 
 // LATE = true: skip the late fields (vel, u, density, ids) and P, c_s, which
 // need u and rho; k_eos writes them after pass A, which reads none of them
+// h_lim: the h_max the step's reach, bin width and culls were sized from
+// (HbStepArgs.h_max).  A gas row above it would silently lose the pairs
+// between 2 h_max and 2 h_i, so it raises HB_CONTRACT (error key code 3)
+// instead (the reference recomputes smoothing.max() per call, hb/hydro.py:67).
 template <bool LATE>
 __global__ void k_gather_state(int64_t n, const int64_t* perm, FieldIn in, FieldOut out,
-                               double gamma, double* st) {
+                               double gamma, double* st, double h_lim,
+                               unsigned long long* err_key) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int64_t r = perm[k];
@@ -126,6 +131,7 @@ __global__ void k_gather_state(int64_t n, const int64_t* perm, FieldIn in, Field
   out.species[k] = sp; out.ghost[k] = in.ghost[r];
   s[C_M] = m; s[C_H] = h;
   s[C_SP] = (double)sp;
+  if (sp == 1 && !(h <= h_lim)) atomicMin(err_key, 3ull);
   if (!LATE) {
     double rho = in.rho[r];
     out.rho[k] = rho;
@@ -169,7 +175,7 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
   w.ent_src = ws.take<int32_t>(lcap + 1); w.ent_code = ws.take<int32_t>(lcap + 1);
   carve_tiling(ws, n, cap > nbins ? cap : nbins, w.Tg);
   carve_tiling(ws, n, cap, w.Ta);
-  w.ntg = ws.take<int64_t>(1); w.nta = ws.take<int64_t>(1);
+  w.ntg = ws.take<int64_t>(1); w.nta = ws.take<int64_t>(2);
   w.state = ws.take<double>(n * NCOL + 1);
   w.rho_new = ws.take<double>(n + 1);
   w.P0 = ws.take<float4>(n + 1); w.P1 = ws.take<float4>(n + 1); w.P2 = ws.take<float4>(n + 1);
@@ -189,6 +195,16 @@ __global__ void k_split_row(const int64_t* bin_ptr, const int64_t* leaf_start, i
   if (threadIdx.x || blockIdx.x) return;
   int64_t l = bin_ptr[half];
   *out = l < n_leaves ? leaf_start[l] : n;
+}
+
+// error key (min over the step): leaf * 4 + code; code 1 non-finite partial,
+// 2 accumulator overflow, 3 gas smoothing length above the step's h_max
+static int step_key_error(unsigned long long ek, HbError* err) {
+  if (err) { err->leaf_a = -1; err->leaf_b = -1; }
+  if (ek % 4 == 3)
+    return set_err(err, HB_CONTRACT, "gas smoothing length exceeds the step's h_max");
+  return set_err(err, (ek % 4) == 1 ? HB_NONFINITE : HB_OVERFLOW,
+                 (ek % 4) == 1 ? "non-finite partial" : "accumulator overflow");
 }
 
 struct GhostZeroCtx {  // zeroes the gravity rows of ghost-only leaves (between halves)
@@ -309,6 +325,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->fields_ready_event)
     HB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a->fields_ready_event, 0));
   bool late_split = a->late_fields_event != nullptr;
+  // SPH passes size every cull from h_max; gravity-only steps read no h
+  double h_lim = (a->passes & ~HB_PASS_GRAVITY) ? a->h_max * (1.0 + 1e-12) : INFINITY;
+  HB_CUDA_TRY(cudaMemsetAsync(w.err_key, 0xff, sizeof(unsigned long long), st));
   {
     unsigned g1 = grid_for(n, 256);
     FieldIn fi = {a->pos_in, a->vel_in, a->mass_in, a->smoothing_in, a->internal_energy_in,
@@ -316,9 +335,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
                    a->species, a->ghost, a->image_shift, a->global_id};
     if (late_split) {
-      k_gather_state<true><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, a->eos_gamma, w.state);
+      k_gather_state<true><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, a->eos_gamma, w.state, h_lim,
+                                               w.err_key);
     } else {
-      k_gather_state<false><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, a->eos_gamma, w.state);
+      k_gather_state<false><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, a->eos_gamma, w.state, h_lim,
+                                                w.err_key);
       if (a->ghost_src_in && a->ghost_src) {
         k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
         k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
@@ -406,7 +427,6 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       if (rc) return rc;
     }
   }
-  HB_CUDA_TRY(cudaMemsetAsync(w.err_key, 0xff, sizeof(unsigned long long), st));
   EvalDev d = {};
   d.ent_ptr = w.ent_ptr; d.ent_src = w.ent_src; d.ent_code = w.ent_code;
   d.P0 = w.P0; d.P1 = w.P1; d.P2 = w.P2; d.state = w.state; d.pshift = a->image_shift;
@@ -520,10 +540,12 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     gb.half_warp = a->gravity_mode == 2;
     gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
     gb.ghost = a->owned_targets ? a->ghost : nullptr;
+    gb.count_only = (a->passes & HB_PASS_COUNT_ONLY) != 0;
+    if (gb.count_only) gb.half_warp = false;
     gb.t0 = tm.on ? tm.kv[0] : nullptr;
     gb.t1 = tm.on ? tm.kv[1] : nullptr;
     GhostZeroCtx zc = {nl, w.leaf_start, w.leaf_end, w.ghost_only, a->grav, st};
-    if (a->grav_half_event) {
+    if (a->grav_half_event && !gb.count_only) {
       gb.split_event = (cudaEvent_t)a->grav_half_event;
       if (zero_ghost) { gb.between = zero_grav_ghost_rows; gb.between_ctx = &zc; }
     }
@@ -538,6 +560,15 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                         a->side_length, w.P0, w.P1, w.P2, st, err);
       if (rc) return rc;
       setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
+      if (a->passes & HB_PASS_COUNT_ONLY) {  // exact in-r_cut counts (see hb.h)
+        EvalDev c = d;
+        c.include_self = 0; c.nchan = 1; c.scale[0] = 1.0f;
+        c.out_int = (int64_t*)a->grav;
+        c.in_count = (unsigned long long*)w.nta + 1;
+        HB_CUDA_TRY(cudaMemsetAsync(a->grav, 0, n * sizeof(int64_t), st));
+        rc = launch_pairs(KID_COUNTING, true, false, c, w.Ta.n_tiles_cap, w.nta, st, err);
+        if (rc) return rc;
+      } else {
       GravTab gt;
       const float4* gtab = gravity_table_device(
           a->r_s, a->r_cut, a->softening, gravity_kind(a->gravity_mode, a->softening, a->r_s), &gt,
@@ -547,13 +578,16 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       rc = launch_gravity_fast(d, gtab, gt, w.Ta.n_tiles_cap, w.nta, st, err);
       tm.kmark(1);
       if (rc) return rc;
+      }
     }
   }
   tm.mark(6);
-  if (a->grav_half_event && !bin_gravity) {   // no split: every row is final at the end
+  // no split (leaf gravity, or the half-warp bin kernel, which runs as one
+  // launch and never records grav_half_event): every row is final at the end
+  if (a->grav_half_event && (!bin_gravity || a->gravity_mode == 2)) {
     a->grav_split_row = 0;
   }
-  if (zero_ghost && (a->passes & HB_PASS_GRAVITY)) {
+  if (zero_ghost && (a->passes & HB_PASS_GRAVITY) && !(a->passes & HB_PASS_COUNT_ONLY)) {
     rc = zero_rows(nullptr, nullptr, nullptr, a->grav);
     if (rc) return rc;
   }
@@ -587,11 +621,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       cudaEventElapsedTime(&a->ms_kernel[2], tm.kv[4], tm.kv[5]);
   }
   if (ovf || ovf2) return set_err(err, HB_CONTRACT, "leaf exceeds the tiling capacity (2048 members)");
-  if (ek != ~0ull) {
-    if (err) { err->leaf_a = -1; err->leaf_b = -1; }
-    return set_err(err, (ek % 4) == 1 ? HB_NONFINITE : HB_OVERFLOW,
-                   (ek % 4) == 1 ? "non-finite partial" : "accumulator overflow");
-  }
+  if (ek != ~0ull) return step_key_error(ek, err);
   return HB_OK;
 }
 
@@ -625,11 +655,7 @@ extern "C" int hb_force_step_check(const void* status, HbError* err) {
   if ((uint32_t)so[1] || (uint32_t)so[2])
     return set_err(err, HB_CONTRACT, "leaf exceeds the tiling capacity (2048 members)");
   uint64_t ek = so[0];
-  if (ek != ~0ull) {
-    if (err) { err->leaf_a = -1; err->leaf_b = -1; }
-    return set_err(err, (ek % 4) == 1 ? HB_NONFINITE : HB_OVERFLOW,
-                   (ek % 4) == 1 ? "non-finite partial" : "accumulator overflow");
-  }
+  if (ek != ~0ull) return step_key_error(ek, err);
   return HB_OK;
 }
 

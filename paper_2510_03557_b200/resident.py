@@ -27,6 +27,7 @@ from .particles import FIELD_SPECS, ParticleSet
 
 PASS_NCOUNT, PASS_DENSITY, PASS_CRK, PASS_GRAVITY, PASS_HYDRO = 1, 2, 4, 8, 16
 PASS_ALL = 31
+PASS_COUNT_ONLY = 32   # with PASS_GRAVITY: exact in-r_cut source counts, no forces (hb.h)
 PHASES = ("build", "list", "tiling", "sph_density", "sph_force", "gravity", "tail", "total")
 KERNELS = ("k_gravity", "k_sph_density", "k_sph_force")  # single-kernel spans (ms_kernel)
 
@@ -234,7 +235,7 @@ class ResidentRank:
         a.late_fields_event = _event_handle(late_fields)
         a.grav_half_event = _event_handle(grav_half)
         a.status_out = P(status.data_ptr()) if status is not None and not timing else P(0)
-        if self.gravity_only and passes & ~PASS_GRAVITY:
+        if self.gravity_only and passes & ~(PASS_GRAVITY | PASS_COUNT_ONLY):
             raise HydroboxError("gravity-only rank: SPH passes requested")
         for k in ("perm", "ncount", "grav", "hydro", "crk_A", "crk_B", "crk_fallback"):
             setattr(a, k, N.ptr(self.out[k]) if k in self.out else P(0))
@@ -268,6 +269,19 @@ class ResidentRank:
                                    **dict(zip(KERNELS, list(a.ms_kernel)[:3]))}
                                   if timing else None)}
         return self.out
+
+    def gravity_pair_count(self, owned_only: bool = False) -> int:
+        """Exact number of ordered (target, source != target) pairs within
+        r_cut over every row (the reference's r2 <= reach2 test with a
+        float64 re-check near the threshold, hb/kernels.py:357-359): an
+        untimed accounting pass for the FP32 roofline.  Reorders the rank's
+        fields like a step does.  owned_only: rows with ghost == 0 only."""
+        out = self.step(PASS_GRAVITY | PASS_COUNT_ONLY)
+        torch = N.torch_cuda()
+        counts = out["grav"].reshape(-1).view(torch.int64)[:self.n]
+        if owned_only:
+            counts = counts[self.fields()["ghost"] == 0]
+        return int(counts.sum().item())
 
     def check_status(self, status) -> None:
         """Raise the error a deferred step (status=...) recorded; call after

@@ -1,0 +1,233 @@
+"""Sampled-receiver oracle parity for full-size force steps (test infrastructure).
+
+The oracle (oracle/hb_oracle.c, pinned bitwise to the reference) evaluates an
+ordered interaction list exactly as eval_interaction_list(mode=RELAXED,
+mirror=False) does (hb/lane.py:122-212).  At the benchmark sizes (2x128^3 ..
+2x512^3) evaluating every receiver on the host would take minutes to hours, so
+these helpers:
+
+* build the oracle's mesh and list for the WHOLE set (hb/cmtree.py:125-196,
+  303-337) -- the GPU's permutation and entry count are compared in full;
+* pick receiver leaves (every stride-th leaf, plus the leaves of the most
+  crowded bins) and keep only the list entries those leaves receive.  A
+  receiver's outputs depend only on its own entries, so the oracle's values on
+  those rows are exact;
+* compact the rows the kept entries touch (receiver and partner leaves) into a
+  small state matrix, so the oracle's (n, channels) accumulators are sized by
+  the sample, not by the 268 M-row set.
+
+CRK moments and the hydro force read the densities of partner rows that are
+not themselves sampled, so they are evaluated on the GPU's densities (which
+are checked on the sampled rows against the oracle's), as the verdict of round
+1 prescribes.  Reference semantics: hb/hydro.py:60-196 (density, EOS, CRK
+moments + solve, hydro), hb/kernels.py:143-278 (pair functions).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from tests.tolerances import assert_fp32_close
+
+
+def sample_leaves(m, stride: int, crowded_bins: int = 4) -> np.ndarray:
+    """Every stride-th non-ghost-only leaf plus every leaf of the
+    `crowded_bins` most populated bins (the clustered configs' hot spots)."""
+    nl = m["leaf_start"].shape[0]
+    active = np.nonzero(~np.asarray(m["leaf_ghost_only"], bool))[0]
+    pick = [active[::max(1, stride)]]
+    if crowded_bins > 0 and nl:
+        sizes = m["leaf_end"] - m["leaf_start"]
+        per_bin = np.bincount(m["leaf_bin"], weights=sizes, minlength=int(np.prod(m["bin_count"])))
+        hot = np.argsort(per_bin, kind="stable")[::-1][:crowded_bins]
+        leaves = np.concatenate([np.arange(m["bin_ptr"][b], m["bin_ptr"][b + 1]) for b in hot])
+        leaves = m["bin_ids"][leaves] if leaves.size else leaves
+        pick.append(leaves[~np.asarray(m["leaf_ghost_only"], bool)[leaves]])
+    return np.unique(np.concatenate(pick)).astype(np.int64)
+
+
+def compact(la, lb, leaf_start, leaf_end):
+    """Rows of every leaf in la U lb, concatenated; (rows, la', lb', start',
+    end') in the compact numbering (each leaf's rows stay contiguous and in
+    order, so per-entry evaluation is unchanged)."""
+    leaves = np.unique(np.concatenate([la, lb]))
+    sizes = (leaf_end[leaves] - leaf_start[leaves]).astype(np.int64)
+    start = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    total = int(sizes.sum())
+    rows = np.repeat(leaf_start[leaves] - start, sizes) + np.arange(total, dtype=np.int64)
+    remap = np.full(int(max(leaves.max(initial=0), 0)) + 1, -1, np.int64)
+    remap[leaves] = np.arange(leaves.size)
+    return rows, remap[la], remap[lb], start, start + sizes, remap
+
+
+class SampledOracle:
+    """The oracle's step on sampled receivers of particle set p0 (input order).
+
+    cfg: resident.StepConfig.  stride: receiver-leaf stride.  After
+    construction: .perm, .n_entries (full list), .rows (leaf-order rows of the
+    compact set), .recv (compact indices of the sampled receivers' rows)."""
+
+    def __init__(self, oracle, p0, cfg, stride: int, crowded_bins: int = 4,
+                 gravity_only: bool = False, workers: int | None = None):
+        import os
+        self.O = oracle
+        self.cfg = cfg
+        self.gravity_only = gravity_only
+        self.workers = workers or os.cpu_count() or 1
+        L = cfg.box.side_length
+        gas = p0.species == 1
+        self.h_max = float(p0.smoothing[gas].max()) if np.any(gas) else 0.0
+        self.reach = max(cfg.r_cut, 2.0 * self.h_max)
+        m = oracle.build_mesh(p0.pos, p0.image_shift, p0.ghost, L, cfg.bin_width,
+                              cfg.max_leaf_size, bounds_lo=cfg.bounds_lo, bounds_hi=cfg.bounds_hi)
+        self.mesh = m
+        self.perm = m["perm"]
+        la, lb, ls = oracle.assemble(m, L, self.reach)
+        self.n_entries = int(la.shape[0])
+        self.sampled = sample_leaves(m, stride, crowded_bins)
+        keep = np.isin(la, self.sampled)
+        la, lb, ls = la[keep], lb[keep], ls[keep]
+        rows, ca, cb, cs, ce, remap = compact(la, lb, m["leaf_start"], m["leaf_end"])
+        self.rows, self.la, self.lb, self.ls = rows, ca, cb, ls
+        self.cstart, self.cend = cs, ce
+        recv = remap[self.sampled]
+        self.recv = np.concatenate([np.arange(cs[k], ce[k]) for k in recv]) if recv.size else \
+            np.zeros(0, np.int64)
+        src = self.perm[rows]                       # input rows of the compact set
+        self.q = p0.select(src)
+        self.pshift = self.q.image_shift if np.any(self.q.image_shift) else None
+
+    def _args(self, st):
+        return (self.la, self.lb, self.ls, st, self.cstart, self.cend, self.cfg.box.side_length)
+
+    def _eval(self, kernel, st, mode="relaxed"):
+        v, _, cnt, err = self.O.eval_pairs(kernel, *self._args(st), mode=mode,
+                                           workers=self.workers, pshift=self.pshift)
+        assert err == 0, f"oracle {kernel.name} raised {err}"
+        return v, cnt
+
+    def _abs(self, kernel, st):
+        return self.O.eval_abs_sums(kernel, *self._args(st), pshift=self.pshift,
+                                    workers=self.workers)
+
+    def state(self, density=None):
+        q = self.q
+        rho = q.density if density is None else density
+        return self.O.state_matrix(q.pos, q.vel, q.mass, q.smoothing, rho, q.internal_energy,
+                                   q.species, self.cfg.eos_gamma)
+
+    # ---- the step's passes on the compact set ---------------------------
+    def counts_density(self):
+        from paper_2510_03557_b200.kernels import density_kernel, neighbor_count_kernel
+        st = self.state()
+        nc, _ = self._eval(neighbor_count_kernel(2 * self.h_max), st, mode="deterministic")
+        rho, _ = self._eval(density_kernel(2 * self.h_max), st)
+        return nc[:, 0], rho[:, 0]
+
+    def crk(self, gpu_density):
+        """CRK moments, their |.| sums and A, B, fallback on the GPU's densities
+        (hb/hydro.py:99-150)."""
+        from paper_2510_03557_b200.kernels import crk_moments_kernel
+        st = self.state(gpu_density)
+        ck = crk_moments_kernel(2 * self.h_max)
+        mom, _ = self._eval(ck, st)
+        mabs = self._abs(ck, st)
+        A, B, fb, *_ = self.O.crk_solve(mom, self.q.species == 1)
+        return mom, mabs, A, B, fb
+
+    def gravity(self):
+        from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
+        st = self.state()
+        gk = short_range_gravity_kernel(ForceSplit(r_s=self.cfg.r_s, r_cut=self.cfg.r_cut),
+                                        self.cfg.softening)
+        g, cnt = self._eval(gk, st)
+        return g, self._abs(gk, st), cnt
+
+    def hydro(self, gpu_density):
+        from paper_2510_03557_b200.kernels import hydro_force_kernel
+        st = self.state(gpu_density)
+        hk = hydro_force_kernel(2 * self.h_max, self.cfg.visc_alpha, self.cfg.visc_beta)
+        h, _ = self._eval(hk, st)
+        return h, self._abs(hk, st)
+
+
+def gpu_rows(t, rows):
+    """Rows `rows` (numpy int64, leaf order) of a device tensor, on the host."""
+    import torch
+    idx = torch.from_numpy(np.ascontiguousarray(rows)).to(t.device)
+    return t.index_select(0, idx).cpu().numpy()
+
+
+def check_step(oracle, p0, cfg, stride: int, crowded_bins: int = 4, passes=None,
+               rank=None, what: str = ""):
+    """Run hb_force_step on p0 (device-resident rank) and compare it with the
+    oracle on the sampled receivers.  Returns a dict of measured errors.
+    Integer outputs bit-exact (permutation, entry count, neighbour counts,
+    CRK fallback flags); floating outputs within tests/tolerances.py."""
+    from paper_2510_03557_b200.resident import PASS_ALL, PASS_GRAVITY, ResidentRank
+    gas_any = bool(np.any(p0.species == 1))
+    passes = passes if passes is not None else (PASS_ALL if gas_any else PASS_GRAVITY)
+    gravity_only = passes == PASS_GRAVITY
+    rr = rank if rank is not None else ResidentRank(p0, cfg, gravity_only=gravity_only)
+    out = rr.step(passes)
+    ref = SampledOracle(oracle, p0, cfg, stride, crowded_bins, gravity_only=gravity_only)
+    perm = out["perm"][:p0.n].cpu().numpy()
+    np.testing.assert_array_equal(perm, ref.perm, err_msg=f"{what}: leaf order")
+    assert rr.last["n_leaves"] == ref.mesh["leaf_start"].shape[0], what
+    assert rr.last["n_entries"] == ref.n_entries, (what, rr.last["n_entries"], ref.n_entries)
+    rows, recv = ref.rows, ref.recv
+    stats = {"sampled_leaves": int(ref.sampled.size), "sampled_rows": int(recv.size),
+             "compact_rows": int(rows.size), "entries": int(ref.la.size)}
+    g, gabs, cnt = ref.gravity()
+    grav = gpu_rows(out["grav"], rows)
+    assert_fp32_close(grav[recv], g[recv], gabs[recv], what=f"{what} gravity")
+    stats["gravity_pairs_in_reach"] = cnt["pairs_in_reach"]
+    if not gravity_only:
+        _check_sph(ref, rr, out, rows, recv, stats, what)
+    # exact in-r_cut source counts per sampled receiver (the FP32 force
+    # tolerance alone would not notice a lost source near r_cut, where
+    # S(r/r_s) < 1e-5): the accounting pass against the oracle's counting
+    # kernel, bit for bit.  It re-steps the leaf-ordered set, which keeps
+    # its order (stable build).
+    from paper_2510_03557_b200.kernels import counting_kernel
+    total = rr.gravity_pair_count()
+    np.testing.assert_array_equal(rr.out["perm"][:p0.n].cpu().numpy(), np.arange(p0.n),
+                                  err_msg=f"{what}: re-step order")
+    import torch
+    gcount = gpu_rows(rr.out["grav"].reshape(-1).view(torch.int64)[:p0.n], rows)
+    oc, _ = ref._eval(counting_kernel(cfg.r_cut), ref.state())
+    np.testing.assert_array_equal(gcount[recv], oc[recv, 0].astype(np.int64),
+                                  err_msg=f"{what}: gravity in-r_cut counts")
+    stats["gravity_pairs_total"] = total
+    return stats
+
+
+def _check_sph(ref, rr, out, rows, recv, stats, what):
+    nc, rho = ref.counts_density()
+    np.testing.assert_array_equal(gpu_rows(out["ncount"], rows)[recv], nc[recv],
+                                  err_msg=f"{what}: neighbour counts")
+    gdens = gpu_rows(rr.fields()["density"], rows)
+    gas = ref.q.species == 1
+    rg = recv[gas[recv]]
+    rel = np.abs(gdens[rg] - rho[rg]) / rho[rg]
+    assert np.median(rel) <= 1e-6 and np.quantile(rel, 0.999) <= 1e-5, \
+        (what, "density", float(np.median(rel)), float(rel.max()))
+    stats["density_rel_max"] = float(rel.max())
+    mom, mabs, A, B, fb = ref.crk(np.where(gas, gdens, ref.q.density))
+    assert_fp32_close(gpu_rows(out["crk_moments"], rows)[recv], mom[recv], mabs[recv],
+                      what=f"{what} crk moments")
+    np.testing.assert_array_equal(gpu_rows(out["crk_fallback"], rows)[recv].astype(bool),
+                                  fb[recv], err_msg=f"{what}: CRK fallback")
+    gA = gpu_rows(out["crk_A"], rows)
+    ok = rg[~fb[rg]]
+    relA = np.abs(gA[ok] - A[ok]) / np.abs(A[ok])
+    assert np.median(relA) <= 1e-5 and np.quantile(relA, 0.999) <= 1e-4, \
+        (what, "A", float(np.median(relA)), float(relA.max()))
+    gB = gpu_rows(out["crk_B"], rows)
+    h = ref.q.smoothing
+    dB = np.abs(gB[ok] - B[ok]).max(axis=1) * h[ok]
+    assert dB.max() <= 1e-5 * max(1.0, float(np.abs(B[ok]).max() * h[ok].max())), \
+        (what, "B", float(dB.max()))
+    hy, habs = ref.hydro(np.where(gas, gdens, ref.q.density))
+    assert_fp32_close(gpu_rows(out["hydro"], rows)[recv], hy[recv], habs[recv],
+                      what=f"{what} hydro")
+    stats["fallbacks"] = int(fb[recv].sum())

@@ -423,6 +423,47 @@ def ckpt_fixture():
     return out
 
 
+def levels_fixture():
+    """assign_timestep_levels (hb/hydro.py:277-317) on one overloaded rank set
+    of a jittered 2x12^3 lattice (ghost-only leaves present): velocities and
+    accelerations spread over decades so the gas CFL and DM acceleration
+    branches both reach levels 0..3; flat and non-flat; plus the inputs of a
+    stiff case (the reference raises StiffStateError)."""
+    from hydrobox.errors import StiffStateError
+    box = BoxGeometry(1.0)
+    p = make_lattice_ic(12, box, 0.2 / 12, seed=21)
+    rng = np.random.default_rng(22)
+    p.vel = rng.normal(0, 1, p.pos.shape) * 10.0 ** rng.uniform(-3, 0, (p.n, 1))
+    p.accel = rng.normal(0, 1, p.pos.shape) * 10.0 ** rng.uniform(-2, 3, (p.n, 1))
+    p.internal_energy[p.species == 1] *= 10.0 ** rng.uniform(-1, 1, int((p.species == 1).sum()))
+    p.accel[5] = 0.0        # |a| = 0: the 1e-300 floor (dt huge, level 0)
+    w = 0.15
+    rs = build_overload(p, decompose(box, (2, 1, 1), w), box, (2, 1, 1))[0][0]
+    mesh = build_mesh_and_leaves(rs, box, 0.25, 64, bounds_lo=np.array([-w, 0, 0]),
+                                 bounds_hi=np.array([0.5 + w, 1, 1]))
+    out = particle_arrays(rs, "in_")
+    out["in_accel"] = rs.accel.copy()
+    out.update(mesh_arrays(mesh))
+    eps = 1.0 / 24 / 50
+    probe = rs.copy()       # dt_pm such that the deepest level is 3
+    assign_timestep_levels(probe, mesh, 1.0, 0.25, 64, eps, 5 / 3)
+    dt_pm = 0.9 * 2.0 ** (3 - int(probe.timestep_level.max()))
+    out["dt_pm"], out["cfl"], out["eps"] = dt_pm, 0.25, eps
+    for tag, flat in (("", False), ("flat_", True)):
+        q = rs.copy()
+        mesh.leaf_level[:] = 0
+        hier = assign_timestep_levels(q, mesh, dt_pm, 0.25, 4, eps, 5 / 3, flat=flat)
+        out[tag + "level"] = q.timestep_level.copy()
+        out[tag + "leaf_level"] = mesh.leaf_level.copy()
+        out[tag + "max_level"] = hier.max_level
+    try:
+        assign_timestep_levels(rs.copy(), mesh, dt_pm * 64, 0.25, 4, eps, 5 / 3)
+        out["stiff_raises"] = 0
+    except StiffStateError:
+        out["stiff_raises"] = 1
+    return out
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
     only = set(sys.argv[1:])
@@ -431,7 +472,8 @@ def main():
                      ("adapt_periodic", adapt_periodic_fixture),
                      ("subcycle", subcycle_fixture), ("pm", pm_fixture),
                      ("pm_L2", lambda: pm_fixture(2.0)),
-                     ("fof", fof_fixture), ("ckpt", ckpt_fixture)):
+                     ("fof", fof_fixture), ("ckpt", ckpt_fixture),
+                     ("levels", levels_fixture)):
         if only and name not in only:
             continue
         data = fn()

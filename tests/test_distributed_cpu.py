@@ -55,7 +55,7 @@ def test_alltoallv_bytes_gloo_world2():
 def test_rank_grid_and_bounds_match_decompose():
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.distributed import domain_bounds, overload_width, rank_grid_for
-    from paper_2510_03557_b200.domain import decompose
+    from oracle.overload import decompose
     box = BoxGeometry(1.0)
     for world in (1, 2, 4, 8):
         g = rank_grid_for(world)

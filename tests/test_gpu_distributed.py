@@ -31,7 +31,8 @@ def _setup(npd=32, sigma=0.3, h_jitter=0.0):
 def test_emulated_ranks_match_single_domain(world, periodic_unsplit, h_jitter, oracle):
     import torch
     from paper_2510_03557_b200.distributed import DistributedRank, rank_grid_for
-    from paper_2510_03557_b200.domain import build_overload, decompose, owner_ranks
+    from oracle.overload import build_overload, decompose
+    from paper_2510_03557_b200.domain import owner_ranks
     from paper_2510_03557_b200.gravity import ForceSplit, short_range_gravity_kernel
     from paper_2510_03557_b200.resident import StepConfig, force_step
     box, p, r_s, r_cut, eps = _setup(h_jitter=h_jitter)
@@ -109,7 +110,8 @@ def test_emulated_migrants_match_reference_overload(world):
     import torch
     from paper_2510_03557_b200.box import wrap_position
     from paper_2510_03557_b200.distributed import DistributedRank, rank_grid_for
-    from paper_2510_03557_b200.domain import build_overload, decompose, owner_ranks
+    from oracle.overload import build_overload, decompose
+    from paper_2510_03557_b200.domain import owner_ranks
     box, p, r_s, r_cut, eps = _setup()
     h_max = float(p.smoothing.max())
     h_min = float(p.smoothing[p.species == 1].min())
