@@ -232,6 +232,12 @@ int hb_crk_solve(int64_t n, const double* moments, int64_t stride, const uint8_t
  * (float64 re-check of every FP32 decision near the threshold, as the
  * reference's r2 <= reach2 test, hb/kernels.py:357-359). */
 #define HB_PASS_COUNT_ONLY 32
+/* Optional, with HB_PASS_CRK: the CRK coefficient gradients gradA / gradB
+ * (the north star's "A, B, gradA, gradB"; not in the reference, whose
+ * compute_crk_coefficients stops at A, B -- hb/hydro.py:99-150).  One more
+ * gas pass after the CRK solve (gradient moments + a float64 per-row solve)
+ * into HbStepArgs.crk_gradA / crk_gradB. */
+#define HB_PASS_CRK_GRAD 64
 
 typedef struct HbStepArgs {
   int64_t n;
@@ -312,6 +318,8 @@ typedef struct HbStepArgs {
                               the end of the step), so their copy-out can
                               overlap the second half                         */
   int64_t grav_split_row;  /* out (host, set before the call returns)         */
+  double* crk_gradA;  /* HB_PASS_CRK_GRAD: (n,3) d A / d x_i, or NULL          */
+  double* crk_gradB;  /* HB_PASS_CRK_GRAD: (n,3,3) d B_a / d x_g, or NULL      */
 } HbStepArgs;
 
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,

@@ -33,20 +33,24 @@ struct SphArgs {
   const int64_t* ent_ptr;
   const int32_t* ent_src;
   const int32_t* ent_code;
-  const float4 *P0, *P1, *P2;
+  const float4 *P0, *P1, *P2, *P3;
   const double* state;
   const int8_t* pshift;
   double L, reach;
   float band;  // relative band of r^2 around a threshold decided in float64
   double alpha, beta;
   double *ncount, *rho, *moments, *hydro;
+  // pass C (gradients): A, B, fallback of the CRK solve; gradA (n,3), gradB (n,9)
+  const double *crk_A, *crk_B;
+  const uint8_t* crk_fallback;
+  double *gradA, *gradB;
   unsigned long long* err_key;
   const uint8_t* skip_leaf;
   int skip_tiles;  // pass B: skip tiles without an owned member
 };
 int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
-             double L, float4* P0, float4* P1, float4* P2, int layout, cudaStream_t st,
-             HbError* err);
+             double L, float4* P0, float4* P1, float4* P2, float4* P3, int layout,
+             cudaStream_t st, HbError* err);
 int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err);
 
 // bin-level short-range gravity (hb_grav2.cu)

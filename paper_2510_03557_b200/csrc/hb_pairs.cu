@@ -970,16 +970,16 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int KIND, int JB, int REP, int NB, int MINB = 4>
-__global__ void __launch_bounds__(kGravWarps * 32, MINB)
+template <int KIND, int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev) {
   extern __shared__ float4 s_tab[];  // gt.rows * REP
-  __shared__ float4 s_src[kGravWarps][kGravStage];
+  __shared__ float4 s_src[WARPS][kGravStage];
   for (int k = threadIdx.x; k < gt.rows * REP; k += blockDim.x) s_tab[k] = table[k / REP];
   __syncthreads();
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t t = (int64_t)blockIdx.x * kGravWarps + wid + (t_begin_dev ? *t_begin_dev : 0);
+  int64_t t = (int64_t)blockIdx.x * WARPS + wid + (t_begin_dev ? *t_begin_dev : 0);
   if (t < *n_tiles_dev)
     grav_tile<KIND, JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
                                  t, lane);
@@ -1010,9 +1010,9 @@ static int gravity_occupancy() {
   return v;
 }
 
-template <int KIND, int JB, int NB, int REP = 8, int MINB = 4>
+template <int KIND, int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
-                               unsigned grid, unsigned blk, const int64_t* ntd,
+                               int64_t tcap, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err) {
   size_t sm = (size_t)gt.rows * REP * sizeof(float4);
   // static staging + dynamic table may pass the 48 KB default: raise the
@@ -1024,38 +1024,40 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<KIND, JB, REP, NB, MINB>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<KIND, JB, REP, NB, MINB, WARPS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
   }
-  k_gravity<KIND, JB, REP, NB, MINB><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
+  unsigned grid = grid_for(tcap, WARPS), blk = WARPS * 32;
+  k_gravity<KIND, JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
   return HB_OK;
 }
 
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
                         const int64_t* ntd, cudaStream_t st, HbError* err,
                         const int64_t* t_begin) {
-  unsigned grid = grid_for(tcap, kGravWarps), blk = kGravWarps * 32;
   int nb = gravity_batch();
   int occ = gravity_occupancy();
   int rc;
   if (gt.kind == GT_SOFT && gt.jbits == 4 && occ)
-    rc = occ == 1   ? launch_gravity_kind<GT_SOFT, 4, 8, 2, 5>(d, table, gt, grid, blk, ntd, t_begin, st, err)
-         : occ == 2 ? launch_gravity_kind<GT_SOFT, 4, 4, 2, 5>(d, table, gt, grid, blk, ntd, t_begin, st, err)
-         : occ == 3 ? launch_gravity_kind<GT_SOFT, 4, 4, 2, 6>(d, table, gt, grid, blk, ntd, t_begin, st, err)
-                    : launch_gravity_kind<GT_SOFT, 4, 4, 1, 6>(d, table, gt, grid, blk, ntd, t_begin, st, err);
+    rc = occ == 1   ? launch_gravity_kind<GT_SOFT, 4, 8, 2, 5>(d, table, gt, tcap, ntd, t_begin, st, err)
+         : occ == 2 ? launch_gravity_kind<GT_SOFT, 4, 4, 2, 5>(d, table, gt, tcap, ntd, t_begin, st, err)
+         : occ == 3 ? launch_gravity_kind<GT_SOFT, 4, 4, 2, 6>(d, table, gt, tcap, ntd, t_begin, st, err)
+                    : launch_gravity_kind<GT_SOFT, 4, 4, 1, 6>(d, table, gt, tcap, ntd, t_begin, st, err);
   else if (gt.kind == GT_SOFT && gt.jbits == 5)
-    rc = launch_gravity_kind<GT_SOFT, 5, 8>(d, table, gt, grid, blk, ntd, t_begin, st, err);
+    // the 32-per-octave table is twice the 8-copy footprint (~70 KB): 16-warp
+    // CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4
+    rc = launch_gravity_kind<GT_SOFT, 5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err);
   else if (gt.kind == GT_SOFT)
-    rc = nb == 1   ? launch_gravity_kind<GT_SOFT, 4, 1>(d, table, gt, grid, blk, ntd, t_begin, st, err)
-         : nb == 2 ? launch_gravity_kind<GT_SOFT, 4, 2>(d, table, gt, grid, blk, ntd, t_begin, st, err)
-         : nb == 8 ? launch_gravity_kind<GT_SOFT, 4, 8>(d, table, gt, grid, blk, ntd, t_begin, st, err)
-                   : launch_gravity_kind<GT_SOFT, 4, 4>(d, table, gt, grid, blk, ntd, t_begin, st, err);
+    rc = nb == 1   ? launch_gravity_kind<GT_SOFT, 4, 1>(d, table, gt, tcap, ntd, t_begin, st, err)
+         : nb == 2 ? launch_gravity_kind<GT_SOFT, 4, 2>(d, table, gt, tcap, ntd, t_begin, st, err)
+         : nb == 8 ? launch_gravity_kind<GT_SOFT, 4, 8>(d, table, gt, tcap, ntd, t_begin, st, err)
+                   : launch_gravity_kind<GT_SOFT, 4, 4>(d, table, gt, tcap, ntd, t_begin, st, err);
   else if (gt.kind == GT_T)
-    rc = launch_gravity_kind<GT_T, 0, 1>(d, table, gt, grid, blk, ntd, t_begin, st, err);
+    rc = launch_gravity_kind<GT_T, 0, 1>(d, table, gt, tcap, ntd, t_begin, st, err);
   else
-    rc = launch_gravity_kind<GT_R, 0, 1>(d, table, gt, grid, blk, ntd, t_begin, st, err);
+    rc = launch_gravity_kind<GT_R, 0, 1>(d, table, gt, tcap, ntd, t_begin, st, err);
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;
@@ -1108,7 +1110,7 @@ int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_o
     static int jb = 0;
     if (!jb) {  // HB_GRAV_JBITS: 4 (default) or 5 intervals-per-octave bits
       const char* e = getenv("HB_GRAV_JBITS");
-      jb = (e && atoi(e) == 5) ? 5 : kGravSoftBitsDefault;
+      jb = e ? (atoi(e) == 4 ? 4 : 5) : kGravSoftBitsDefault;
     }
     gt->jbits = jb;
     const int sh = 23 - jb;

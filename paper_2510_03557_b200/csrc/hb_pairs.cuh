@@ -46,6 +46,31 @@ __device__ __forceinline__ void walk_masks(const unsigned (*mask)[32], unsigned 
     }
   }
 }
+// walk_masks taking two set bits of the current word per iteration (the
+// second may be absent: q2 = -1), so two independent pair chains are in
+// flight per lane
+template <class Body2>
+__device__ __forceinline__ void walk_masks2(const unsigned (*mask)[32], unsigned nz, Body2 body) {
+  int lane = threadIdx.x & 31;
+  int wi = 0;
+  unsigned m = 0u;
+  while (true) {
+    if (m == 0u && nz != 0u) {
+      wi = __ffs(nz) - 1;
+      nz &= nz - 1;
+      m = mask[wi][lane];
+    }
+    bool has = m != 0u;
+    if (!__any_sync(0xffffffffu, has)) break;
+    if (has) {
+      int q1 = wi * 32 + __ffs(m) - 1;
+      m &= m - 1;
+      int q2 = m ? wi * 32 + __ffs(m) - 1 : -1;
+      m &= m - 1;
+      body(q1, q2);
+    }
+  }
+}
 // MUFU.RSQ without the denormal fix-up rsqrtf() wraps around it (inputs here
 // are >= 1e-30, normal in FP32)
 __device__ __forceinline__ float rsqrt_ftz(float x) {
@@ -314,7 +339,12 @@ int kid_selects_gas(int kid);
 constexpr int kGravTableN = 128;            // GT_R / GT_T intervals over [0, r_cut]
 constexpr int kGravTableRMax = kGravTableN + 2;
 constexpr int kGravSoftBitsMax = 5;         // GT_SOFT: 2^jbits intervals per octave of soft
-constexpr int kGravSoftBitsDefault = 4;
+// 32 intervals per octave (cubic fit error ~2e-8 relative; 16 per octave leave
+// ~3e-7, which near-cancelling dark-matter lattices amplify past the 1e-5
+// relative gate).  The twice larger table runs in 16-warp CTAs so residency
+// stays at 32 warps per SM: 10.13 vs 10.04 ms at c2 (HB_GRAV_JBITS=4 selects
+// the coarser table).
+constexpr int kGravSoftBitsDefault = 5;
 constexpr int kGravSoftOctaves = 40;
 constexpr int kGravTableMax = (kGravSoftOctaves + 1) * (1 << kGravSoftBitsMax) + 2;
 constexpr bool kGravitySoftTable = true;    // gravity_mode 0/1/4 use GT_SOFT

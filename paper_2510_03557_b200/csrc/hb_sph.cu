@@ -21,19 +21,21 @@ namespace hb {
 
 constexpr int kSphWarps = 4;
 constexpr int kStageA = 256;  // pass A staged sources per warp (8 mask words per lane)
-constexpr int kStageB = 192;  // pass B (3 records per source)
 
 struct SphDev {
   Tiling T;
   const int64_t* ent_ptr;
   const int32_t* ent_src;
   const int32_t* ent_code;
-  const float4 *P0, *P1, *P2;  // (x,y,z,m) (vx,vy,vz,h) (P/rho^2, c_s, rho, sigma/h^5)
+  const float4 *P0, *P1, *P2, *P3;  // layouts: k_pack_sph
   const double* state;         // exact predicate re-checks (float64 rows)
   const int8_t* pshift;
   double L, reach;
   float reach2, band, alpha, beta;
   double *ncount, *rho, *moments, *hydro;
+  const double *crk_A, *crk_B;
+  const uint8_t* crk_fallback;
+  double *gradA, *gradB;
   unsigned long long* err_key;
   const uint8_t* skip_leaf;  // pass B: ghost-only receivers to skip (or null)
   int skip_tiles;            // pass B: skip tiles without an owned member
@@ -61,7 +63,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 // staging shared by both passes: walks the receiver's entries, culls source
 // tiles and sources against the target box, calls consume() when the stage
-// would overflow and at the end.
+// would overflow and at the end.  (A two-phase variant -- tile candidates
+// collected into a per-warp list, then drained with the next tile's records
+// prefetched into registers -- measured slower at c2: pass A 1.535 -> 1.563
+// ms, pass B 2.84 -> 2.97 ms with spills at pass B's register budget.)
 template <int NP, bool HYDRO, int CAP, class Consume>
 __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, int64_t e1,
                                           float4 tlo, float4 thi, float hmax_t, float Rcap,
@@ -71,6 +76,9 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
   int lane = threadIdx.x & 31;
   double oA0 = T.origin[3 * A], oA1 = T.origin[3 * A + 1], oA2 = T.origin[3 * A + 2];
   float Rt = fminf(Rcap, 2.0f * hmax_t * 1.0001f);
+  // pass B: support radius^2 of the pair (i, j) is 4 max(h_i, h_j)^2 (h_j:
+  // the source record's P0.w)
+  float Rt2 = Rt * Rt, Rcap2 = Rcap * Rcap;
   for (int64_t e = e0; e < e1; ++e) {
     int B = a.ent_src[e];
     if (B < 0) continue;  // bin stencil: off-mesh / duplicate cell
@@ -106,11 +114,11 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
           if (NP > 1) sj[1] = a.P1[k_j];
           if (NP > 2) sj[2] = a.P2[k_j];
           sj[0].x -= D0; sj[0].y -= D1; sj[0].z -= D2;
-          float R = HYDRO ? fminf(Rcap, 2.0f * fmaxf(hmax_t, sj[0].w) * 1.0001f) : Rt;
+          float R2 = HYDRO ? fminf(Rcap2, fmaxf(Rt2, 4.0008f * sj[0].w * sj[0].w)) : Rt2;
           float gx = fmaxf(fmaxf(tlo.x - sj[0].x, sj[0].x - thi.x), 0.0f);
           float gy = fmaxf(fmaxf(tlo.y - sj[0].y, sj[0].y - thi.y), 0.0f);
           float gz = fmaxf(fmaxf(tlo.z - sj[0].z, sj[0].z - thi.z), 0.0f);
-          ok = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) <= R * R;
+          ok = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) <= R2;
         }
         unsigned sm = __ballot_sync(0xffffffffu, ok);
         if (cnt + 32 > CAP) consume();
@@ -148,11 +156,8 @@ __device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, fl
       float4 s = stage[w * 32 + b][0];
       float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      float thr = thr_i;
-      if (HYDRO) {
-        float hm = fmaxf(hi, s.w);
-        thr = fminf(reach2c, 4.0f * hm * hm * 1.0002f);
-      }
+      float thr = thr_i;  // pass B: thr_i = 4 h_i^2 (1 + 2e-4), s.w = h_j
+      if (HYDRO) thr = fminf(reach2c, fmaxf(thr_i, 4.0008f * s.w * s.w));
       bits |= (r2 <= thr ? 1u : 0u) << b;
     }
     mask[w][lane] = bits;
@@ -184,8 +189,8 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   float hinv = h > 0.0f ? 1.0f / h : 0.0f;
   double h64 = a.state[row_i * NCOL + C_H];
   double thr4_64 = __dmul_rn(__dmul_rn(4.0, h64), h64);   // (4 h) h as hb/kernels.py:191
-  double reach2_64 = __dmul_rn(a.reach, a.reach);
   float thr4 = (float)thr4_64;
+  float thr4b = thr4 * a.band;
   float thr_mask = fminf(a.reach2, thr4) * (1.0f + 2.0f * a.band);
   float4 tlo = a.T.tile_lo[t], thi = a.T.tile_hi[t];
   float rho = 0.0f;
@@ -197,24 +202,28 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   auto consume = [&]() {
     __syncwarp();
     unsigned nz = build_masks<1, false>(stage, cnt, ti0, h, live ? thr_mask : -1.0f, 0.0f, mask);
-    walk_masks(mask, nz, [&](int q) {
+    // two pairs per iteration (walk_masks2): independent chains for ILP
+    auto pair = [&](int q, bool on) {
       float4 s = stage[q][0];
       float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      bool in = r2 <= a.reach2, c4 = r2 <= thr4;
-      bool near_r = fabsf(r2 - a.reach2) <= a.reach2 * a.band;
-      bool near_h = fabsf(r2 - thr4) <= thr4 * a.band;
-      if (near_r || near_h) {  // exact float64 decision, reference expression
+      // 4 h_i^2 <= reach^2 = (2 h_max)^2 exactly, so c4 implies the reach
+      // test, and W(r, h_i) vanishes past 2 h_i: only the count's predicate
+      // needs the float64 decision near its threshold
+      bool c4 = r2 <= thr4;
+      if (on && fabsf(r2 - thr4) <= thr4b) {  // exact float64 decision, reference expression
         int2 mt = meta[q];
         double e2 = exact_r2_rows(a.state, a.pshift, a.L, row_i, T.tperm[mt.x], mt.y & 31);
-        in = e2 <= reach2_64;
         c4 = e2 <= thr4_64;
       }
-      if (in) {
-        count += c4 ? 1u : 0u;
-        float qq = r2 * rsqrt_ftz(fmaxf(r2, 1e-30f)) * hinv;  // MUFU.RSQ, no IEEE sqrt fix-up
-        rho = fmaf(s.w, w_body(qq), rho);
-      }
+      float qq = r2 * rsqrt_ftz(fmaxf(r2, 1e-30f)) * hinv;  // MUFU.RSQ, no IEEE sqrt fix-up
+      count += (on && c4) ? 1u : 0u;
+      return on ? s.w * w_body(qq) : 0.0f;
+    };
+    walk_masks2(mask, nz, [&](int q1, int q2) {
+      float w1 = pair(q1, true);
+      float w2 = pair(q2 >= 0 ? q2 : q1, q2 >= 0);
+      rho += w1 + w2;
     });
     __syncwarp();
     cnt = 0;
@@ -222,8 +231,7 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   // cull radius from the tile's largest h (k_tile_boxes: tile_lo.w), not this
   // lane's: every lane culls sources for the whole tile
   sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
-                               cnt,
-                               consume);
+                               cnt, consume);
   if (live) {
     float norm3 = h > 0.0f ? kSigma * hinv * hinv * hinv : 0.0f;
     a.ncount[row_i] += (double)count;
@@ -232,8 +240,15 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
 }
 
 // ---------------------------------------------------------------- pass B
-// 5 CTAs / SM (<= 102 registers, no spills): 2.90 -> 2.82 ms at c2 vs the
-// compiler's 113-register choice (4 CTAs)
+// records (k_pack_sph layout 1): P0 = (x, y, z, h), P1 = (vx, vy, vz, m),
+// P2 = (P/rho^2, c_s, rho, sigma/h^5).  1/q = h r^-1 reuses the rsqrt the
+// separation needs: a pair issues 3 MUFU (rsqrt, 1/h_j, 1/rho_j), two more on
+// the approaching-pair viscosity branch.  (A fourth record with 1/h_j and
+// m_j/rho_j precomputed, and 160-source stages to stay at 4 CTAs / SM, measured
+// 3.32 vs 2.83 ms at c2: staging and flush count outweigh the two MUFU.)
+// 5 CTAs / SM (<= 102 registers, no spills; 2.90 -> 2.82 ms at c2 against the
+// compiler's 4-CTA choice in round 1).
+constexpr int kStageB = 192;
 __global__ void __launch_bounds__(kSphWarps * 32, 5)
 k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   __shared__ float4 s_stage[kSphWarps][kStageB][3];
@@ -251,10 +266,10 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   int n_t = T.tile_n[t];
   bool live = lane < n_t;
   int k_i = T.tile_start[t] + (live ? lane : 0);
-  // records: P0 = (x, y, z, h), P1 = (vx, vy, vz, m), P2 = (P/rho^2, c_s, rho, sigma/h^5)
   float4 ti0 = a.P0[k_i], ti1 = a.P1[k_i], ti2 = a.P2[k_i];
   float hi = ti0.w;
   float hinv = hi > 0.0f ? 1.0f / hi : 0.0f;
+  float thr_i = 4.0008f * hi * hi;
   float reach2c = a.reach2 * (1.0f + 2.0f * a.band);
   float4 tlo = a.T.tile_lo[t], thi = a.T.tile_hi[t];
   float mo[10];
@@ -267,29 +282,35 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   unsigned(*mask)[32] = s_mask[wid];
   auto consume = [&]() {
     __syncwarp();
-    unsigned nz =
-        build_masks<3, true>(stage, cnt, ti0, live ? hi : -1.0f, 0.0f, live ? reach2c : -1.0f, mask);
+    unsigned nz = build_masks<3, true>(stage, cnt, ti0, hi, live ? thr_i : -1.0f,
+                                       live ? reach2c : -1.0f, mask);
     walk_masks(mask, nz, [&](int q) {
       float4 s0 = stage[q][0], s1 = stage[q][1], s2 = stage[q][2];
+      float hj = s0.w;
       float dx = ti0.x - s0.x, dy = ti0.y - s0.y, dz = ti0.z - s0.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
       if (!(r2 <= a.reach2)) return;
       float rinv = rsqrt_ftz(fmaxf(r2, 1e-30f));
       float r = r2 * rinv;
+      // cubic spline at q_i (value and (dW/dr)/r, hb/kernels.py:71-93) and
+      // (dW/dr)/r at q_j; 1/q = h / r
+      float qi = r * hinv, qj = r * rcp_approx(hj);
+      float ui = 2.0f - qi, uj = 2.0f - qj;
+      float wi = qi < 1.0f ? fmaf(qi * qi, fmaf(0.75f, qi, -1.5f), 1.0f)
+                           : (qi < 2.0f ? 0.25f * ui * ui * ui : 0.0f);
+      float gi = qi < 1.0f ? fmaf(2.25f, qi, -3.0f)
+                           : (qi < 2.0f ? -0.75f * ui * ui * (hi * rinv) : 0.0f);
+      float gj = qj < 1.0f ? fmaf(2.25f, qj, -3.0f)
+                           : (qj < 2.0f ? -0.75f * uj * uj * (hj * rinv) : 0.0f);
       // CRK moments: w = V_j W(r, h_i) (hb/kernels.py:205-220)
-      float qi = r * hinv;
-      float mj = s1.w;
-      float vj = s2.z > 0.0f ? mj * rcp_approx(s2.z) : 0.0f;
-      float wk = vj * w_body(qi);
+      float wk = (s2.z > 0.0f ? s1.w * rcp_approx(s2.z) : 0.0f) * wi;
       float wx = wk * dx, wy = wk * dy, wz = wk * dz;
       mo[0] += wk;
       mo[1] -= wx; mo[2] -= wy; mo[3] -= wz;
       mo[4] = fmaf(wx, dx, mo[4]); mo[5] = fmaf(wx, dy, mo[5]); mo[6] = fmaf(wx, dz, mo[6]);
       mo[7] = fmaf(wy, dy, mo[7]); mo[8] = fmaf(wy, dz, mo[8]); mo[9] = fmaf(wz, dz, mo[9]);
       // hydro (hb/kernels.py:227-258), m_i factored out
-      float hj = s0.w;
-      float qj = r * rcp_approx(hj);
-      float gw = 0.5f * (gradw_body(qi) * ti2.w + gradw_body(qj) * s2.w);
+      float gw = 0.5f * fmaf(gi, ti2.w, gj * s2.w);
       float vx = ti1.x - s1.x, vy = ti1.y - s1.y, vz = ti1.z - s1.z;
       float vdotr = fmaf(vz, dz, fmaf(vy, dy, vx * dx));
       float visc = 0.0f;
@@ -300,18 +321,19 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
         float mu = hbar * vdotr * rcp_approx(fmaf(0.01f * hbar, hbar, r2));
         visc = fmaf(a.beta * mu, mu, -(a.alpha * cbar * mu)) * rcp_approx(rhobar);
       }
-      float w = mj * (ti2.x + s2.x + visc) * gw;
+      float mjg = s1.w * gw;
+      float w = (ti2.x + s2.x + visc) * mjg;
       fx = fmaf(-w, dx, fx); fy = fmaf(-w, dy, fy); fz = fmaf(-w, dz, fz);
-      float work = mj * vdotr * gw;
-      ei = fmaf(fmaf(0.5f, visc, ti2.x), work, ei);
-      ej = fmaf(fmaf(0.5f, visc, s2.x), work, ej);
+      float work = vdotr * mjg;
+      float hv = 0.5f * visc;
+      ei = fmaf(ti2.x + hv, work, ei);
+      ej = fmaf(s2.x + hv, work, ej);
     });
     __syncwarp();
     cnt = 0;
   };
   sph_sweep<3, true, kStageB>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
-                              cnt,
-                              consume);
+                              cnt, consume);
   bool bad = !(isfinite(fx) && isfinite(fy) && isfinite(fz) && isfinite(ei) && isfinite(mo[0]));
   if (__ballot_sync(0xffffffffu, live && bad)) {
     if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e0 * 4 + 1));
@@ -330,12 +352,170 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   }
 }
 
+// ---------------------------------------------------------------- pass C
+// gradA / gradB of the CRK coefficients (north star; the reference computes
+// only A and B, hb/hydro.py:99-150).  With G = V_j (dW/dr)/r at h_i and
+// dr = x_i - x_j, the gradient moments are sum G dr (3), sum G dr dr (6) and
+// sum G dr dr dr (10) over gas-gas pairs within 2 h_i -- the compat path's
+// KID_CRK_GRAD1/2 channels (hb_pairs.cuh).  The epilogue solves, in float64
+// per target lane, from the pass-B moments and the CRK solve's A, B:
+//   d_g m0 = S1_g;  d_g m1_a = -S2_ag - delta_ag m0;
+//   d_g m2_ab = S3_abg - delta_ag m1_b - delta_bg m1_a;
+//   d_g B = m2^-1 (d_g m1 - d_g m2 B);  d_g A = -A^2 (d_g m0 - d_g B.m1 - B.d_g m1);
+//   fallback rows (A = 1/m0, B = 0): d_g A = -d_g m0 / m0^2, d_g B = 0
+// (hydro.crk_gradients_from_moments is the same algebra on the compat path).
+__device__ __forceinline__ void crk_grad_solve(const double* mom, double A, const double* B,
+                                               bool fb, const double* S1, const double* S2v,
+                                               const double* S3v, double* dA, double* dB) {
+  double m0 = mom[0];
+  double m1[3] = {mom[1], mom[2], mom[3]};
+  for (int k = 0; k < 3; ++k) dA[k] = 0.0;
+  for (int k = 0; k < 9; ++k) dB[k] = 0.0;
+  if (!(m0 > 0.0)) return;
+  if (fb) {
+    for (int g = 0; g < 3; ++g) dA[g] = -S1[g] / (m0 * m0);
+    return;
+  }
+  // symmetric tensors from the packed channels
+  const int i2[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+  double S2[3][3];
+  for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) S2[a][b] = S2v[i2[a][b]];
+  // S3 channel order (KID_CRK_GRAD2): xxx xxy xxz xyy xyz xzz yyy yyz yzz zzz
+  auto s3 = [&](int a, int b, int c) -> double {
+    int n[3] = {0, 0, 0};
+    n[a]++; n[b]++; n[c]++;
+    int x = n[0], y = n[1];
+    if (x == 3) return S3v[0];
+    if (x == 2) return y == 1 ? S3v[1] : S3v[2];
+    if (x == 1) return y == 2 ? S3v[3] : (y == 1 ? S3v[4] : S3v[5]);
+    return y == 3 ? S3v[6] : (y == 2 ? S3v[7] : (y == 1 ? S3v[8] : S3v[9]));
+  };
+  double dm1[3][3], rhs[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int g = 0; g < 3; ++g) dm1[a][g] = -S2[a][g] - (a == g ? m0 : 0.0);
+  for (int a = 0; a < 3; ++a)
+    for (int g = 0; g < 3; ++g) {
+      double t = dm1[a][g];
+      for (int b = 0; b < 3; ++b) {
+        double dm2 = s3(a, b, g) - (a == g ? m1[b] : 0.0) - (b == g ? m1[a] : 0.0);
+        t -= dm2 * B[b];
+      }
+      rhs[a][g] = t;
+    }
+  // m2 dB = rhs (Gaussian elimination with partial pivoting, 3 right-hand sides)
+  double m[3][6] = {{mom[4], mom[5], mom[6]}, {mom[5], mom[7], mom[8]}, {mom[6], mom[8], mom[9]}};
+  for (int r = 0; r < 3; ++r) for (int g = 0; g < 3; ++g) m[r][3 + g] = rhs[r][g];
+  for (int c = 0; c < 3; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < 3; ++r) if (fabs(m[r][c]) > fabs(m[piv][c])) piv = r;
+    if (piv != c) for (int k = 0; k < 6; ++k) { double t = m[c][k]; m[c][k] = m[piv][k]; m[piv][k] = t; }
+    for (int r = c + 1; r < 3; ++r) {
+      double f = m[r][c] / m[c][c];
+      for (int k = c; k < 6; ++k) m[r][k] -= f * m[c][k];
+    }
+  }
+  double X[3][3];
+  for (int g = 0; g < 3; ++g)
+    for (int r = 2; r >= 0; --r) {
+      double t = m[r][3 + g];
+      for (int k = r + 1; k < 3; ++k) t -= m[r][k] * X[k][g];
+      X[r][g] = t / m[r][r];
+    }
+  for (int a = 0; a < 3; ++a) for (int g = 0; g < 3; ++g) dB[3 * a + g] = X[a][g];
+  for (int g = 0; g < 3; ++g) {
+    double dD = S1[g];
+    for (int a = 0; a < 3; ++a) dD -= X[a][g] * m1[a] + B[a] * dm1[a][g];
+    dA[g] = -(A * A) * dD;
+  }
+}
+
+__global__ void __launch_bounds__(kSphWarps * 32, 4)
+k_sph_grad(SphDev a, const int64_t* n_tiles_dev) {
+  __shared__ float4 s_stage[kSphWarps][kStageA][1];
+  __shared__ int2 s_meta[kSphWarps][kStageA];
+  __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
+  if (t >= *n_tiles_dev) return;
+  const Tiling& T = a.T;
+  int A = T.tile_leaf[t];
+  if (a.skip_leaf && a.skip_leaf[A]) return;
+  if (a.skip_tiles && T.tile_skip[t]) return;
+  int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
+  if (e0 == e1) return;
+  int n_t = T.tile_n[t];
+  bool live = lane < n_t;
+  int k_i = T.tile_start[t] + (live ? lane : 0);
+  float4 ti0 = a.P0[k_i];
+  float h = a.P1[k_i].w;
+  float hinv = h > 0.0f ? 1.0f / h : 0.0f;
+  float thr_mask = fminf(a.reach2, 4.0f * h * h) * (1.0f + 2.0f * a.band);
+  float4 tlo = a.T.tile_lo[t], thi = a.T.tile_hi[t];
+  float g1[9], g2[10];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) g1[c] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 10; ++c) g2[c] = 0.0f;
+  int cnt = 0;
+  float4(*stage)[1] = s_stage[wid];
+  int2* meta = s_meta[wid];
+  unsigned(*mask)[32] = s_mask[wid];
+  auto consume = [&]() {
+    __syncwarp();
+    unsigned nz = build_masks<1, false>(stage, cnt, ti0, h, live ? thr_mask : -1.0f, 0.0f, mask);
+    walk_masks(mask, nz, [&](int q) {
+      float4 s = stage[q][0];
+      float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
+      float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      float rinv = rsqrt_ftz(fmaxf(r2, 1e-30f));
+      float qq = r2 * rinv * hinv;
+      float u = 2.0f - qq;
+      float gw = qq < 1.0f ? fmaf(2.25f, qq, -3.0f)
+                           : (qq < 2.0f ? -0.75f * u * u * (h * rinv) : 0.0f);
+      float g = s.w * gw;
+      float gx = g * dx, gy = g * dy, gz = g * dz;
+      g1[0] += gx; g1[1] += gy; g1[2] += gz;
+      g1[3] = fmaf(gx, dx, g1[3]); g1[4] = fmaf(gx, dy, g1[4]); g1[5] = fmaf(gx, dz, g1[5]);
+      g1[6] = fmaf(gy, dy, g1[6]); g1[7] = fmaf(gy, dz, g1[7]); g1[8] = fmaf(gz, dz, g1[8]);
+      float gxx = gx * dx, gyy = gy * dy, gzz = gz * dz, gxy = gx * dy;
+      g2[0] = fmaf(gxx, dx, g2[0]); g2[1] = fmaf(gxx, dy, g2[1]); g2[2] = fmaf(gxx, dz, g2[2]);
+      g2[3] = fmaf(gyy, dx, g2[3]); g2[4] = fmaf(gxy, dz, g2[4]); g2[5] = fmaf(gzz, dx, g2[5]);
+      g2[6] = fmaf(gyy, dy, g2[6]); g2[7] = fmaf(gyy, dz, g2[7]); g2[8] = fmaf(gzz, dy, g2[8]);
+      g2[9] = fmaf(gzz, dz, g2[9]);
+    });
+    __syncwarp();
+    cnt = 0;
+  };
+  sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
+                               cnt, consume);
+  bool bad = !(isfinite(g1[0]) && isfinite(g1[3]) && isfinite(g2[0]) && isfinite(g2[9]));
+  if (__ballot_sync(0xffffffffu, live && bad)) {
+    if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e0 * 4 + 1));
+    return;
+  }
+  if (!live) return;
+  int64_t row = T.tperm[k_i];
+  double norm5 = h > 0.0f ? (double)kSigma * pow((double)hinv, 5.0) : 0.0;
+  double S1[3], S2[6], S3[10];
+  for (int c = 0; c < 3; ++c) S1[c] = norm5 * (double)g1[c];
+  for (int c = 0; c < 6; ++c) S2[c] = norm5 * (double)g1[3 + c];
+  for (int c = 0; c < 10; ++c) S3[c] = norm5 * (double)g2[c];
+  double Bi[3] = {a.crk_B[3 * row], a.crk_B[3 * row + 1], a.crk_B[3 * row + 2]};
+  double dA[3], dB[9];
+  crk_grad_solve(a.moments + row * 10, a.crk_A[row], Bi, a.crk_fallback[row] != 0, S1, S2, S3,
+                 dA, dB);
+  for (int c = 0; c < 3; ++c) a.gradA[row * 3 + c] = dA[c];
+  for (int c = 0; c < 9; ++c) a.gradB[row * 9 + c] = dB[c];
+}
+
 // gas records for both passes
 // layout 0 (pass A): P0 = (x, y, z, m), P1 = (.., .., .., h)
-// layout 1 (pass B): P0 = (x, y, z, h), P1 = (vx, vy, vz, m), P2 = (P/rho^2, c_s, rho, sigma/h^5)
+// layout 2 (pass C): P0 = (x, y, z, V = m/rho), P1 = (.., .., .., h)
+// layout 1 (pass B): P0 = (x, y, z, h), P1 = (vx, vy, vz, m),
+//                    P2 = (P/rho^2, c_s, rho, sigma/h^5)
 __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tiling T,
                            const double* state, const int8_t* pshift, double L, float4* P0,
-                           float4* P1, float4* P2, int layout) {
+                           float4* P1, float4* P2, float4* P3, int layout) {
   int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (t >= *n_tiles_dev || lane >= T.tile_n[t]) return;
@@ -355,6 +535,9 @@ __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tilin
   if (layout == 0) {
     P0[k] = make_float4(c[0], c[1], c[2], (float)st[C_M]);
     P1[k] = make_float4(0.f, 0.f, 0.f, (float)h);
+  } else if (layout == 2) {
+    P0[k] = make_float4(c[0], c[1], c[2], rho > 0 ? (float)(st[C_M] / rho) : 0.0f);
+    P1[k] = make_float4(0.f, 0.f, 0.f, (float)h);
   } else {
     P0[k] = make_float4(c[0], c[1], c[2], (float)h);
     P1[k] = make_float4((float)st[C_VX], (float)st[C_VY], (float)st[C_VZ], (float)st[C_M]);
@@ -363,10 +546,10 @@ __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tilin
 }
 
 int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
-             double L, float4* P0, float4* P1, float4* P2, int layout, cudaStream_t st,
-             HbError* err) {
+             double L, float4* P0, float4* P1, float4* P2, float4* P3, int layout,
+             cudaStream_t st, HbError* err) {
   k_pack_sph<<<grid_for(T.n_tiles_cap * 32, 256), 256, 0, st>>>(T.n_tiles_cap, ntd, T, state,
-                                                                pshift, L, P0, P1, P2, layout);
+                                                                pshift, L, P0, P1, P2, P3, layout);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
@@ -374,16 +557,19 @@ int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int
 int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   SphDev a;
   a.T = *s.T; a.ent_ptr = s.ent_ptr; a.ent_src = s.ent_src; a.ent_code = s.ent_code;
-  a.P0 = s.P0; a.P1 = s.P1; a.P2 = s.P2; a.state = s.state; a.pshift = s.pshift;
+  a.P0 = s.P0; a.P1 = s.P1; a.P2 = s.P2; a.P3 = s.P3; a.state = s.state; a.pshift = s.pshift;
   a.L = s.L; a.reach = s.reach; a.reach2 = (float)(s.reach * s.reach); a.band = s.band;
   a.alpha = (float)s.alpha; a.beta = (float)s.beta;
   a.ncount = s.ncount; a.rho = s.rho; a.moments = s.moments; a.hydro = s.hydro;
+  a.crk_A = s.crk_A; a.crk_B = s.crk_B; a.crk_fallback = s.crk_fallback;
+  a.gradA = s.gradA; a.gradB = s.gradB;
   a.err_key = s.err_key;
   a.skip_leaf = s.skip_leaf;
   a.skip_tiles = s.skip_tiles;
   unsigned grid = grid_for(s.T->n_tiles_cap, kSphWarps);
   if (pass == 0) k_sph_density<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-  else k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  else if (pass == 1) k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  else k_sph_grad<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }

@@ -453,12 +453,12 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   double wmax = fmax(a->width[0], fmax(a->width[1], a->width[2]));
   double rmin = fmax(fmin(a->reach, 2.0 * a->h_min), 1e-300);
   float band = (float)fmax(64.0 * 5.9604644775390625e-08 * wmax / rmin, 9.5367431640625e-07);
-  SphArgs sa;
+  SphArgs sa{};
   sa.T = &w.Tg; sa.n_tiles_dev = w.ntg;
   sa.ent_ptr = sph_bins ? w.st_ptr : w.ent_ptr;
   sa.ent_src = sph_bins ? w.st_src : w.ent_src;
   sa.ent_code = sph_bins ? w.st_code : w.ent_code;
-  sa.P0 = w.P0; sa.P1 = w.P1; sa.P2 = w.P2; sa.state = w.state;
+  sa.P0 = w.P0; sa.P1 = w.P1; sa.P2 = w.P2; sa.P3 = nullptr; sa.state = w.state;
   sa.pshift = a->image_shift; sa.L = a->side_length; sa.reach = sph_reach; sa.band = band;
   sa.alpha = a->visc_alpha; sa.beta = a->visc_beta; sa.err_key = w.err_key;
   sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = mom; sa.hydro = a->hydro;
@@ -469,7 +469,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY)) {
     HB_CUDA_TRY(cudaMemsetAsync(a->ncount, 0, n * sizeof(double), st));
     HB_CUDA_TRY(cudaMemsetAsync(w.rho_new, 0, n * sizeof(double), st));
-    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, 0, st,
+    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, nullptr, 0, st,
                   err);
     if (rc) return rc;
     tm.kmark(2);
@@ -497,7 +497,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->passes & (HB_PASS_CRK | HB_PASS_HYDRO)) {
     HB_CUDA_TRY(cudaMemsetAsync(mom, 0, n * 10 * sizeof(double), st));
     HB_CUDA_TRY(cudaMemsetAsync(a->hydro, 0, n * 5 * sizeof(double), st));
-    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, 1, st,
+    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, nullptr, 1, st,
                   err);
     if (rc) return rc;
     tm.kmark(4);
@@ -513,6 +513,18 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     rc = crk_solve_rows(n, mom, 10, a->species, 1e8, a->crk_A, a->crk_B, a->crk_fallback,
                         w.Tg.tperm, w.Tg.sel_off + n_seg, st, err);
     if (rc) return rc;
+    // 6. optional pass C: gradA / gradB (HB_PASS_CRK_GRAD), on the solved A, B
+    if ((a->passes & HB_PASS_CRK_GRAD) && a->crk_gradA && a->crk_gradB) {
+      HB_CUDA_TRY(cudaMemsetAsync(a->crk_gradA, 0, n * 3 * sizeof(double), st));
+      HB_CUDA_TRY(cudaMemsetAsync(a->crk_gradB, 0, n * 9 * sizeof(double), st));
+      rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2,
+                    nullptr, 2, st, err);
+      if (rc) return rc;
+      sa.crk_A = a->crk_A; sa.crk_B = a->crk_B; sa.crk_fallback = a->crk_fallback;
+      sa.gradA = a->crk_gradA; sa.gradB = a->crk_gradB;
+      rc = launch_sph(2, sa, st, err);
+      if (rc) return rc;
+    }
   }
   if (zero_ghost_sph && !a->ghost_density && (a->passes & HB_PASS_NCOUNT)) {
     rc = zero_rows(a->ncount, nullptr, nullptr, nullptr);

@@ -28,6 +28,7 @@ from .particles import FIELD_SPECS, ParticleSet
 PASS_NCOUNT, PASS_DENSITY, PASS_CRK, PASS_GRAVITY, PASS_HYDRO = 1, 2, 4, 8, 16
 PASS_ALL = 31
 PASS_COUNT_ONLY = 32   # with PASS_GRAVITY: exact in-r_cut source counts, no forces (hb.h)
+PASS_CRK_GRAD = 64     # with PASS_CRK: gradA / gradB into out["crk_gradA"], out["crk_gradB"]
 PHASES = ("build", "list", "tiling", "sph_density", "sph_force", "gravity", "tail", "total")
 KERNELS = ("k_gravity", "k_sph_density", "k_sph_force")  # single-kernel spans (ms_kernel)
 
@@ -56,7 +57,7 @@ class HbStepArgs(C.Structure):
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
                    ("ms_phase", C.c_float * 8), ("status_out", P), ("ms_kernel", C.c_float * 4),
                    ("crk_moments_out", P), ("grav_half_event", P),
-                   ("grav_split_row", C.c_int64)])
+                   ("grav_split_row", C.c_int64), ("crk_gradA", P), ("crk_gradB", P)])
 
 
 def _bind(lib):
@@ -106,7 +107,8 @@ class ResidentRank:
 
     def __init__(self, particles: ParticleSet | None, cfg: StepConfig, fields: dict | None = None,
                  ghost_density: bool = False, h_range: tuple | None = None,
-                 owned_targets: bool = False, gravity_only: bool = False):
+                 owned_targets: bool = False, gravity_only: bool = False,
+                 crk_gradients: bool = False):
         """Either host ``particles`` or device ``fields`` (dict of STEP_FIELDS
         tensors).  ``h_range`` = (h_min_gas, h_max) when given as fields.
         ``owned_targets``: gravity / CRK / hydro outputs are needed for owned
@@ -132,6 +134,8 @@ class ResidentRank:
         # gravity-only ranks (PASS_GRAVITY, e.g. the dark-matter configs) keep
         # no SPH output buffers
         self.gravity_only = gravity_only
+        # gradA / gradB outputs (96 B per row) only when asked for
+        self.crk_gradients = crk_gradients and not gravity_only
         if particles is not None:
             gas = particles.species == 1
             h_range = ((float(particles.smoothing[gas].min()), float(particles.smoothing.max()))
@@ -164,6 +168,11 @@ class ResidentRank:
                     "crk_A": torch.zeros(cap, dtype=f64, device="cuda"),
                     "crk_B": torch.zeros((cap, 3), dtype=f64, device="cuda"),
                     "crk_fallback": torch.zeros(cap, dtype=torch.uint8, device="cuda"),
+                })
+            if sph and self.crk_gradients:
+                self._out_store.update({
+                    "crk_gradA": torch.zeros((cap, 3), dtype=f64, device="cuda"),
+                    "crk_gradB": torch.zeros((cap, 3, 3), dtype=f64, device="cuda"),
                 })
             self._cap = cap
         self.buf[0] = fields
@@ -237,8 +246,12 @@ class ResidentRank:
         a.status_out = P(status.data_ptr()) if status is not None and not timing else P(0)
         if self.gravity_only and passes & ~(PASS_GRAVITY | PASS_COUNT_ONLY):
             raise HydroboxError("gravity-only rank: SPH passes requested")
-        for k in ("perm", "ncount", "grav", "hydro", "crk_A", "crk_B", "crk_fallback"):
+        for k in ("perm", "ncount", "grav", "hydro", "crk_A", "crk_B", "crk_fallback",
+                  "crk_gradA", "crk_gradB"):
             setattr(a, k, N.ptr(self.out[k]) if k in self.out else P(0))
+        if passes & PASS_CRK_GRAD and not (passes & PASS_CRK and "crk_gradA" in self.out):
+            raise HydroboxError("PASS_CRK_GRAD needs PASS_CRK and a rank built with "
+                                "crk_gradients=True")
         a.crk_moments = P(0)   # moments live in the workspace (include/hb.h)
         for d in range(3):
             if a.reach > self.width[d] and self.nb[d] > 3:
