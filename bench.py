@@ -49,11 +49,17 @@ CONFIGS = {
                               "at 2/4/8 B200"),
     "c5": (1024, 0.05, "dm", "gravity-only 1024^3 dark-matter particles, short-range PP kernel "
                              "sweep (>= 4 B200)"),
+    # stress variant of configs[2]: the reference's own clumped
+    # generator (hb/ic.py:137-169, 70% of the particles in 8 Gaussian clumps of
+    # sigma L/40), sigma_psi unused; GPU arm only (the CPU reference needs hours)
+    "c3k": (128, None, "both", "2x128^3 particles, clustered (hb/ic.py make_clustered_ic): "
+                               "neighbour-count imbalance stress case, single B200"),
 }
 DEVICE_IC_ABOVE = 1 << 29   # particles: displacement field built on the GPU (numpy: ~60 GB/rank)
 # default workload at every GPU count (see the module docstring)
 DEFAULT_CONFIG = "c4"
-SUBBOX_ABOVE = 40_000_000   # CPU samples above this size use an interior sub-box
+SUBBOX_ABOVE = 40_000_000
+ZELDOVICH_SEED_CLUSTERED = 3   # CPU samples above this size use an interior sub-box
 
 
 def peaks():
@@ -193,7 +199,12 @@ def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = Fa
             select = lambda pos: owner_ranks_torch(pos, box, grid) == rank  # noqa: E731
         else:
             select = lambda pos: owner_ranks(pos, box, grid) == rank  # noqa: E731
-    if on_device:
+    if sigma is None:   # the reference's clustered generator
+        from paper_2510_03557_b200.ic import make_clustered_ic
+        if select is not None:
+            raise ValueError(f"{cfg_name}: the clustered generator is built whole")
+        p = make_clustered_ic(npd, box, seed=ZELDOVICH_SEED_CLUSTERED)
+    elif on_device:
         if select is None:
             raise ValueError(f"{cfg_name} is built per rank or per region only (--gpus >= 4)")
         p = make_zeldovich_ic_device(npd, box, sigma, select, species=species)
@@ -221,7 +232,8 @@ def make_workload(cfg_name: str, rank: int = 0, world: int = 1, local: bool = Fa
             "r_s": "d", "r_cut": "5 d", "softening": "L/N^(1/3)/50", "max_leaf_size": 256,
             "mesh": "bare periodic box, bin width max(4 PM cells, reach)",
             "bins_per_axis": int(np.floor(1.0 / bin_width)),
-            "ic": "Zel'dovich, seed 2510035570, P(k)~k^-2 exp(-(kd)^2)",
+            "ic": ("Zel'dovich, seed 2510035570, P(k)~k^-2 exp(-(kd)^2)" if sigma is not None
+                   else f"make_clustered_ic(seed={ZELDOVICH_SEED_CLUSTERED})"),
             "l2": "working set > 126 MB L2 (no flush needed)"}
     return p, cfg, meta
 
@@ -353,6 +365,12 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     species = CONFIGS[args.config][2]
+    if CONFIGS[args.config][1] is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"{args.config}: clump size is a fixed fraction of the box, so no "
+                          "bounded replica carries the per-particle work, and the whole set "
+                          "needs hours on the host"}), flush=True)
+        return 0
     npd = getattr(args, "cpu_npd", None) or CPU_SAMPLE_NPD[species]
     p, cfg, meta, bounds, desc = reference_sample(args.config, npd)
     gonly = species == "dm"
@@ -616,7 +634,7 @@ def run_gpu_arm(args):
     roof["step_frac"] = roof["step_algorithmic_tflops"] / (peak * world)
     roof["kflop_per_update"] = step_flops / n_total / 1e3
     base = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and CONFIGS[args.config][1] is not None:
         # one complete reference step on a bounded replica of this workload
         # (~10 s on the host cores), after the GPU timings
         q, qcfg, _, _, desc = reference_sample(args.config, CPU_BASELINE_NPD[species_c])
