@@ -68,14 +68,39 @@ __global__ void k_crk_solve(int64_t n, const double* mom, int64_t stride, const 
   bool fb = false;
   if (species[i] == 1 && m0 > 0.0) {
     double m2[3][3] = {{v[4], v[5], v[6]}, {v[5], v[7], v[8]}, {v[6], v[8], v[9]}};
-    double e[3][3];
-    for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) e[r][c] = m2[r][c];
-    double ev[3];
-    jacobi_eig3(e, ev);
-    double smax = fmax(fabs(ev[0]), fmax(fabs(ev[1]), fabs(ev[2])));
-    double smin = fmin(fabs(ev[0]), fmin(fabs(ev[1]), fabs(ev[2])));
-    double cond = smax / smin;  // inf (or nan) when singular
-    bool good = isfinite(cond) && cond < cond_limit;
+    // cond_2 <= cond_F = |m2|_F |m2^-1|_F: when that bound (with a margin far
+    // above the inverse's rounding, <= cond * 1e-16) clears the limit the
+    // reference's np.linalg.cond test passes too and the Jacobi eigenvalues
+    // are not needed; otherwise decide exactly as before.  (Lattice-like sets:
+    // cond_F ~ 3, so nearly every row takes the short path.)
+    double c00 = m2[1][1] * m2[2][2] - m2[1][2] * m2[2][1];
+    double c01 = m2[1][2] * m2[2][0] - m2[1][0] * m2[2][2];
+    double c02 = m2[1][0] * m2[2][1] - m2[1][1] * m2[2][0];
+    double det = m2[0][0] * c00 + m2[0][1] * c01 + m2[0][2] * c02;
+    double c11 = m2[0][0] * m2[2][2] - m2[0][2] * m2[2][0];
+    double c12 = m2[0][1] * m2[2][0] - m2[0][0] * m2[2][1];
+    double c22 = m2[0][0] * m2[1][1] - m2[0][1] * m2[1][0];
+    double c10 = m2[0][2] * m2[2][1] - m2[0][1] * m2[2][2];
+    double c20 = m2[0][1] * m2[1][2] - m2[0][2] * m2[1][1];
+    double c21 = m2[0][2] * m2[1][0] - m2[0][0] * m2[1][2];
+    double na = 0.0, ni = 0.0;
+    for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) na += m2[r][c] * m2[r][c];
+    ni = c00 * c00 + c01 * c01 + c02 * c02 + c10 * c10 + c11 * c11 + c12 * c12 + c20 * c20 +
+         c21 * c21 + c22 * c22;
+    double cond_f = sqrt(na) * sqrt(ni) / fabs(det);
+    bool good;
+    if (isfinite(cond_f) && cond_f * (1.0 + 1e-6) < cond_limit) {
+      good = true;
+    } else {
+      double e[3][3];
+      for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) e[r][c] = m2[r][c];
+      double ev[3];
+      jacobi_eig3(e, ev);
+      double smax = fmax(fabs(ev[0]), fmax(fabs(ev[1]), fabs(ev[2])));
+      double smin = fmin(fabs(ev[0]), fmin(fabs(ev[1]), fabs(ev[2])));
+      double cond = smax / smin;  // inf (or nan) when singular
+      good = isfinite(cond) && cond < cond_limit;
+    }
     if (good) {
       double m[3][4];
       for (int r = 0; r < 3; ++r) { for (int c = 0; c < 3; ++c) m[r][c] = m2[r][c]; m[r][3] = m1[r]; }

@@ -440,7 +440,10 @@ __global__ void k_tile_boxes(int64_t n_tiles, const int64_t* n_tiles_dev, Tiling
   unsigned ob = __ballot_sync(0xffffffffu, own);
   if (lane == 0) {
     T.tile_lo[t] = make_float4(lo[0], lo[1], lo[2], hm);
-    T.tile_hi[t] = make_float4(hi[0], hi[1], hi[2], 0.0f);
+    // .w carries the tile's first record index (int bits): the culling loops
+    // read it with the box, so a passing tile needs no dependent load of
+    // tile_start before its records
+    T.tile_hi[t] = make_float4(hi[0], hi[1], hi[2], __int_as_float(ks));
     T.tile_skip[t] = (ghost && ob == 0u) ? 1 : 0;
   }
 }
@@ -922,8 +925,11 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
     for (int64_t ub = u0; ub < u1; ub += 32) {
       int64_t u = ub + lane;
       bool pass = false;
+      int my_start = 0, my_n = 0;
       if (u < u1) {
         float4 lo = T.tile_lo[u], hi = T.tile_hi[u];
+        my_n = T.tile_n[u];
+        my_start = __float_as_int(hi.w);
         float gx = fmaxf(fmaxf((lo.x - D0) - thi.x, tlo.x - (hi.x - D0)), 0.0f);
         float gy = fmaxf(fmaxf((lo.y - D1) - thi.y, tlo.y - (hi.y - D1)), 0.0f);
         float gz = fmaxf(fmaxf((lo.z - D2) - thi.z, tlo.z - (hi.z - D2)), 0.0f);
@@ -933,12 +939,12 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
       while (tm) {
         int j = __ffs(tm) - 1;
         tm &= tm - 1;
-        int64_t uu = ub + j;
-        int n_u = T.tile_n[uu];
+        int n_u = __shfl_sync(0xffffffffu, my_n, j);
+        int s_u = __shfl_sync(0xffffffffu, my_start, j);
         bool ok = false;
         float4 sj;
         if (lane < n_u) {
-          sj = a.P0[T.tile_start[uu] + lane];
+          sj = a.P0[s_u + lane];
           sj.x -= D0; sj.y -= D1; sj.z -= D2;
           ok = box_gap2(sj.x, sj.y, sj.z, tlo, thi) <= R2;
         }

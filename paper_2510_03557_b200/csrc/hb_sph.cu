@@ -92,8 +92,11 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
     for (int64_t ub = u0; ub < u1; ub += 32) {
       int64_t u = ub + lane;
       bool pass = false;
+      int my_start = 0, my_n = 0;
       if (u < u1) {
         float4 lo = T.tile_lo[u], hi = T.tile_hi[u];
+        my_n = T.tile_n[u];
+        my_start = __float_as_int(hi.w);  // k_tile_boxes: first record index
         float R = HYDRO ? fminf(Rcap, 2.0f * fmaxf(hmax_t, lo.w) * 1.0001f) : Rt;
         float gx = fmaxf(fmaxf((lo.x - D0) - thi.x, tlo.x - (hi.x - D0)), 0.0f);
         float gy = fmaxf(fmaxf((lo.y - D1) - thi.y, tlo.y - (hi.y - D1)), 0.0f);
@@ -104,9 +107,8 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
       while (tm) {
         int j = __ffs(tm) - 1;
         tm &= tm - 1;
-        int64_t uu = ub + j;
-        int n_u = T.tile_n[uu];
-        int k_j = T.tile_start[uu] + lane;
+        int n_u = __shfl_sync(0xffffffffu, my_n, j);
+        int k_j = __shfl_sync(0xffffffffu, my_start, j) + lane;
         bool ok = false;
         float4 sj[NP];
         if (lane < n_u) {
