@@ -320,6 +320,13 @@ typedef struct HbStepArgs {
   int64_t grav_split_row;  /* out (host, set before the call returns)         */
   double* crk_gradA;  /* HB_PASS_CRK_GRAD: (n,3) d A / d x_i, or NULL          */
   double* crk_gradB;  /* HB_PASS_CRK_GRAD: (n,3,3) d B_a / d x_g, or NULL      */
+  void* last_fields_event; /* optional, with late_fields_event, for sets with
+                              no ghost rows (ghost == 0, ghost_src < 0
+                              everywhere): late_fields then covers only vel and
+                              internal_energy; density, global_id and ghost_src
+                              are first read after the step waits on this one,
+                              which happens after SPH pass B (the non-gas rows'
+                              density and the ids are outputs only)           */
 } HbStepArgs;
 
 size_t hb_force_step_workspace(int64_t n, const int64_t nb[3], int64_t max_leaf_size,

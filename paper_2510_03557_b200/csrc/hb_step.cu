@@ -27,9 +27,17 @@ __global__ void k_alias_sync(int64_t n, const int64_t* ghost_src, double* densit
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && ghost_src[i] >= 0) density[i] = density[ghost_src[i]];
 }
-__global__ void k_eos(int64_t n, const double* rho, const double* u, double gamma, double* st) {
+// gas_only: non-gas rows get P = c_s = 0 (their density lands later, with
+// HbStepArgs.last_fields_event; no pass reads a non-gas row's P or c_s)
+__global__ void k_eos(int64_t n, const double* rho, const double* u, double gamma, double* st,
+                      const uint8_t* gas_only) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (gas_only && gas_only[i] != 1) {
+    st[i * NCOL + C_P] = 0.0;
+    st[i * NCOL + C_CS] = 0.0;
+    return;
+  }
   double gm1 = gamma - 1.0;
   st[i * NCOL + C_RHO] = rho[i];
   st[i * NCOL + C_P] = gm1 * rho[i] * u[i];
@@ -79,24 +87,34 @@ struct FieldOut {
   int64_t* gid;
 };
 // late half of a split gather (HbStepArgs.late_fields_event): the fields SPH
-// pass A does not read, plus the state columns built from them
+// pass A does not read, plus the state columns built from them.  PART 0: all
+// of them; PART 1: vel, internal energy (the EOS and pass B need them);
+// PART 2: density of the non-gas rows (gas rows hold pass A's) and global id
+// (HbStepArgs.last_fields_event: needed only by the outputs)
+template <int PART>
 __global__ void k_gather_late(int64_t n, const int64_t* perm, FieldIn in, FieldOut out,
                               double* st) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int64_t r = perm[k];
   double* s = st + k * NCOL;
+  if (PART != 2) {
 #pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    double v = in.vel[3 * r + d];
-    out.vel[3 * k + d] = v;
-    s[C_VX + d] = v;
+    for (int d = 0; d < 3; ++d) {
+      double v = in.vel[3 * r + d];
+      out.vel[3 * k + d] = v;
+      s[C_VX + d] = v;
+    }
+    out.u[k] = in.u[r];
   }
-  out.u[k] = in.u[r];
-  out.gid[k] = in.gid[r];
-  double rho = in.rho[r];   // only non-gas rows keep it; gas rows get pass A's
-  out.rho[k] = rho;
-  s[C_RHO] = rho;
+  if (PART != 1) {
+    out.gid[k] = in.gid[r];
+    if (PART == 0 || out.species[k] != 1) {
+      double rho = in.rho[r];   // only non-gas rows keep it; gas rows get pass A's
+      out.rho[k] = rho;
+      s[C_RHO] = rho;
+    }
+  }
 }
 
 // LATE = true: skip the late fields (vel, u, density, ids) and P, c_s, which
@@ -325,6 +343,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->fields_ready_event)
     HB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a->fields_ready_event, 0));
   bool late_split = a->late_fields_event != nullptr;
+  // four upload groups (include/hb.h): density / ids / ghost sources last
+  bool last_split = late_split && a->last_fields_event != nullptr;
   // SPH passes size every cull from h_max; gravity-only steps read no h
   double h_lim = (a->passes & ~HB_PASS_GRAVITY) ? a->h_max * (1.0 + 1e-12) : INFINITY;
   HB_CUDA_TRY(cudaMemsetAsync(w.err_key, 0xff, sizeof(unsigned long long), st));
@@ -358,7 +378,31 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                   a->density_in, a->species_in, a->ghost_in, a->image_shift_in, a->global_id_in};
     FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
                    a->species, a->ghost, a->image_shift, a->global_id};
-    k_gather_late<<<g1, 256, 0, st>>>(n, a->perm, fi, fo, w.state);
+    if (last_split) {
+      k_gather_late<1><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, w.state);
+      HB_LAUNCH_CHECK();
+      return HB_OK;
+    }
+    k_gather_late<0><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, w.state);
+    if (a->ghost_src_in && a->ghost_src) {
+      k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
+      k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
+      HB_COUNT_LAUNCH(2);
+    }
+    HB_LAUNCH_CHECK();
+    return HB_OK;
+  };
+  // the last fields (density of non-gas rows, ids, ghost sources): outputs only
+  auto gather_last = [&]() -> int {
+    if (!last_split) return HB_OK;
+    last_split = false;
+    HB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a->last_fields_event, 0));
+    unsigned g1 = grid_for(n, 256);
+    FieldIn fi = {a->pos_in, a->vel_in, a->mass_in, a->smoothing_in, a->internal_energy_in,
+                  a->density_in, a->species_in, a->ghost_in, a->image_shift_in, a->global_id_in};
+    FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
+                   a->species, a->ghost, a->image_shift, a->global_id};
+    k_gather_late<2><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, w.state);
     if (a->ghost_src_in && a->ghost_src) {
       k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
       k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
@@ -483,13 +527,13 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     k_density_update<<<grid_for(nl * 32, 256), 256, 0, st>>>(
         nl, w.leaf_start, w.leaf_end, a->ghost_density ? w.no_ghost : w.ghost_only, a->species,
         w.rho_new, a->density);
-    if (a->ghost_src_in && a->ghost_src) {
+    if (a->ghost_src_in && a->ghost_src && !last_split) {
       k_alias_sync<<<grid_for(n, 256), 256, 0, st>>>(n, a->ghost_src, a->density);
       HB_COUNT_LAUNCH(1);
     }
     HB_COUNT_LAUNCH(1);
     k_eos<<<grid_for(n, 256), 256, 0, st>>>(n, a->density, a->internal_energy, a->eos_gamma,
-                                            w.state);
+                                            w.state, last_split ? a->species : nullptr);
     HB_LAUNCH_CHECK();
   }
   tm.mark(4);
@@ -530,6 +574,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     rc = zero_rows(a->ncount, nullptr, nullptr, nullptr);
     if (rc) return rc;
   }
+  rc = gather_last();  // before sph_done: the density output includes the non-gas rows
+  if (rc) return rc;
   // the SPH outputs are final here (ghost rows included): copies may start
   if (a->sph_done_event) HB_CUDA_TRY(cudaEventRecord((cudaEvent_t)a->sph_done_event, st));
   tm.mark(5);

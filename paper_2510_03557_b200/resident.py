@@ -57,7 +57,8 @@ class HbStepArgs(C.Structure):
                    ("n_entries", C.c_int64), ("list_capacity_needed", C.c_int64),
                    ("ms_phase", C.c_float * 8), ("status_out", P), ("ms_kernel", C.c_float * 4),
                    ("crk_moments_out", P), ("grav_half_event", P),
-                   ("grav_split_row", C.c_int64), ("crk_gradA", P), ("crk_gradB", P)])
+                   ("grav_split_row", C.c_int64), ("crk_gradA", P), ("crk_gradB", P),
+                   ("last_fields_event", P)])
 
 
 def _bind(lib):
@@ -208,12 +209,15 @@ class ResidentRank:
         return self.buf[self.cur]
 
     def step(self, passes: int = PASS_ALL, timing: bool = False, fields_ready=None,
-             sph_done=None, status=None, late_fields=None, grav_half=None) -> dict:
+             sph_done=None, status=None, late_fields=None, grav_half=None,
+             last_fields=None) -> dict:
         """One force evaluation; returns the device outputs (leaf order).
         fields_ready / sph_done: optional torch.cuda.Event for copy overlap
         (see HbStepArgs in include/hb.h); late_fields: event after which vel,
         internal_energy, density, global_id and ghost_src are ready (read only from
-        the EOS on; fields_ready then covers the rest).  status: optional zeroed pinned
+        the EOS on; fields_ready then covers the rest); last_fields (with
+        late_fields, sets without ghost rows only): density, global_id and
+        ghost_src are ready, late_fields then covering vel and internal_energy.  status: optional zeroed pinned
         int64[3] tensor; when given (and timing is off) the step returns
         without its final synchronisation and the caller must synchronise the
         stream and call check_status(status) before trusting the outputs."""
@@ -242,6 +246,7 @@ class ResidentRank:
         a.fields_ready_event = _event_handle(fields_ready)
         a.sph_done_event = _event_handle(sph_done)
         a.late_fields_event = _event_handle(late_fields)
+        a.last_fields_event = _event_handle(last_fields) if late_fields is not None else P(0)
         a.grav_half_event = _event_handle(grav_half)
         a.status_out = P(status.data_ptr()) if status is not None and not timing else P(0)
         if self.gravity_only and passes & ~(PASS_GRAVITY | PASS_COUNT_ONLY):
@@ -324,13 +329,21 @@ class HostStepper:
     FIRST = ("pos", "image_shift", "ghost")                  # the mesh build
     EARLY = ("mass", "smoothing", "species")                     # + SPH pass A
     LATE = ("vel", "internal_energy", "density", "global_id", "ghost_src")  # EOS on
+    # sets without ghost rows: only vel / internal_energy gate the EOS and
+    # pass B; density (non-gas rows), ids and ghost sources are outputs only
+    # and land while pass B runs (HbStepArgs.last_fields_event)
+    LATE4 = ("vel", "internal_energy")
+    LAST4 = ("density", "global_id", "ghost_src")
 
     def __init__(self, rank: "ResidentRank", pinned_in: dict, pinned_out: dict,
                  passes: int = PASS_ALL):
         torch = N.torch_cuda()
         self.passes = int(passes)
         assert sorted(self.FIRST + self.EARLY + self.LATE) == sorted(STEP_FIELDS)
+        assert sorted(self.LATE4 + self.LAST4) == sorted(self.LATE)
         self.rank, self.pin_in, self.pin_out = rank, pinned_in, pinned_out
+        self.four_groups = bool(not pinned_in["ghost"].any().item()
+                                and not (pinned_in["ghost_src"] >= 0).any().item())
         self.s_in = torch.cuda.Stream()
         self.s_out = torch.cuda.Stream()
         self.ev_first = torch.cuda.Event()
@@ -338,10 +351,11 @@ class HostStepper:
         self.ev_sph = torch.cuda.Event()
         self.ev_done = torch.cuda.Event()
         self.ev_late = torch.cuda.Event()
+        self.ev_last = torch.cuda.Event()
         self.ev_ghalf = torch.cuda.Event()
         self.status = torch.zeros(3, dtype=torch.int64, pin_memory=True)
         for ev in (self.ev_first, self.ev_fields, self.ev_sph, self.ev_done, self.ev_late,
-                   self.ev_ghalf):
+                   self.ev_last, self.ev_ghalf):
             ev.record()   # materialise the CUDA events (torch creates them lazily)
 
     def __call__(self):
@@ -357,13 +371,18 @@ class HostStepper:
             for f in self.EARLY:
                 dst[f].copy_(self.pin_in[f], non_blocking=True)
             self.ev_fields.record(self.s_in)
-            for f in self.LATE:
+            for f in (self.LATE4 if self.four_groups else self.LATE):
                 dst[f].copy_(self.pin_in[f], non_blocking=True)
             self.ev_late.record(self.s_in)
+            if self.four_groups:
+                for f in self.LAST4:
+                    dst[f].copy_(self.pin_in[f], non_blocking=True)
+                self.ev_last.record(self.s_in)
         main.wait_event(self.ev_first)
         self.status.zero_()   # no copy into it is pending: every call ends synchronised
         out = rk.step(self.passes, fields_ready=self.ev_fields, sph_done=self.ev_sph,
-                      status=self.status, late_fields=self.ev_late, grav_half=self.ev_ghalf)
+                      status=self.status, late_fields=self.ev_late, grav_half=self.ev_ghalf,
+                      last_fields=self.ev_last if self.four_groups else None)
         split = rk.last["grav_split_row"]
         self.ev_done.record(main)
         with torch.cuda.stream(self.s_out):

@@ -396,3 +396,38 @@ def test_gpu_resident_nonfinite_raises_sync_and_deferred(golden):
     pin_out["density"] = torch.empty(rk.n, dtype=torch.float64).pin_memory()
     with pytest.raises(HydroboxError):
         HostStepper(rk, pin_in, pin_out)()
+
+
+def test_gpu_host_stepper_four_groups_matches_sync_step():
+    """A set without ghost rows takes HostStepper's four-group upload (density,
+    ids and ghost sources land while pass B runs, HbStepArgs.last_fields_event):
+    every output and every reordered field equals the synchronous step's."""
+    import torch
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.ic import make_zeldovich_ic
+    from paper_2510_03557_b200.resident import STEP_FIELDS, HostStepper, ResidentRank, StepConfig
+    box = BoxGeometry(1.0)
+    p = make_zeldovich_ic(20, box, 1.0)
+    p.density[:] = np.linspace(0.5, 1.5, p.n)   # input densities: the DM rows keep theirs
+    d = 1.0 / 20
+    reach = max(5 * d, 2 * float(p.smoothing.max()))
+    cfg = StepConfig(box=box, bin_width=reach * (1 + 1e-9), max_leaf_size=256, r_s=d,
+                     r_cut=5 * d, softening=(1.0 / p.n ** (1 / 3)) / 50)
+    ref = ResidentRank(p.copy(), cfg)
+    ref_out = {k: v[:p.n].cpu().numpy().copy() for k, v in ref.step().items()}
+    ref_fields = {f: v.cpu().numpy().copy() for f, v in ref.fields().items()}
+    rk = ResidentRank(p.copy(), cfg)
+    pin_in = {f: torch.from_numpy(np.ascontiguousarray(getattr(p, f))).pin_memory()
+              for f in STEP_FIELDS}
+    names = ("grav", "hydro", "ncount", "crk_A", "crk_B", "perm")
+    pin_out = {k: torch.empty(rk.out[k].shape, dtype=rk.out[k].dtype).pin_memory() for k in names}
+    pin_out["density"] = torch.empty(rk.n, dtype=torch.float64).pin_memory()
+    hs = HostStepper(rk, pin_in, pin_out)
+    assert hs.four_groups
+    for _ in range(2):
+        got = {k: v.numpy().copy() for k, v in hs().items()}
+        for k in names:
+            np.testing.assert_array_equal(got[k][:p.n], ref_out[k], err_msg=k)
+        np.testing.assert_array_equal(got["density"], ref_fields["density"])
+        for f, v in rk.fields().items():
+            np.testing.assert_array_equal(v.cpu().numpy(), ref_fields[f], err_msg=f)
