@@ -312,11 +312,11 @@ typedef struct HbStepArgs {
                            pass B kernel, 0 (reserved) -- roofline inputs     */
   double* crk_moments_out; /* out: where the (n,10) moments were written     */
   void* grav_half_event;   /* optional cudaEvent_t: bin gravity runs in two
-                              launches split at bin nb/2 and records this
+                              launches split at bin 4 nb/5 and records this
                               event between them; rows [0, grav_split_row)
                               of `grav` are final from then on (the rest at
                               the end of the step), so their copy-out can
-                              overlap the second half                         */
+                              overlap the second launch                       */
   int64_t grav_split_row;  /* out (host, set before the call returns)         */
   double* crk_gradA;  /* HB_PASS_CRK_GRAD: (n,3) d A / d x_i, or NULL          */
   double* crk_gradB;  /* HB_PASS_CRK_GRAD: (n,3,3) d B_a / d x_g, or NULL      */

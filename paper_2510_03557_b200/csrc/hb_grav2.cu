@@ -361,7 +361,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     if (g.t0) HB_CUDA_TRY(cudaEventRecord(g.t0, st));
     int rc2;
     if (g.split_event) {  // tiles of bins < nbins/2, then the rest (tile_ptr is per bin)
-      const int64_t* mid = T.tile_ptr + nbins / 2;
+      const int64_t* mid = T.tile_ptr + grav_split_bin(nbins);
       rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, mid, st, err);
       if (rc2) return rc2;
       if (g.between) {

@@ -54,6 +54,12 @@ int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int
 int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err);
 
 // bin-level short-range gravity (hb_grav2.cu)
+// bin at which the two-launch bin gravity splits (HbStepArgs.grav_half_event):
+// 4/5 of the bins go first, so the rows that drain after the step are a fifth
+// of the gravity output, while the first part's copy (4/5 of it) still fits
+// under the last fifth of the kernel behind the SPH outputs' copy
+__host__ __device__ inline int64_t grav_split_bin(int64_t nbins) { return nbins * 4 / 5; }
+
 struct GravBinArgs {
   int64_t n, nbins;
   const int64_t *bin_ptr, *leaf_start, *leaf_end;

@@ -334,7 +334,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->grav_half_event) {  // rows of bins < nbins/2, final after the first gravity half
     // scratch: the 256-B arena slot of err_key has room after its 8 bytes
     int64_t* split_dev = (int64_t*)(w.err_key + 1);
-    k_split_row<<<1, 32, 0, st>>>(w.bin_ptr, w.leaf_start, nbins / 2, nl, n, split_dev);
+    k_split_row<<<1, 32, 0, st>>>(w.bin_ptr, w.leaf_start, grav_split_bin(nbins), nl, n,
+                                  split_dev);
     HB_LAUNCH_CHECK();
     HB_CUDA_TRY(cudaMemcpyAsync(&a->grav_split_row, split_dev, sizeof(int64_t),
                                 cudaMemcpyDeviceToHost, st));

@@ -20,7 +20,7 @@ from paper_2510_03557_b200.resident import PASS_ALL, STEP_FIELDS, HostStepper
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
     p, cfg, meta = bench.make_workload(args.config)
     rr = bench._make_rank(args, p, cfg, 0, 1, meta)
@@ -31,7 +31,7 @@ def main():
                   for k in out_names}
     pinned_out["density"] = torch.empty(rr.n, dtype=torch.float64).pin_memory()
     hs = HostStepper(rr, pinned_in, pinned_out, PASS_ALL)
-    names = ("ev_first", "ev_fields", "ev_late", "ev_sph", "ev_ghalf", "ev_done")
+    names = ("ev_first", "ev_fields", "ev_late", "ev_last", "ev_sph", "ev_ghalf", "ev_done")
     for nm in names:
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
@@ -53,7 +53,9 @@ def main():
     h2d = sum(t.numel() * t.element_size() for t in pinned_in.values())
     d2h = sum(t.numel() * t.element_size() for t in pinned_out.values())
     print(f"h2d {h2d / 1e6:.1f} MB  d2h {d2h / 1e6:.1f} MB")
-    groups = {"FIRST": HostStepper.FIRST, "EARLY": HostStepper.EARLY, "LATE": HostStepper.LATE}
+    groups = {"FIRST": HostStepper.FIRST, "EARLY": HostStepper.EARLY, "LATE4": HostStepper.LATE4,
+              "LAST4": HostStepper.LAST4}
+    print("four groups:", hs.four_groups)
     for g, fs in groups.items():
         print(g, {f: round(pinned_in[f].numel() * pinned_in[f].element_size() / 1e6, 1) for f in fs})
     print({k: round(v.numel() * v.element_size() / 1e6, 1) for k, v in pinned_out.items()})
