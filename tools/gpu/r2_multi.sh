@@ -1,0 +1,11 @@
+#!/bin/bash
+# multi-GPU (run with gpurun --gpus 4): NCCL tests, c4 at N = 2 and 4 (bench contract launch)
+cd $GRAFT_REPO_ROOT
+nvidia-smi -L > gpurun_out/multi_smi.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_nccl.py -x -q -p no:cacheprovider > gpurun_out/multi_nccl.log 2>&1
+echo "rc=$?" >> gpurun_out/multi_nccl.log
+for N in 2 4; do
+  timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+    --master-port $((29500 + N)) bench.py --gpus $N --steps 5 --warmup 3 > gpurun_out/multi_c4_n$N.log 2>&1
+  echo "rc=$?" >> gpurun_out/multi_c4_n$N.log
+done
