@@ -250,8 +250,8 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
 // 3.32 vs 2.83 ms at c2: staging and flush count outweigh the two MUFU.)
 // 5 CTAs / SM (<= 102 registers, no spills; 2.90 -> 2.82 ms at c2 against the
 // compiler's 4-CTA choice in round 1).
-constexpr int kStageB = 224;
-__global__ void __launch_bounds__(kSphWarps * 32, 4)
+constexpr int kStageB = 192;
+__global__ void __launch_bounds__(kSphWarps * 32, 5)
 k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   __shared__ float4 s_stage[kSphWarps][kStageB][3];
   __shared__ int2 s_meta[kSphWarps][kStageB];
