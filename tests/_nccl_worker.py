@@ -8,7 +8,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def main(outdir, move=False):
+def main(outdir, move=False, drop_ghost=False):
     import torch
     import torch.distributed as dist
     from paper_2510_03557_b200.box import BoxGeometry
@@ -34,7 +34,17 @@ def main(outdir, move=False):
         fields["pos"] += d
         fields["pos"].remainder_(1.0)
         fields["pos"][fields["pos"] >= 1.0] = 0.0
-    out, fields = rr.step()
+    if drop_ghost:   # negative control: one shell row loses its mass after the exchange
+        rr.exchange()
+        f = rr.engine.fields()
+        g = torch.nonzero(f["ghost"] != 0)[0, 0] if rank == 0 else None
+        if g is not None:
+            f["mass"][g] = 0.0
+        out = rr.engine.step(rr.passes)
+        fields = rr.engine.fields()
+        rr.owned_fields = fields
+    else:
+        out, fields = rr.step()
     torch.cuda.synchronize()
     o = (fields["ghost"] == 0).cpu().numpy()
     res = {"gid": fields["global_id"].cpu().numpy()[o],
@@ -42,9 +52,14 @@ def main(outdir, move=False):
            "pos": fields["pos"].cpu().numpy()[o]}
     for k in ("grav", "hydro", "ncount", "crk_A"):
         res[k] = out[k].cpu().numpy()[:o.size][o]
+    # exact in-r_cut source counts of the owned rows (counting pass; it re-steps
+    # the rank set, which keeps its leaf order)
+    rr.engine.gravity_pair_count()
+    counts = rr.engine.out["grav"].reshape(-1).view(torch.int64)[:o.size].cpu().numpy()
+    res["gcount"] = counts[o]
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), **res)
     dist.destroy_process_group()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], move=len(sys.argv) > 2 and sys.argv[2] == "move")
+    main(sys.argv[1], move="move" in sys.argv[2:], drop_ghost="dropghost" in sys.argv[2:])

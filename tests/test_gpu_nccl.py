@@ -1,9 +1,10 @@
 """GPU, 2 or 4 processes over NCCL (skipped with fewer GPUs): the real
 all-to-all overload exchange, which the emulated-rank tests route in-process.
 The ranks step twice (move: every row drifts by up to 0.3 overload widths in
-between, so migrants change owner through NCCL); their owned rows must equal
-one single-domain step of the same set (counts exactly, the rest to FP32
-rounding)."""
+between, so migrants change owner through NCCL); their owned rows must match
+the oracle on the whole set -- neighbour counts and exact in-r_cut gravity
+source counts bit for bit, the rest within tests/tolerances.py -- and a run
+with one ghost's mass zeroed must fail the same checks."""
 import os
 import socket
 import subprocess
@@ -22,22 +23,28 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,move", [(2, False), (4, False), (2, True), (4, True)])
-def test_nccl_ranks_match_single_domain(tmp_path, world, move):
-    import torch
-    if torch.cuda.device_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+def _run(tmp_path, world, *flags):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
            str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(HERE, "_nccl_worker.py"), str(tmp_path)] + (["move"] if move else [])
+           os.path.join(HERE, "_nccl_worker.py"), str(tmp_path)] + list(flags)
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     got = [dict(np.load(tmp_path / f"rank{k}.npz")) for k in range(world)]
-    merged = {k: np.concatenate([g[k] for g in got]) for k in got[0]}
+    return {k: np.concatenate([g[k] for g in got]) for k in got[0]}
+
+
+def _check(oracle, merged, move):
+    """The ranks' owned rows against the oracle on the whole 2x32^3 set (every
+    leaf a sampled receiver): neighbour counts and exact in-r_cut gravity
+    counts bit for bit, density, gravity and hydro within tests/tolerances.py
+    (per particle, normalised by the oracle's sum_j |phi_ij|)."""
     from paper_2510_03557_b200.box import BoxGeometry
     from paper_2510_03557_b200.ic import make_zeldovich_ic
-    from paper_2510_03557_b200.resident import StepConfig, force_step
+    from paper_2510_03557_b200.kernels import counting_kernel
+    from paper_2510_03557_b200.resident import StepConfig
+    from tests._parity import SampledOracle
+    from tests.tolerances import assert_fp32_close
     box = BoxGeometry(1.0)
     p = make_zeldovich_ic(32, box, 0.3)
     if move:   # the ranks' second step saw the drifted positions: use them
@@ -48,17 +55,43 @@ def test_nccl_ranks_match_single_domain(tmp_path, world, move):
     reach = max(10 * pm, 2 * float(p.smoothing.max()))
     cfg = StepConfig(box=box, bin_width=reach * (1 + 1e-9), max_leaf_size=256, r_s=2 * pm,
                      r_cut=10 * pm, softening=(1.0 / p.n ** (1 / 3)) / 50)
-    ref = force_step(p, cfg)
-    a, b = np.argsort(merged["gid"]), np.argsort(p.global_id)
-    assert merged["gid"].size == p.n
-    np.testing.assert_array_equal(merged["gid"][a], p.global_id[b])
-    np.testing.assert_array_equal(merged["ncount"][a], ref["ncount"][b])
-    for k, refv in (("grav", ref["grav"]), ("hydro", ref["hydro"]), ("crk_A", ref["crk_A"]),
-                    ("density", p.density)):
-        # FP32 pair sums in different orders: worst particle 1e-4, median 1e-6
-        # of the field's scale (a missing pair would be ~1e-3 or more)
-        x, y = merged[k][a], refv[b]
-        scale = np.abs(y).max()
-        err = np.abs(x - y).reshape(len(x), -1).max(axis=1)
-        assert err.max() <= 1e-4 * scale, (k, err.max() / scale)
-        assert np.median(err) <= 1e-6 * scale, (k, np.median(err) / scale)
+    ref = SampledOracle(oracle, p, cfg, stride=1, crowded_bins=0)
+    gid = ref.q.global_id[ref.recv]
+    assert np.array_equal(np.sort(gid), np.sort(merged["gid"]))
+    pos = np.searchsorted(merged["gid"], gid, sorter=np.argsort(merged["gid"]))
+    row = np.argsort(merged["gid"])[pos]          # merged row of each receiver
+    nc, rho = ref.counts_density()
+    np.testing.assert_array_equal(merged["ncount"][row], nc[ref.recv], err_msg="ncount")
+    oc, _ = ref._eval(counting_kernel(cfg.r_cut), ref.state())
+    np.testing.assert_array_equal(merged["gcount"][row], oc[ref.recv, 0].astype(np.int64),
+                                  err_msg="gravity in-r_cut counts")
+    gas = ref.q.species[ref.recv] == 1
+    rel = np.abs(merged["density"][row][gas] - rho[ref.recv][gas]) / rho[ref.recv][gas]
+    assert np.median(rel) <= 1e-6 and np.quantile(rel, 0.999) <= 1e-5, rel.max()
+    g, gabs, _ = ref.gravity()
+    assert_fp32_close(merged["grav"][row], g[ref.recv], gabs[ref.recv], what="nccl gravity")
+    dens = ref.q.density.copy()
+    gq = ref.q.species == 1
+    dens[ref.recv[gas]] = merged["density"][row][gas]
+    hy, habs = ref.hydro(np.where(gq, dens, ref.q.density))
+    assert_fp32_close(merged["hydro"][row], hy[ref.recv], habs[ref.recv], what="nccl hydro")
+
+
+@pytest.mark.parametrize("world,move", [(2, False), (4, False), (2, True), (4, True)])
+def test_nccl_ranks_match_oracle(tmp_path, oracle, world, move):
+    import torch
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    merged = _run(tmp_path, world, *(["move"] if move else []))
+    _check(oracle, merged, move)
+
+
+def test_nccl_dropped_ghost_fails(tmp_path, oracle):
+    """Negative control: one shell row of rank 0 loses its mass after the
+    exchange -- the same checks must fail."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    merged = _run(tmp_path, 2, "dropghost")
+    with pytest.raises(AssertionError):
+        _check(oracle, merged, False)
