@@ -53,9 +53,46 @@ __device__ __forceinline__ double bin_coord(double p, int8_t s, double L) {
   return __dadd_rn(p, __dmul_rn((double)s, L));
 }
 
+// a tile's box (FP32, segment frame, exactly as the members' coordinates
+// were computed for the splits) with the members' largest h in lo.w and the
+// first record index in hi.w, and its owned-target skip flag: emitted by the
+// builders as each tile is cut (no separate pass over the state rows).
+// Called by one full warp; lanes < m hold members (c = frame coordinates, r =
+// state row).
+__device__ __forceinline__ void emit_tile_box(Tiling& T, int64_t t, int start, int m, bool have,
+                                              float cx, float cy, float cz, int64_t r,
+                                              const double* state, const uint8_t* ghost) {
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  float hm = 0.0f;
+  bool own = false;
+  if (have) {
+    lo[0] = hi[0] = cx; lo[1] = hi[1] = cy; lo[2] = hi[2] = cz;
+    hm = (float)state[r * NCOL + C_H];
+    own = ghost && ghost[r] == 0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+    hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  }
+  unsigned ob = __ballot_sync(0xffffffffu, own);
+  if ((threadIdx.x & 31) == 0) {
+    T.tile_lo[t] = make_float4(lo[0], lo[1], lo[2], hm);
+    // .w carries the tile's first record index (int bits): the culling loops
+    // read it with the box, so a passing tile needs no dependent load of
+    // tile_start before its records
+    T.tile_hi[t] = make_float4(hi[0], hi[1], hi[2], __int_as_float(start));
+    T.tile_skip[t] = (ghost && ob == 0u) ? 1 : 0;
+  }
+}
+
 __global__ void __launch_bounds__(kTileBuildBlock)
 k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const double* state,
-             const int8_t* pshift, double L, int sel) {
+             const int8_t* pshift, double L, int sel, const uint8_t* ghost) {
   __shared__ int32_t s_row[kTileBuildCap];
   __shared__ int32_t s_tmp[kTileBuildCap];
   __shared__ float s_c[3][kTileBuildCap];
@@ -147,8 +184,15 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
     int a0 = stk_a[sp - 1], m = stk_m[sp - 1], kk = stk_k[sp - 1];
     __syncthreads();
     if (kk == 1) {
+      int64_t t = T.tile_ptr[leaf] + tile_j;
+      if (threadIdx.x < 32) {
+        bool have = (int)threadIdx.x < m;
+        int k = a0 + (have ? (int)threadIdx.x : 0);
+        emit_tile_box(T, t, (int)(T.sel_off[leaf] + a0), m, have, s_c[0][k], s_c[1][k],
+                      s_c[2][k], s_row[k], state, ghost);
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
-        int64_t t = T.tile_ptr[leaf] + tile_j;
         T.tile_start[t] = (int32_t)(T.sel_off[leaf] + a0);
         T.tile_n[t] = m;
         T.tile_leaf[t] = (int32_t)leaf;
@@ -237,7 +281,8 @@ constexpr int kTileWarpCap = 384;
 constexpr int kTileWarps = 4;
 __global__ void __launch_bounds__(kTileWarps * 32)
 k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
-                  const double* state, const int8_t* pshift, double L, int sel, int nl) {
+                  const double* state, const int8_t* pshift, double L, int sel, int nl,
+                  const uint8_t* ghost) {
   __shared__ int32_t s_row[kTileWarps][kTileWarpCap];
   __shared__ int32_t s_tmp[kTileWarps][kTileWarpCap];
   __shared__ float s_c[kTileWarps][3][kTileWarpCap];
@@ -310,8 +355,14 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     --sp;
     int a0 = stk_a[sp], m = stk_m[sp], kk = stk_k[sp];
     if (kk == 1) {
+      int64_t t = tbase + tile_j;
+      {
+        bool have = lane < m;
+        int id = have ? ord[a0 + lane] : 0;
+        emit_tile_box(T, t, (int)(so + a0), m, have, cc[0][id], cc[1][id], cc[2][id], row[id],
+                      state, ghost);
+      }
       if (lane == 0) {
-        int64_t t = tbase + tile_j;
         T.tile_start[t] = (int32_t)(so + a0);
         T.tile_n[t] = m;
         T.tile_leaf[t] = (int32_t)leaf;
@@ -402,50 +453,6 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     stk_a[sp] = a0; stk_m[sp] = left; stk_k[sp] = k1; ++sp;              // left first
   }
   for (int k = lane; k < m_sel; k += 32) T.tperm[so + k] = row[ord[k]];
-}
-
-// tile boxes (FP32, leaf frame) and hmax, one warp per tile
-__global__ void k_tile_boxes(int64_t n_tiles, const int64_t* n_tiles_dev, Tiling T,
-                             const double* state, const int8_t* pshift, double L,
-                             const uint8_t* ghost) {
-  int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (t >= *n_tiles_dev) return;
-  int leaf = T.tile_leaf[t];
-  int n = T.tile_n[t];
-  int ks = T.tile_start[t];
-  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  float hm = 0.0f;
-  if (lane < n) {
-    int64_t r = T.tperm[ks + lane];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      double v = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
-      float c = (float)(v - T.origin[3 * leaf + d]);
-      lo[d] = c; hi[d] = c;
-    }
-    hm = (float)state[r * NCOL + C_H];
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
-      hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
-    }
-    hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-  }
-  // owned-target skip flag (only when built with a ghost array)
-  bool own = lane < n && ghost && ghost[T.tperm[ks + lane]] == 0;
-  unsigned ob = __ballot_sync(0xffffffffu, own);
-  if (lane == 0) {
-    T.tile_lo[t] = make_float4(lo[0], lo[1], lo[2], hm);
-    // .w carries the tile's first record index (int bits): the culling loops
-    // read it with the box, so a passing tile needs no dependent load of
-    // tile_start before its records
-    T.tile_hi[t] = make_float4(hi[0], hi[1], hi[2], __int_as_float(ks));
-    T.tile_skip[t] = (ghost && ob == 0u) ? 1 : 0;
-  }
 }
 
 // ---------------------------------------------------------------- packing
@@ -1276,15 +1283,12 @@ int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t
     HB_CUDA_TRY(cudaMemcpyAsync(T.tile_ptr + nl, n_tiles_dev, sizeof(int64_t),
                                 cudaMemcpyDeviceToDevice, st));
   }
+  // the builders emit each tile's box as they cut it (emit_tile_box)
   k_tile_build_warp<<<grid_for(nl, kTileWarps), kTileWarps * 32, 0, st>>>(
-      T, leaf_start, leaf_end, state, pshift, L, sel, (int)nl);
+      T, leaf_start, leaf_end, state, pshift, L, sel, (int)nl, ghost);
   HB_LAUNCH_CHECK();
   k_tile_build<<<(unsigned)nl, kTileBuildBlock, 0, st>>>(T, leaf_start, leaf_end, state, pshift,
-                                                         L, sel);
-  HB_LAUNCH_CHECK();
-  int64_t tcap = T.n_tiles_cap;
-  k_tile_boxes<<<grid_for(tcap * 32, 256), 256, 0, st>>>(tcap, n_tiles_dev, T, state, pshift, L,
-                                                       ghost);
+                                                         L, sel, ghost);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }

@@ -96,7 +96,7 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
       if (u < u1) {
         float4 lo = T.tile_lo[u], hi = T.tile_hi[u];
         my_n = T.tile_n[u];
-        my_start = __float_as_int(hi.w);  // k_tile_boxes: first record index
+        my_start = __float_as_int(hi.w);  // emit_tile_box: first record index
         float R = HYDRO ? fminf(Rcap, 2.0f * fmaxf(hmax_t, lo.w) * 1.0001f) : Rt;
         float gx = fmaxf(fmaxf((lo.x - D0) - thi.x, tlo.x - (hi.x - D0)), 0.0f);
         float gy = fmaxf(fmaxf((lo.y - D1) - thi.y, tlo.y - (hi.y - D1)), 0.0f);
@@ -230,7 +230,7 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
     __syncwarp();
     cnt = 0;
   };
-  // cull radius from the tile's largest h (k_tile_boxes: tile_lo.w), not this
+  // cull radius from the tile's largest h (emit_tile_box: tile_lo.w), not this
   // lane's: every lane culls sources for the whole tile
   sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
                                cnt, consume);

@@ -18,17 +18,20 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--npd", type=int, default=None, help="lattice override (make_workload npd)")
     args = ap.parse_args()
     import torch
     from bench import make_workload
-    from paper_2510_03557_b200.resident import ResidentRank
-    p, cfg, meta = make_workload(args.config)
-    rr = ResidentRank(p, cfg)
+    from paper_2510_03557_b200.resident import PASS_ALL, PASS_GRAVITY, ResidentRank
+    p, cfg, meta = make_workload(args.config, npd=args.npd)
+    gonly = meta["n_gas"] == 0
+    passes = PASS_GRAVITY if gonly else PASS_ALL
+    rr = ResidentRank(p, cfg, gravity_only=gonly)
     for _ in range(3):
-        rr.step()
+        rr.step(passes)
     ph = []
     for _ in range(args.steps):
-        rr.step(timing=True)
+        rr.step(passes, timing=True)
         ph.append(rr.last["ms_phase"])
     torch.cuda.synchronize()
     med = {k: float(np.median([x[k] for x in ph])) for k in ph[0]}
