@@ -248,10 +248,10 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
 // the approaching-pair viscosity branch.  (A fourth record with 1/h_j and
 // m_j/rho_j precomputed, and 160-source stages to stay at 4 CTAs / SM, measured
 // 3.32 vs 2.83 ms at c2: staging and flush count outweigh the two MUFU.)
-// 5 CTAs / SM (<= 102 registers, no spills; 2.90 -> 2.82 ms at c2 against the
-// compiler's 4-CTA choice in round 1).
+// Two pairs per walk iteration at 4 CTAs / SM (120 registers, no spills):
+// 2.763 -> 2.728 ms at c2 against one pair at 5 CTAs / SM (96 registers).
 constexpr int kStageB = 192;
-__global__ void __launch_bounds__(kSphWarps * 32, 5)
+__global__ void __launch_bounds__(kSphWarps * 32, 4)
 k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   __shared__ float4 s_stage[kSphWarps][kStageB][3];
   __shared__ int2 s_meta[kSphWarps][kStageB];
@@ -286,12 +286,12 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
     __syncwarp();
     unsigned nz = build_masks<3, true>(stage, cnt, ti0, hi, live ? thr_i : -1.0f,
                                        live ? reach2c : -1.0f, mask);
-    walk_masks(mask, nz, [&](int q) {
+    auto pair = [&](int q, bool on) {
       float4 s0 = stage[q][0], s1 = stage[q][1], s2 = stage[q][2];
       float hj = s0.w;
       float dx = ti0.x - s0.x, dy = ti0.y - s0.y, dz = ti0.z - s0.z;
       float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      if (!(r2 <= a.reach2)) return;
+      if (!(on && r2 <= a.reach2)) return;
       float rinv = rsqrt_ftz(fmaxf(r2, 1e-30f));
       float r = r2 * rinv;
       // cubic spline at q_i (value and (dW/dr)/r, hb/kernels.py:71-93) and
@@ -330,6 +330,11 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
       float hv = 0.5f * visc;
       ei = fmaf(ti2.x + hv, work, ei);
       ej = fmaf(s2.x + hv, work, ej);
+    };
+    // two pairs per iteration (walk_masks2): independent chains for ILP
+    walk_masks2(mask, nz, [&](int q1, int q2) {
+      pair(q1, true);
+      pair(q2 >= 0 ? q2 : q1, q2 >= 0);
     });
     __syncwarp();
     cnt = 0;
