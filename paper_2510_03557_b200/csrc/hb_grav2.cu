@@ -307,26 +307,29 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     return HB_OK;
   }
   if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (gravity bins)");
-  k_bin_segments<<<grid_for(nbins, 256), 256, 0, st>>>(nbins, g.bin_ptr, g.leaf_start, g.leaf_end,
-                                                       seg_s, seg_e);
-  HB_LAUNCH_CHECK();
-  k_bin_stencil<<<grid_for(nbins * 27, 256), 256, 0, st>>>(nbins, g.geom, st_src, st_code);
-  HB_LAUNCH_CHECK();
-  {
-    Arena s = ws;
-    int rc = build_tiling(T, nbins, seg_s, seg_e, g.state, g.pshift, g.L, 0, ntd, s, st, err,
-                          g.ghost);
+  int rc = HB_OK;
+  if (g.phase != 2) {
+    k_bin_segments<<<grid_for(nbins, 256), 256, 0, st>>>(nbins, g.bin_ptr, g.leaf_start,
+                                                         g.leaf_end, seg_s, seg_e);
+    HB_LAUNCH_CHECK();
+    k_bin_stencil<<<grid_for(nbins * 27, 256), 256, 0, st>>>(nbins, g.geom, st_src, st_code);
+    HB_LAUNCH_CHECK();
+    {
+      Arena s = ws;
+      rc = build_tiling(T, nbins, seg_s, seg_e, g.state, g.pshift, g.L, 0, ntd, s, st, err,
+                        g.ghost);
+      if (rc) return rc;
+    }
+    rc = pack_records(KID_GRAVITY, T, ntd, g.state, g.pshift, nullptr, 0, g.L, P0, nullptr,
+                      nullptr, st, err);
     if (rc) return rc;
   }
-  int rc = pack_records(KID_GRAVITY, T, ntd, g.state, g.pshift, nullptr, 0, g.L, P0, nullptr,
-                        nullptr, st, err);
-  if (rc) return rc;
   GravTab gt;
   // k_gravity2 only has the r / t tables
   int kind = g.half_warp ? (g.eps <= 0.05 * g.r_s ? GT_T : GT_R) : g.table_kind;
   const float4* tab = gravity_table_device(g.r_s, g.r_cut, g.eps, kind, &gt, st, err);
   if (!tab) return err ? err->status : HB_CUDA;
-  if (!g.half_warp) {
+  if (!g.half_warp && g.phase != 2) {
     if (tile_order_levels() > 0) {
       k_tile_order<<<grid_for(T.n_tiles_cap, kTOWarps), kTOWarps * 32, 0, st>>>(
           ntd, T, P0, tile_order_levels());
@@ -335,6 +338,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     k_stride_ptr<<<grid_for(nbins + 1, 256), 256, 0, st>>>(nbins, 27, st_ptr);
     HB_LAUNCH_CHECK();
   }
+  if (g.phase == 1) return HB_OK;
   if (g.count_only) {  // k_eval<KID_COUNTING>, float64 band re-check, no self pair
     EvalDev e = {};
     e.T = T; e.ent_ptr = st_ptr; e.ent_src = st_src; e.ent_code = st_code; e.P0 = P0;

@@ -50,7 +50,8 @@ struct SphArgs {
 };
 int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
              double L, float4* P0, float4* P1, float4* P2, float4* P3, int layout,
-             cudaStream_t st, HbError* err);
+             cudaStream_t st, HbError* err, const double* rho = nullptr,
+             const double* u = nullptr, double gamma = 0.0);
 int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err);
 
 // bin-level short-range gravity (hb_grav2.cu)
@@ -83,6 +84,10 @@ struct GravBinArgs {
   // count instead of sum: exact in-r_cut source counts per row into
   // (int64_t*)out (HB_PASS_COUNT_ONLY)
   bool count_only = false;
+  // 0: prepare (segments, stencil, tiling, records) and launch; 1: prepare
+  // only; 2: launch only, on what a phase-1 call with the same arena offset
+  // prepared (the step prepares gravity while pass B waits for its inputs)
+  int phase = 0;
 };
 int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);
 // hb_crk_solve over a row list (rows[0, *n_rows), device count); other rows get

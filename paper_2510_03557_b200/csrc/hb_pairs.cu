@@ -418,13 +418,32 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     // bits above the highest one where kmin and kmax differ are common to all
     int top = 31 - __clz(kmin ^ kmax | 1u);
     unsigned K = top >= 31 ? 0u : (kmin >> (top + 1)) << (top + 1);
-    for (int b = top; b >= 0; --b) {
+    // radix-4 descent: three candidates per pass, their counts packed in
+    // 10-bit fields of one warp reduction (counts <= 384), so half the passes
+    // of the binary descent -- the same K (two binary steps pick the largest
+    // of K, K+1, K+2, K+3 (x 2^(b-1)) whose count stays below `left`)
+    int b = top;
+    if ((top + 1) & 1) {  // odd number of bits: one binary step first
       unsigned cand = K | (1u << b);
       int c = 0;
 #pragma unroll
       for (int jj = 0; jj < J; ++jj)
         if (jj < nj) c += key[jj] < cand ? 1 : 0;  // padding keys are 0xffffffff
       if (__reduce_add_sync(0xffffffffu, c) < left) K = cand;
+      --b;
+    }
+    for (; b >= 1; b -= 2) {
+      unsigned c1 = K | (1u << (b - 1)), c2 = K | (2u << (b - 1)), c3 = K | (3u << (b - 1));
+      int c = 0;
+#pragma unroll
+      for (int jj = 0; jj < J; ++jj)
+        if (jj < nj) {
+          unsigned kj = key[jj];
+          c += (kj < c1 ? 1 : 0) + (kj < c2 ? 1 << 10 : 0) + (kj < c3 ? 1 << 20 : 0);
+        }
+      int tot = __reduce_add_sync(0xffffffffu, c);
+      int n1 = tot & 1023, n2 = (tot >> 10) & 1023, n3 = (tot >> 20) & 1023;
+      K = n3 < left ? c3 : (n2 < left ? c2 : (n1 < left ? c1 : K));
     }
     int c_lt = 0;
 #pragma unroll

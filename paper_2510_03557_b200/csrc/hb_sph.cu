@@ -520,9 +520,14 @@ k_sph_grad(SphDev a, const int64_t* n_tiles_dev) {
 // layout 2 (pass C): P0 = (x, y, z, V = m/rho), P1 = (.., .., .., h)
 // layout 1 (pass B): P0 = (x, y, z, h), P1 = (vx, vy, vz, m),
 //                    P2 = (P/rho^2, c_s, rho, sigma/h^5)
+// rho_f / u_f (optional, leaf-order SoA density and internal energy): rho, P
+// and c_s come from them with the EOS of hb/hydro.py:48-57 evaluated here
+// (P = ((gamma - 1) rho) u, c_s = sqrt(max((gamma (gamma - 1)) u, 0))), so the
+// step needs no separate pass writing those state-matrix columns
 __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tiling T,
                            const double* state, const int8_t* pshift, double L, float4* P0,
-                           float4* P1, float4* P2, float4* P3, int layout) {
+                           float4* P1, float4* P2, float4* P3, int layout, const double* rho_f,
+                           const double* u_f, double gamma) {
   int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (t >= *n_tiles_dev || lane >= T.tile_n[t]) return;
@@ -536,9 +541,15 @@ __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tilin
     double v = __dadd_rn(st[d], __dmul_rn((double)(pshift ? pshift[3 * r + d] : 0), L));
     c[d] = (float)(v - T.origin[3 * leaf + d]);
   }
-  double h = st[C_H], rho = st[C_RHO];
+  double h = st[C_H], rho = rho_f ? rho_f[r] : st[C_RHO];
+  double P = st[C_P], cs = st[C_CS];
+  if (rho_f && u_f) {
+    double gm1 = gamma - 1.0, u = u_f[r];
+    P = gm1 * rho * u;
+    cs = sqrt(fmax(gamma * gm1 * u, 0.0));
+  }
   double norm5 = h > 0 ? 0.31830988618379067 / (h * h * h * h * h) : 0.0;
-  double fpart = rho > 0 ? st[C_P] / (rho * rho) : 0.0;
+  double fpart = rho > 0 ? P / (rho * rho) : 0.0;
   if (layout == 0) {
     P0[k] = make_float4(c[0], c[1], c[2], (float)st[C_M]);
     P1[k] = make_float4(0.f, 0.f, 0.f, (float)h);
@@ -548,15 +559,15 @@ __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tilin
   } else {
     P0[k] = make_float4(c[0], c[1], c[2], (float)h);
     P1[k] = make_float4((float)st[C_VX], (float)st[C_VY], (float)st[C_VZ], (float)st[C_M]);
-    P2[k] = make_float4((float)fpart, (float)st[C_CS], (float)rho, (float)norm5);
+    P2[k] = make_float4((float)fpart, (float)cs, (float)rho, (float)norm5);
   }
 }
 
 int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
              double L, float4* P0, float4* P1, float4* P2, float4* P3, int layout,
-             cudaStream_t st, HbError* err) {
-  k_pack_sph<<<grid_for(T.n_tiles_cap * 32, 256), 256, 0, st>>>(T.n_tiles_cap, ntd, T, state,
-                                                                pshift, L, P0, P1, P2, P3, layout);
+             cudaStream_t st, HbError* err, const double* rho, const double* u, double gamma) {
+  k_pack_sph<<<grid_for(T.n_tiles_cap * 32, 256), 256, 0, st>>>(
+      T.n_tiles_cap, ntd, T, state, pshift, L, P0, P1, P2, P3, layout, rho, u, gamma);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }

@@ -27,23 +27,6 @@ __global__ void k_alias_sync(int64_t n, const int64_t* ghost_src, double* densit
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && ghost_src[i] >= 0) density[i] = density[ghost_src[i]];
 }
-// gas_only: non-gas rows get P = c_s = 0 (their density lands later, with
-// HbStepArgs.last_fields_event; no pass reads a non-gas row's P or c_s)
-__global__ void k_eos(int64_t n, const double* rho, const double* u, double gamma, double* st,
-                      const uint8_t* gas_only) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (gas_only && gas_only[i] != 1) {
-    st[i * NCOL + C_P] = 0.0;
-    st[i * NCOL + C_CS] = 0.0;
-    return;
-  }
-  double gm1 = gamma - 1.0;
-  st[i * NCOL + C_RHO] = rho[i];
-  st[i * NCOL + C_P] = gm1 * rho[i] * u[i];
-  st[i * NCOL + C_CS] = sqrt(fmax(gamma * gm1 * u[i], 0.0));
-}
-
 __global__ void k_zero_ghost_rows(int64_t n_leaves, const int64_t* leaf_start,
                                   const int64_t* leaf_end, const uint8_t* ghost_only,
                                   double* ncount, double* moments, double* hydro, double* grav) {
@@ -118,7 +101,8 @@ __global__ void k_gather_late(int64_t n, const int64_t* perm, FieldIn in, FieldO
 }
 
 // LATE = true: skip the late fields (vel, u, density, ids) and P, c_s, which
-// need u and rho; k_eos writes them after pass A, which reads none of them
+// need u and rho (pass B's records compute P and c_s from the SoA density and
+// internal energy; pass A reads none of them)
 // h_lim: the h_max the step's reach, bin width and culls were sized from
 // (HbStepArgs.h_max).  A gas row above it would silently lose the pairs
 // between 2 h_max and 2 h_i, so it raises HB_CONTRACT (error key code 3)
@@ -126,8 +110,8 @@ __global__ void k_gather_late(int64_t n, const int64_t* perm, FieldIn in, FieldO
 // The state rows go through shared memory: each thread assembles its row,
 // then the block writes its 256 contiguous rows with 16-B stores (a per-thread
 // row store touches 12 sectors 96 B apart per warp instruction: 0.62 ms at c2).
-// Columns a LATE gather leaves for later kernels are written as 0 here and
-// filled by k_gather_late / k_eos before anything reads them.
+// Columns a LATE gather leaves for later kernels are written as 0 here; the
+// velocity columns are filled by k_gather_late before anything reads them.
 constexpr int kGatherBlock = 256;
 template <bool LATE>
 __global__ void __launch_bounds__(kGatherBlock)
@@ -542,7 +526,33 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     tm.kmark(3);
     if (rc) return rc;
   }
-  rc = gather_late();  // before the EOS and the ghost alias sync read them
+  // bin gravity's preparation (segments, stencil, all-species tiling, records)
+  // needs only positions and masses: it runs here, where a host-buffer step
+  // would otherwise wait for the late input group (vel, internal energy)
+  bool bin_gravity = (a->passes & HB_PASS_GRAVITY) && !use_leaf_gravity;
+  auto gravity_args = [&]() {
+    GravBinArgs gb;
+    gb.n = n; gb.nbins = nbins; gb.bin_ptr = w.bin_ptr; gb.leaf_start = w.leaf_start;
+    gb.leaf_end = w.leaf_end; gb.geom = ld.g; gb.state = w.state; gb.pshift = a->image_shift;
+    gb.L = a->side_length; gb.r_s = a->r_s; gb.r_cut = a->r_cut; gb.eps = a->softening;
+    gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
+    gb.half_warp = a->gravity_mode == 2;
+    gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
+    gb.ghost = a->owned_targets ? a->ghost : nullptr;
+    gb.count_only = (a->passes & HB_PASS_COUNT_ONLY) != 0;
+    if (gb.count_only) gb.half_warp = false;
+    return gb;
+  };
+  bool gravity_prepared = false;
+  if (bin_gravity) {
+    GravBinArgs gb = gravity_args();
+    gb.phase = 1;
+    Arena s = ws;
+    rc = gravity_bins(gb, s, st, err);
+    if (rc) return rc;
+    gravity_prepared = true;
+  }
+  rc = gather_late();  // before pass B and the ghost alias sync read them
   if (rc) return rc;
   if (a->passes & HB_PASS_DENSITY) {
     k_density_update<<<grid_for(nl * 32, 256), 256, 0, st>>>(
@@ -552,10 +562,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       k_alias_sync<<<grid_for(n, 256), 256, 0, st>>>(n, a->ghost_src, a->density);
       HB_COUNT_LAUNCH(1);
     }
-    HB_COUNT_LAUNCH(1);
-    k_eos<<<grid_for(n, 256), 256, 0, st>>>(n, a->density, a->internal_energy, a->eos_gamma,
-                                            w.state, last_split ? a->species : nullptr);
     HB_LAUNCH_CHECK();
+    // the EOS (P, c_s; hb/hydro.py:48-57) is evaluated where pass B's records
+    // are packed, from the leaf-order density and internal energy
   }
   tm.mark(4);
   // 5. pass B: CRK moments (+ 3x3 solve, hb/hydro.py:99-150) + hydro force (hb/kernels.py:222-258)
@@ -563,7 +572,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     HB_CUDA_TRY(cudaMemsetAsync(mom, 0, n * 10 * sizeof(double), st));
     HB_CUDA_TRY(cudaMemsetAsync(a->hydro, 0, n * 5 * sizeof(double), st));
     rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, nullptr, 1, st,
-                  err);
+                  err, a->density, a->internal_energy, a->eos_gamma);
     if (rc) return rc;
     tm.kmark(4);
     rc = launch_sph(1, sa, st, err);
@@ -583,7 +592,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       HB_CUDA_TRY(cudaMemsetAsync(a->crk_gradA, 0, n * 3 * sizeof(double), st));
       HB_CUDA_TRY(cudaMemsetAsync(a->crk_gradB, 0, n * 9 * sizeof(double), st));
       rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2,
-                    nullptr, 2, st, err);
+                    nullptr, 2, st, err, a->density, a->internal_energy, a->eos_gamma);
       if (rc) return rc;
       sa.crk_A = a->crk_A; sa.crk_B = a->crk_B; sa.crk_fallback = a->crk_fallback;
       sa.gradA = a->crk_gradA; sa.gradB = a->crk_gradB;
@@ -600,27 +609,16 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   // the SPH outputs are final here (ghost rows included): copies may start
   if (a->sph_done_event) HB_CUDA_TRY(cudaEventRecord((cudaEvent_t)a->sph_done_event, st));
   tm.mark(5);
-  // 7. short-range gravity (hb/kernels.py:152-163): bin segments (hb_grav2.cu)
-  // unless a bin outgrows the block tiler, then leaf tiles.  (Running it on a
-  // second stream concurrently with the SPH chain was measured: the two
-  // throughput-bound grids time-slice the SMs -- whichever has dispatch
-  // priority starves the other -- so the step time did not change.  So was
-  // running only its preparation (segments, tiling, records: 0.95 ms) on a
-  // high-priority side stream during the SPH passes: gravity phase -0.93 ms,
-  // SPH pass A +0.97 ms, step unchanged.)
-  bool bin_gravity = (a->passes & HB_PASS_GRAVITY) && !use_leaf_gravity;
+  // 7. short-range gravity (hb/kernels.py:152-163): bin segments (hb_grav2.cu,
+  // prepared after pass A above) unless a bin outgrows the block tiler, then
+  // leaf tiles.  (Running it on a second stream concurrently with the SPH
+  // chain was measured: the two throughput-bound grids time-slice the SMs --
+  // whichever has dispatch priority starves the other -- so the step time did
+  // not change.)
   if (bin_gravity) {
     HB_CUDA_TRY(cudaMemsetAsync(a->grav, 0, n * 3 * sizeof(double), st));
-    GravBinArgs gb;
-    gb.n = n; gb.nbins = nbins; gb.bin_ptr = w.bin_ptr; gb.leaf_start = w.leaf_start;
-    gb.leaf_end = w.leaf_end; gb.geom = ld.g; gb.state = w.state; gb.pshift = a->image_shift;
-    gb.L = a->side_length; gb.r_s = a->r_s; gb.r_cut = a->r_cut; gb.eps = a->softening;
-    gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
-    gb.half_warp = a->gravity_mode == 2;
-    gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
-    gb.ghost = a->owned_targets ? a->ghost : nullptr;
-    gb.count_only = (a->passes & HB_PASS_COUNT_ONLY) != 0;
-    if (gb.count_only) gb.half_warp = false;
+    GravBinArgs gb = gravity_args();
+    gb.phase = gravity_prepared ? 2 : 0;
     gb.t0 = tm.on ? tm.kv[0] : nullptr;
     gb.t1 = tm.on ? tm.kv[1] : nullptr;
     GhostZeroCtx zc = {nl, w.leaf_start, w.leaf_end, w.ghost_only, a->grav, st};
