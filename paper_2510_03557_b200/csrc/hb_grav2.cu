@@ -308,15 +308,23 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   }
   if (!ws.ok()) return set_err(err, HB_CONTRACT, "workspace too small (gravity bins)");
   int rc = HB_OK;
+  bool reuse = g.pre_seg_s && g.pre_seg_e && g.pre_st_ptr && g.pre_st_src && g.pre_st_code;
+  const int64_t* segs = reuse ? g.pre_seg_s : seg_s;
+  const int64_t* sege = reuse ? g.pre_seg_e : seg_e;
+  const int64_t* sptr = reuse ? g.pre_st_ptr : st_ptr;
+  const int32_t* ssrc = reuse ? g.pre_st_src : st_src;
+  const int32_t* scode = reuse ? g.pre_st_code : st_code;
   if (g.phase != 2) {
-    k_bin_segments<<<grid_for(nbins, 256), 256, 0, st>>>(nbins, g.bin_ptr, g.leaf_start,
-                                                         g.leaf_end, seg_s, seg_e);
-    HB_LAUNCH_CHECK();
-    k_bin_stencil<<<grid_for(nbins * 27, 256), 256, 0, st>>>(nbins, g.geom, st_src, st_code);
-    HB_LAUNCH_CHECK();
+    if (!reuse) {
+      k_bin_segments<<<grid_for(nbins, 256), 256, 0, st>>>(nbins, g.bin_ptr, g.leaf_start,
+                                                           g.leaf_end, seg_s, seg_e);
+      HB_LAUNCH_CHECK();
+      k_bin_stencil<<<grid_for(nbins * 27, 256), 256, 0, st>>>(nbins, g.geom, st_src, st_code);
+      HB_LAUNCH_CHECK();
+    }
     {
       Arena s = ws;
-      rc = build_tiling(T, nbins, seg_s, seg_e, g.state, g.pshift, g.L, 0, ntd, s, st, err,
+      rc = build_tiling(T, nbins, segs, sege, g.state, g.pshift, g.L, 0, ntd, s, st, err,
                         g.ghost);
       if (rc) return rc;
     }
@@ -335,13 +343,15 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
           ntd, T, P0, tile_order_levels());
       HB_LAUNCH_CHECK();
     }
-    k_stride_ptr<<<grid_for(nbins + 1, 256), 256, 0, st>>>(nbins, 27, st_ptr);
-    HB_LAUNCH_CHECK();
+    if (!reuse) {
+      k_stride_ptr<<<grid_for(nbins + 1, 256), 256, 0, st>>>(nbins, 27, st_ptr);
+      HB_LAUNCH_CHECK();
+    }
   }
   if (g.phase == 1) return HB_OK;
   if (g.count_only) {  // k_eval<KID_COUNTING>, float64 band re-check, no self pair
     EvalDev e = {};
-    e.T = T; e.ent_ptr = st_ptr; e.ent_src = st_src; e.ent_code = st_code; e.P0 = P0;
+    e.T = T; e.ent_ptr = sptr; e.ent_src = ssrc; e.ent_code = scode; e.P0 = P0;
     e.state = g.state; e.pshift = g.pshift;
     e.L = g.L; e.reach = g.r_cut;
     e.pp.reach2 = (float)(g.r_cut * g.r_cut);
@@ -355,7 +365,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   }
   if (!g.half_warp) {
     EvalDev e = {};
-    e.T = T; e.ent_ptr = st_ptr; e.ent_src = st_src; e.ent_code = st_code; e.P0 = P0;
+    e.T = T; e.ent_ptr = sptr; e.ent_src = ssrc; e.ent_code = scode; e.P0 = P0;
     e.L = g.L; e.reach = g.r_cut;
     e.pp.p0 = (float)g.r_s; e.pp.p1 = (float)(g.eps * g.eps);
     e.cull_reach = (float)(g.r_cut * (1.0 + 1e-4)) + 1e-30f;
@@ -381,7 +391,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     return rc2;
   }
   G2Dev d;
-  d.T = T; d.st_src = st_src; d.st_code = st_code; d.P0 = P0; d.L = g.L;
+  d.T = T; d.st_src = ssrc; d.st_code = scode; d.P0 = P0; d.L = g.L;
   d.cull_reach = (float)(g.r_cut * (1.0 + 1e-4)) + 1e-30f;
   d.eps2 = (float)(g.eps * g.eps);
   d.tab_scale = gt.scale; d.tab_last = (int)gt.last;

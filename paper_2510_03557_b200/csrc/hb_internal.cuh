@@ -88,6 +88,10 @@ struct GravBinArgs {
   // only; 2: launch only, on what a phase-1 call with the same arena offset
   // prepared (the step prepares gravity while pass B waits for its inputs)
   int phase = 0;
+  // optional: the step's bin segments and 27-stencil (bin_stencil_csr),
+  // reused instead of recomputed
+  const int64_t *pre_seg_s = nullptr, *pre_seg_e = nullptr, *pre_st_ptr = nullptr;
+  const int32_t *pre_st_src = nullptr, *pre_st_code = nullptr;
 };
 int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err);
 // hb_crk_solve over a row list (rows[0, *n_rows), device count); other rows get

@@ -541,6 +541,10 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     gb.ghost = a->owned_targets ? a->ghost : nullptr;
     gb.count_only = (a->passes & HB_PASS_COUNT_ONLY) != 0;
     if (gb.count_only) gb.half_warp = false;
+    if (sph_bins) {  // the SPH tiling's bin segments and stencil are the same arrays
+      gb.pre_seg_s = w.seg_s; gb.pre_seg_e = w.seg_e; gb.pre_st_ptr = w.st_ptr;
+      gb.pre_st_src = w.st_src; gb.pre_st_code = w.st_code;
+    }
     return gb;
   };
   bool gravity_prepared = false;
