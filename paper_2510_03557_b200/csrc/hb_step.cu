@@ -116,7 +116,7 @@ constexpr int kGatherBlock = 256;
 template <bool LATE>
 __global__ void __launch_bounds__(kGatherBlock)
 k_gather_state(int64_t n, const int64_t* perm, FieldIn in, FieldOut out, double gamma,
-               double* st, double h_lim, unsigned long long* err_key) {
+               double* st, double h_lim, unsigned long long* err_key, int no_ghosts) {
   __shared__ double s_st[kGatherBlock * NCOL];
   int64_t k0 = (int64_t)blockIdx.x * kGatherBlock;
   int64_t k = k0 + threadIdx.x;
@@ -140,7 +140,11 @@ k_gather_state(int64_t n, const int64_t* perm, FieldIn in, FieldOut out, double 
     double m = in.mass[r], h = in.h[r];
     uint8_t sp = in.species[r];
     out.mass[k] = m; out.h[k] = h;
-    out.species[k] = sp; out.ghost[k] = in.ghost[r];
+    uint8_t gh = in.ghost[r];
+    out.species[k] = sp; out.ghost[k] = gh;
+    // HbStepArgs.last_fields_event is for sets without ghost rows (ghost rows
+    // would need their input density before pass B)
+    if (no_ghosts && gh != 0) atomicMin(err_key, 7ull);
     row[C_M] = m; row[C_H] = h;
     row[C_SP] = (double)sp;
     if (sp == 1 && !(h <= h_lim)) atomicMin(err_key, 3ull);
@@ -221,6 +225,8 @@ __global__ void k_split_row(const int64_t* bin_ptr, const int64_t* leaf_start, i
 // 2 accumulator overflow, 3 gas smoothing length above the step's h_max
 static int step_key_error(unsigned long long ek, HbError* err) {
   if (err) { err->leaf_a = -1; err->leaf_b = -1; }
+  if (ek == 7)
+    return set_err(err, HB_CONTRACT, "last_fields_event given for a set with ghost rows");
   if (ek % 4 == 3)
     return set_err(err, HB_CONTRACT, "gas smoothing length exceeds the step's h_max");
   return set_err(err, (ek % 4) == 1 ? HB_NONFINITE : HB_OVERFLOW,
@@ -359,12 +365,10 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                    a->species, a->ghost, a->image_shift, a->global_id};
     if (late_split) {
       k_gather_state<true><<<grid_for(n, kGatherBlock), kGatherBlock, 0, st>>>(
-          n, a->perm, fi, fo, a->eos_gamma, w.state, h_lim,
-                                               w.err_key);
+          n, a->perm, fi, fo, a->eos_gamma, w.state, h_lim, w.err_key, last_split ? 1 : 0);
     } else {
       k_gather_state<false><<<grid_for(n, kGatherBlock), kGatherBlock, 0, st>>>(
-          n, a->perm, fi, fo, a->eos_gamma, w.state, h_lim,
-                                                w.err_key);
+          n, a->perm, fi, fo, a->eos_gamma, w.state, h_lim, w.err_key, 0);
       if (a->ghost_src_in && a->ghost_src) {
         k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
         k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);

@@ -431,3 +431,24 @@ def test_gpu_host_stepper_four_groups_matches_sync_step():
         np.testing.assert_array_equal(got["density"], ref_fields["density"])
         for f, v in rk.fields().items():
             np.testing.assert_array_equal(v.cpu().numpy(), ref_fields[f], err_msg=f)
+
+
+def test_gpu_last_fields_event_rejects_ghost_rows(golden):
+    """The four-group upload (HbStepArgs.last_fields_event) is only for sets
+    without ghost rows; on an overloaded set the step raises HydroboxError."""
+    import torch
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.errors import HydroboxError
+    from paper_2510_03557_b200.resident import ResidentRank, StepConfig
+    g = golden("step")
+    cfg = StepConfig(box=BoxGeometry(1.0), bin_width=float(g["bin_width"]), max_leaf_size=256,
+                     r_s=float(g["r_s"]), r_cut=float(g["r_cut"]), softening=float(g["eps"]),
+                     bounds_lo=g["bounds_lo"], bounds_hi=g["bounds_hi"])
+    p = particle_set(g, "in_")
+    assert np.any(p.ghost)
+    rk = ResidentRank(p, cfg)
+    ev_late, ev_last = torch.cuda.Event(), torch.cuda.Event()
+    ev_late.record()
+    ev_last.record()
+    with pytest.raises(HydroboxError, match="ghost rows"):
+        rk.step(late_fields=ev_late, last_fields=ev_last)
