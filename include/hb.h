@@ -261,9 +261,10 @@ typedef struct HbStepArgs {
   int32_t passes;    /* HB_PASS_* mask                                        */
   int32_t timing;    /* 1: fill ms_phase with per-phase device times          */
   int32_t gravity_mode; /* 0 auto (= 4 when every bin fits the tiler, else 1),
-                           1 leaf tiles + leaf list, 2 bin half-warp tiles
-                           (k_gravity2, r/t table), 3 bin tiles + 27-bin stencil
-                           (k_gravity, r/t table), 4 as 3 with the soft-bits table */
+                           1 leaf tiles + leaf list, 4 bin tiles + 27-bin
+                           stencil (k_gravity, soft-bits table).  2 and 3
+                           (round 1's half-warp and r/t-table variants) were
+                           removed and return HB_CONTRACT                     */
   int32_t ghost_density; /* 1: ghost-only leaves are density receivers too, so
                             ghost rows near the rank face get fresh rho, P, c_s
                             (multi-rank; fixes SURVEY.md finding 4); gravity,

@@ -71,8 +71,6 @@ struct GravBinArgs {
   double* out;
   unsigned long long* err_key;
   int* overflow_host;
-  bool half_warp;
-  int table_kind;  // GT_* for k_gravity (hb_pairs.cuh)
   const uint8_t* ghost = nullptr;  // owned_targets: skip tiles without an owned row
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // optional: recorded around the pair kernel
   // optional: run the pair kernel in two launches split at bin nbins / 2 and

@@ -838,19 +838,14 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 // per-source cull against the target tile box; survivors staged in shared
 // memory and broadcast to the 32 target lanes), but the pair function comes
 // from a cubic-per-interval table in shared memory and m_i is applied once
-// per target.  Table kinds (host fit in float64 at Chebyshev nodes):
-//   GT_SOFT: indexed by the float bits of soft = r^2 + eps^2 (2^JB intervals
-//            per octave: index = bits >> (23 - JB), in-interval variable = the
-//            low 23 - JB mantissa bits as a float in [1, 1 + 2^-JB) minus 1),
-//            storing G(soft) = S(sqrt(soft - eps^2) / r_s) * soft^{-3/2}.  Per
-//            pair: 3 FADD + 3 FFMA (soft) + LEA.HI + VIMNMX + 2 LOP3 + FADD +
-//            LEA + LDS + 3 FFMA + FMUL + 3 FFMA, no MUFU.  FP32 abs. error in S
-//            < 1.2e-7 (JB = 5) / 3.4e-7 (JB = 4).  The gather is the bound: its
-//            shared-memory wavefronts grow with the number of distinct rows the
-//            32 (nearby) targets touch, so the coarser JB = 4 table is cheaper.
-//   GT_T:    indexed by t = sqrt(r^2 + eps^2) = soft * rsqrt(soft) with the
-//            float magic-number trick, storing S(sqrt(t^2 - eps^2) / r_s)
-//            (eps <= 0.05 r_s); GT_R: by r = r^2 * rsqrt(r^2).  One or two MUFU.
+// per target.  The table (host fit in float64 at Chebyshev nodes) is indexed
+// by the float bits of soft = r^2 + eps^2 (2^JB intervals per octave: index =
+// bits >> (23 - JB), in-interval variable = the low 23 - JB mantissa bits as a
+// float in [1, 1 + 2^-JB) minus 1) and stores G(soft) = S(sqrt(soft - eps^2) /
+// r_s) * soft^{-3/2}.  Per pair: 3 FADD + 3 FFMA (soft) + LEA.HI + VIMNMX + 2
+// LOP3 + FADD + LEA + LDS + 3 FFMA + FMUL + 3 FFMA, no MUFU.  Fit error ~2e-8
+// relative (JB = 5, default) / ~3e-7 (JB = 4).  (Round 1's r- and t-indexed S
+// tables -- one or two MUFU and 27 instructions per pair -- were removed.)
 // Rows past r_cut (to the end of the interval holding r_cut) carry the smooth
 // continuation (|S| <= S(r_cut/r_s) < 1e-5 by the ForceSplit guard); the next
 // row is zero.  (A persistent grid loading the table once per CTA measured
@@ -858,7 +853,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 constexpr int kGravWarps = 8;
 constexpr int kGravStage = 128;
 
-template <int KIND, int JB, int REP, int kGravBatch>
+template <int JB, int REP, int kGravBatch>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -880,7 +875,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   auto flush = [&]() {
     __syncwarp();
     int q0 = 0;
-    if (KIND == GT_SOFT && kGravBatch > 1) {
+    {
       // batches of kGravBatch sources: every table row is requested before the
       // first one is used, so the gathers' latency overlaps within the warp
       // (the unrolled per-pair loop stalled on each row: short scoreboard).
@@ -912,26 +907,12 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
     for (int q = q0; q < cnt; ++q) {
       float4 s = stage[q];
       float dx = ti.x - s.x, dy = ti.y - s.y, dz = ti.z - s.z;
-      float w;
-      if (KIND == GT_SOFT) {
-        float soft = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
-        unsigned bits = __float_as_uint(soft);
-        unsigned k = min((bits >> (23 - JB)) - gt.base, gt.last);
-        float u = __uint_as_float((bits & ((1u << (23 - JB)) - 1u)) | 0x3F800000u) - 1.0f;
-        float4 c = s_tab[k * REP];
-        w = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x) * s.w;
-      } else {
-        float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        float soft = r2 + eps2;
-        float ri = rsqrt_ftz(soft);
-        float rr = KIND == GT_T ? soft * ri : r2 * rsqrt_ftz(fmaxf(r2, 1e-30f));
-        float fm = fmaf(rr, gt.scale, 12582912.0f);
-        int k = min(__float_as_int(fm) - 0x4B400000, (int)gt.last);
-        float u = fmaf(rr, gt.scale, 12582912.0f - fm);
-        float4 c = s_tab[k * REP];
-        float S = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x);
-        w = (S * (ri * ri)) * (ri * s.w);
-      }
+      float soft = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
+      unsigned bits = __float_as_uint(soft);
+      unsigned k = min((bits >> (23 - JB)) - gt.base, gt.last);
+      float u = __uint_as_float((bits & ((1u << (23 - JB)) - 1u)) | 0x3F800000u) - 1.0f;
+      float4 c = s_tab[k * REP];
+      float w = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x) * s.w;
       ax = fmaf(w, dx, ax);
       ay = fmaf(w, dy, ay);
       az = fmaf(w, dz, az);
@@ -1002,7 +983,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int KIND, int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
+template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev) {
@@ -1013,36 +994,11 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * WARPS + wid + (t_begin_dev ? *t_begin_dev : 0);
   if (t < *n_tiles_dev)
-    grav_tile<KIND, JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
+    grav_tile<JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
                                  t, lane);
 }
 
-// HB_GRAV_BATCH: sources per pipelined batch (1, 2, 4, 8).  c2 k_gravity:
-// 10.31 / 10.17 / 10.15 / 10.04 ms -> 8
-static int gravity_batch() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HB_GRAV_BATCH");
-    int x = e ? atoi(e) : 8;
-    v = (x == 1 || x == 2 || x == 4) ? x : 8;
-  }
-  return v;
-}
-
-// HB_GRAV_OCC (A/B only): 0 = 8 table copies, 4 CTAs/SM (64 regs); 1 = 2
-// copies, 5 CTAs (51 regs), batch 8; 2 = same, batch 4; 3 = 2 copies, 6 CTAs
-// (42 regs), batch 4; 4 = 1 copy, 6 CTAs, batch 4.
-static int gravity_occupancy() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HB_GRAV_OCC");
-    int x = e ? atoi(e) : 0;
-    v = (x >= 0 && x <= 4) ? x : 0;
-  }
-  return v;
-}
-
-template <int KIND, int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
+template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                int64_t tcap, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err) {
@@ -1056,40 +1012,28 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<KIND, JB, REP, NB, MINB, WARPS>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
   }
   unsigned grid = grid_for(tcap, WARPS), blk = WARPS * 32;
-  k_gravity<KIND, JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
+  k_gravity<JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
   return HB_OK;
 }
 
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
                         const int64_t* ntd, cudaStream_t st, HbError* err,
                         const int64_t* t_begin) {
-  int nb = gravity_batch();
-  int occ = gravity_occupancy();
-  int rc;
-  if (gt.kind == GT_SOFT && gt.jbits == 4 && occ)
-    rc = occ == 1   ? launch_gravity_kind<GT_SOFT, 4, 8, 2, 5>(d, table, gt, tcap, ntd, t_begin, st, err)
-         : occ == 2 ? launch_gravity_kind<GT_SOFT, 4, 4, 2, 5>(d, table, gt, tcap, ntd, t_begin, st, err)
-         : occ == 3 ? launch_gravity_kind<GT_SOFT, 4, 4, 2, 6>(d, table, gt, tcap, ntd, t_begin, st, err)
-                    : launch_gravity_kind<GT_SOFT, 4, 4, 1, 6>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else if (gt.kind == GT_SOFT && gt.jbits == 5)
-    // the 32-per-octave table is twice the 8-copy footprint (~70 KB): 16-warp
-    // CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4
-    rc = launch_gravity_kind<GT_SOFT, 5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else if (gt.kind == GT_SOFT)
-    rc = nb == 1   ? launch_gravity_kind<GT_SOFT, 4, 1>(d, table, gt, tcap, ntd, t_begin, st, err)
-         : nb == 2 ? launch_gravity_kind<GT_SOFT, 4, 2>(d, table, gt, tcap, ntd, t_begin, st, err)
-         : nb == 8 ? launch_gravity_kind<GT_SOFT, 4, 8>(d, table, gt, tcap, ntd, t_begin, st, err)
-                   : launch_gravity_kind<GT_SOFT, 4, 4>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else if (gt.kind == GT_T)
-    rc = launch_gravity_kind<GT_T, 0, 1>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else
-    rc = launch_gravity_kind<GT_R, 0, 1>(d, table, gt, tcap, ntd, t_begin, st, err);
+  // batches of 8 sources per pipelined table gather (1 / 2 / 4: 10.31 / 10.17 /
+  // 10.15 ms against 10.04 ms at c2 in round 1); 8 interleaved table copies.
+  // The 32-per-octave table (default) is twice the 8-copy footprint (~70 KB):
+  // 16-warp CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4.
+  // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
+  // gone.)
+  int rc = gt.jbits == 4
+               ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err)
+               : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err);
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;
@@ -1122,62 +1066,44 @@ static float4 cheb_cubic(double lo, double hi, double (*f)(double, const double*
 static double split_s(double x) { return erfc(x) + 1.1283791670955126 * x * exp(-x * x); }
 static unsigned f2u(float f) { unsigned u; memcpy(&u, &f, 4); return u; }
 static float u2f(unsigned u) { float f; memcpy(&f, &u, 4); return f; }
-// prm: r_s, eps, x0, kind, scale.  GT_SOFT: u in [0, 2^-5) is the in-interval
-// mantissa offset, soft = x0 + scale * u (x0 = interval start, scale = 2^exponent).
-// GT_R / GT_T: u in [-1/2, 1/2] interval units around x0 = k * dr, r = x0 + scale * u.
+// prm: r_s, eps, x0, scale.  u in [0, 2^-jb) is the in-interval mantissa
+// offset, soft = x0 + scale * u (x0 = interval start, scale = 2^exponent).
 static double tab_fn(double u, const double* p) {
-  double rs = p[0], eps = p[1], x0 = p[2], sc = p[4];
-  if ((int)p[3] == GT_SOFT) {
-    double soft = x0 + sc * u;
-    return split_s(sqrt(fmax(soft - eps * eps, 0.0)) / rs) * pow(soft, -1.5);
-  }
-  double rv = x0 + sc * u;
-  if ((int)p[3] == GT_T) rv = sqrt(fmax(rv * rv - eps * eps, 0.0));
-  return split_s(rv / rs);
+  double rs = p[0], eps = p[1], x0 = p[2], sc = p[3];
+  double soft = x0 + sc * u;
+  return split_s(sqrt(fmax(soft - eps * eps, 0.0)) / rs) * pow(soft, -1.5);
 }
 
-int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_out, GravTab* gt) {
-  gt->kind = kind;
-  if (kind == GT_SOFT) {
-    static int jb = 0;
-    if (!jb) {  // HB_GRAV_JBITS: 4 (default) or 5 intervals-per-octave bits
-      const char* e = getenv("HB_GRAV_JBITS");
-      jb = e ? (atoi(e) == 4 ? 4 : 5) : kGravSoftBitsDefault;
-    }
-    gt->jbits = jb;
-    const int sh = 23 - jb;
-    float scut = (float)(r_cut * r_cut + eps * eps);
-    // lowest row: eps^2, floored so the table spans <= kGravSoftOctaves octaves
-    // (soft below the floor -- only r < 2^-20 r_cut at eps = 0 -- reads zero)
-    double fl = fmax(eps * eps, ldexp((double)scut, -kGravSoftOctaves + 1));
-    float smin = (float)fl;
-    unsigned base = f2u(smin) >> sh;
-    unsigned kc = f2u(scut) >> sh;
-    unsigned rows = kc - base + 1;
-    if (rows + 1 > (unsigned)kGravTableMax) return -1;
-    for (unsigned k = 0; k < rows; ++k) {
-      unsigned b = (base + k) << sh;
-      float f0 = u2f(b);
-      int e = 0;
-      frexp((double)f0, &e);
-      double prm[5] = {r_s, eps, (double)f0, (double)GT_SOFT, ldexp(1.0, e - 1)};
-      host_out[k] = cheb_cubic(0.0, ldexp(1.0, -jb), tab_fn, prm);
-      if (!(isfinite(host_out[k].x) && isfinite(host_out[k].y) && isfinite(host_out[k].z) &&
-            isfinite(host_out[k].w)))
-        return -1;
-    }
-    host_out[rows] = make_float4(0.f, 0.f, 0.f, 0.f);
-    gt->base = base; gt->last = rows; gt->rows = (int)rows + 1; gt->scale = 0.f;
-    return gt->rows;
+int gravity_table(double r_s, double r_cut, double eps, float4* host_out, GravTab* gt) {
+  static int jb = 0;
+  if (!jb) {  // HB_GRAV_JBITS: 5 (default) or 4 intervals-per-octave bits
+    const char* e = getenv("HB_GRAV_JBITS");
+    jb = e ? (atoi(e) == 4 ? 4 : 5) : kGravSoftBitsDefault;
   }
-  double dr = r_cut / kGravTableN;
-  for (int k = 0; k <= kGravTableN; ++k) {
-    double prm[5] = {r_s, eps, k * dr, (double)kind, dr};
-    host_out[k] = cheb_cubic(-0.5, 0.5, tab_fn, prm);
+  gt->jbits = jb;
+  const int sh = 23 - jb;
+  float scut = (float)(r_cut * r_cut + eps * eps);
+  // lowest row: eps^2, floored so the table spans <= kGravSoftOctaves octaves
+  // (soft below the floor -- only r < 2^-20 r_cut at eps = 0 -- reads zero)
+  double fl = fmax(eps * eps, ldexp((double)scut, -kGravSoftOctaves + 1));
+  float smin = (float)fl;
+  unsigned base = f2u(smin) >> sh;
+  unsigned kc = f2u(scut) >> sh;
+  unsigned rows = kc - base + 1;
+  if (rows + 1 > (unsigned)kGravTableMax) return -1;
+  for (unsigned k = 0; k < rows; ++k) {
+    unsigned b = (base + k) << sh;
+    float f0 = u2f(b);
+    int e = 0;
+    frexp((double)f0, &e);
+    double prm[4] = {r_s, eps, (double)f0, ldexp(1.0, e - 1)};
+    host_out[k] = cheb_cubic(0.0, ldexp(1.0, -jb), tab_fn, prm);
+    if (!(isfinite(host_out[k].x) && isfinite(host_out[k].y) && isfinite(host_out[k].z) &&
+          isfinite(host_out[k].w)))
+      return -1;
   }
-  host_out[kGravTableN + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-  gt->base = 0; gt->last = kGravTableN + 1; gt->rows = kGravTableN + 2; gt->jbits = 0;
-  gt->scale = (float)(kGravTableN / r_cut);
+  host_out[rows] = make_float4(0.f, 0.f, 0.f, 0.f);
+  gt->base = base; gt->last = rows; gt->rows = (int)rows + 1;
   return gt->rows;
 }
 
@@ -1185,12 +1111,11 @@ int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_o
 // parameters change.  A per-step upload from pageable host memory would be
 // host-synchronous (and on the legacy stream wait for all device work),
 // which serialised the gravity chain behind the concurrent SPH chain.
-const float4* gravity_table_device(double r_s, double r_cut, double eps, int kind, GravTab* gt,
+const float4* gravity_table_device(double r_s, double r_cut, double eps, GravTab* gt,
                                    cudaStream_t st, HbError* err) {
   struct Slot {
     bool ok = false;
     double r_s, r_cut, eps;
-    int kind;
     GravTab gt;
     float4* dev = nullptr;
     float4* host = nullptr;
@@ -1213,7 +1138,7 @@ const float4* gravity_table_device(double r_s, double r_cut, double eps, int kin
   Slot* victim = &slots[dev][0];
   for (int k = 0; k < kSlots; ++k) {
     Slot& c = slots[dev][k];
-    if (c.ok && c.r_s == r_s && c.r_cut == r_cut && c.eps == eps && c.kind == kind) {
+    if (c.ok && c.r_s == r_s && c.r_cut == r_cut && c.eps == eps) {
       c.used = ++tick;
       *gt = c.gt;
       return c.dev;
@@ -1232,7 +1157,7 @@ const float4* gravity_table_device(double r_s, double r_cut, double eps, int kin
     set_err(err, HB_CUDA, "gravity table allocation failed");
     return nullptr;
   }
-  if (gravity_table(r_s, r_cut, eps, kind, sl.host, gt) < 0) {
+  if (gravity_table(r_s, r_cut, eps, sl.host, gt) < 0) {
     set_err(err, HB_CONTRACT, "gravity table: r_cut / softening not representable");
     return nullptr;
   }
@@ -1244,15 +1169,10 @@ const float4* gravity_table_device(double r_s, double r_cut, double eps, int kin
     return nullptr;
   }
   sl.used = ++tick;
-  sl.ok = true; sl.r_s = r_s; sl.r_cut = r_cut; sl.eps = eps; sl.kind = kind; sl.gt = *gt;
+  sl.ok = true; sl.r_s = r_s; sl.r_cut = r_cut; sl.eps = eps; sl.gt = *gt;
   return sl.dev;
 }
 
-int gravity_kind(int gravity_mode, double eps, double r_s) {
-  if (gravity_mode == 3 || gravity_mode == 2 || !kGravitySoftTable)
-    return eps <= 0.05 * r_s ? GT_T : GT_R;
-  return GT_SOFT;
-}
 
 // ---------------------------------------------------------------- driver pieces
 int64_t tile_capacity(int64_t n, int64_t n_leaves) { return n / 8 + 2 * n_leaves + 2; }

@@ -335,10 +335,10 @@ int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, const dou
 int launch_pairs(int kid, bool det, bool lean, const EvalDev& d, int64_t tile_cap,
                  const int64_t* n_tiles_dev, cudaStream_t st, HbError* err);
 int kid_selects_gas(int kid);
-// resident fast gravity: table of S(r/r_s), 128 cubic intervals over [0, r_cut]
-constexpr int kGravTableN = 128;            // GT_R / GT_T intervals over [0, r_cut]
-constexpr int kGravTableRMax = kGravTableN + 2;
-constexpr int kGravSoftBitsMax = 5;         // GT_SOFT: 2^jbits intervals per octave of soft
+// resident fast gravity: table of G(soft) = S(sqrt(soft - eps^2)/r_s) soft^-3/2,
+// cubic per interval of soft, 2^jbits intervals per octave (indexed by the
+// float bits of soft)
+constexpr int kGravSoftBitsMax = 5;
 // 32 intervals per octave (cubic fit error ~2e-8 relative; 16 per octave leave
 // ~3e-7, which near-cancelling dark-matter lattices amplify past the 1e-5
 // relative gate).  The twice larger table runs in 16-warp CTAs so residency
@@ -347,20 +347,16 @@ constexpr int kGravSoftBitsMax = 5;         // GT_SOFT: 2^jbits intervals per oc
 constexpr int kGravSoftBitsDefault = 5;
 constexpr int kGravSoftOctaves = 40;
 constexpr int kGravTableMax = (kGravSoftOctaves + 1) * (1 << kGravSoftBitsMax) + 2;
-constexpr bool kGravitySoftTable = true;    // gravity_mode 0/1/4 use GT_SOFT
-enum { GT_R = 0, GT_T = 1, GT_SOFT = 2 };
 struct GravTab {
-  int kind, rows;  // rows to stage in shared memory (the last one is zero)
-  float scale;     // GT_R / GT_T: intervals per unit r (or t)
-  unsigned base;   // GT_SOFT: (bits of the lowest soft) >> (23 - jbits)
+  int rows;        // rows to stage in shared memory (the last one is zero)
+  unsigned base;   // (bits of the lowest soft) >> (23 - jbits)
   unsigned last;   // zero row index
-  int jbits;       // GT_SOFT: log2(intervals per octave), 4 or 5
+  int jbits;       // log2(intervals per octave), 4 or 5
 };
 // host: fill host_out (kGravTableMax rows) and gt; returns rows or -1 (unrepresentable)
-int gravity_table(double r_s, double r_cut, double eps, int kind, float4* host_out, GravTab* gt);
-int gravity_kind(int gravity_mode, double eps, double r_s);
+int gravity_table(double r_s, double r_cut, double eps, float4* host_out, GravTab* gt);
 // cached device copy (library-owned, per device); nullptr + err on failure
-const float4* gravity_table_device(double r_s, double r_cut, double eps, int kind, GravTab* gt,
+const float4* gravity_table_device(double r_s, double r_cut, double eps, GravTab* gt,
                                    cudaStream_t st, HbError* err);
 // tiles [*t_begin (0 if null), *ntd)
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,

@@ -289,7 +289,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     Arena g = ws;
     g.dry = true;
     GravBinArgs gd = {};
-    gd.n = n; gd.nbins = nbins; gd.half_warp = true;  // the larger tiling of the two
+    gd.n = n; gd.nbins = nbins;
     gravity_bins(gd, g, st, err);
     Arena mm = ws;
     mm.used = g.used;
@@ -320,13 +320,15 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     build_tiling(w.Tg, cap, nullptr, nullptr, nullptr, nullptr, 0.0, 1, nullptr, s3, st, err);
     if (s3.used > mx) mx = s3.used;
     GravBinArgs gb = {};
-    gb.n = n; gb.nbins = nbins; gb.half_warp = true;
+    gb.n = n; gb.nbins = nbins;
     Arena s4 = ws; gravity_bins(gb, s4, st, err); if (s4.used > mx) mx = s4.used;
     if (mom_end > mx) mx = mom_end;
     ws.used = mx;
     return HB_OK;
   }
   if (!ws.ok() || mom_end > ws.cap) return set_err(err, HB_CONTRACT, "workspace too small (step)");
+  if (a->gravity_mode == 2 || a->gravity_mode == 3)
+    return set_err(err, HB_CONTRACT, "gravity_mode 2 / 3 (half-warp, r/t tables) were removed");
   if (n <= 0) return HB_OK;
   if (n >= (1LL << 31)) return set_err(err, HB_CONTRACT, "too many rows for one rank");
   PhaseTimer tm(a->timing != 0, st);
@@ -540,11 +542,8 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     gb.leaf_end = w.leaf_end; gb.geom = ld.g; gb.state = w.state; gb.pshift = a->image_shift;
     gb.L = a->side_length; gb.r_s = a->r_s; gb.r_cut = a->r_cut; gb.eps = a->softening;
     gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
-    gb.half_warp = a->gravity_mode == 2;
-    gb.table_kind = gravity_kind(a->gravity_mode, a->softening, a->r_s);
     gb.ghost = a->owned_targets ? a->ghost : nullptr;
     gb.count_only = (a->passes & HB_PASS_COUNT_ONLY) != 0;
-    if (gb.count_only) gb.half_warp = false;
     if (sph_bins) {  // the SPH tiling's bin segments and stencil are the same arrays
       gb.pre_seg_s = w.seg_s; gb.pre_seg_e = w.seg_e; gb.pre_st_ptr = w.st_ptr;
       gb.pre_st_src = w.st_src; gb.pre_st_code = w.st_code;
@@ -656,7 +655,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
       } else {
       GravTab gt;
       const float4* gtab = gravity_table_device(
-          a->r_s, a->r_cut, a->softening, gravity_kind(a->gravity_mode, a->softening, a->r_s), &gt,
+          a->r_s, a->r_cut, a->softening, &gt,
           st, err);
       if (!gtab) return err ? err->status : HB_CUDA;
       tm.kmark(0);

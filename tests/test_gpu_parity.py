@@ -262,18 +262,16 @@ def test_gpu_resident_force_step(golden, oracle):
 
 @pytest.mark.parametrize("sigma,h_jitter,mode,L,phys", [
     (0.05, 0.0, 0, 1.0, None), (1.0, 0.0, 0, 1.0, None), (2.5, 0.0, 0, 1.0, None),
-    (1.0, 0.35, 0, 1.0, None), (1.0, 0.35, 1, 1.0, None), (1.0, 0.35, 2, 1.0, None),
-    (1.0, 0.35, 3, 1.0, None), (1.0, 0.35, 0, 3.0, None), (1.0, 0.35, 0, 1.0, (1.4, 0.5, 1.0)),
-    (1.0, 0.35, 1, 1.0, "leaf64")])
+    (1.0, 0.35, 0, 1.0, None), (1.0, 0.35, 1, 1.0, None), (1.0, 0.35, 0, 3.0, None),
+    (1.0, 0.35, 0, 1.0, (1.4, 0.5, 1.0)), (1.0, 0.35, 1, 1.0, "leaf64")])
 def test_gpu_force_step_vs_oracle_c1(oracle, sigma, h_jitter, mode, L, phys, monkeypatch):
     """hb_force_step at 2x32^3 (config C1, near-uniform and shell-crossing
     Zel'dovich ICs) against the oracle's ordered evaluation of the same step:
     leaf order and neighbour counts bit-exact, the rest within FP32 tolerance.
     h_jitter > 0: gas smoothing lengths scattered by +-h_jitter (adapted h
     varies between neighbours; the tile culls must use the tile's largest h).
-    mode: HbStepArgs.gravity_mode -- 0 the default (bin tiles, soft table); 1
-    leaf tiles for gravity and SPH (the fallback when a bin outgrows the tiler);
-    2 half-warp bin gravity; 3 bin gravity with the r/t table.  L: box side
+    mode: HbStepArgs.gravity_mode -- 0 the default (bin tiles); 1 leaf tiles for
+    gravity and SPH (the fallback when a bin outgrows the tiler).  L: box side
     (every length scales with it).  phys: (eos_gamma, visc_alpha, visc_beta)
     other than the defaults (5/3, 1, 2)."""
     max_leaf = 64 if phys == "leaf64" else 256     # "leaf64": leaves of <= 64
@@ -452,3 +450,29 @@ def test_gpu_last_fields_event_rejects_ghost_rows(golden):
     ev_last.record()
     with pytest.raises(HydroboxError, match="ghost rows"):
         rk.step(late_fields=ev_late, last_fields=ev_last)
+
+
+def test_gpu_removed_gravity_modes_raise():
+    """HbStepArgs.gravity_mode 2 / 3 (round 1's half-warp and r/t-table
+    variants) were removed: the step says so instead of silently running
+    something else."""
+    import os
+    from paper_2510_03557_b200.box import BoxGeometry
+    from paper_2510_03557_b200.errors import HydroboxError
+    from paper_2510_03557_b200.ic import make_zeldovich_ic
+    from paper_2510_03557_b200.resident import ResidentRank, StepConfig
+    box = BoxGeometry(1.0)
+    p = make_zeldovich_ic(12, box, 0.5)
+    d = 1.0 / 12
+    cfg = StepConfig(box=box, bin_width=max(5 * d, 2 * float(p.smoothing.max())) * (1 + 1e-9),
+                     max_leaf_size=256, r_s=d, r_cut=5 * d, softening=d / 60)
+    old = os.environ.get("HB_GRAVITY_MODE")
+    try:
+        os.environ["HB_GRAVITY_MODE"] = "2"
+        with pytest.raises(HydroboxError, match="removed"):
+            ResidentRank(p, cfg).step()
+    finally:
+        if old is None:
+            os.environ.pop("HB_GRAVITY_MODE", None)
+        else:
+            os.environ["HB_GRAVITY_MODE"] = old
