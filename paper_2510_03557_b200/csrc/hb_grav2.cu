@@ -95,7 +95,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   float4* P0 = ws.take<float4>(g.n + 1);
   if (ws.dry) {
     Arena s = ws;
-    build_tiling(T, nbins, nullptr, nullptr, nullptr, nullptr, 0.0, 0, nullptr, s, st, err);
+    build_tiling(T, nbins, nullptr, nullptr, Rows{}, nullptr, 0.0, 0, nullptr, s, st, err);
     ws.used = s.used;
     return HB_OK;
   }
@@ -117,11 +117,11 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     }
     {
       Arena s = ws;
-      rc = build_tiling(T, nbins, segs, sege, g.state, g.pshift, g.L, 0, ntd, s, st, err,
+      rc = build_tiling(T, nbins, segs, sege, g.rows, g.pshift, g.L, 0, ntd, s, st, err,
                         g.ghost);
       if (rc) return rc;
     }
-    rc = pack_records(KID_GRAVITY, T, ntd, g.state, g.pshift, nullptr, 0, g.L, P0, nullptr,
+    rc = pack_records(KID_GRAVITY, T, ntd, g.rows, g.pshift, nullptr, 0, g.L, P0, nullptr,
                       nullptr, st, err);
     if (rc) return rc;
   }
@@ -138,7 +138,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   if (g.count_only) {  // k_eval<KID_COUNTING>, float64 band re-check, no self pair
     EvalDev e = {};
     e.T = T; e.ent_ptr = sptr; e.ent_src = ssrc; e.ent_code = scode; e.P0 = P0;
-    e.state = g.state; e.pshift = g.pshift;
+    e.rows = g.rows; e.pshift = g.pshift;
     e.L = g.L; e.reach = g.r_cut;
     e.pp.reach2 = (float)(g.r_cut * g.r_cut);
     e.cull_reach = (float)(g.r_cut * (1.0 + 1e-4)) + 1e-30f;

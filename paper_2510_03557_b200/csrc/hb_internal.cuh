@@ -34,7 +34,7 @@ struct SphArgs {
   const int32_t* ent_src;
   const int32_t* ent_code;
   const float4 *P0, *P1, *P2, *P3;
-  const double* state;
+  Rows rows;
   const int8_t* pshift;
   double L, reach;
   float band;  // relative band of r^2 around a threshold decided in float64
@@ -48,7 +48,7 @@ struct SphArgs {
   const uint8_t* skip_leaf;
   int skip_tiles;  // pass B: skip tiles without an owned member
 };
-int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
+int pack_sph(const Tiling& T, const int64_t* ntd, Rows rows, const int8_t* pshift,
              double L, float4* P0, float4* P1, float4* P2, float4* P3, int layout,
              cudaStream_t st, HbError* err, const double* rho = nullptr,
              const double* u = nullptr, double gamma = 0.0);
@@ -65,7 +65,7 @@ struct GravBinArgs {
   int64_t n, nbins;
   const int64_t *bin_ptr, *leaf_start, *leaf_end;
   ListGeom geom;
-  const double* state;
+  Rows rows;
   const int8_t* pshift;
   double L, r_s, r_cut, eps;
   double* out;

@@ -33,14 +33,14 @@ constexpr int kStage = 64;           // staged sources per warp
 
 // ---------------------------------------------------------------- tiling
 __global__ void k_tile_count(int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
-                             const double* state, int sel, int64_t* sel_cnt, int64_t* tile_cnt,
+                             Rows rows, int sel, int64_t* sel_cnt, int64_t* tile_cnt,
                              int tile_max, int even) {
   int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (leaf >= n_leaves) return;
   int64_t s = leaf_start[leaf], e = leaf_end[leaf];
   int c = 0;
-  for (int64_t r = s + lane; r < e; r += 32) c += (sel == 0 || state[r * NCOL + C_SP] == 1.0);
+  for (int64_t r = s + lane; r < e; r += 32) c += (sel == 0 || rows.gas(r));
 #pragma unroll
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if (lane == 0) {
@@ -61,13 +61,13 @@ __device__ __forceinline__ double bin_coord(double p, int8_t s, double L) {
 // state row).
 __device__ __forceinline__ void emit_tile_box(Tiling& T, int64_t t, int start, int m, bool have,
                                               float cx, float cy, float cz, int64_t r,
-                                              const double* state, const uint8_t* ghost) {
+                                              const Rows& rows, const uint8_t* ghost) {
   float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   float hm = 0.0f;
   bool own = false;
   if (have) {
     lo[0] = hi[0] = cx; lo[1] = hi[1] = cy; lo[2] = hi[2] = cz;
-    hm = (float)state[r * NCOL + C_H];
+    hm = (float)rows.hh(r);
     own = ghost && ghost[r] == 0;
   }
 #pragma unroll
@@ -91,7 +91,7 @@ __device__ __forceinline__ void emit_tile_box(Tiling& T, int64_t t, int start, i
 }
 
 __global__ void __launch_bounds__(kTileBuildBlock)
-k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const double* state,
+k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, Rows rows,
              const int8_t* pshift, double L, int sel, const uint8_t* ghost) {
   __shared__ int32_t s_row[kTileBuildCap];
   __shared__ int32_t s_tmp[kTileBuildCap];
@@ -118,7 +118,7 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
   int base = 0;
   for (int64_t r0 = s; r0 < e; r0 += blockDim.x) {
     int64_t r = r0 + threadIdx.x;
-    int f = r < e && (sel == 0 || state[r * NCOL + C_SP] == 1.0);
+    int f = r < e && (sel == 0 || rows.gas(r));
     // block exclusive scan of f
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned b = __ballot_sync(0xffffffffu, f);
@@ -141,7 +141,7 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
     int64_t r = s_row[k];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double v = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+      double v = bin_coord(rows.x(r, d), pshift ? pshift[3 * r + d] : (int8_t)0, L);
       mn[d] = fmin(mn[d], v); mx[d] = fmax(mx[d], v);
     }
   }
@@ -170,7 +170,7 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
     int64_t r = s_row[k];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double v = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+      double v = bin_coord(rows.x(r, d), pshift ? pshift[3 * r + d] : (int8_t)0, L);
       s_c[d][k] = (float)(v - org[d]);
     }
   }
@@ -189,7 +189,7 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, const
         bool have = (int)threadIdx.x < m;
         int k = a0 + (have ? (int)threadIdx.x : 0);
         emit_tile_box(T, t, (int)(T.sel_off[leaf] + a0), m, have, s_c[0][k], s_c[1][k],
-                      s_c[2][k], s_row[k], state, ghost);
+                      s_c[2][k], s_row[k], rows, ghost);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -281,7 +281,7 @@ constexpr int kTileWarpCap = 384;
 constexpr int kTileWarps = 4;
 __global__ void __launch_bounds__(kTileWarps * 32)
 k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
-                  const double* state, const int8_t* pshift, double L, int sel, int nl,
+                  Rows rows, const int8_t* pshift, double L, int sel, int nl,
                   const uint8_t* ghost) {
   __shared__ int32_t s_row[kTileWarps][kTileWarpCap];
   __shared__ int32_t s_tmp[kTileWarps][kTileWarpCap];
@@ -302,7 +302,7 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
   int base = 0;
   for (int64_t r0 = s; r0 < e; r0 += 32) {
     int64_t r = r0 + lane;
-    bool f = r < e && (sel == 0 || state[r * NCOL + C_SP] == 1.0);
+    bool f = r < e && (sel == 0 || rows.gas(r));
     unsigned b = __ballot_sync(0xffffffffu, f);
     if (f) row[base + __popc(b & lanemask_lt())] = (int32_t)r;
     base += __popc(b);
@@ -314,7 +314,7 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     int64_t r = row[k];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double v = bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+      double v = bin_coord(rows.x(r, d), pshift ? pshift[3 * r + d] : (int8_t)0, L);
       mn[d] = fmin(mn[d], v); mx[d] = fmax(mx[d], v);
     }
   }
@@ -333,7 +333,7 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
     int64_t r = row[k];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
-      cc[d][k] = (float)(bin_coord(state[r * NCOL + d], pshift ? pshift[3 * r + d] : (int8_t)0, L) -
+      cc[d][k] = (float)(bin_coord(rows.x(r, d), pshift ? pshift[3 * r + d] : (int8_t)0, L) -
                          org[d]);
   }
   __syncwarp();
@@ -360,7 +360,7 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
         bool have = lane < m;
         int id = have ? ord[a0 + lane] : 0;
         emit_tile_box(T, t, (int)(so + a0), m, have, cc[0][id], cc[1][id], cc[2][id], row[id],
-                      state, ghost);
+                      rows, ghost);
       }
       if (lane == 0) {
         T.tile_start[t] = (int32_t)(so + a0);
@@ -476,7 +476,7 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
 
 // ---------------------------------------------------------------- packing
 __global__ void k_pack(int kid, int64_t n_tiles_cap, const int64_t* n_tiles_dev, const Tiling T,
-                       const double* state, const int8_t* pshift, const double* aux, int naux,
+                       Rows rows, const int8_t* pshift, const double* aux, int naux,
                        double L, float4* P0, float4* P1, float4* P2) {
   int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
@@ -485,14 +485,19 @@ __global__ void k_pack(int kid, int64_t n_tiles_cap, const int64_t* n_tiles_dev,
   int leaf = T.tile_leaf[t];
   int64_t k = T.tile_start[t] + lane;
   int64_t r = T.tperm[k];
-  const double* st = state + r * NCOL;
   float c[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    double v = bin_coord(st[d], pshift ? pshift[3 * r + d] : (int8_t)0, L);
+    double v = bin_coord(rows.x(r, d), pshift ? pshift[3 * r + d] : (int8_t)0, L);
     c[d] = (float)(v - T.origin[3 * leaf + d]);
   }
-  double m = st[C_M], h = st[C_H], rho = st[C_RHO];
+  double m = rows.m(r);
+  if (kid == KID_GRAVITY || kid == KID_GRAV_POT || kid == KID_COUNTING ||
+      kid == KID_STUB_ZERO) {  // position + mass records only
+    P0[k] = make_float4(c[0], c[1], c[2], (float)m);
+    return;
+  }
+  double h = rows.hh(r), rho = rows.dens(r);
   double sig = 0.31830988618379067;
   double norm3 = h > 0 ? sig / (h * h * h) : 0.0;
   double hinv = h > 0 ? 1.0 / h : 0.0;
@@ -512,11 +517,11 @@ __global__ void k_pack(int kid, int64_t n_tiles_cap, const int64_t* n_tiles_dev,
       break;
     }
     case KID_HYDRO_FORCE: {
-      double fpart = rho > 0 ? st[C_P] / (rho * rho) : 0.0;
+      double fpart = rho > 0 ? rows.pres(r) / (rho * rho) : 0.0;
       double norm5 = h > 0 ? sig / (h * h * h * h * h) : 0.0;
       P0[k] = make_float4(c[0], c[1], c[2], (float)m);
-      P1[k] = make_float4((float)st[C_VX], (float)st[C_VY], (float)st[C_VZ], (float)h);
-      P2[k] = make_float4((float)fpart, (float)st[C_CS], (float)rho, (float)norm5);
+      P1[k] = make_float4((float)rows.v(r, 0), (float)rows.v(r, 1), (float)rows.v(r, 2), (float)h);
+      P2[k] = make_float4((float)fpart, (float)rows.snd(r), (float)rho, (float)norm5);
       break;
     }
     case KID_CRK_INTERP: {
@@ -607,7 +612,7 @@ __device__ __forceinline__ double exact_r2(const EvalDev& a, int64_t i, int64_t 
   for (int d = 0; d < 3; ++d) {
     int64_t pi = a.pshift ? a.pshift[3 * i + d] : 0, pj = a.pshift ? a.pshift[3 * j + d] : 0;
     int64_t tau = pi - pj - s[d];
-    double dx = __dadd_rn(__dsub_rn(a.state[i * NCOL + d], a.state[j * NCOL + d]),
+    double dx = __dadd_rn(__dsub_rn(a.rows.x(i, d), a.rows.x(j, d)),
                           __dmul_rn((double)tau, a.L));
     r2 = d == 0 ? __dmul_rn(dx, dx) : __dadd_rn(r2, __dmul_rn(dx, dx));
   }
@@ -655,7 +660,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
   float thr_n = 0.0f;
   double thr_n64 = 0.0;
   if (KID == KID_NEIGHBOR_COUNT) {
-    double h = a.state[row_i * NCOL + C_H];
+    double h = a.rows.hh(row_i);
     thr_n64 = __dmul_rn(__dmul_rn(4.0, h), h);
     thr_n = (float)thr_n64;
   }
@@ -1199,7 +1204,7 @@ int kid_selects_gas(int kid) {
 }
 
 int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t* leaf_end,
-                 const double* state, const int8_t* pshift, double L, int sel,
+                 Rows rows, const int8_t* pshift, double L, int sel,
                  int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err,
                  const uint8_t* ghost) {
   if (ws.dry) {
@@ -1209,7 +1214,7 @@ int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t
     return HB_OK;
   }
   HB_CUDA_TRY(cudaMemsetAsync(T.overflow, 0, sizeof(int), st));
-  k_tile_count<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, leaf_start, leaf_end, state, sel,
+  k_tile_count<<<grid_for(nl * 32, 256), 256, 0, st>>>(nl, leaf_start, leaf_end, rows, sel,
                                                        T.sel_cnt, T.tile_cnt, T.tile_max, T.even);
   HB_LAUNCH_CHECK();
   {
@@ -1224,19 +1229,19 @@ int build_tiling(Tiling& T, int64_t nl, const int64_t* leaf_start, const int64_t
   }
   // the builders emit each tile's box as they cut it (emit_tile_box)
   k_tile_build_warp<<<grid_for(nl, kTileWarps), kTileWarps * 32, 0, st>>>(
-      T, leaf_start, leaf_end, state, pshift, L, sel, (int)nl, ghost);
+      T, leaf_start, leaf_end, rows, pshift, L, sel, (int)nl, ghost);
   HB_LAUNCH_CHECK();
-  k_tile_build<<<(unsigned)nl, kTileBuildBlock, 0, st>>>(T, leaf_start, leaf_end, state, pshift,
+  k_tile_build<<<(unsigned)nl, kTileBuildBlock, 0, st>>>(T, leaf_start, leaf_end, rows, pshift,
                                                          L, sel, ghost);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
 
-int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, const double* state,
+int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, Rows rows,
                  const int8_t* pshift, const double* aux, int naux, double L, float4* P0,
                  float4* P1, float4* P2, cudaStream_t st, HbError* err) {
   int64_t tcap = T.n_tiles_cap;
-  k_pack<<<grid_for(tcap * 32, 256), 256, 0, st>>>(kid, tcap, n_tiles_dev, T, state, pshift, aux,
+  k_pack<<<grid_for(tcap * 32, 256), 256, 0, st>>>(kid, tcap, n_tiles_dev, T, rows, pshift, aux,
                                                    naux, L, P0, P1, P2);
   HB_LAUNCH_CHECK();
   return HB_OK;
@@ -1307,7 +1312,7 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     radix_sort_u64_u32(w.keys, w.vals, E, 40, s1, st, err);
     exclusive_scan_i64(nullptr, nullptr, a->n_leaves + 1, nullptr, s2, st, err);
     exclusive_scan_i64(nullptr, nullptr, a->n_pairs + 1, nullptr, s3, st, err);
-    build_tiling(w.T, a->n_leaves, nullptr, nullptr, nullptr, nullptr, 0.0, 0, nullptr, s4, st, err);
+    build_tiling(w.T, a->n_leaves, nullptr, nullptr, Rows{}, nullptr, 0.0, 0, nullptr, s4, st, err);
     size_t mx = s1.used;
     if (s2.used > mx) mx = s2.used;
     if (s3.used > mx) mx = s3.used;
@@ -1363,10 +1368,10 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                                                       w.s_src, w.s_code, w.s_orig);
   HB_LAUNCH_CHECK();
   Tiling& T = w.T;
-  int rc0 = build_tiling(T, nl, a->leaf_start, a->leaf_end, a->state, a->pshift, a->side_length,
+  int rc0 = build_tiling(T, nl, a->leaf_start, a->leaf_end, Rows::state(a->state), a->pshift, a->side_length,
                          sel, w.n_tiles_dev, ws, st, err);
   if (rc0) return rc0;
-  rc0 = pack_records(a->kid, T, w.n_tiles_dev, a->state, a->pshift, a->aux, a->naux,
+  rc0 = pack_records(a->kid, T, w.n_tiles_dev, Rows::state(a->state), a->pshift, a->aux, a->naux,
                      a->side_length, w.P0, w.P1, w.P2, st, err);
   if (rc0) return rc0;
   int64_t tcap = T.n_tiles_cap;
@@ -1378,7 +1383,7 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   HB_LAUNCH_CHECK();
   EvalDev d = {};
   d.T = T; d.ent_ptr = w.ent_ptr; d.ent_src = w.s_src; d.ent_code = w.s_code;
-  d.P0 = w.P0; d.P1 = w.P1; d.P2 = w.P2; d.state = a->state; d.pshift = a->pshift;
+  d.P0 = w.P0; d.P1 = w.P1; d.P2 = w.P2; d.rows = Rows::state(a->state); d.pshift = a->pshift;
   d.L = a->side_length; d.reach = a->reach;
   d.pp.p0 = (float)a->params[0]; d.pp.p1 = (float)a->params[1];
   d.pp.inv_rs = a->params[0] != 0.0 ? (float)(1.0 / a->params[0]) : 0.0f;
@@ -1398,10 +1403,10 @@ int eval_pairs(HbEvalArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->exact_counters && sel) {
     // the reference counts pairs in reach over every species (hb/kernels.py:356-359)
     HB_CUDA_TRY(cudaMemsetAsync(w.dev_cnt + 2, 0, sizeof(unsigned long long), st));
-    rc = build_tiling(T, nl, a->leaf_start, a->leaf_end, a->state, a->pshift, a->side_length, 0,
+    rc = build_tiling(T, nl, a->leaf_start, a->leaf_end, Rows::state(a->state), a->pshift, a->side_length, 0,
                       w.n_tiles_dev, ws, st, err);
     if (rc) return rc;
-    rc = pack_records(KID_COUNTING, T, w.n_tiles_dev, a->state, a->pshift, nullptr, 0,
+    rc = pack_records(KID_COUNTING, T, w.n_tiles_dev, Rows::state(a->state), a->pshift, nullptr, 0,
                       a->side_length, w.P0, w.P1, w.P2, st, err);
     if (rc) return rc;
     EvalDev c = d;

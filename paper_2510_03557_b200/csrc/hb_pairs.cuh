@@ -292,13 +292,47 @@ struct Tiling {
 };
 
 // Everything one pair-kernel launch reads.
+// Row source of the tiling, packing and exact-recheck kernels: the (n,12)
+// float64 state matrix the compat API is handed (hb/particles.py:135-154), or
+// the resident step's leaf-order SoA fields -- the step keeps no state matrix
+// (SURVEY.md 8a row a2); P and c_s then come from density and internal energy
+// with the EOS of hb/hydro.py:48-57.  The branch on `st` is warp-uniform.
+struct Rows {
+  const double* st = nullptr;
+  const double *pos = nullptr, *vel = nullptr, *mass = nullptr, *h = nullptr, *rho = nullptr,
+               *u = nullptr;
+  const uint8_t* sp = nullptr;
+  double gamma = 0.0;
+  __host__ __device__ static Rows state(const double* s) { Rows r; r.st = s; return r; }
+  __device__ __forceinline__ double x(int64_t r, int d) const {
+    return st ? st[r * NCOL + d] : pos[3 * r + d];
+  }
+  __device__ __forceinline__ double v(int64_t r, int d) const {
+    return st ? st[r * NCOL + C_VX + d] : vel[3 * r + d];
+  }
+  __device__ __forceinline__ double m(int64_t r) const { return st ? st[r * NCOL + C_M] : mass[r]; }
+  __device__ __forceinline__ double hh(int64_t r) const { return st ? st[r * NCOL + C_H] : h[r]; }
+  __device__ __forceinline__ double dens(int64_t r) const {
+    return st ? st[r * NCOL + C_RHO] : rho[r];
+  }
+  __device__ __forceinline__ double pres(int64_t r) const {
+    return st ? st[r * NCOL + C_P] : (gamma - 1.0) * rho[r] * u[r];
+  }
+  __device__ __forceinline__ double snd(int64_t r) const {
+    return st ? st[r * NCOL + C_CS] : sqrt(fmax(gamma * (gamma - 1.0) * u[r], 0.0));
+  }
+  __device__ __forceinline__ bool gas(int64_t r) const {
+    return st ? st[r * NCOL + C_SP] == 1.0 : sp[r] == 1;
+  }
+};
+
 struct EvalDev {
   Tiling T;
   const int64_t* ent_ptr;  // (n_leaves+1)
   const int32_t* ent_src;
   const int32_t* ent_code;  // shift code | fwd << 8 | scatter-eligible << 9
   const float4 *P0, *P1, *P2;
-  const double* state;
+  Rows rows;
   const int8_t* pshift;
   double L, reach;
   PairParams pp;
@@ -325,10 +359,10 @@ __host__ __device__ inline int tiles_for(int m, int tile_max, int even) {
   return even ? 2 * ((m + 2 * tile_max - 1) / (2 * tile_max)) : (m + tile_max - 1) / tile_max;
 }
 int build_tiling(Tiling& T, int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
-                 const double* state, const int8_t* pshift, double L, int sel,
+                 Rows rows, const int8_t* pshift, double L, int sel,
                  int64_t* n_tiles_dev, Arena& ws, cudaStream_t st, HbError* err,
                  const uint8_t* ghost = nullptr);
-int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, const double* state,
+int pack_records(int kid, const Tiling& T, const int64_t* n_tiles_dev, Rows rows,
                  const int8_t* pshift, const double* aux, int naux, double L, float4* P0,
                  float4* P1, float4* P2, cudaStream_t st, HbError* err);
 // lean: resident hot path (no exact counters / per-entry error attribution)

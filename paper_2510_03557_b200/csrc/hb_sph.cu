@@ -28,7 +28,7 @@ struct SphDev {
   const int32_t* ent_src;
   const int32_t* ent_code;
   const float4 *P0, *P1, *P2, *P3;  // layouts: k_pack_sph
-  const double* state;         // exact predicate re-checks (float64 rows)
+  Rows rows;                   // exact predicate re-checks (float64 rows)
   const int8_t* pshift;
   double L, reach;
   float reach2, band, alpha, beta;
@@ -41,14 +41,14 @@ struct SphDev {
   int skip_tiles;            // pass B: skip tiles without an owned member
 };
 
-__device__ __forceinline__ double exact_r2_rows(const double* st, const int8_t* ps, double L,
+__device__ __forceinline__ double exact_r2_rows(const Rows& st, const int8_t* ps, double L,
                                                 int64_t i, int64_t j, int code) {
   int s[3] = {code / 9 - 1, (code / 3) % 3 - 1, code % 3 - 1};
   double r2 = 0.0;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     int64_t pi = ps ? ps[3 * i + d] : 0, pj = ps ? ps[3 * j + d] : 0;
-    double dx = __dadd_rn(__dsub_rn(st[i * NCOL + d], st[j * NCOL + d]),
+    double dx = __dadd_rn(__dsub_rn(st.x(i, d), st.x(j, d)),
                           __dmul_rn((double)(pi - pj - s[d]), L));
     r2 = d == 0 ? __dmul_rn(dx, dx) : __dadd_rn(r2, __dmul_rn(dx, dx));
   }
@@ -61,17 +61,63 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
+// ---- bulk-async (TMA engine) source ring: the records of a passing source
+// tile are contiguous runs of <= 32 float4s per record array, so each one is a
+// single cp.async.bulk into a per-warp ring slot completing on that slot's
+// mbarrier.  Every passing tile of a 32-tile cull batch is requested at once
+// (lane j issues tile j's copies), so the loads of a batch overlap instead of
+// each tile's LDG waiting behind the previous tile's cull.
+template <int NP, int RS>
+struct BulkRing {
+  float4 rec[RS > 0 ? RS : 1][NP][32];
+  unsigned long long bar[RS > 0 ? RS : 1];
+};
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void ring_init(unsigned long long* bar, int rs) {
+  if ((threadIdx.x & 31) == 0) {
+    for (int i = 0; i < rs; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar + i)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void ring_arm(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ring_copy(unsigned long long* bar, float4* dst, const float4* src,
+                                          unsigned bytes) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ring_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+        "p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
 // staging shared by both passes: walks the receiver's entries, culls source
 // tiles and sources against the target box, calls consume() when the stage
 // would overflow and at the end.  (A two-phase variant -- tile candidates
 // collected into a per-warp list, then drained with the next tile's records
 // prefetched into registers -- measured slower at c2: pass A 1.535 -> 1.563
 // ms, pass B 2.84 -> 2.97 ms with spills at pass B's register budget.)
-template <int NP, bool HYDRO, int CAP, class Consume>
+template <int NP, bool HYDRO, int CAP, int RS = 0, class Consume>
 __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, int64_t e1,
                                           float4 tlo, float4 thi, float hmax_t, float Rcap,
                                           float4 (*stage)[NP], int2* meta, int& cnt,
-                                          Consume consume) {
+                                          Consume consume, BulkRing<NP, RS>* ring = nullptr) {
   const Tiling& T = a.T;
   int lane = threadIdx.x & 31;
   double oA0 = T.origin[3 * A], oA1 = T.origin[3 * A + 1], oA2 = T.origin[3 * A + 2];
@@ -79,6 +125,8 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
   // pass B: support radius^2 of the pair (i, j) is 4 max(h_i, h_j)^2 (h_j:
   // the source record's P0.w)
   float Rt2 = Rt * Rt, Rcap2 = Rcap * Rcap;
+  unsigned ring_phase = 0u;
+  if (RS > 0) ring_init(ring->bar, RS);
   for (int64_t e = e0; e < e1; ++e) {
     int B = a.ent_src[e];
     if (B < 0) continue;  // bin stencil: off-mesh / duplicate cell
@@ -104,17 +152,46 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
         pass = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) <= R * R;
       }
       unsigned tm = __ballot_sync(0xffffffffu, pass);
+      unsigned chunk = 0u;
+      int slot = 0;
       while (tm) {
+        if (RS > 0 && chunk == 0u) {  // request the next <= RS passing tiles
+          unsigned t2 = tm;
+#pragma unroll
+          for (int i = 0; i < (RS > 0 ? RS : 1); ++i) t2 &= t2 - 1;
+          chunk = tm & ~t2;
+          __syncwarp();  // the ring's previous contents are consumed
+          if ((chunk >> lane) & 1u) {
+            int sl = __popc(chunk & lanemask_lt());
+            unsigned bytes = (unsigned)my_n * 16u;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            ring_arm(&ring->bar[sl], NP * bytes);
+            ring_copy(&ring->bar[sl], ring->rec[sl][0], a.P0 + my_start, bytes);
+            if (NP > 1) ring_copy(&ring->bar[sl], ring->rec[sl][1], a.P1 + my_start, bytes);
+            if (NP > 2) ring_copy(&ring->bar[sl], ring->rec[sl][2], a.P2 + my_start, bytes);
+          }
+          slot = 0;
+        }
         int j = __ffs(tm) - 1;
         tm &= tm - 1;
+        if (RS > 0) chunk &= chunk - 1u;
         int n_u = __shfl_sync(0xffffffffu, my_n, j);
         int k_j = __shfl_sync(0xffffffffu, my_start, j) + lane;
         bool ok = false;
         float4 sj[NP];
+        if (RS > 0) {
+          ring_wait(&ring->bar[slot], (ring_phase >> slot) & 1u);
+          ring_phase ^= 1u << slot;
+        }
         if (lane < n_u) {
-          sj[0] = a.P0[k_j];
-          if (NP > 1) sj[1] = a.P1[k_j];
-          if (NP > 2) sj[2] = a.P2[k_j];
+          if (RS > 0) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) sj[p] = ring->rec[slot][p][lane];
+          } else {
+            sj[0] = a.P0[k_j];
+            if (NP > 1) sj[1] = a.P1[k_j];
+            if (NP > 2) sj[2] = a.P2[k_j];
+          }
           sj[0].x -= D0; sj[0].y -= D1; sj[0].z -= D2;
           float R2 = HYDRO ? fminf(Rcap2, fmaxf(Rt2, 4.0008f * sj[0].w * sj[0].w)) : Rt2;
           float gx = fmaxf(fmaxf(tlo.x - sj[0].x, sj[0].x - thi.x), 0.0f);
@@ -131,6 +208,7 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
           meta[slot] = make_int2(k_j, cw);
         }
         cnt += __popc(sm);
+        ++slot;
       }
     }
   }
@@ -170,8 +248,10 @@ __device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, fl
 }
 
 // ---------------------------------------------------------------- pass A
+template <int RS>
 __global__ void __launch_bounds__(kSphWarps * 32, 6)
 k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
+  __shared__ BulkRing<1, RS> s_ring[RS > 0 ? kSphWarps : 1];
   __shared__ float4 s_stage[kSphWarps][kStageA][1];
   __shared__ int2 s_meta[kSphWarps][kStageA];
   __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
@@ -189,7 +269,7 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   float4 ti0 = a.P0[k_i];
   float h = a.P1[k_i].w;
   float hinv = h > 0.0f ? 1.0f / h : 0.0f;
-  double h64 = a.state[row_i * NCOL + C_H];
+  double h64 = a.rows.hh(row_i);
   double thr4_64 = __dmul_rn(__dmul_rn(4.0, h64), h64);   // (4 h) h as hb/kernels.py:191
   float thr4 = (float)thr4_64;
   float thr4b = thr4 * a.band;
@@ -215,7 +295,7 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
       bool c4 = r2 <= thr4;
       if (on && fabsf(r2 - thr4) <= thr4b) {  // exact float64 decision, reference expression
         int2 mt = meta[q];
-        double e2 = exact_r2_rows(a.state, a.pshift, a.L, row_i, T.tperm[mt.x], mt.y & 31);
+        double e2 = exact_r2_rows(a.rows, a.pshift, a.L, row_i, T.tperm[mt.x], mt.y & 31);
         c4 = e2 <= thr4_64;
       }
       float qq = r2 * rsqrt_ftz(fmaxf(r2, 1e-30f)) * hinv;  // MUFU.RSQ, no IEEE sqrt fix-up
@@ -232,8 +312,8 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   };
   // cull radius from the tile's largest h (emit_tile_box: tile_lo.w), not this
   // lane's: every lane culls sources for the whole tile
-  sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
-                               cnt, consume);
+  sph_sweep<1, false, kStageA, RS>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage,
+                                   meta, cnt, consume, &s_ring[RS > 0 ? wid : 0]);
   if (live) {
     float norm3 = h > 0.0f ? kSigma * hinv * hinv * hinv : 0.0f;
     a.ncount[row_i] += (double)count;
@@ -251,11 +331,13 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
 // Two pairs per walk iteration at 4 CTAs / SM (120 registers, no spills):
 // 2.763 -> 2.728 ms at c2 against one pair at 5 CTAs / SM (96 registers).
 constexpr int kStageB = 192;
+template <int RS, int STAGE>
 __global__ void __launch_bounds__(kSphWarps * 32, 4)
 k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
-  __shared__ float4 s_stage[kSphWarps][kStageB][3];
-  __shared__ int2 s_meta[kSphWarps][kStageB];
-  __shared__ unsigned s_mask[kSphWarps][kStageB / 32][32];
+  __shared__ BulkRing<3, RS> s_ring[RS > 0 ? kSphWarps : 1];
+  __shared__ float4 s_stage[kSphWarps][STAGE][3];
+  __shared__ int2 s_meta[kSphWarps][STAGE];
+  __shared__ unsigned s_mask[kSphWarps][STAGE / 32][32];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
   if (t >= *n_tiles_dev) return;
@@ -339,8 +421,8 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
     __syncwarp();
     cnt = 0;
   };
-  sph_sweep<3, true, kStageB>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
-                              cnt, consume);
+  sph_sweep<3, true, STAGE, RS>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage,
+                                  meta, cnt, consume, &s_ring[RS > 0 ? wid : 0]);
   bool bad = !(isfinite(fx) && isfinite(fy) && isfinite(fz) && isfinite(ei) && isfinite(mo[0]));
   if (__ballot_sync(0xffffffffu, live && bad)) {
     if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e0 * 4 + 1));
@@ -523,9 +605,9 @@ k_sph_grad(SphDev a, const int64_t* n_tiles_dev) {
 // rho_f / u_f (optional, leaf-order SoA density and internal energy): rho, P
 // and c_s come from them with the EOS of hb/hydro.py:48-57 evaluated here
 // (P = ((gamma - 1) rho) u, c_s = sqrt(max((gamma (gamma - 1)) u, 0))), so the
-// step needs no separate pass writing those state-matrix columns
+// step needs no separate EOS pass
 __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tiling T,
-                           const double* state, const int8_t* pshift, double L, float4* P0,
+                           Rows rows, const int8_t* pshift, double L, float4* P0,
                            float4* P1, float4* P2, float4* P3, int layout, const double* rho_f,
                            const double* u_f, double gamma) {
   int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -534,40 +616,45 @@ __global__ void k_pack_sph(int64_t tcap, const int64_t* n_tiles_dev, const Tilin
   int leaf = T.tile_leaf[t];
   int64_t k = T.tile_start[t] + lane;
   int64_t r = T.tperm[k];
-  const double* st = state + r * NCOL;
   float c[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    double v = __dadd_rn(st[d], __dmul_rn((double)(pshift ? pshift[3 * r + d] : 0), L));
+    double v = __dadd_rn(rows.x(r, d), __dmul_rn((double)(pshift ? pshift[3 * r + d] : 0), L));
     c[d] = (float)(v - T.origin[3 * leaf + d]);
   }
-  double h = st[C_H], rho = rho_f ? rho_f[r] : st[C_RHO];
-  double P = st[C_P], cs = st[C_CS];
+  double h = rows.hh(r), m = rows.m(r);
+  if (layout == 0) {
+    P0[k] = make_float4(c[0], c[1], c[2], (float)m);
+    P1[k] = make_float4(0.f, 0.f, 0.f, (float)h);
+    return;
+  }
+  double rho = rho_f ? rho_f[r] : rows.dens(r);
+  if (layout == 2) {
+    P0[k] = make_float4(c[0], c[1], c[2], rho > 0 ? (float)(m / rho) : 0.0f);
+    P1[k] = make_float4(0.f, 0.f, 0.f, (float)h);
+    return;
+  }
+  double P, cs;
   if (rho_f && u_f) {
     double gm1 = gamma - 1.0, u = u_f[r];
     P = gm1 * rho * u;
     cs = sqrt(fmax(gamma * gm1 * u, 0.0));
+  } else {
+    P = rows.pres(r);
+    cs = rows.snd(r);
   }
   double norm5 = h > 0 ? 0.31830988618379067 / (h * h * h * h * h) : 0.0;
   double fpart = rho > 0 ? P / (rho * rho) : 0.0;
-  if (layout == 0) {
-    P0[k] = make_float4(c[0], c[1], c[2], (float)st[C_M]);
-    P1[k] = make_float4(0.f, 0.f, 0.f, (float)h);
-  } else if (layout == 2) {
-    P0[k] = make_float4(c[0], c[1], c[2], rho > 0 ? (float)(st[C_M] / rho) : 0.0f);
-    P1[k] = make_float4(0.f, 0.f, 0.f, (float)h);
-  } else {
-    P0[k] = make_float4(c[0], c[1], c[2], (float)h);
-    P1[k] = make_float4((float)st[C_VX], (float)st[C_VY], (float)st[C_VZ], (float)st[C_M]);
-    P2[k] = make_float4((float)fpart, (float)cs, (float)rho, (float)norm5);
-  }
+  P0[k] = make_float4(c[0], c[1], c[2], (float)h);
+  P1[k] = make_float4((float)rows.v(r, 0), (float)rows.v(r, 1), (float)rows.v(r, 2), (float)m);
+  P2[k] = make_float4((float)fpart, (float)cs, (float)rho, (float)norm5);
 }
 
-int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int8_t* pshift,
+int pack_sph(const Tiling& T, const int64_t* ntd, Rows rows, const int8_t* pshift,
              double L, float4* P0, float4* P1, float4* P2, float4* P3, int layout,
              cudaStream_t st, HbError* err, const double* rho, const double* u, double gamma) {
   k_pack_sph<<<grid_for(T.n_tiles_cap * 32, 256), 256, 0, st>>>(
-      T.n_tiles_cap, ntd, T, state, pshift, L, P0, P1, P2, P3, layout, rho, u, gamma);
+      T.n_tiles_cap, ntd, T, rows, pshift, L, P0, P1, P2, P3, layout, rho, u, gamma);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }
@@ -575,7 +662,7 @@ int pack_sph(const Tiling& T, const int64_t* ntd, const double* state, const int
 int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   SphDev a;
   a.T = *s.T; a.ent_ptr = s.ent_ptr; a.ent_src = s.ent_src; a.ent_code = s.ent_code;
-  a.P0 = s.P0; a.P1 = s.P1; a.P2 = s.P2; a.P3 = s.P3; a.state = s.state; a.pshift = s.pshift;
+  a.P0 = s.P0; a.P1 = s.P1; a.P2 = s.P2; a.P3 = s.P3; a.rows = s.rows; a.pshift = s.pshift;
   a.L = s.L; a.reach = s.reach; a.reach2 = (float)(s.reach * s.reach); a.band = s.band;
   a.alpha = (float)s.alpha; a.beta = (float)s.beta;
   a.ncount = s.ncount; a.rho = s.rho; a.moments = s.moments; a.hydro = s.hydro;
@@ -585,8 +672,19 @@ int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   a.skip_leaf = s.skip_leaf;
   a.skip_tiles = s.skip_tiles;
   unsigned grid = grid_for(s.T->n_tiles_cap, kSphWarps);
-  if (pass == 0) k_sph_density<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-  else if (pass == 1) k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  // HB_SPH_BULK (A/B switch): 1 = pass A sources through the bulk-async ring,
+  // 2 = pass B too (2 slots, 160-source stages to stay at 4 CTAs / SM)
+  static const int bulk = [] {
+    const char* e = getenv("HB_SPH_BULK");
+    return e ? atoi(e) : 0;
+  }();
+  if (pass == 0) {
+    if (bulk >= 1) k_sph_density<4><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+    else k_sph_density<0><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  } else if (pass == 1) {
+    if (bulk >= 2) k_sph_force<2, 160><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+    else k_sph_force<0, kStageB><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  }
   else k_sph_grad<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   HB_LAUNCH_CHECK();
   return HB_OK;

@@ -54,9 +54,10 @@ __global__ void k_ghost_src(int64_t n, const int64_t* perm, const int64_t* inv,
 }
 
 
-// mesh order <- input order for every field and the (n,12) float64 state
-// matrix (hb/particles.py:135-154) in one pass: each row reads its source row
-// once (10 fields) and writes the gathered fields and its state row
+// mesh order <- input order for every field (hb/particles.py:135-154 reorder):
+// each row reads its source row once.  The gathered leaf-order SoA fields are
+// both the step's outputs and the rows every later kernel reads (Rows); no
+// (n,12) state matrix is built.
 struct FieldIn {
   const double *pos, *vel, *mass, *h, *u, *rho;
   const uint8_t *species, *ghost;
@@ -70,103 +71,60 @@ struct FieldOut {
   int64_t* gid;
 };
 // late half of a split gather (HbStepArgs.late_fields_event): the fields SPH
-// pass A does not read, plus the state columns built from them.  PART 0: all
-// of them; PART 1: vel, internal energy (the EOS and pass B need them);
-// PART 2: density of the non-gas rows (gas rows hold pass A's) and global id
-// (HbStepArgs.last_fields_event: needed only by the outputs)
+// pass A does not read.  PART 0: all of them; PART 1: vel, internal energy
+// (pass B needs them); PART 2: density of the non-gas rows (gas rows hold pass
+// A's) and global id (HbStepArgs.last_fields_event: needed only by the outputs)
 template <int PART>
-__global__ void k_gather_late(int64_t n, const int64_t* perm, FieldIn in, FieldOut out,
-                              double* st) {
+__global__ void k_gather_late(int64_t n, const int64_t* perm, FieldIn in, FieldOut out) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int64_t r = perm[k];
-  double* s = st + k * NCOL;
   if (PART != 2) {
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      double v = in.vel[3 * r + d];
-      out.vel[3 * k + d] = v;
-      s[C_VX + d] = v;
-    }
+    for (int d = 0; d < 3; ++d) out.vel[3 * k + d] = in.vel[3 * r + d];
     out.u[k] = in.u[r];
   }
   if (PART != 1) {
     out.gid[k] = in.gid[r];
-    if (PART == 0 || out.species[k] != 1) {
-      double rho = in.rho[r];   // only non-gas rows keep it; gas rows get pass A's
-      out.rho[k] = rho;
-      s[C_RHO] = rho;
-    }
+    if (PART == 0 || out.species[k] != 1)   // gas rows get pass A's density
+      out.rho[k] = in.rho[r];
   }
 }
 
-// LATE = true: skip the late fields (vel, u, density, ids) and P, c_s, which
-// need u and rho (pass B's records compute P and c_s from the SoA density and
-// internal energy; pass A reads none of them)
+// LATE = true: skip the late fields (vel, u, density, ids), which pass A does
+// not read (pass B's records compute P and c_s from the SoA density and
+// internal energy)
 // h_lim: the h_max the step's reach, bin width and culls were sized from
 // (HbStepArgs.h_max).  A gas row above it would silently lose the pairs
 // between 2 h_max and 2 h_i, so it raises HB_CONTRACT (error key code 3)
 // instead (the reference recomputes smoothing.max() per call, hb/hydro.py:67).
-// The state rows go through shared memory: each thread assembles its row,
-// then the block writes its 256 contiguous rows with 16-B stores (a per-thread
-// row store touches 12 sectors 96 B apart per warp instruction: 0.62 ms at c2).
-// Columns a LATE gather leaves for later kernels are written as 0 here; the
-// velocity columns are filled by k_gather_late before anything reads them.
 constexpr int kGatherBlock = 256;
 template <bool LATE>
 __global__ void __launch_bounds__(kGatherBlock)
-k_gather_state(int64_t n, const int64_t* perm, FieldIn in, FieldOut out, double gamma,
-               double* st, double h_lim, unsigned long long* err_key, int no_ghosts) {
-  __shared__ double s_st[kGatherBlock * NCOL];
-  int64_t k0 = (int64_t)blockIdx.x * kGatherBlock;
-  int64_t k = k0 + threadIdx.x;
-  double row[NCOL];
+k_gather_fields(int64_t n, const int64_t* perm, FieldIn in, FieldOut out, double h_lim,
+               unsigned long long* err_key, int no_ghosts) {
+  int64_t k = (int64_t)blockIdx.x * kGatherBlock + threadIdx.x;
+  if (k >= n) return;
+  int64_t r = perm[k];
 #pragma unroll
-  for (int c = 0; c < NCOL; ++c) row[c] = 0.0;
-  if (k < n) {
-    int64_t r = perm[k];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      double x = in.pos[3 * r + d];
-      out.pos[3 * k + d] = x;
-      row[C_X + d] = x;
-      if (!LATE) {
-        double v = in.vel[3 * r + d];
-        out.vel[3 * k + d] = v;
-        row[C_VX + d] = v;
-      }
-      out.shift[3 * k + d] = in.shift[3 * r + d];
-    }
-    double m = in.mass[r], h = in.h[r];
-    uint8_t sp = in.species[r];
-    out.mass[k] = m; out.h[k] = h;
-    uint8_t gh = in.ghost[r];
-    out.species[k] = sp; out.ghost[k] = gh;
-    // HbStepArgs.last_fields_event is for sets without ghost rows (ghost rows
-    // would need their input density before pass B)
-    if (no_ghosts && gh != 0) atomicMin(err_key, 7ull);
-    row[C_M] = m; row[C_H] = h;
-    row[C_SP] = (double)sp;
-    if (sp == 1 && !(h <= h_lim)) atomicMin(err_key, 3ull);
-    if (!LATE) {
-      double rho = in.rho[r];
-      out.rho[k] = rho;
-      row[C_RHO] = rho;
-      double u = in.u[r];
-      out.u[k] = u;
-      out.gid[k] = in.gid[r];
-      double gm1 = gamma - 1.0;
-      row[C_P] = gm1 * rho * u;
-      row[C_CS] = sqrt(fmax(gamma * gm1 * u, 0.0));
-    }
+  for (int d = 0; d < 3; ++d) {
+    out.pos[3 * k + d] = in.pos[3 * r + d];
+    if (!LATE) out.vel[3 * k + d] = in.vel[3 * r + d];
+    out.shift[3 * k + d] = in.shift[3 * r + d];
   }
-#pragma unroll
-  for (int c = 0; c < NCOL; ++c) s_st[threadIdx.x * NCOL + c] = row[c];
-  __syncthreads();
-  int64_t rows = n - k0 < kGatherBlock ? n - k0 : kGatherBlock;
-  const double2* src = reinterpret_cast<const double2*>(s_st);
-  double2* dst = reinterpret_cast<double2*>(st + k0 * NCOL);
-  for (int i = threadIdx.x; i < rows * (NCOL / 2); i += kGatherBlock) dst[i] = src[i];
+  double h = in.h[r];
+  uint8_t sp = in.species[r], gh = in.ghost[r];
+  out.mass[k] = in.mass[r]; out.h[k] = h;
+  out.species[k] = sp; out.ghost[k] = gh;
+  // HbStepArgs.last_fields_event is for sets without ghost rows (ghost rows
+  // would need their input density before pass B)
+  if (no_ghosts && gh != 0) atomicMin(err_key, 7ull);
+  if (sp == 1 && !(h <= h_lim)) atomicMin(err_key, 3ull);
+  if (!LATE) {
+    out.rho[k] = in.rho[r];
+    out.u[k] = in.u[r];
+    out.gid[k] = in.gid[r];
+  }
 }
 
 struct StepWs {
@@ -180,7 +138,7 @@ struct StepWs {
   // engine
   Tiling Tg, Ta;
   int64_t *ntg, *nta;
-  double *state, *rho_new, *inv_tmp;
+  double *rho_new, *inv_tmp;
   float4 *P0, *P1, *P2;
   unsigned long long* err_key;
   int64_t* inv;
@@ -200,7 +158,6 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
   carve_tiling(ws, n, cap > nbins ? cap : nbins, w.Tg);
   carve_tiling(ws, n, cap, w.Ta);
   w.ntg = ws.take<int64_t>(1); w.nta = ws.take<int64_t>(2);
-  w.state = ws.take<double>(n * NCOL + 1);
   w.rho_new = ws.take<double>(n + 1);
   w.P0 = ws.take<float4>(n + 1); w.P1 = ws.take<float4>(n + 1); w.P2 = ws.take<float4>(n + 1);
   w.err_key = ws.take<unsigned long long>(1);
@@ -317,7 +274,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     Arena s2 = ws; assemble_csr(ld, a->list_capacity, nullptr, nullptr, nullptr, nullptr, s2, st, err);
     if (s2.used > mx) mx = s2.used;
     Arena s3 = ws;
-    build_tiling(w.Tg, cap, nullptr, nullptr, nullptr, nullptr, 0.0, 1, nullptr, s3, st, err);
+    build_tiling(w.Tg, cap, nullptr, nullptr, Rows{}, nullptr, 0.0, 1, nullptr, s3, st, err);
     if (s3.used > mx) mx = s3.used;
     GravBinArgs gb = {};
     gb.n = n; gb.nbins = nbins;
@@ -359,6 +316,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   // SPH passes size every cull from h_max; gravity-only steps read no h
   double h_lim = (a->passes & ~HB_PASS_GRAVITY) ? a->h_max * (1.0 + 1e-12) : INFINITY;
   HB_CUDA_TRY(cudaMemsetAsync(w.err_key, 0xff, sizeof(unsigned long long), st));
+  // every kernel after the gather reads the leaf-order output fields
+  Rows rows;
+  rows.pos = a->pos; rows.vel = a->vel; rows.mass = a->mass; rows.h = a->smoothing;
+  rows.rho = a->density; rows.u = a->internal_energy; rows.sp = a->species;
+  rows.gamma = a->eos_gamma;
   {
     unsigned g1 = grid_for(n, 256);
     FieldIn fi = {a->pos_in, a->vel_in, a->mass_in, a->smoothing_in, a->internal_energy_in,
@@ -366,11 +328,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
                    a->species, a->ghost, a->image_shift, a->global_id};
     if (late_split) {
-      k_gather_state<true><<<grid_for(n, kGatherBlock), kGatherBlock, 0, st>>>(
-          n, a->perm, fi, fo, a->eos_gamma, w.state, h_lim, w.err_key, last_split ? 1 : 0);
+      k_gather_fields<true><<<grid_for(n, kGatherBlock), kGatherBlock, 0, st>>>(
+          n, a->perm, fi, fo, h_lim, w.err_key, last_split ? 1 : 0);
     } else {
-      k_gather_state<false><<<grid_for(n, kGatherBlock), kGatherBlock, 0, st>>>(
-          n, a->perm, fi, fo, a->eos_gamma, w.state, h_lim, w.err_key, 0);
+      k_gather_fields<false><<<grid_for(n, kGatherBlock), kGatherBlock, 0, st>>>(
+          n, a->perm, fi, fo, h_lim, w.err_key, 0);
       if (a->ghost_src_in && a->ghost_src) {
         k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
         k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
@@ -390,11 +352,11 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
                    a->species, a->ghost, a->image_shift, a->global_id};
     if (last_split) {
-      k_gather_late<1><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, w.state);
+      k_gather_late<1><<<g1, 256, 0, st>>>(n, a->perm, fi, fo);
       HB_LAUNCH_CHECK();
       return HB_OK;
     }
-    k_gather_late<0><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, w.state);
+    k_gather_late<0><<<g1, 256, 0, st>>>(n, a->perm, fi, fo);
     if (a->ghost_src_in && a->ghost_src) {
       k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
       k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
@@ -413,7 +375,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
                   a->density_in, a->species_in, a->ghost_in, a->image_shift_in, a->global_id_in};
     FieldOut fo = {a->pos, a->vel, a->mass, a->smoothing, a->internal_energy, a->density,
                    a->species, a->ghost, a->image_shift, a->global_id};
-    k_gather_late<2><<<g1, 256, 0, st>>>(n, a->perm, fi, fo, w.state);
+    k_gather_late<2><<<g1, 256, 0, st>>>(n, a->perm, fi, fo);
     if (a->ghost_src_in && a->ghost_src) {
       k_gather_inverse<<<g1, 256, 0, st>>>(n, a->perm, w.inv);
       k_ghost_src<<<g1, 256, 0, st>>>(n, a->perm, w.inv, a->ghost_src_in, a->ghost_src);
@@ -441,7 +403,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     if (rc) return rc;
   }
   tm.mark(2);
-  // 3. tilings (the state matrix was written by the gather)
+  // 3. tilings over the gathered leaf-order fields
   w.Tg.n_leaves = nl; w.Ta.n_leaves = nl;
   // gravity over bin segments (half-warp tiles) or leaf tiles; bins beyond the
   // block tiler's capacity force the leaf path
@@ -472,19 +434,19 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   }
   {
     Arena s = ws;
-    int rc = build_tiling(w.Tg, n_seg, seg_s, seg_e, w.state, a->image_shift, a->side_length, 1,
+    int rc = build_tiling(w.Tg, n_seg, seg_s, seg_e, rows, a->image_shift, a->side_length, 1,
                           w.ntg, s, st, err, a->owned_targets ? a->ghost : nullptr);
     if (rc) return rc;
     if ((a->passes & HB_PASS_GRAVITY) && use_leaf_gravity) {
       Arena s2 = ws;
-      rc = build_tiling(w.Ta, nl, w.leaf_start, w.leaf_end, w.state, a->image_shift,
+      rc = build_tiling(w.Ta, nl, w.leaf_start, w.leaf_end, rows, a->image_shift,
                         a->side_length, 0, w.nta, s2, st, err);
       if (rc) return rc;
     }
   }
   EvalDev d = {};
   d.ent_ptr = w.ent_ptr; d.ent_src = w.ent_src; d.ent_code = w.ent_code;
-  d.P0 = w.P0; d.P1 = w.P1; d.P2 = w.P2; d.state = w.state; d.pshift = a->image_shift;
+  d.P0 = w.P0; d.P1 = w.P1; d.P2 = w.P2; d.rows = rows; d.pshift = a->image_shift;
   d.L = a->side_length; d.include_self = 1; d.write_out = 1; d.err_key = w.err_key;
   d.in_count = nullptr; d.out_int = nullptr;
   double sph_reach = 2.0 * a->h_max;
@@ -513,7 +475,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   sa.ent_ptr = sph_bins ? w.st_ptr : w.ent_ptr;
   sa.ent_src = sph_bins ? w.st_src : w.ent_src;
   sa.ent_code = sph_bins ? w.st_code : w.ent_code;
-  sa.P0 = w.P0; sa.P1 = w.P1; sa.P2 = w.P2; sa.P3 = nullptr; sa.state = w.state;
+  sa.P0 = w.P0; sa.P1 = w.P1; sa.P2 = w.P2; sa.P3 = nullptr; sa.rows = rows;
   sa.pshift = a->image_shift; sa.L = a->side_length; sa.reach = sph_reach; sa.band = band;
   sa.alpha = a->visc_alpha; sa.beta = a->visc_beta; sa.err_key = w.err_key;
   sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = mom; sa.hydro = a->hydro;
@@ -524,7 +486,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY)) {
     HB_CUDA_TRY(cudaMemsetAsync(a->ncount, 0, n * sizeof(double), st));
     HB_CUDA_TRY(cudaMemsetAsync(w.rho_new, 0, n * sizeof(double), st));
-    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, nullptr, 0, st,
+    rc = pack_sph(w.Tg, w.ntg, rows, a->image_shift, a->side_length, w.P0, w.P1, w.P2, nullptr, 0, st,
                   err);
     if (rc) return rc;
     tm.kmark(2);
@@ -539,7 +501,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   auto gravity_args = [&]() {
     GravBinArgs gb;
     gb.n = n; gb.nbins = nbins; gb.bin_ptr = w.bin_ptr; gb.leaf_start = w.leaf_start;
-    gb.leaf_end = w.leaf_end; gb.geom = ld.g; gb.state = w.state; gb.pshift = a->image_shift;
+    gb.leaf_end = w.leaf_end; gb.geom = ld.g; gb.rows = rows; gb.pshift = a->image_shift;
     gb.L = a->side_length; gb.r_s = a->r_s; gb.r_cut = a->r_cut; gb.eps = a->softening;
     gb.out = a->grav; gb.err_key = w.err_key; gb.overflow_host = nullptr;
     gb.ghost = a->owned_targets ? a->ghost : nullptr;
@@ -578,7 +540,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if (a->passes & (HB_PASS_CRK | HB_PASS_HYDRO)) {
     HB_CUDA_TRY(cudaMemsetAsync(mom, 0, n * 10 * sizeof(double), st));
     HB_CUDA_TRY(cudaMemsetAsync(a->hydro, 0, n * 5 * sizeof(double), st));
-    rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2, nullptr, 1, st,
+    rc = pack_sph(w.Tg, w.ntg, rows, a->image_shift, a->side_length, w.P0, w.P1, w.P2, nullptr, 1, st,
                   err, a->density, a->internal_energy, a->eos_gamma);
     if (rc) return rc;
     tm.kmark(4);
@@ -598,7 +560,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     if ((a->passes & HB_PASS_CRK_GRAD) && a->crk_gradA && a->crk_gradB) {
       HB_CUDA_TRY(cudaMemsetAsync(a->crk_gradA, 0, n * 3 * sizeof(double), st));
       HB_CUDA_TRY(cudaMemsetAsync(a->crk_gradB, 0, n * 9 * sizeof(double), st));
-      rc = pack_sph(w.Tg, w.ntg, w.state, a->image_shift, a->side_length, w.P0, w.P1, w.P2,
+      rc = pack_sph(w.Tg, w.ntg, rows, a->image_shift, a->side_length, w.P0, w.P1, w.P2,
                     nullptr, 2, st, err, a->density, a->internal_energy, a->eos_gamma);
       if (rc) return rc;
       sa.crk_A = a->crk_A; sa.crk_B = a->crk_B; sa.crk_fallback = a->crk_fallback;
@@ -640,7 +602,7 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   if ((a->passes & HB_PASS_GRAVITY) && !bin_gravity) {
     HB_CUDA_TRY(cudaMemsetAsync(a->grav, 0, n * 3 * sizeof(double), st));
     {
-      rc = pack_records(KID_GRAVITY, w.Ta, w.nta, w.state, a->image_shift, nullptr, 0,
+      rc = pack_records(KID_GRAVITY, w.Ta, w.nta, rows, a->image_shift, nullptr, 0,
                         a->side_length, w.P0, w.P1, w.P2, st, err);
       if (rc) return rc;
       setup(KID_GRAVITY, a->r_cut, a->r_s, a->softening * a->softening, 3, w.Ta, a->grav);
