@@ -858,7 +858,15 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 constexpr int kGravWarps = 8;
 constexpr int kGravStage = 128;
 
-template <int JB, int REP, int kGravBatch>
+// (a & b) | c as one LOP3 (ptxas splits it in two when b and c are both
+// immediates; here they are loop-invariant registers)
+__device__ __forceinline__ unsigned and_or(unsigned a, unsigned b, unsigned c) {
+  unsigned d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+template <int JB, int REP, int kGravBatch, int ACC>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -874,40 +882,83 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   float4 tlo = T.tile_lo[t], thi = T.tile_hi[t];
   float R2 = a.cull_reach * a.cull_reach;
   float eps2 = a.pp.p1;
-  float ax = 0.0f, ay = 0.0f, az = 0.0f;
-  double oA[3] = {T.origin[3 * A], T.origin[3 * A + 1], T.origin[3 * A + 2]};
+  float2 eps2x2 = make_float2(eps2, eps2);
+  const unsigned lowmask = (1u << (23 - JB)) - 1u, one_bits = 0x3F800000u;
+  // float64 accumulators fed with FP32 partial sums of 8 sources: the FP32
+  // rounding then scales with a partial, not with the running total of ~500
+  // cancelling terms (the relative error of the lattice's small net forces
+  // halves: see DESIGN.md 3)
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  float2 rx = make_float2(0.0f, 0.0f), ry = rx, rz = rx;  // ACC 0 / 1 / 3 running sums
+  const double* oA = T.origin + 3 * A;  // re-read per entry (L1): 6 registers fewer
   int cnt = 0;
   auto flush = [&]() {
     __syncwarp();
     int q0 = 0;
+    if (ACC >= 3) rx = ry = rz = make_float2(0.0f, 0.0f);
+    int nb = 0;
     {
       // batches of kGravBatch sources: every table row is requested before the
       // first one is used, so the gathers' latency overlaps within the warp
       // (the unrolled per-pair loop stalled on each row: short scoreboard).
-      // Accumulation order is unchanged.
+      // The order within each accumulator is fixed (deterministic).
       for (; q0 + kGravBatch <= cnt; q0 += kGravBatch) {
-        float bx[kGravBatch], by[kGravBatch], bz[kGravBatch], bu[kGravBatch], bm[kGravBatch];
+        // sources in pairs: soft, u - 1 and the accumulation run as packed
+        // FP32x2 instructions (FFMA2 / FADD2, one issue slot for two lanes'
+        // worth of a pair of sources); dx, the table index and the cubic stay
+        // scalar, their results landing in the pair registers
+        float2 bx[kGravBatch / 2], by[kGravBatch / 2], bz[kGravBatch / 2], bu[kGravBatch / 2];
+        float bm[kGravBatch];
         float4 bc[kGravBatch];
 #pragma unroll
-        for (int b = 0; b < kGravBatch; ++b) {
-          float4 s = stage[q0 + b];
-          bx[b] = ti.x - s.x; by[b] = ti.y - s.y; bz[b] = ti.z - s.z; bm[b] = s.w;
-          float soft = fmaf(bz[b], bz[b], fmaf(by[b], by[b], fmaf(bx[b], bx[b], eps2)));
-          unsigned bits = __float_as_uint(soft);
-          unsigned kk = min((bits >> (23 - JB)) - gt.base, gt.last);
-          bu[b] = __uint_as_float((bits & ((1u << (23 - JB)) - 1u)) | 0x3F800000u) - 1.0f;
-          bc[b] = s_tab[kk * REP];
+        for (int p = 0; p < kGravBatch / 2; ++p) {
+          float4 s0 = stage[q0 + 2 * p], s1 = stage[q0 + 2 * p + 1];
+          bx[p] = make_float2(ti.x - s0.x, ti.x - s1.x);
+          by[p] = make_float2(ti.y - s0.y, ti.y - s1.y);
+          bz[p] = make_float2(ti.z - s0.z, ti.z - s1.z);
+          bm[2 * p] = s0.w; bm[2 * p + 1] = s1.w;
+          float2 soft = __ffma2_rn(bz[p], bz[p], __ffma2_rn(by[p], by[p], __ffma2_rn(bx[p], bx[p], eps2x2)));
+          unsigned b0 = __float_as_uint(soft.x), b1 = __float_as_uint(soft.y);
+          unsigned k0 = min((b0 >> (23 - JB)) - gt.base, gt.last);
+          unsigned k1 = min((b1 >> (23 - JB)) - gt.base, gt.last);
+          float2 um = make_float2(__uint_as_float(and_or(b0, lowmask, one_bits)),
+                                  __uint_as_float(and_or(b1, lowmask, one_bits)));
+          bu[p] = __fadd2_rn(um, make_float2(-1.0f, -1.0f));
+          bc[2 * p] = s_tab[k0 * REP];
+          bc[2 * p + 1] = s_tab[k1 * REP];
         }
+        float2 fx = make_float2(0.0f, 0.0f), fy = fx, fz = fx;
+        if (ACC == 0 || ACC >= 3) { fx = rx; fy = ry; fz = rz; }
 #pragma unroll
-        for (int b = 0; b < kGravBatch; ++b) {
-          float4 c = bc[b];
-          float w = fmaf(fmaf(fmaf(c.w, bu[b], c.z), bu[b], c.y), bu[b], c.x) * bm[b];
-          ax = fmaf(w, bx[b], ax);
-          ay = fmaf(w, by[b], ay);
-          az = fmaf(w, bz[b], az);
+        for (int p = 0; p < kGravBatch / 2; ++p) {
+          float4 c0 = bc[2 * p], c1 = bc[2 * p + 1];
+          float u0 = bu[p].x, u1 = bu[p].y;
+          float2 w = make_float2(fmaf(fmaf(fmaf(c0.w, u0, c0.z), u0, c0.y), u0, c0.x) * bm[2 * p],
+                                 fmaf(fmaf(fmaf(c1.w, u1, c1.z), u1, c1.y), u1, c1.x) * bm[2 * p + 1]);
+          fx = __ffma2_rn(w, bx[p], fx);
+          fy = __ffma2_rn(w, by[p], fy);
+          fz = __ffma2_rn(w, bz[p], fz);
+        }
+        if (ACC == 0 || ACC >= 3) {
+          rx = fx; ry = fy; rz = fz;
+          // ACC 5 / 6: fold the FP32 partial into float64 every 2 / 4 batches
+          if ((ACC == 5 && (nb & 1)) || (ACC == 6 && (nb & 3) == 3)) {
+            ax += (double)(rx.x + rx.y);
+            ay += (double)(ry.x + ry.y);
+            az += (double)(rz.x + rz.y);
+            rx = ry = rz = make_float2(0.0f, 0.0f);
+          }
+          ++nb;
+        } else if (ACC == 1) {
+          rx = __fadd2_rn(rx, fx); ry = __fadd2_rn(ry, fy); rz = __fadd2_rn(rz, fz);
+        } else {
+          ax += (double)(fx.x + fx.y);
+          ay += (double)(fy.x + fy.y);
+          az += (double)(fz.x + fz.y);
         }
       }
     }
+    float tx = 0.0f, ty = 0.0f, tz = 0.0f;
 #pragma unroll 4
     for (int q = q0; q < cnt; ++q) {
       float4 s = stage[q];
@@ -918,9 +969,17 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
       float u = __uint_as_float((bits & ((1u << (23 - JB)) - 1u)) | 0x3F800000u) - 1.0f;
       float4 c = s_tab[k * REP];
       float w = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x) * s.w;
-      ax = fmaf(w, dx, ax);
-      ay = fmaf(w, dy, ay);
-      az = fmaf(w, dz, az);
+      tx = fmaf(w, dx, tx);
+      ty = fmaf(w, dy, ty);
+      tz = fmaf(w, dz, tz);
+    }
+    if (ACC >= 2) {
+      ax += (double)(tx + (rx.x + rx.y));
+      ay += (double)(ty + (ry.x + ry.y));
+      az += (double)(tz + (rz.x + rz.y));
+      if (ACC >= 3) rx = ry = rz = make_float2(0.0f, 0.0f);
+    } else {
+      rx.x += tx; ry.x += ty; rz.x += tz;
     }
     __syncwarp();
     cnt = 0;
@@ -968,6 +1027,9 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
     }
   }
   flush();
+  if (ACC == 0 || ACC == 1) {
+    ax = (double)(rx.x + rx.y); ay = (double)(ry.x + ry.y); az = (double)(rz.x + rz.y);
+  }
   bool bad = !(isfinite(ax) && isfinite(ay) && isfinite(az));
   unsigned bm = __ballot_sync(0xffffffffu, live && bad);
   if (bm) {
@@ -988,7 +1050,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
+template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps, int ACC = 2>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev) {
@@ -999,11 +1061,11 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * WARPS + wid + (t_begin_dev ? *t_begin_dev : 0);
   if (t < *n_tiles_dev)
-    grav_tile<JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
+    grav_tile<JB, REP, NB, ACC>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
                                  t, lane);
 }
 
-template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
+template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps, int ACC = 2>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                int64_t tcap, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err) {
@@ -1017,13 +1079,13 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS, ACC>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
   }
   unsigned grid = grid_for(tcap, WARPS), blk = WARPS * 32;
-  k_gravity<JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
+  k_gravity<JB, REP, NB, MINB, WARPS, ACC><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
   return HB_OK;
 }
 
@@ -1036,9 +1098,18 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
   // 16-warp CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4.
   // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
   // gone.)
-  int rc = gt.jbits == 4
-               ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err)
-               : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err);
+  static const int acc = [] {
+    const char* e = getenv("HB_GRAV_ACC");
+    return e ? atoi(e) : 2;
+  }();
+  int rc;
+  if (gt.jbits == 4) rc = launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err);
+  else if (acc == 0) rc = launch_gravity_kind<5, 8, 8, 2, 16, 0>(d, table, gt, tcap, ntd, t_begin, st, err);
+  else if (acc == 1) rc = launch_gravity_kind<5, 8, 8, 2, 16, 1>(d, table, gt, tcap, ntd, t_begin, st, err);
+  else if (acc == 3) rc = launch_gravity_kind<5, 8, 8, 2, 16, 3>(d, table, gt, tcap, ntd, t_begin, st, err);
+  else if (acc == 5) rc = launch_gravity_kind<5, 8, 8, 2, 16, 5>(d, table, gt, tcap, ntd, t_begin, st, err);
+  else if (acc == 6) rc = launch_gravity_kind<5, 8, 8, 2, 16, 6>(d, table, gt, tcap, ntd, t_begin, st, err);
+  else rc = launch_gravity_kind<5, 8, 8, 2, 16, 2>(d, table, gt, tcap, ntd, t_begin, st, err);
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;

@@ -61,63 +61,22 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// ---- bulk-async (TMA engine) source ring: the records of a passing source
-// tile are contiguous runs of <= 32 float4s per record array, so each one is a
-// single cp.async.bulk into a per-warp ring slot completing on that slot's
-// mbarrier.  Every passing tile of a 32-tile cull batch is requested at once
-// (lane j issues tile j's copies), so the loads of a batch overlap instead of
-// each tile's LDG waiting behind the previous tile's cull.
-template <int NP, int RS>
-struct BulkRing {
-  float4 rec[RS > 0 ? RS : 1][NP][32];
-  unsigned long long bar[RS > 0 ? RS : 1];
-};
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void ring_init(unsigned long long* bar, int rs) {
-  if ((threadIdx.x & 31) == 0) {
-    for (int i = 0; i < rs; ++i)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar + i)) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-}
-__device__ __forceinline__ void ring_arm(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void ring_copy(unsigned long long* bar, float4* dst, const float4* src,
-                                          unsigned bytes) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void ring_wait(unsigned long long* bar, unsigned parity) {
-  unsigned done;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
-        "p; }"
-        : "=r"(done)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
 // staging shared by both passes: walks the receiver's entries, culls source
 // tiles and sources against the target box, calls consume() when the stage
 // would overflow and at the end.  (A two-phase variant -- tile candidates
 // collected into a per-warp list, then drained with the next tile's records
 // prefetched into registers -- measured slower at c2: pass A 1.535 -> 1.563
-// ms, pass B 2.84 -> 2.97 ms with spills at pass B's register budget.)
-template <int NP, bool HYDRO, int CAP, int RS = 0, class Consume>
+// ms, pass B 2.84 -> 2.97 ms with spills at pass B's register budget.  A
+// bulk-async variant -- each passing source tile's record runs requested with
+// cp.async.bulk into a per-warp mbarrier ring, all of a cull batch's passing
+// tiles in flight at once -- measured slower too: pass A 1.466 -> 1.558 ms,
+// pass B 2.730 -> 2.959 ms (2 slots, 160-source stages to keep 4 CTAs / SM);
+// commit 54c0e54, profiles/ab_r02.md.)
+template <int NP, bool HYDRO, int CAP, class Consume>
 __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, int64_t e1,
                                           float4 tlo, float4 thi, float hmax_t, float Rcap,
                                           float4 (*stage)[NP], int2* meta, int& cnt,
-                                          Consume consume, BulkRing<NP, RS>* ring = nullptr) {
+                                          Consume consume) {
   const Tiling& T = a.T;
   int lane = threadIdx.x & 31;
   double oA0 = T.origin[3 * A], oA1 = T.origin[3 * A + 1], oA2 = T.origin[3 * A + 2];
@@ -125,8 +84,6 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
   // pass B: support radius^2 of the pair (i, j) is 4 max(h_i, h_j)^2 (h_j:
   // the source record's P0.w)
   float Rt2 = Rt * Rt, Rcap2 = Rcap * Rcap;
-  unsigned ring_phase = 0u;
-  if (RS > 0) ring_init(ring->bar, RS);
   for (int64_t e = e0; e < e1; ++e) {
     int B = a.ent_src[e];
     if (B < 0) continue;  // bin stencil: off-mesh / duplicate cell
@@ -152,46 +109,17 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
         pass = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) <= R * R;
       }
       unsigned tm = __ballot_sync(0xffffffffu, pass);
-      unsigned chunk = 0u;
-      int slot = 0;
       while (tm) {
-        if (RS > 0 && chunk == 0u) {  // request the next <= RS passing tiles
-          unsigned t2 = tm;
-#pragma unroll
-          for (int i = 0; i < (RS > 0 ? RS : 1); ++i) t2 &= t2 - 1;
-          chunk = tm & ~t2;
-          __syncwarp();  // the ring's previous contents are consumed
-          if ((chunk >> lane) & 1u) {
-            int sl = __popc(chunk & lanemask_lt());
-            unsigned bytes = (unsigned)my_n * 16u;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            ring_arm(&ring->bar[sl], NP * bytes);
-            ring_copy(&ring->bar[sl], ring->rec[sl][0], a.P0 + my_start, bytes);
-            if (NP > 1) ring_copy(&ring->bar[sl], ring->rec[sl][1], a.P1 + my_start, bytes);
-            if (NP > 2) ring_copy(&ring->bar[sl], ring->rec[sl][2], a.P2 + my_start, bytes);
-          }
-          slot = 0;
-        }
         int j = __ffs(tm) - 1;
         tm &= tm - 1;
-        if (RS > 0) chunk &= chunk - 1u;
         int n_u = __shfl_sync(0xffffffffu, my_n, j);
         int k_j = __shfl_sync(0xffffffffu, my_start, j) + lane;
         bool ok = false;
         float4 sj[NP];
-        if (RS > 0) {
-          ring_wait(&ring->bar[slot], (ring_phase >> slot) & 1u);
-          ring_phase ^= 1u << slot;
-        }
         if (lane < n_u) {
-          if (RS > 0) {
-#pragma unroll
-            for (int p = 0; p < NP; ++p) sj[p] = ring->rec[slot][p][lane];
-          } else {
-            sj[0] = a.P0[k_j];
-            if (NP > 1) sj[1] = a.P1[k_j];
-            if (NP > 2) sj[2] = a.P2[k_j];
-          }
+          sj[0] = a.P0[k_j];
+          if (NP > 1) sj[1] = a.P1[k_j];
+          if (NP > 2) sj[2] = a.P2[k_j];
           sj[0].x -= D0; sj[0].y -= D1; sj[0].z -= D2;
           float R2 = HYDRO ? fminf(Rcap2, fmaxf(Rt2, 4.0008f * sj[0].w * sj[0].w)) : Rt2;
           float gx = fmaxf(fmaxf(tlo.x - sj[0].x, sj[0].x - thi.x), 0.0f);
@@ -208,7 +136,6 @@ __device__ __forceinline__ void sph_sweep(const SphDev& a, int A, int64_t e0, in
           meta[slot] = make_int2(k_j, cw);
         }
         cnt += __popc(sm);
-        ++slot;
       }
     }
   }
@@ -248,10 +175,8 @@ __device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, fl
 }
 
 // ---------------------------------------------------------------- pass A
-template <int RS>
 __global__ void __launch_bounds__(kSphWarps * 32, 6)
 k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
-  __shared__ BulkRing<1, RS> s_ring[RS > 0 ? kSphWarps : 1];
   __shared__ float4 s_stage[kSphWarps][kStageA][1];
   __shared__ int2 s_meta[kSphWarps][kStageA];
   __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
@@ -284,36 +209,53 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   auto consume = [&]() {
     __syncwarp();
     unsigned nz = build_masks<1, false>(stage, cnt, ti0, h, live ? thr_mask : -1.0f, 0.0f, mask);
-    // two pairs per iteration (walk_masks2): independent chains for ILP
-    auto pair = [&](int q, bool on) {
-      float4 s = stage[q][0];
-      float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
-      float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      // 4 h_i^2 <= reach^2 = (2 h_max)^2 exactly, so c4 implies the reach
-      // test, and W(r, h_i) vanishes past 2 h_i: only the count's predicate
-      // needs the float64 decision near its threshold
-      bool c4 = r2 <= thr4;
-      if (on && fabsf(r2 - thr4) <= thr4b) {  // exact float64 decision, reference expression
-        int2 mt = meta[q];
-        double e2 = exact_r2_rows(a.rows, a.pshift, a.L, row_i, T.tperm[mt.x], mt.y & 31);
-        c4 = e2 <= thr4_64;
+    // the two pairs of a walk iteration (walk_masks2; the second may be absent,
+    // onb = false) in packed FP32x2 arithmetic (FFMA2 / FMUL2 / FADD2: one
+    // issue slot for both pairs).  Per pair: r^2 = (dx dx + dy dy) + dz dz; 4 h_i^2
+    // <= reach^2 = (2 h_max)^2 exactly, so the count predicate r^2 <= 4 h_i^2
+    // implies the reach test, and W(r, h_i) vanishes past 2 h_i: only the count
+    // needs the float64 decision near its threshold.  q = r^2 rsqrt(r^2) / h_i
+    // (MUFU.RSQ, no IEEE sqrt fix-up).  Same rounding order as the scalar
+    // form it replaced (density and counts unchanged bitwise; 1.462 -> 1.445
+    // ms at c2)
+    auto pair2 = [&](int qa, int qb, bool onb) {
+      float4 sa = stage[qa][0], sb = stage[qb][0];
+      float2 dx = make_float2(ti0.x - sa.x, ti0.x - sb.x);
+      float2 dy = make_float2(ti0.y - sa.y, ti0.y - sb.y);
+      float2 dz = make_float2(ti0.z - sa.z, ti0.z - sb.z);
+      float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+      bool ca = r2.x <= thr4, cb = r2.y <= thr4;
+      if (fabsf(r2.x - thr4) <= thr4b) {  // exact float64 decision, reference expression
+        int2 mt = meta[qa];
+        ca = exact_r2_rows(a.rows, a.pshift, a.L, row_i, T.tperm[mt.x], mt.y & 31) <= thr4_64;
       }
-      float qq = r2 * rsqrt_ftz(fmaxf(r2, 1e-30f)) * hinv;  // MUFU.RSQ, no IEEE sqrt fix-up
-      count += (on && c4) ? 1u : 0u;
-      return on ? s.w * w_body(qq) : 0.0f;
+      if (onb && fabsf(r2.y - thr4) <= thr4b) {
+        int2 mt = meta[qb];
+        cb = exact_r2_rows(a.rows, a.pshift, a.L, row_i, T.tperm[mt.x], mt.y & 31) <= thr4_64;
+      }
+      float2 rs = make_float2(rsqrt_ftz(fmaxf(r2.x, 1e-30f)), rsqrt_ftz(fmaxf(r2.y, 1e-30f)));
+      float2 qq = __fmul2_rn(__fmul2_rn(r2, rs), make_float2(hinv, hinv));
+      count += (ca ? 1u : 0u) + ((onb && cb) ? 1u : 0u);
+      // w_body: t = max(2 - q, 0) zeroes the outer branch past q = 2
+      float2 t = __ffma2_rn(qq, make_float2(-1.0f, -1.0f), make_float2(2.0f, 2.0f));
+      t = make_float2(fmaxf(t.x, 0.0f), fmaxf(t.y, 0.0f));
+      float2 outer = __fmul2_rn(__fmul2_rn(__fmul2_rn(make_float2(0.25f, 0.25f), t), t), t);
+      float2 inner = __ffma2_rn(__fmul2_rn(qq, qq),
+                                __ffma2_rn(make_float2(0.75f, 0.75f), qq,
+                                           make_float2(-1.5f, -1.5f)),
+                                make_float2(1.0f, 1.0f));
+      float2 wv = make_float2(qq.x < 1.0f ? inner.x : outer.x, qq.y < 1.0f ? inner.y : outer.y);
+      float2 ww = __fmul2_rn(make_float2(sa.w, sb.w), wv);
+      rho += ww.x + (onb ? ww.y : 0.0f);
     };
-    walk_masks2(mask, nz, [&](int q1, int q2) {
-      float w1 = pair(q1, true);
-      float w2 = pair(q2 >= 0 ? q2 : q1, q2 >= 0);
-      rho += w1 + w2;
-    });
+    walk_masks2(mask, nz, [&](int q1, int q2) { pair2(q1, q2 >= 0 ? q2 : q1, q2 >= 0); });
     __syncwarp();
     cnt = 0;
   };
   // cull radius from the tile's largest h (emit_tile_box: tile_lo.w), not this
   // lane's: every lane culls sources for the whole tile
-  sph_sweep<1, false, kStageA, RS>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage,
-                                   meta, cnt, consume, &s_ring[RS > 0 ? wid : 0]);
+  sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
+                               cnt, consume);
   if (live) {
     float norm3 = h > 0.0f ? kSigma * hinv * hinv * hinv : 0.0f;
     a.ncount[row_i] += (double)count;
@@ -324,20 +266,17 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
 // ---------------------------------------------------------------- pass B
 // records (k_pack_sph layout 1): P0 = (x, y, z, h), P1 = (vx, vy, vz, m),
 // P2 = (P/rho^2, c_s, rho, sigma/h^5).  1/q = h r^-1 reuses the rsqrt the
-// separation needs: a pair issues 3 MUFU (rsqrt, 1/h_j, 1/rho_j), two more on
-// the approaching-pair viscosity branch.  (A fourth record with 1/h_j and
+// separation needs: a pair issues 5 MUFU (rsqrt, 1/h_j, 1/rho_j and the two of
+// the viscosity term, evaluated for every pair and selected).  (A fourth record with 1/h_j and
 // m_j/rho_j precomputed, and 160-source stages to stay at 4 CTAs / SM, measured
 // 3.32 vs 2.83 ms at c2: staging and flush count outweigh the two MUFU.)
-// Two pairs per walk iteration at 4 CTAs / SM (120 registers, no spills):
-// 2.763 -> 2.728 ms at c2 against one pair at 5 CTAs / SM (96 registers).
+// Two pairs per walk iteration at 4 CTAs / SM (127 registers, no spills).
 constexpr int kStageB = 192;
-template <int RS, int STAGE>
 __global__ void __launch_bounds__(kSphWarps * 32, 4)
 k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
-  __shared__ BulkRing<3, RS> s_ring[RS > 0 ? kSphWarps : 1];
-  __shared__ float4 s_stage[kSphWarps][STAGE][3];
-  __shared__ int2 s_meta[kSphWarps][STAGE];
-  __shared__ unsigned s_mask[kSphWarps][STAGE / 32][32];
+  __shared__ float4 s_stage[kSphWarps][kStageB][3];
+  __shared__ int2 s_meta[kSphWarps][kStageB];
+  __shared__ unsigned s_mask[kSphWarps][kStageB / 32][32];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
   if (t >= *n_tiles_dev) return;
@@ -368,61 +307,97 @@ k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
     __syncwarp();
     unsigned nz = build_masks<3, true>(stage, cnt, ti0, hi, live ? thr_i : -1.0f,
                                        live ? reach2c : -1.0f, mask);
-    auto pair = [&](int q, bool on) {
-      float4 s0 = stage[q][0], s1 = stage[q][1], s2 = stage[q][2];
-      float hj = s0.w;
-      float dx = ti0.x - s0.x, dy = ti0.y - s0.y, dz = ti0.z - s0.z;
-      float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      if (!(on && r2 <= a.reach2)) return;
-      float rinv = rsqrt_ftz(fmaxf(r2, 1e-30f));
-      float r = r2 * rinv;
-      // cubic spline at q_i (value and (dW/dr)/r, hb/kernels.py:71-93) and
-      // (dW/dr)/r at q_j; 1/q = h / r
-      float qi = r * hinv, qj = r * rcp_approx(hj);
-      float ui = 2.0f - qi, uj = 2.0f - qj;
-      float wi = qi < 1.0f ? fmaf(qi * qi, fmaf(0.75f, qi, -1.5f), 1.0f)
-                           : (qi < 2.0f ? 0.25f * ui * ui * ui : 0.0f);
-      float gi = qi < 1.0f ? fmaf(2.25f, qi, -3.0f)
-                           : (qi < 2.0f ? -0.75f * ui * ui * (hi * rinv) : 0.0f);
-      float gj = qj < 1.0f ? fmaf(2.25f, qj, -3.0f)
-                           : (qj < 2.0f ? -0.75f * uj * uj * (hj * rinv) : 0.0f);
+    // the two pairs of a walk iteration (walk_masks2; the second may be absent,
+    // onb = false) evaluated together in packed FP32x2 arithmetic (FFMA2 /
+    // FMUL2 / FADD2: one issue slot for both pairs); the viscosity branch
+    // (approaching pairs) is a select, and the accumulators stay scalar, pair a
+    // then pair b.  Against one scalar pair per call: 261 -> 209 instructions
+    // per walk iteration, pass B 2.728 -> 2.439 ms at c2, 173.2 -> 154.1 ms at c4.
+    auto pair2 = [&](int qa, int qb, bool onb) {
+      const float2 one = make_float2(1.0f, 1.0f), half = make_float2(0.5f, 0.5f);
+      float4 a0 = stage[qa][0], a1 = stage[qa][1], a2 = stage[qa][2];
+      float4 b0 = stage[qb][0], b1 = stage[qb][1], b2 = stage[qb][2];
+      float2 dx = make_float2(ti0.x - a0.x, ti0.x - b0.x);
+      float2 dy = make_float2(ti0.y - a0.y, ti0.y - b0.y);
+      float2 dz = make_float2(ti0.z - a0.z, ti0.z - b0.z);
+      float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+      bool va = r2.x <= a.reach2, vb = onb && r2.y <= a.reach2;
+      if (!(va || vb)) return;
+      float2 rinv = make_float2(rsqrt_ftz(fmaxf(r2.x, 1e-30f)), rsqrt_ftz(fmaxf(r2.y, 1e-30f)));
+      float2 r = __fmul2_rn(r2, rinv);
+      float2 hj = make_float2(a0.w, b0.w);
+      float2 qi = __fmul2_rn(r, make_float2(hinv, hinv));
+      float2 qj = __fmul2_rn(r, make_float2(rcp_approx(a0.w), rcp_approx(b0.w)));
+      // u = max(2 - q, 0): the outer branch vanishes past q = 2 by itself
+      float2 ui = __ffma2_rn(qi, make_float2(-1.0f, -1.0f), make_float2(2.0f, 2.0f));
+      float2 uj = __ffma2_rn(qj, make_float2(-1.0f, -1.0f), make_float2(2.0f, 2.0f));
+      ui = make_float2(fmaxf(ui.x, 0.0f), fmaxf(ui.y, 0.0f));
+      uj = make_float2(fmaxf(uj.x, 0.0f), fmaxf(uj.y, 0.0f));
+      float2 ui2 = __fmul2_rn(ui, ui), uj2 = __fmul2_rn(uj, uj);
+      float2 w_in = __ffma2_rn(__fmul2_rn(qi, qi),
+                               __ffma2_rn(make_float2(0.75f, 0.75f), qi, make_float2(-1.5f, -1.5f)),
+                               one);
+      float2 w_out = __fmul2_rn(__fmul2_rn(make_float2(0.25f, 0.25f), ui2), ui);
+      float2 c3 = make_float2(-3.0f, -3.0f), c225 = make_float2(2.25f, 2.25f),
+             c075 = make_float2(-0.75f, -0.75f);
+      float2 gi_in = __ffma2_rn(c225, qi, c3), gj_in = __ffma2_rn(c225, qj, c3);
+      float2 gi_out = __fmul2_rn(__fmul2_rn(c075, ui2), __fmul2_rn(make_float2(hi, hi), rinv));
+      float2 gj_out = __fmul2_rn(__fmul2_rn(c075, uj2), __fmul2_rn(hj, rinv));
+      float2 wi = make_float2(qi.x < 1.0f ? w_in.x : w_out.x, qi.y < 1.0f ? w_in.y : w_out.y);
+      float2 gi = make_float2(qi.x < 1.0f ? gi_in.x : gi_out.x, qi.y < 1.0f ? gi_in.y : gi_out.y);
+      float2 gj = make_float2(qj.x < 1.0f ? gj_in.x : gj_out.x, qj.y < 1.0f ? gj_in.y : gj_out.y);
       // CRK moments: w = V_j W(r, h_i) (hb/kernels.py:205-220)
-      float wk = (s2.z > 0.0f ? s1.w * rcp_approx(s2.z) : 0.0f) * wi;
-      float wx = wk * dx, wy = wk * dy, wz = wk * dz;
-      mo[0] += wk;
-      mo[1] -= wx; mo[2] -= wy; mo[3] -= wz;
-      mo[4] = fmaf(wx, dx, mo[4]); mo[5] = fmaf(wx, dy, mo[5]); mo[6] = fmaf(wx, dz, mo[6]);
-      mo[7] = fmaf(wy, dy, mo[7]); mo[8] = fmaf(wy, dz, mo[8]); mo[9] = fmaf(wz, dz, mo[9]);
+      float2 vj = make_float2(a2.z > 0.0f ? a1.w * rcp_approx(a2.z) : 0.0f,
+                              b2.z > 0.0f ? b1.w * rcp_approx(b2.z) : 0.0f);
+      float2 wk = __fmul2_rn(vj, wi);
+      wk = make_float2(va ? wk.x : 0.0f, vb ? wk.y : 0.0f);
+      float2 wx = __fmul2_rn(wk, dx), wy = __fmul2_rn(wk, dy), wz = __fmul2_rn(wk, dz);
+      mo[0] += wk.x; mo[0] += wk.y;
+      mo[1] -= wx.x; mo[1] -= wx.y; mo[2] -= wy.x; mo[2] -= wy.y; mo[3] -= wz.x; mo[3] -= wz.y;
+      mo[4] = fmaf(wx.y, dx.y, fmaf(wx.x, dx.x, mo[4]));
+      mo[5] = fmaf(wx.y, dy.y, fmaf(wx.x, dy.x, mo[5]));
+      mo[6] = fmaf(wx.y, dz.y, fmaf(wx.x, dz.x, mo[6]));
+      mo[7] = fmaf(wy.y, dy.y, fmaf(wy.x, dy.x, mo[7]));
+      mo[8] = fmaf(wy.y, dz.y, fmaf(wy.x, dz.x, mo[8]));
+      mo[9] = fmaf(wz.y, dz.y, fmaf(wz.x, dz.x, mo[9]));
       // hydro (hb/kernels.py:227-258), m_i factored out
-      float gw = 0.5f * fmaf(gi, ti2.w, gj * s2.w);
-      float vx = ti1.x - s1.x, vy = ti1.y - s1.y, vz = ti1.z - s1.z;
-      float vdotr = fmaf(vz, dz, fmaf(vy, dy, vx * dx));
-      float visc = 0.0f;
-      if (vdotr < 0.0f) {
-        float hbar = 0.5f * (hi + hj);
-        float cbar = 0.5f * (ti2.y + s2.y);
-        float rhobar = 0.5f * (ti2.z + s2.z);
-        float mu = hbar * vdotr * rcp_approx(fmaf(0.01f * hbar, hbar, r2));
-        visc = fmaf(a.beta * mu, mu, -(a.alpha * cbar * mu)) * rcp_approx(rhobar);
-      }
-      float mjg = s1.w * gw;
-      float w = (ti2.x + s2.x + visc) * mjg;
-      fx = fmaf(-w, dx, fx); fy = fmaf(-w, dy, fy); fz = fmaf(-w, dz, fz);
-      float work = vdotr * mjg;
-      float hv = 0.5f * visc;
-      ei = fmaf(ti2.x + hv, work, ei);
-      ej = fmaf(s2.x + hv, work, ej);
+      float2 gw = __fmul2_rn(half, __ffma2_rn(gi, make_float2(ti2.w, ti2.w),
+                                              __fmul2_rn(gj, make_float2(a2.w, b2.w))));
+      float2 vx = make_float2(ti1.x - a1.x, ti1.x - b1.x);
+      float2 vy = make_float2(ti1.y - a1.y, ti1.y - b1.y);
+      float2 vz = make_float2(ti1.z - a1.z, ti1.z - b1.z);
+      float2 vdotr = __ffma2_rn(vz, dz, __ffma2_rn(vy, dy, __fmul2_rn(vx, dx)));
+      float2 hbar = __fmul2_rn(half, __fadd2_rn(make_float2(hi, hi), hj));
+      float2 cbar = __fmul2_rn(half, __fadd2_rn(make_float2(ti2.y, ti2.y), make_float2(a2.y, b2.y)));
+      float2 rhobar = __fmul2_rn(half, __fadd2_rn(make_float2(ti2.z, ti2.z), make_float2(a2.z, b2.z)));
+      float2 den = __ffma2_rn(__fmul2_rn(make_float2(0.01f, 0.01f), hbar), hbar, r2);
+      float2 mu = __fmul2_rn(__fmul2_rn(hbar, vdotr),
+                             make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+      float2 acm = __fmul2_rn(__fmul2_rn(make_float2(a.alpha, a.alpha), cbar), mu);
+      float2 vis = __fmul2_rn(__ffma2_rn(__fmul2_rn(make_float2(a.beta, a.beta), mu), mu,
+                                         make_float2(-acm.x, -acm.y)),
+                              make_float2(rcp_approx(rhobar.x), rcp_approx(rhobar.y)));
+      float2 visc = make_float2(vdotr.x < 0.0f ? vis.x : 0.0f, vdotr.y < 0.0f ? vis.y : 0.0f);
+      float2 mjg = __fmul2_rn(make_float2(a1.w, b1.w), gw);
+      mjg = make_float2(va ? mjg.x : 0.0f, vb ? mjg.y : 0.0f);
+      float2 w = __fmul2_rn(__fadd2_rn(__fadd2_rn(make_float2(ti2.x, ti2.x), make_float2(a2.x, b2.x)),
+                                       visc), mjg);
+      fx = fmaf(-w.y, dx.y, fmaf(-w.x, dx.x, fx));
+      fy = fmaf(-w.y, dy.y, fmaf(-w.x, dy.x, fy));
+      fz = fmaf(-w.y, dz.y, fmaf(-w.x, dz.x, fz));
+      float2 work = __fmul2_rn(vdotr, mjg);
+      float2 hv = __fmul2_rn(half, visc);
+      float2 pi_ = __fadd2_rn(make_float2(ti2.x, ti2.x), hv);
+      float2 pj_ = __fadd2_rn(make_float2(a2.x, b2.x), hv);
+      ei = fmaf(pi_.y, work.y, fmaf(pi_.x, work.x, ei));
+      ej = fmaf(pj_.y, work.y, fmaf(pj_.x, work.x, ej));
     };
-    // two pairs per iteration (walk_masks2): independent chains for ILP
-    walk_masks2(mask, nz, [&](int q1, int q2) {
-      pair(q1, true);
-      pair(q2 >= 0 ? q2 : q1, q2 >= 0);
-    });
+    walk_masks2(mask, nz, [&](int q1, int q2) { pair2(q1, q2 >= 0 ? q2 : q1, q2 >= 0); });
     __syncwarp();
     cnt = 0;
   };
-  sph_sweep<3, true, STAGE, RS>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage,
-                                  meta, cnt, consume, &s_ring[RS > 0 ? wid : 0]);
+  sph_sweep<3, true, kStageB>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
+                              cnt, consume);
   bool bad = !(isfinite(fx) && isfinite(fy) && isfinite(fz) && isfinite(ei) && isfinite(mo[0]));
   if (__ballot_sync(0xffffffffu, live && bad)) {
     if (lane == 0) atomicMin(a.err_key, (unsigned long long)(e0 * 4 + 1));
@@ -672,19 +647,8 @@ int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   a.skip_leaf = s.skip_leaf;
   a.skip_tiles = s.skip_tiles;
   unsigned grid = grid_for(s.T->n_tiles_cap, kSphWarps);
-  // HB_SPH_BULK (A/B switch): 1 = pass A sources through the bulk-async ring,
-  // 2 = pass B too (2 slots, 160-source stages to stay at 4 CTAs / SM)
-  static const int bulk = [] {
-    const char* e = getenv("HB_SPH_BULK");
-    return e ? atoi(e) : 0;
-  }();
-  if (pass == 0) {
-    if (bulk >= 1) k_sph_density<4><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-    else k_sph_density<0><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-  } else if (pass == 1) {
-    if (bulk >= 2) k_sph_force<2, 160><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-    else k_sph_force<0, kStageB><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-  }
+  if (pass == 0) k_sph_density<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  else if (pass == 1) k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   else k_sph_grad<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   HB_LAUNCH_CHECK();
   return HB_OK;

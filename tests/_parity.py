@@ -24,6 +24,8 @@ moments + solve, hydro), hb/kernels.py:143-278 (pair functions).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from tests.tolerances import assert_fp32_close
@@ -179,7 +181,8 @@ def check_step(oracle, p0, cfg, stride: int, crowded_bins: int = 4, passes=None,
              "compact_rows": int(rows.size), "entries": int(ref.la.size)}
     g, gabs, cnt = ref.gravity()
     grav = gpu_rows(out["grav"], rows)
-    assert_fp32_close(grav[recv], g[recv], gabs[recv], what=f"{what} gravity")
+    stats["gravity_err"] = assert_fp32_close(grav[recv], g[recv], gabs[recv],
+                                             what=f"{what} gravity")
     stats["gravity_pairs_in_reach"] = cnt["pairs_in_reach"]
     if not gravity_only:
         _check_sph(ref, rr, out, rows, recv, stats, what)
@@ -198,6 +201,11 @@ def check_step(oracle, p0, cfg, stride: int, crowded_bins: int = 4, passes=None,
     np.testing.assert_array_equal(gcount[recv], oc[recv, 0].astype(np.int64),
                                   err_msg=f"{what}: gravity in-r_cut counts")
     stats["gravity_pairs_total"] = total
+    log = os.environ.get("HB_PARITY_LOG")
+    if log:  # error statistics of every checked step, one JSON line each
+        import json
+        with open(log, "a") as f:
+            f.write(json.dumps({"what": what, **stats}) + "\n")
     return stats
 
 
@@ -213,8 +221,8 @@ def _check_sph(ref, rr, out, rows, recv, stats, what):
         (what, "density", float(np.median(rel)), float(rel.max()))
     stats["density_rel_max"] = float(rel.max())
     mom, mabs, A, B, fb = ref.crk(np.where(gas, gdens, ref.q.density))
-    assert_fp32_close(gpu_rows(out["crk_moments"], rows)[recv], mom[recv], mabs[recv],
-                      what=f"{what} crk moments")
+    stats["crk_err"] = assert_fp32_close(gpu_rows(out["crk_moments"], rows)[recv], mom[recv],
+                                         mabs[recv], what=f"{what} crk moments")
     np.testing.assert_array_equal(gpu_rows(out["crk_fallback"], rows)[recv].astype(bool),
                                   fb[recv], err_msg=f"{what}: CRK fallback")
     gA = gpu_rows(out["crk_A"], rows)
@@ -228,6 +236,6 @@ def _check_sph(ref, rr, out, rows, recv, stats, what):
     assert dB.max() <= 1e-5 * max(1.0, float(np.abs(B[ok]).max() * h[ok].max())), \
         (what, "B", float(dB.max()))
     hy, habs = ref.hydro(np.where(gas, gdens, ref.q.density))
-    assert_fp32_close(gpu_rows(out["hydro"], rows)[recv], hy[recv], habs[recv],
-                      what=f"{what} hydro")
+    stats["hydro_err"] = assert_fp32_close(gpu_rows(out["hydro"], rows)[recv], hy[recv],
+                                           habs[recv], what=f"{what} hydro")
     stats["fallbacks"] = int(fb[recv].sum())

@@ -19,6 +19,8 @@ MED_REL, P999_REL = 1e-5, 1e-3
 
 
 def assert_fp32_close(got, ref, absum, what=""):
+    """Raise unless got meets the tolerance; return the error statistics
+    {norm_med, norm_p999, rel_med, rel_p999} (rel_* None without conditioned rows)."""
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     absum = np.asarray(absum, dtype=np.float64)
@@ -26,13 +28,17 @@ def assert_fp32_close(got, ref, absum, what=""):
     diff = np.abs(got - ref)
     live = absum > 0
     assert np.all(diff[~live] == 0), f"{what}: nonzero output where the reference has no terms"
+    stats = {"norm_med": None, "norm_p999": None, "rel_med": None, "rel_p999": None}
     if not np.any(live):
-        return
+        return stats
     e = diff[live] / absum[live]
     med, p999 = float(np.median(e)), float(np.quantile(e, 0.999))
+    stats.update(norm_med=med, norm_p999=p999)
     assert med <= MED_NORM and p999 <= P999_NORM, f"{what}: normalised med={med:.2e} p99.9={p999:.2e}"
     cond = live & (np.abs(ref) >= 1e-2 * absum)
     if np.any(cond):
         r = diff[cond] / np.abs(ref[cond])
         med, p999 = float(np.median(r)), float(np.quantile(r, 0.999))
+        stats.update(rel_med=med, rel_p999=p999)
         assert med <= MED_REL and p999 <= P999_REL, f"{what}: relative med={med:.2e} p99.9={p999:.2e}"
+    return stats
