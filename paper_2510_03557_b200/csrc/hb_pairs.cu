@@ -32,6 +32,19 @@ constexpr int kStage = 64;           // staged sources per warp
 
 
 // ---------------------------------------------------------------- tiling
+// Segment origins on a global grid of q = 2^(ilogb(L) - 23): the difference of
+// two origins minus a periodic shift s L (L a multiple of q, as for L = 1) is a
+// multiple of q below 2 L, so the per-entry FP32 offset D = (o_A - o_B) - s L
+// the interaction kernels apply to a whole source segment is exact.  A rounded
+// D would move every source of that segment by up to half an ulp of D
+// together -- a coherent error, unlike the independent per-record roundings;
+// it was the largest FP32 error term of the lattice gravity.
+__device__ __forceinline__ double grid_origin(double o, double L) {
+  if (!(L > 0.0) || !isfinite(L)) return o;
+  double q = ldexp(1.0, ilogb(L) - 23);
+  return rint(o / q) * q;
+}
+
 __global__ void k_tile_count(int64_t n_leaves, const int64_t* leaf_start, const int64_t* leaf_end,
                              Rows rows, int sel, int64_t* sel_cnt, int64_t* tile_cnt,
                              int tile_max, int even) {
@@ -161,7 +174,7 @@ k_tile_build(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end, Rows 
       int d = threadIdx.x;
       double a = red[0][d][0], b = red[1][d][0];
       for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { a = fmin(a, red[0][d][w]); b = fmax(b, red[1][d][w]); }
-      org[d] = 0.5 * (a + b);
+      org[d] = grid_origin(0.5 * (a + b), L);
       T.origin[3 * leaf + d] = org[d];
     }
     __syncthreads();
@@ -326,7 +339,7 @@ k_tile_build_warp(Tiling T, const int64_t* leaf_start, const int64_t* leaf_end,
       mn[d] = fmin(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
       mx[d] = fmax(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
     }
-    org[d] = 0.5 * (mn[d] + mx[d]);
+    org[d] = grid_origin(0.5 * (mn[d] + mx[d]), L);
   }
   if (lane < 3) T.origin[3 * leaf + lane] = org[lane];
   for (int k = lane; k < m_sel; k += 32) {  // second pass (L1-hot): leaf-frame FP32
@@ -847,8 +860,11 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 // by the float bits of soft = r^2 + eps^2 (2^JB intervals per octave: index =
 // bits >> (23 - JB), in-interval variable = the low 23 - JB mantissa bits as a
 // float in [1, 1 + 2^-JB) minus 1) and stores G(soft) = S(sqrt(soft - eps^2) /
-// r_s) * soft^{-3/2}.  Per pair: 3 FADD + 3 FFMA (soft) + LEA.HI + VIMNMX + 2
-// LOP3 + FADD + LEA + LDS + 3 FFMA + FMUL + 3 FFMA, no MUFU.  Fit error ~2e-8
+// r_s) * soft^{-3/2}.  Sources go in pairs through Blackwell's packed FP32x2
+// instructions: per two sources 6 FADD (dx) + 3 FFMA2 (soft) + 2 LEA.HI + 2
+// VIMNMX + 2 LOP3 + FADD2 + 2 LEA + 2 LDS + 6 FFMA + 2 FMUL (cubic, m_j) + 3
+// FFMA2 (accumulate), no MUFU: 18 SASS instructions per source in the
+// 8-source batch loop against 22 scalar (c2: 10.06 -> 9.70 ms).  Fit error ~2e-8
 // relative (JB = 5, default) / ~3e-7 (JB = 4).  (Round 1's r- and t-indexed S
 // tables -- one or two MUFU and 27 instructions per pair -- were removed.)
 // Rows past r_cut (to the end of the interval holding r_cut) carry the smooth
@@ -866,7 +882,7 @@ __device__ __forceinline__ unsigned and_or(unsigned a, unsigned b, unsigned c) {
   return d;
 }
 
-template <int JB, int REP, int kGravBatch, int ACC>
+template <int JB, int REP, int kGravBatch>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -884,19 +900,16 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   float eps2 = a.pp.p1;
   float2 eps2x2 = make_float2(eps2, eps2);
   const unsigned lowmask = (1u << (23 - JB)) - 1u, one_bits = 0x3F800000u;
-  // float64 accumulators fed with FP32 partial sums of 8 sources: the FP32
-  // rounding then scales with a partial, not with the running total of ~500
-  // cancelling terms (the relative error of the lattice's small net forces
-  // halves: see DESIGN.md 3)
-  double ax = 0.0, ay = 0.0, az = 0.0;
-  float2 rx = make_float2(0.0f, 0.0f), ry = rx, rz = rx;  // ACC 0 / 1 / 3 running sums
+  // even / odd-source running sums (packed pairs), fed with fresh FP32x2
+  // partial sums of each 8-source batch: a running sum takes one rounding per
+  // batch instead of one per source (the lattice gravity's relative error,
+  // dark matter 512^3 median 8.7e-6 -> 6.3e-6 for 3% of the kernel)
+  float2 rx = make_float2(0.0f, 0.0f), ry = rx, rz = rx;
   const double* oA = T.origin + 3 * A;  // re-read per entry (L1): 6 registers fewer
   int cnt = 0;
   auto flush = [&]() {
     __syncwarp();
     int q0 = 0;
-    if (ACC >= 3) rx = ry = rz = make_float2(0.0f, 0.0f);
-    int nb = 0;
     {
       // batches of kGravBatch sources: every table row is requested before the
       // first one is used, so the gathers' latency overlaps within the warp
@@ -928,7 +941,6 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
           bc[2 * p + 1] = s_tab[k1 * REP];
         }
         float2 fx = make_float2(0.0f, 0.0f), fy = fx, fz = fx;
-        if (ACC == 0 || ACC >= 3) { fx = rx; fy = ry; fz = rz; }
 #pragma unroll
         for (int p = 0; p < kGravBatch / 2; ++p) {
           float4 c0 = bc[2 * p], c1 = bc[2 * p + 1];
@@ -939,23 +951,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
           fy = __ffma2_rn(w, by[p], fy);
           fz = __ffma2_rn(w, bz[p], fz);
         }
-        if (ACC == 0 || ACC >= 3) {
-          rx = fx; ry = fy; rz = fz;
-          // ACC 5 / 6: fold the FP32 partial into float64 every 2 / 4 batches
-          if ((ACC == 5 && (nb & 1)) || (ACC == 6 && (nb & 3) == 3)) {
-            ax += (double)(rx.x + rx.y);
-            ay += (double)(ry.x + ry.y);
-            az += (double)(rz.x + rz.y);
-            rx = ry = rz = make_float2(0.0f, 0.0f);
-          }
-          ++nb;
-        } else if (ACC == 1) {
-          rx = __fadd2_rn(rx, fx); ry = __fadd2_rn(ry, fy); rz = __fadd2_rn(rz, fz);
-        } else {
-          ax += (double)(fx.x + fx.y);
-          ay += (double)(fy.x + fy.y);
-          az += (double)(fz.x + fz.y);
-        }
+        rx = __fadd2_rn(rx, fx); ry = __fadd2_rn(ry, fy); rz = __fadd2_rn(rz, fz);
       }
     }
     float tx = 0.0f, ty = 0.0f, tz = 0.0f;
@@ -973,14 +969,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
       ty = fmaf(w, dy, ty);
       tz = fmaf(w, dz, tz);
     }
-    if (ACC >= 2) {
-      ax += (double)(tx + (rx.x + rx.y));
-      ay += (double)(ty + (ry.x + ry.y));
-      az += (double)(tz + (rz.x + rz.y));
-      if (ACC >= 3) rx = ry = rz = make_float2(0.0f, 0.0f);
-    } else {
-      rx.x += tx; ry.x += ty; rz.x += tz;
-    }
+    rx.x += tx; ry.x += ty; rz.x += tz;
     __syncwarp();
     cnt = 0;
   };
@@ -1027,9 +1016,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
     }
   }
   flush();
-  if (ACC == 0 || ACC == 1) {
-    ax = (double)(rx.x + rx.y); ay = (double)(ry.x + ry.y); az = (double)(rz.x + rz.y);
-  }
+  float ax = rx.x + rx.y, ay = ry.x + ry.y, az = rz.x + rz.y;
   bool bad = !(isfinite(ax) && isfinite(ay) && isfinite(az));
   unsigned bm = __ballot_sync(0xffffffffu, live && bad);
   if (bm) {
@@ -1050,7 +1037,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps, int ACC = 2>
+template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev) {
@@ -1061,11 +1048,11 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * WARPS + wid + (t_begin_dev ? *t_begin_dev : 0);
   if (t < *n_tiles_dev)
-    grav_tile<JB, REP, NB, ACC>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
+    grav_tile<JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
                                  t, lane);
 }
 
-template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps, int ACC = 2>
+template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                int64_t tcap, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err) {
@@ -1079,13 +1066,13 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS, ACC>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
   }
   unsigned grid = grid_for(tcap, WARPS), blk = WARPS * 32;
-  k_gravity<JB, REP, NB, MINB, WARPS, ACC><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
+  k_gravity<JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
   return HB_OK;
 }
 
@@ -1098,18 +1085,9 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
   // 16-warp CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4.
   // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
   // gone.)
-  static const int acc = [] {
-    const char* e = getenv("HB_GRAV_ACC");
-    return e ? atoi(e) : 2;
-  }();
-  int rc;
-  if (gt.jbits == 4) rc = launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else if (acc == 0) rc = launch_gravity_kind<5, 8, 8, 2, 16, 0>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else if (acc == 1) rc = launch_gravity_kind<5, 8, 8, 2, 16, 1>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else if (acc == 3) rc = launch_gravity_kind<5, 8, 8, 2, 16, 3>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else if (acc == 5) rc = launch_gravity_kind<5, 8, 8, 2, 16, 5>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else if (acc == 6) rc = launch_gravity_kind<5, 8, 8, 2, 16, 6>(d, table, gt, tcap, ntd, t_begin, st, err);
-  else rc = launch_gravity_kind<5, 8, 8, 2, 16, 2>(d, table, gt, tcap, ntd, t_begin, st, err);
+  int rc = gt.jbits == 4
+               ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err)
+               : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err);
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;

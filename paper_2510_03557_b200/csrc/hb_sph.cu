@@ -158,14 +158,22 @@ __device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, fl
   unsigned nz = 0u;  // non-empty words of this lane
   for (int w = 0; w < nw; ++w) {
     unsigned bits = 0u;
+    // two sources per step in packed FP32x2 (same rounding as the scalar form)
 #pragma unroll
-    for (int b = 0; b < 32; ++b) {
-      float4 s = stage[w * 32 + b][0];
-      float dx = ti0.x - s.x, dy = ti0.y - s.y, dz = ti0.z - s.z;
-      float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      float thr = thr_i;  // pass B: thr_i = 4 h_i^2 (1 + 2e-4), s.w = h_j
-      if (HYDRO) thr = fminf(reach2c, fmaxf(thr_i, 4.0008f * s.w * s.w));
-      bits |= (r2 <= thr ? 1u : 0u) << b;
+    for (int b = 0; b < 32; b += 2) {
+      float4 s = stage[w * 32 + b][0], t = stage[w * 32 + b + 1][0];
+      float2 dx = make_float2(ti0.x - s.x, ti0.x - t.x);
+      float2 dy = make_float2(ti0.y - s.y, ti0.y - t.y);
+      float2 dz = make_float2(ti0.z - s.z, ti0.z - t.z);
+      float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+      float2 thr = make_float2(thr_i, thr_i);  // pass B: thr_i = 4 h_i^2 (1 + 2e-4), s.w = h_j
+      if (HYDRO) {
+        float2 hj = make_float2(s.w, t.w);
+        float2 t4 = __fmul2_rn(__fmul2_rn(make_float2(4.0008f, 4.0008f), hj), hj);
+        thr = make_float2(fminf(reach2c, fmaxf(thr_i, t4.x)), fminf(reach2c, fmaxf(thr_i, t4.y)));
+      }
+      bits |= (r2.x <= thr.x ? 1u : 0u) << b;
+      bits |= (r2.y <= thr.y ? 1u : 0u) << (b + 1);
     }
     mask[w][lane] = bits;
     nz |= (bits != 0u ? 1u : 0u) << w;
