@@ -1043,11 +1043,17 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
           const int64_t* t_begin_dev) {
   extern __shared__ float4 s_tab[];  // gt.rows * REP
   __shared__ float4 s_src[WARPS][kGravStage];
+  // the grid covers the tiling's capacity; a range launch (t_begin_dev, a
+  // bin-range end in n_tiles_dev) leaves whole CTAs past its end: they leave
+  // before loading the 66 KB table
+  int64_t t0 = (int64_t)blockIdx.x * WARPS + (t_begin_dev ? *t_begin_dev : 0);
+  int64_t t_end = *n_tiles_dev;
+  if (t0 >= t_end) return;
   for (int k = threadIdx.x; k < gt.rows * REP; k += blockDim.x) s_tab[k] = table[k / REP];
   __syncthreads();
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t t = (int64_t)blockIdx.x * WARPS + wid + (t_begin_dev ? *t_begin_dev : 0);
-  if (t < *n_tiles_dev)
+  int64_t t = t0 + wid;
+  if (t < t_end)
     grav_tile<JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
                                  t, lane);
 }

@@ -628,9 +628,9 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
     }
   }
   tm.mark(6);
-  // no split (leaf gravity, or the half-warp bin kernel, which runs as one
-  // launch and never records grav_half_event): every row is final at the end
-  if (a->grav_half_event && (!bin_gravity || a->gravity_mode == 2)) {
+  // no split (leaf gravity runs as one launch and never records
+  // grav_half_event): every row is final at the end
+  if (a->grav_half_event && !bin_gravity) {
     a->grav_split_row = 0;
   }
   if (zero_ghost && (a->passes & HB_PASS_GRAVITY) && !(a->passes & HB_PASS_COUNT_ONLY)) {

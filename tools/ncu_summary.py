@@ -21,6 +21,9 @@ KEYS = [
     ("sm__sass_thread_inst_executed_op_ffma_pred_on.sum", "thread_ffma_G", 1e-9),
     ("sm__sass_thread_inst_executed_op_fadd_pred_on.sum", "thread_fadd_G", 1e-9),
     ("sm__sass_thread_inst_executed_op_fmul_pred_on.sum", "thread_fmul_G", 1e-9),
+    ("sm__sass_thread_inst_executed_op_ffma2_pred_on.sum", "thread_ffma2_G", 1e-9),
+    ("sm__sass_thread_inst_executed_op_fadd2_pred_on.sum", "thread_fadd2_G", 1e-9),
+    ("sm__sass_thread_inst_executed_op_fmul2_pred_on.sum", "thread_fmul2_G", 1e-9),
     ("launch__registers_per_thread", "regs", 1),
 ]
 STALL = "smsp__average_warp_latency_issue_stalled_"
