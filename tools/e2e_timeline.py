@@ -21,6 +21,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--phases", action="store_true",
+                    help="also run the step with its phase timer (the step then syncs at "
+                         "its end, so the outputs' copy-out no longer overlaps gravity) and "
+                         "print the phase times under the concurrent uploads")
     args = ap.parse_args()
     p, cfg, meta = bench.make_workload(args.config)
     rr = bench._make_rank(args, p, cfg, 0, 1, meta)
@@ -59,6 +63,19 @@ def main():
     for g, fs in groups.items():
         print(g, {f: round(pinned_in[f].numel() * pinned_in[f].element_size() / 1e6, 1) for f in fs})
     print({k: round(v.numel() * v.element_size() / 1e6, 1) for k, v in pinned_out.items()})
+    if args.phases:
+        step0 = rr.step
+
+        def timed(*a, **k):   # the timed step checks its own status: mark the word clean
+            out = step0(*a, **{**k, "timing": True})
+            hs.status[0], hs.status[1], hs.status[2] = -1, 0, 0
+            return out
+        rr.step = timed
+        hs()
+        print("phases under uploads:", {k: round(v, 3) for k, v in rr.last["ms_phase"].items()})
+        rr.step = step0
+        rr.step(PASS_ALL, timing=True)
+        print("phases device-only:  ", {k: round(v, 3) for k, v in rr.last["ms_phase"].items()})
 
 
 if __name__ == "__main__":

@@ -18,6 +18,10 @@ KEYS = [
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe %"),
+    ("sm__sass_thread_inst_executed_op_ffma2_pred_on.sum", "FFMA2 thread instructions"),
+    ("sm__sass_thread_inst_executed_op_fmul2_pred_on.sum", "FMUL2 thread instructions"),
+    ("sm__sass_thread_inst_executed_op_fadd2_pred_on.sum", "FADD2 thread instructions"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("sm__sass_thread_inst_executed_op_ffma_pred_on.sum", "thread FFMA"),
