@@ -14,7 +14,7 @@ copy into pinned host memory.  ``encode_rank_checkpoint`` /
 ``decode_rank_checkpoint`` keep the reference's host signatures.
 
 The two-tier store around the codec (crash-safe renames, tier-2 bleed,
-retention) is filesystem orchestration, outside this engine's scope.
+retention, recovery) is ``tiered.TieredStore``.
 """
 from __future__ import annotations
 
@@ -80,9 +80,12 @@ def _column_device(fields: dict, name: str, tag: int, attr: str, col):
                 ).contiguous()
 
 
-def encode_rank_checkpoint_device(fields: dict, step: int, rank: int) -> bytes:
+def encode_rank_checkpoint_device(fields: dict, step: int, rank: int,
+                                  with_file_crc: bool = False):
     """Blob of a device-resident rank field set (dict of CUDA tensors with the
-    ParticleSet field names), assembled on the GPU, one D2H copy."""
+    ParticleSet field names), assembled on the GPU, one D2H copy.  With
+    ``with_file_crc`` returns (blob, CRC32C of the whole blob), the latter
+    taken on the device before the copy (the tiered store's manifest CRC)."""
     torch = N.torch_cuda()
     n = int(fields["pos"].shape[0])
     n_ghost = int((fields["ghost"] == 1).sum().item())
@@ -110,9 +113,11 @@ def encode_rank_checkpoint_device(fields: dict, step: int, rank: int) -> bytes:
             off += nb
     footer = crc32c_device(blob[:total])
     blob[total:].copy_(torch.frombuffer(bytearray(struct.pack("<I", footer)), dtype=torch.uint8))
+    fcrc = crc32c_device(blob) if with_file_crc else None
     host = _pinned(total + 4)
     host.copy_(blob)
-    return host.numpy().tobytes()
+    out = host.numpy().tobytes()
+    return (out, fcrc) if with_file_crc else out
 
 
 _PINNED = {"buf": None}
@@ -128,11 +133,11 @@ def _pinned(nbytes: int):
     return b[:nbytes]
 
 
-def encode_rank_checkpoint(p: ParticleSet, step: int, rank: int) -> bytes:
+def encode_rank_checkpoint(p: ParticleSet, step: int, rank: int, with_file_crc: bool = False):
     """Bit-exact rank state in the versioned block format (hb/tiered_io.py:80-96)."""
     fields = {k: N.dev(np.ascontiguousarray(getattr(p, k)))
               for k in {a for _, _, a, _ in FIELDS}}
-    return encode_rank_checkpoint_device(fields, step, rank)
+    return encode_rank_checkpoint_device(fields, step, rank, with_file_crc)
 
 
 def decode_rank_checkpoint(blob: bytes):
