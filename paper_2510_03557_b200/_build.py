@@ -14,7 +14,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--extended-lambda", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-diag-suppress", "177"]
-SOURCES = ["hb_sort.cu", "hb_mesh.cu", "hb_pairs.cu", "hb_crk.cu", "hb_step.cu", "hb_sph.cu", "hb_halo.cu", "hb_grav2.cu", "hb_gravg.cu", "hb_pm.cu", "hb_fof.cu", "hb_crc.cu", "hb_levels.cu"]
+SOURCES = ["hb_sort.cu", "hb_mesh.cu", "hb_pairs.cu", "hb_crk.cu", "hb_step.cu", "hb_sph.cu", "hb_halo.cu", "hb_grav2.cu", "hb_pm.cu", "hb_fof.cu", "hb_crc.cu", "hb_levels.cu"]
 
 
 def _compile(src: str, obj: str) -> None:

@@ -1091,12 +1091,6 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
   // 16-warp CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4.
   // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
   // gone.)
-  static int groups = -1;
-  if (groups < 0) {  // HB_GRAV_GROUPS: 1 = one list per warp (k_gravity), 2 / 4 / 8 = grouped
-    const char* e = getenv("HB_GRAV_GROUPS");
-    groups = e ? atoi(e) : kGravGroupsDefault;
-  }
-  if (groups > 1) return launch_gravity_groups(groups, d, table, gt, tcap, ntd, st, err, t_begin);
   int rc = gt.jbits == 4
                ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err)
                : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err);

@@ -392,11 +392,6 @@ int gravity_table(double r_s, double r_cut, double eps, float4* host_out, GravTa
 // cached device copy (library-owned, per device); nullptr + err on failure
 const float4* gravity_table_device(double r_s, double r_cut, double eps, GravTab* gt,
                                    cudaStream_t st, HbError* err);
-// grouped-target gravity (hb_gravg.cu): G = 2, 4 or 8 target groups per warp
-constexpr int kGravGroupsDefault = 4;
-int launch_gravity_groups(int G, const EvalDev& d, const float4* table, const GravTab& gt,
-                          int64_t tcap, const int64_t* ntd, cudaStream_t st, HbError* err,
-                          const int64_t* t_begin);
 // tiles [*t_begin (0 if null), *ntd)
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
                         const int64_t* ntd, cudaStream_t st, HbError* err,
