@@ -882,13 +882,7 @@ __device__ __forceinline__ unsigned and_or(unsigned a, unsigned b, unsigned c) {
   return d;
 }
 
-// SOA: the stage holds sources in blocks of 8 (x[8], y[8], z[8], m[8], the
-// four runs rotated by the block index so the staging's scalar stores are
-// conflict-free), so a batch's coordinates and masses arrive in register
-// pairs: dx / dy / dz issue as FADD2 and m_j as FMUL2 (per 8 sources 119
-// instead of 135 instructions, same 8 LDS.128 source loads); the final batch
-// is padded with mass-0 sources far away instead of a scalar tail loop.
-template <int JB, int REP, int kGravBatch, bool SOA = false>
+template <int JB, int REP, int kGravBatch>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -913,67 +907,6 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   float2 rx = make_float2(0.0f, 0.0f), ry = rx, rz = rx;
   const double* oA = T.origin + 3 * A;  // re-read per entry (L1): 6 registers fewer
   int cnt = 0;
-  float* stf = reinterpret_cast<float*>(stage);
-  auto flush_soa = [&]() {
-    // pad to whole blocks of 8 with mass-0 sources at ~1e15 (soft ~3e30: the
-    // zero table row, an exact 0 contribution)
-    int n8 = (cnt + 7) & ~7;
-    if (cnt + lane < n8) {
-      int q = cnt + lane, b = q >> 3, i = q & 7;
-      float* blk = stf + b * 32 + i;
-      blk[((0 + b) & 3) * 8] = 1e15f; blk[((1 + b) & 3) * 8] = 1e15f;
-      blk[((2 + b) & 3) * 8] = 1e15f; blk[((3 + b) & 3) * 8] = 0.0f;
-    }
-    __syncwarp();
-    const unsigned lowmask = (1u << (23 - JB)) - 1u, one_bits = 0x3F800000u;
-    for (int b = 0; b < (n8 >> 3); ++b) {
-      const float* blk = stf + b * 32;
-      int r = b & 3;
-      const float4* cx = reinterpret_cast<const float4*>(blk + ((0 + r) & 3) * 8);
-      const float4* cy = reinterpret_cast<const float4*>(blk + ((1 + r) & 3) * 8);
-      const float4* cz = reinterpret_cast<const float4*>(blk + ((2 + r) & 3) * 8);
-      const float4* cm = reinterpret_cast<const float4*>(blk + ((3 + r) & 3) * 8);
-      float4 X[2] = {cx[0], cx[1]}, Y[2] = {cy[0], cy[1]}, Z[2] = {cz[0], cz[1]};
-      float4 M[2] = {cm[0], cm[1]};
-      float2 bx[4], by[4], bz[4], bu[4], bm[4];
-      float4 bc[8];
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        float4 xs = X[p >> 1], ys = Y[p >> 1], zs = Z[p >> 1], ms = M[p >> 1];
-        float2 sx = (p & 1) ? make_float2(xs.z, xs.w) : make_float2(xs.x, xs.y);
-        float2 sy = (p & 1) ? make_float2(ys.z, ys.w) : make_float2(ys.x, ys.y);
-        float2 sz = (p & 1) ? make_float2(zs.z, zs.w) : make_float2(zs.x, zs.y);
-        bm[p] = (p & 1) ? make_float2(ms.z, ms.w) : make_float2(ms.x, ms.y);
-        bx[p] = __fadd2_rn(make_float2(ti.x, ti.x), make_float2(-sx.x, -sx.y));
-        by[p] = __fadd2_rn(make_float2(ti.y, ti.y), make_float2(-sy.x, -sy.y));
-        bz[p] = __fadd2_rn(make_float2(ti.z, ti.z), make_float2(-sz.x, -sz.y));
-        float2 soft = __ffma2_rn(bz[p], bz[p], __ffma2_rn(by[p], by[p], __ffma2_rn(bx[p], bx[p], eps2x2)));
-        unsigned b0 = __float_as_uint(soft.x), b1 = __float_as_uint(soft.y);
-        unsigned k0 = min((b0 >> (23 - JB)) - gt.base, gt.last);
-        unsigned k1 = min((b1 >> (23 - JB)) - gt.base, gt.last);
-        float2 um = make_float2(__uint_as_float(and_or(b0, lowmask, one_bits)),
-                                __uint_as_float(and_or(b1, lowmask, one_bits)));
-        bu[p] = __fadd2_rn(um, make_float2(-1.0f, -1.0f));
-        bc[2 * p] = s_tab[k0 * REP];
-        bc[2 * p + 1] = s_tab[k1 * REP];
-      }
-      float2 fx = make_float2(0.0f, 0.0f), fy = fx, fz = fx;
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        float4 c0 = bc[2 * p], c1 = bc[2 * p + 1];
-        float u0 = bu[p].x, u1 = bu[p].y;
-        float2 w = __fmul2_rn(make_float2(fmaf(fmaf(fmaf(c0.w, u0, c0.z), u0, c0.y), u0, c0.x),
-                                          fmaf(fmaf(fmaf(c1.w, u1, c1.z), u1, c1.y), u1, c1.x)),
-                              bm[p]);
-        fx = __ffma2_rn(w, bx[p], fx);
-        fy = __ffma2_rn(w, by[p], fy);
-        fz = __ffma2_rn(w, bz[p], fz);
-      }
-      rx = __fadd2_rn(rx, fx); ry = __fadd2_rn(ry, fy); rz = __fadd2_rn(rz, fz);
-    }
-    __syncwarp();
-    cnt = 0;
-  };
   auto flush = [&]() {
     __syncwarp();
     int q0 = 0;
@@ -1076,25 +1009,13 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
           ok = box_gap2(sj.x, sj.y, sj.z, tlo, thi) <= R2;
         }
         unsigned sm = __ballot_sync(0xffffffffu, ok);
-        if (cnt + 32 > kGravStage) {
-          if constexpr (SOA) flush_soa(); else flush();
-        }
-        if (ok) {
-          int q = cnt + __popc(sm & lanemask_lt());
-          if constexpr (SOA) {
-            int b = q >> 3;
-            float* blk = stf + b * 32 + (q & 7);
-            blk[((0 + b) & 3) * 8] = sj.x; blk[((1 + b) & 3) * 8] = sj.y;
-            blk[((2 + b) & 3) * 8] = sj.z; blk[((3 + b) & 3) * 8] = sj.w;
-          } else {
-            stage[q] = sj;
-          }
-        }
+        if (cnt + 32 > kGravStage) flush();
+        if (ok) stage[cnt + __popc(sm & lanemask_lt())] = sj;
         cnt += __popc(sm);
       }
     }
   }
-  if constexpr (SOA) flush_soa(); else flush();
+  flush();
   float ax = rx.x + rx.y, ay = ry.x + ry.y, az = rz.x + rz.y;
   bool bad = !(isfinite(ax) && isfinite(ay) && isfinite(az));
   unsigned bm = __ballot_sync(0xffffffffu, live && bad);
@@ -1116,7 +1037,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps, bool SOA = false>
+template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev) {
@@ -1133,11 +1054,11 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = t0 + wid;
   if (t < t_end)
-    grav_tile<JB, REP, NB, SOA>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
+    grav_tile<JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
                                  t, lane);
 }
 
-template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps, bool SOA = false>
+template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                int64_t tcap, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err) {
@@ -1151,13 +1072,13 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS, SOA>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
   }
   unsigned grid = grid_for(tcap, WARPS), blk = WARPS * 32;
-  k_gravity<JB, REP, NB, MINB, WARPS, SOA><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
+  k_gravity<JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
   return HB_OK;
 }
 
@@ -1170,16 +1091,9 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
   // 16-warp CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4.
   // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
   // gone.)
-  static int soa = -1;
-  if (soa < 0) {  // HB_GRAV_SOA: 1 = blocked-SoA stage (FADD2 / FMUL2 source terms), 0 = float4 stage
-    const char* e = getenv("HB_GRAV_SOA");
-    soa = e ? atoi(e) != 0 : 1;
-  }
   int rc = gt.jbits == 4
-               ? (soa ? launch_gravity_kind<4, 8, 8, 4, kGravWarps, true>(d, table, gt, tcap, ntd, t_begin, st, err)
-                      : launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err))
-               : (soa ? launch_gravity_kind<5, 8, 8, 2, 16, true>(d, table, gt, tcap, ntd, t_begin, st, err)
-                      : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err));
+               ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err)
+               : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err);
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;
