@@ -93,6 +93,7 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
   int32_t* st_code = ws.take<int32_t>(nbins * 27 + 1);
   int64_t* ntd = ws.take<int64_t>(2);
   float4* P0 = ws.take<float4>(g.n + 1);
+  unsigned long long* ctr = ws.take<unsigned long long>(2);  // persistent-grid tile counters
   if (ws.dry) {
     Arena s = ws;
     build_tiling(T, nbins, nullptr, nullptr, Rows{}, nullptr, 0.0, 0, nullptr, s, st, err);
@@ -162,16 +163,16 @@ int gravity_bins(const GravBinArgs& g, Arena& ws, cudaStream_t st, HbError* err)
     int rc2;
     if (g.split_event) {  // tiles of bins < grav_split_bin, then the rest (tile_ptr is per bin)
       const int64_t* mid = T.tile_ptr + grav_split_bin(nbins);
-      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, mid, st, err);
+      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, mid, st, err, nullptr, ctr);
       if (rc2) return rc2;
       if (g.between) {
         rc2 = g.between(g.between_ctx);
         if (rc2) return rc2;
       }
       HB_CUDA_TRY(cudaEventRecord(g.split_event, st));
-      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err, mid);
+      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err, mid, ctr + 1);
     } else {
-      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err);
+      rc2 = launch_gravity_fast(e, tab, gt, T.n_tiles_cap, ntd, st, err, nullptr, ctr);
     }
     if (g.t1) HB_CUDA_TRY(cudaEventRecord(g.t1, st));
     return rc2;

@@ -1040,18 +1040,37 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
-          const int64_t* t_begin_dev) {
+          const int64_t* t_begin_dev, unsigned long long* ctr) {
   extern __shared__ float4 s_tab[];  // gt.rows * REP
   __shared__ float4 s_src[WARPS][kGravStage];
+  int64_t tb = t_begin_dev ? *t_begin_dev : 0;
+  int64_t t_end = *n_tiles_dev;
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (ctr) {
+    // persistent: the grid is the resident CTAs; each warp takes the next
+    // tile from a counter (zeroed by the launcher), so warps never wait for
+    // their CTA's slowest tile and the table is staged once per CTA
+    if ((int64_t)blockIdx.x * WARPS + tb >= t_end) return;
+    for (int k = threadIdx.x; k < gt.rows * REP; k += blockDim.x) s_tab[k] = table[k / REP];
+    __syncthreads();
+    const float4* tab = s_tab + (REP > 1 ? (lane & (REP - 1)) : 0);
+    while (true) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(ctr, 1ull);
+      int64_t t = tb + (int64_t)__shfl_sync(0xffffffffu, u, 0);
+      if (t >= t_end) break;
+      grav_tile<JB, REP, NB>(a, tab, gt, s_src[wid], t, lane);
+      __syncwarp();
+    }
+    return;
+  }
   // the grid covers the tiling's capacity; a range launch (t_begin_dev, a
   // bin-range end in n_tiles_dev) leaves whole CTAs past its end: they leave
   // before loading the 66 KB table
-  int64_t t0 = (int64_t)blockIdx.x * WARPS + (t_begin_dev ? *t_begin_dev : 0);
-  int64_t t_end = *n_tiles_dev;
+  int64_t t0 = (int64_t)blockIdx.x * WARPS + tb;
   if (t0 >= t_end) return;
   for (int k = threadIdx.x; k < gt.rows * REP; k += blockDim.x) s_tab[k] = table[k / REP];
   __syncthreads();
-  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = t0 + wid;
   if (t < t_end)
     grav_tile<JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
@@ -1061,7 +1080,8 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
 template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                int64_t tcap, const int64_t* ntd,
-                               const int64_t* t_begin, cudaStream_t st, HbError* err) {
+                               const int64_t* t_begin, cudaStream_t st, HbError* err,
+                               unsigned long long* ctr) {
   size_t sm = (size_t)gt.rows * REP * sizeof(float4);
   // static staging + dynamic table may pass the 48 KB default: raise the
   // per-kernel limit whenever the table grows (per device and instantiation)
@@ -1078,13 +1098,27 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
     }
   }
   unsigned grid = grid_for(tcap, WARPS), blk = WARPS * 32;
-  k_gravity<JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin);
+  if (ctr) {  // persistent: MINB resident CTAs per SM
+    static int sms[64] = {};
+    if (dev >= 0 && dev < 64 && !sms[dev])
+      HB_CUDA_TRY(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
+    unsigned cap = (unsigned)MINB * (unsigned)(dev >= 0 && dev < 64 ? sms[dev] : 148);
+    grid = grid < cap ? grid : cap;
+    HB_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+  }
+  k_gravity<JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin, ctr);
   return HB_OK;
 }
 
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
                         const int64_t* ntd, cudaStream_t st, HbError* err,
-                        const int64_t* t_begin) {
+                        const int64_t* t_begin, unsigned long long* ctr) {
+  static int persist = -1;
+  if (persist < 0) {  // HB_GRAV_PERSIST: 1 = persistent grid with a tile counter (when given one)
+    const char* e = getenv("HB_GRAV_PERSIST");
+    persist = e ? atoi(e) != 0 : 1;
+  }
+  if (!persist) ctr = nullptr;
   // batches of 8 sources per pipelined table gather (1 / 2 / 4: 10.31 / 10.17 /
   // 10.15 ms against 10.04 ms at c2 in round 1); 8 interleaved table copies.
   // The 32-per-octave table (default) is twice the 8-copy footprint (~70 KB):
@@ -1092,8 +1126,8 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
   // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
   // gone.)
   int rc = gt.jbits == 4
-               ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err)
-               : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err);
+               ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
+               : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err, ctr);
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;

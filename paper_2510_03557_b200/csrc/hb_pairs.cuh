@@ -393,8 +393,10 @@ int gravity_table(double r_s, double r_cut, double eps, float4* host_out, GravTa
 const float4* gravity_table_device(double r_s, double r_cut, double eps, GravTab* gt,
                                    cudaStream_t st, HbError* err);
 // tiles [*t_begin (0 if null), *ntd)
+// ctr (optional): a device counter the launch zeroes and the persistent grid
+// hands tiles out from (one per concurrent launch)
 int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt, int64_t tcap,
                         const int64_t* ntd, cudaStream_t st, HbError* err,
-                        const int64_t* t_begin = nullptr);
+                        const int64_t* t_begin = nullptr, unsigned long long* ctr = nullptr);
 
 }  // namespace hb
