@@ -869,8 +869,11 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval(EvalDev a, int64_t n_t
 // tables -- one or two MUFU and 27 instructions per pair -- were removed.)
 // Rows past r_cut (to the end of the interval holding r_cut) carry the smooth
 // continuation (|S| <= S(r_cut/r_s) < 1e-5 by the ForceSplit guard); the next
-// row is zero.  (A persistent grid loading the table once per CTA measured
-// 5% slower: static tile striding leaves warps idle at the tail.)
+// row is zero.  The resident step launches a persistent grid (2 CTAs per SM)
+// whose warps take tiles from a device counter: a one-tile-per-warp grid
+// keeps each CTA's slots (and its 66 KB table) until its slowest warp ends,
+// and a static-stride persistent grid (round 1) idled warps at the tail;
+// with the counter k_gravity went 9.69 -> 9.03 ms at c2, 596 -> 556 ms at c4.
 constexpr int kGravWarps = 8;
 constexpr int kGravStage = 128;
 
