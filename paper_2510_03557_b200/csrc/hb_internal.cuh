@@ -47,7 +47,6 @@ struct SphArgs {
   unsigned long long* err_key;
   const uint8_t* skip_leaf;
   int skip_tiles;  // pass B: skip tiles without an owned member
-  unsigned long long* ctr = nullptr;  // optional: persistent-grid tile counter (zeroed per launch)
 };
 int pack_sph(const Tiling& T, const int64_t* ntd, Rows rows, const int8_t* pshift,
              double L, float4* P0, float4* P1, float4* P2, float4* P3, int layout,

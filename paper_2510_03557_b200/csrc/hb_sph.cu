@@ -182,34 +182,15 @@ __device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, fl
   return nz;
 }
 
-// one tile per warp (ctr == null: the grid covers the tiling), or a
-// persistent grid of resident CTAs whose warps take tiles from a counter the
-// launcher zeroed (no warp waits for its CTA's slowest tile)
-template <class F>
-__device__ __forceinline__ void sph_tiles(const int64_t* n_tiles_dev, unsigned long long* ctr,
-                                          F tile) {
-  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t t_end = *n_tiles_dev;
-  if (!ctr) {
-    int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
-    if (t < t_end) tile(t);
-    return;
-  }
-  while (true) {
-    unsigned long long u = 0;
-    if (lane == 0) u = atomicAdd(ctr, 1ull);
-    int64_t t = (int64_t)__shfl_sync(0xffffffffu, u, 0);
-    if (t >= t_end) break;
-    tile(t);
-    __syncwarp();
-  }
-}
-
 // ---------------------------------------------------------------- pass A
-__device__ __forceinline__ void sph_density_tile(const SphDev& a, int64_t t,
-                                         float4 (*s_stage)[kStageA][1], int2 (*s_meta)[kStageA],
-                                         unsigned (*s_mask)[kStageA / 32][32]) {
+__global__ void __launch_bounds__(kSphWarps * 32, 6)
+k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
+  __shared__ float4 s_stage[kSphWarps][kStageA][1];
+  __shared__ int2 s_meta[kSphWarps][kStageA];
+  __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
+  if (t >= *n_tiles_dev) return;
   const Tiling& T = a.T;
   int A = T.tile_leaf[t];
   int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
@@ -290,14 +271,6 @@ __device__ __forceinline__ void sph_density_tile(const SphDev& a, int64_t t,
   }
 }
 
-__global__ void __launch_bounds__(kSphWarps * 32, 6)
-k_sph_density(SphDev a, const int64_t* n_tiles_dev, unsigned long long* ctr) {
-  __shared__ float4 s_stage[kSphWarps][kStageA][1];
-  __shared__ int2 s_meta[kSphWarps][kStageA];
-  __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
-  sph_tiles(n_tiles_dev, ctr, [&](int64_t t) { sph_density_tile(a, t, s_stage, s_meta, s_mask); });
-}
-
 // ---------------------------------------------------------------- pass B
 // records (k_pack_sph layout 1): P0 = (x, y, z, h), P1 = (vx, vy, vz, m),
 // P2 = (P/rho^2, c_s, rho, sigma/h^5).  1/q = h r^-1 reuses the rsqrt the
@@ -307,10 +280,14 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev, unsigned long long* ctr) {
 // 3.32 vs 2.83 ms at c2: staging and flush count outweigh the two MUFU.)
 // Two pairs per walk iteration at 4 CTAs / SM (127 registers, no spills).
 constexpr int kStageB = 192;
-__device__ __forceinline__ void sph_force_tile(const SphDev& a, int64_t t,
-                                         float4 (*s_stage)[kStageB][3], int2 (*s_meta)[kStageB],
-                                         unsigned (*s_mask)[kStageB / 32][32]) {
+__global__ void __launch_bounds__(kSphWarps * 32, 4)
+k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
+  __shared__ float4 s_stage[kSphWarps][kStageB][3];
+  __shared__ int2 s_meta[kSphWarps][kStageB];
+  __shared__ unsigned s_mask[kSphWarps][kStageB / 32][32];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
+  if (t >= *n_tiles_dev) return;
   const Tiling& T = a.T;
   int A = T.tile_leaf[t];
   if (a.skip_leaf && a.skip_leaf[A]) return;
@@ -447,14 +424,6 @@ __device__ __forceinline__ void sph_force_tile(const SphDev& a, int64_t t,
   }
 }
 
-__global__ void __launch_bounds__(kSphWarps * 32, 4)
-k_sph_force(SphDev a, const int64_t* n_tiles_dev, unsigned long long* ctr) {
-  __shared__ float4 s_stage[kSphWarps][kStageB][3];
-  __shared__ int2 s_meta[kSphWarps][kStageB];
-  __shared__ unsigned s_mask[kSphWarps][kStageB / 32][32];
-  sph_tiles(n_tiles_dev, ctr, [&](int64_t t) { sph_force_tile(a, t, s_stage, s_meta, s_mask); });
-}
-
 // ---------------------------------------------------------------- pass C
 // gradA / gradB of the CRK coefficients (north star; the reference computes
 // only A and B, hb/hydro.py:99-150).  With G = V_j (dW/dr)/r at h_i and
@@ -532,10 +501,14 @@ __device__ __forceinline__ void crk_grad_solve(const double* mom, double A, cons
   }
 }
 
-__device__ __forceinline__ void sph_grad_tile(const SphDev& a, int64_t t,
-                                         float4 (*s_stage)[kStageA][1], int2 (*s_meta)[kStageA],
-                                         unsigned (*s_mask)[kStageA / 32][32]) {
+__global__ void __launch_bounds__(kSphWarps * 32, 4)
+k_sph_grad(SphDev a, const int64_t* n_tiles_dev) {
+  __shared__ float4 s_stage[kSphWarps][kStageA][1];
+  __shared__ int2 s_meta[kSphWarps][kStageA];
+  __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
+  if (t >= *n_tiles_dev) return;
   const Tiling& T = a.T;
   int A = T.tile_leaf[t];
   if (a.skip_leaf && a.skip_leaf[A]) return;
@@ -605,14 +578,6 @@ __device__ __forceinline__ void sph_grad_tile(const SphDev& a, int64_t t,
                  dA, dB);
   for (int c = 0; c < 3; ++c) a.gradA[row * 3 + c] = dA[c];
   for (int c = 0; c < 9; ++c) a.gradB[row * 9 + c] = dB[c];
-}
-
-__global__ void __launch_bounds__(kSphWarps * 32, 4)
-k_sph_grad(SphDev a, const int64_t* n_tiles_dev, unsigned long long* ctr) {
-  __shared__ float4 s_stage[kSphWarps][kStageA][1];
-  __shared__ int2 s_meta[kSphWarps][kStageA];
-  __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
-  sph_tiles(n_tiles_dev, ctr, [&](int64_t t) { sph_grad_tile(a, t, s_stage, s_meta, s_mask); });
 }
 
 // gas records for both passes
@@ -690,23 +655,9 @@ int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   a.skip_leaf = s.skip_leaf;
   a.skip_tiles = s.skip_tiles;
   unsigned grid = grid_for(s.T->n_tiles_cap, kSphWarps);
-  static int persist = -1;
-  if (persist < 0) {  // HB_SPH_PERSIST: 1 = persistent grid with a tile counter (when given one)
-    const char* e = getenv("HB_SPH_PERSIST");
-    persist = e ? atoi(e) != 0 : 1;
-  }
-  unsigned long long* ctr = persist ? s.ctr : nullptr;
-  if (ctr) {  // resident CTAs only: the launch bounds' blocks per SM on every SM
-    int dev = 0, sms = 148;
-    HB_CUDA_TRY(cudaGetDevice(&dev));
-    HB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    unsigned cap = (unsigned)sms * (pass == 0 ? 6u : 4u);
-    grid = grid < cap ? grid : cap;
-    HB_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-  }
-  if (pass == 0) k_sph_density<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev, ctr);
-  else if (pass == 1) k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev, ctr);
-  else k_sph_grad<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev, ctr);
+  if (pass == 0) k_sph_density<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  else if (pass == 1) k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  else k_sph_grad<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   HB_LAUNCH_CHECK();
   return HB_OK;
 }

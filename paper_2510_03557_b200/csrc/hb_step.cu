@@ -128,7 +128,6 @@ k_gather_fields(int64_t n, const int64_t* perm, FieldIn in, FieldOut out, double
 }
 
 struct StepWs {
-  unsigned long long* sph_ctr;  // persistent SPH grids' tile counter
   // mesh
   int64_t *leaf_start, *leaf_end, *leaf_bin, *bin_ptr, *n_leaves_dev;
   double *leaf_lo, *leaf_hi;
@@ -167,7 +166,6 @@ static void carve_step(Arena& ws, int64_t n, int64_t nbins, int64_t cap, int64_t
   w.seg_s = ws.take<int64_t>(nbins + 1); w.seg_e = ws.take<int64_t>(nbins + 1);
   w.st_ptr = ws.take<int64_t>(nbins + 1);
   w.st_src = ws.take<int32_t>(nbins * 27 + 1); w.st_code = ws.take<int32_t>(nbins * 27 + 1);
-  w.sph_ctr = ws.take<unsigned long long>(1);
 }
 
 constexpr bool kGravityBinsDefault = true;
@@ -483,7 +481,6 @@ int force_step(HbStepArgs* a, Arena& ws, cudaStream_t st, HbError* err) {
   sa.ncount = a->ncount; sa.rho = w.rho_new; sa.moments = mom; sa.hydro = a->hydro;
   sa.skip_leaf = (a->ghost_density && !sph_bins) ? w.ghost_only : nullptr;
   sa.skip_tiles = a->owned_targets ? 1 : 0;
-  sa.ctr = w.sph_ctr;
   d.skip_leaf = a->ghost_density ? w.ghost_only : nullptr;
   // 4. pass A: neighbour count + density (hb/hydro.py:223-227, 60-84), EOS (48-57)
   if (a->passes & (HB_PASS_NCOUNT | HB_PASS_DENSITY)) {
