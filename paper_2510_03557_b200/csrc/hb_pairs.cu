@@ -1122,23 +1122,6 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
     persist = e ? atoi(e) != 0 : 1;
   }
   if (!persist) ctr = nullptr;
-  static int cta = -1;
-  if (cta < 0) {  // HB_GRAV_CTA (A/B, persistent grid only): 24 / 32 warps in one CTA per SM
-    const char* e = getenv("HB_GRAV_CTA");
-    cta = e ? atoi(e) : 0;
-  }
-  if (ctr && gt.jbits == 5 && cta == 24) {
-    int rc = launch_gravity_kind<5, 8, 8, 1, 24>(d, table, gt, tcap, ntd, t_begin, st, err, ctr);
-    if (rc) return rc;
-    HB_LAUNCH_CHECK();
-    return HB_OK;
-  }
-  if (ctr && gt.jbits == 5 && cta == 32) {
-    int rc = launch_gravity_kind<5, 8, 8, 1, 32>(d, table, gt, tcap, ntd, t_begin, st, err, ctr);
-    if (rc) return rc;
-    HB_LAUNCH_CHECK();
-    return HB_OK;
-  }
   // batches of 8 sources per pipelined table gather (1 / 2 / 4: 10.31 / 10.17 /
   // 10.15 ms against 10.04 ms at c2 in round 1); 8 interleaved table copies.
   // The 32-per-octave table (default) is twice the 8-copy footprint (~70 KB):
