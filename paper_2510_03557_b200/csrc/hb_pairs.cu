@@ -885,7 +885,60 @@ __device__ __forceinline__ unsigned and_or(unsigned a, unsigned b, unsigned c) {
   return d;
 }
 
-template <int JB, int REP, int kGravBatch>
+// 16-B shared-memory load from a 32-bit shared-window byte address
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+// targets into 4 spatially compact quarters of 8 lanes (two median splits
+// along the longest axis of each half's live box; ranks by coordinate, ties
+// by lane; moved through the warp's stage so that lane == position).  The
+// table gather's bank groups are the lanes l & 7 = g, one lane per quarter,
+// so the in-range lanes of a source spread over the groups instead of piling
+// into a few (a 16-B gather takes max over groups of the distinct rows).
+__device__ __forceinline__ void quarter_order(float4& ti, int& k_i, int& live, float4* scratch,
+                                              int lane) {
+  const unsigned FULL = 0xffffffffu;
+#pragma unroll
+  for (int S = 32; S > 8; S >>= 1) {
+    float lx = live ? ti.x : INFINITY, ly = live ? ti.y : INFINITY, lz = live ? ti.z : INFINITY;
+    float hx = live ? ti.x : -INFINITY, hy = live ? ti.y : -INFINITY, hz = live ? ti.z : -INFINITY;
+#pragma unroll
+    for (int o = S / 2; o; o >>= 1) {
+      lx = fminf(lx, __shfl_xor_sync(FULL, lx, o)); hx = fmaxf(hx, __shfl_xor_sync(FULL, hx, o));
+      ly = fminf(ly, __shfl_xor_sync(FULL, ly, o)); hy = fmaxf(hy, __shfl_xor_sync(FULL, hy, o));
+      lz = fminf(lz, __shfl_xor_sync(FULL, lz, o)); hz = fmaxf(hz, __shfl_xor_sync(FULL, hz, o));
+    }
+    float ex = hx - lx, ey = hy - ly, ez = hz - lz;
+    float key = (ex >= ey && ex >= ez) ? ti.x : (ey >= ez ? ti.y : ti.z);
+    if (!live) key = INFINITY;
+    int seg0 = lane & ~(S - 1);
+    int r = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      float kk = __shfl_sync(FULL, key, seg0 + k);
+      r += (kk < key) || (kk == key && seg0 + k < lane);
+    }
+    __syncwarp();
+    scratch[seg0 + r] = ti;
+    scratch[32 + seg0 + r] = make_float4(__int_as_float(k_i), __int_as_float(live), 0.0f, 0.0f);
+    __syncwarp();
+    ti = scratch[lane];
+    float4 x = scratch[32 + lane];
+    k_i = __float_as_int(x.x);
+    live = __float_as_int(x.y);
+    __syncwarp();
+  }
+}
+
+// s_tab: the table's base (row r, copy j at float4 8 r + j).  A lane reads
+// copy lane & 7 of its row; rows past r_cut (and soft below the table, whose
+// index wraps) read ONE word, copy 0 of the zero row, so the out-of-range
+// lanes of a gather add a single distinct address instead of one per bank group.
+template <int JB, int REP, int kGravBatch, bool QORD = true>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -895,12 +948,18 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
   if (e0 == e1) return;
   int n_t = T.tile_n[t];
-  bool live = lane < n_t;
+  int live = lane < n_t;
   int k_i = T.tile_start[t] + (live ? lane : 0);
   float4 ti = a.P0[k_i];
+  if (QORD) quarter_order(ti, k_i, live, stage, lane);
   float4 tlo = T.tile_lo[t], thi = T.tile_hi[t];
   float R2 = a.cull_reach * a.cull_reach;
   float eps2 = a.pp.p1;
+  // shared-memory byte addresses: this lane's copy of row 0, and the one word
+  // every out-of-range lane reads (copy 0 of the zero row)
+  const unsigned tab_s = (unsigned)__cvta_generic_to_shared(s_tab);
+  const unsigned lane_a = tab_s + (((unsigned)lane & (REP - 1)) << 4);
+  const unsigned zero_a = tab_s + ((gt.last * REP) << 4);
   float2 eps2x2 = make_float2(eps2, eps2);
   const unsigned lowmask = (1u << (23 - JB)) - 1u, one_bits = 0x3F800000u;
   // even / odd-source running sums (packed pairs), fed with fresh FP32x2
@@ -935,13 +994,13 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
           bm[2 * p] = s0.w; bm[2 * p + 1] = s1.w;
           float2 soft = __ffma2_rn(bz[p], bz[p], __ffma2_rn(by[p], by[p], __ffma2_rn(bx[p], bx[p], eps2x2)));
           unsigned b0 = __float_as_uint(soft.x), b1 = __float_as_uint(soft.y);
-          unsigned k0 = min((b0 >> (23 - JB)) - gt.base, gt.last);
-          unsigned k1 = min((b1 >> (23 - JB)) - gt.base, gt.last);
+          unsigned k0 = min(((b0 >> (23 - JB)) - gt.base) * (REP * 16) + lane_a, zero_a);
+          unsigned k1 = min(((b1 >> (23 - JB)) - gt.base) * (REP * 16) + lane_a, zero_a);
           float2 um = make_float2(__uint_as_float(and_or(b0, lowmask, one_bits)),
                                   __uint_as_float(and_or(b1, lowmask, one_bits)));
           bu[p] = __fadd2_rn(um, make_float2(-1.0f, -1.0f));
-          bc[2 * p] = s_tab[k0 * REP];
-          bc[2 * p + 1] = s_tab[k1 * REP];
+          bc[2 * p] = lds128(k0);
+          bc[2 * p + 1] = lds128(k1);
         }
         float2 fx = make_float2(0.0f, 0.0f), fy = fx, fz = fx;
 #pragma unroll
@@ -964,9 +1023,9 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
       float dx = ti.x - s.x, dy = ti.y - s.y, dz = ti.z - s.z;
       float soft = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
       unsigned bits = __float_as_uint(soft);
-      unsigned k = min((bits >> (23 - JB)) - gt.base, gt.last);
+      unsigned k = min(((bits >> (23 - JB)) - gt.base) * (REP * 16) + lane_a, zero_a);
       float u = __uint_as_float((bits & ((1u << (23 - JB)) - 1u)) | 0x3F800000u) - 1.0f;
-      float4 c = s_tab[k * REP];
+      float4 c = lds128(k);
       float w = fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x) * s.w;
       tx = fmaf(w, dx, tx);
       ty = fmaf(w, dy, ty);
@@ -1040,7 +1099,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
+template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps, bool QORD = true>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev, unsigned long long* ctr) {
@@ -1056,13 +1115,12 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
     if ((int64_t)blockIdx.x * WARPS + tb >= t_end) return;
     for (int k = threadIdx.x; k < gt.rows * REP; k += blockDim.x) s_tab[k] = table[k / REP];
     __syncthreads();
-    const float4* tab = s_tab + (REP > 1 ? (lane & (REP - 1)) : 0);
     while (true) {
       unsigned long long u = 0;
       if (lane == 0) u = atomicAdd(ctr, 1ull);
       int64_t t = tb + (int64_t)__shfl_sync(0xffffffffu, u, 0);
       if (t >= t_end) break;
-      grav_tile<JB, REP, NB>(a, tab, gt, s_src[wid], t, lane);
+      grav_tile<JB, REP, NB, QORD>(a, s_tab, gt, s_src[wid], t, lane);
       __syncwarp();
     }
     return;
@@ -1076,11 +1134,10 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
   __syncthreads();
   int64_t t = t0 + wid;
   if (t < t_end)
-    grav_tile<JB, REP, NB>(a, s_tab + (REP > 1 ? (lane & (REP - 1)) : 0), gt, s_src[wid],
-                                 t, lane);
+    grav_tile<JB, REP, NB, QORD>(a, s_tab, gt, s_src[wid], t, lane);
 }
 
-template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
+template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps, bool QORD = true>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                int64_t tcap, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err,
@@ -1095,7 +1152,7 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS, QORD>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
@@ -1109,7 +1166,7 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
     grid = grid < cap ? grid : cap;
     HB_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
   }
-  k_gravity<JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin, ctr);
+  k_gravity<JB, REP, NB, MINB, WARPS, QORD><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin, ctr);
   return HB_OK;
 }
 
@@ -1128,9 +1185,15 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
   // 16-warp CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4.
   // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
   // gone.)
+  static int qord = -1;
+  if (qord < 0) {  // HB_GRAV_QORD: 1 = targets in spatial quarters (bank-group spread), 0 = tile order
+    const char* e = getenv("HB_GRAV_QORD");
+    qord = e ? atoi(e) != 0 : 1;
+  }
   int rc = gt.jbits == 4
                ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
-               : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err, ctr);
+               : (qord ? launch_gravity_kind<5, 8, 8, 2, 16, true>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
+                       : launch_gravity_kind<5, 8, 8, 2, 16, false>(d, table, gt, tcap, ntd, t_begin, st, err, ctr));
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;
