@@ -892,6 +892,15 @@ __device__ __forceinline__ float4 lds128(unsigned addr) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+// the same, issued only when k < last (zeros otherwise): a lane past the
+// table's end generates no shared-memory request at all
+__device__ __forceinline__ float4 lds128_if(unsigned addr, unsigned k, unsigned last) {
+  float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %4, %5;\n\t"
+               "@p ld.shared.v4.f32 {%0, %1, %2, %3}, [%6];\n\t}"
+               : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w) : "r"(k), "r"(last), "r"(addr));
+  return v;
+}
 
 // targets into 4 spatially compact quarters of 8 lanes (two median splits
 // along the longest axis of each half's live box; ranks by coordinate, ties
@@ -938,7 +947,7 @@ __device__ __forceinline__ void quarter_order(float4& ti, int& k_i, int& live, f
 // copy lane & 7 of its row; rows past r_cut (and soft below the table, whose
 // index wraps) read ONE word, copy 0 of the zero row, so the out-of-range
 // lanes of a gather add a single distinct address instead of one per bank group.
-template <int JB, int REP, int kGravBatch, bool QORD = true>
+template <int JB, int REP, int kGravBatch, bool QORD = true, bool PRED = true>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -959,7 +968,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   // every out-of-range lane reads (copy 0 of the zero row)
   const unsigned tab_s = (unsigned)__cvta_generic_to_shared(s_tab);
   const unsigned lane_a = tab_s + (((unsigned)lane & (REP - 1)) << 4);
-  const unsigned zero_a = tab_s + ((gt.last * REP) << 4);
+  const unsigned zero_a = lane_a + ((gt.last * REP) << 4);  // this lane's copy of the zero row
   float2 eps2x2 = make_float2(eps2, eps2);
   const unsigned lowmask = (1u << (23 - JB)) - 1u, one_bits = 0x3F800000u;
   // even / odd-source running sums (packed pairs), fed with fresh FP32x2
@@ -994,13 +1003,17 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
           bm[2 * p] = s0.w; bm[2 * p + 1] = s1.w;
           float2 soft = __ffma2_rn(bz[p], bz[p], __ffma2_rn(by[p], by[p], __ffma2_rn(bx[p], bx[p], eps2x2)));
           unsigned b0 = __float_as_uint(soft.x), b1 = __float_as_uint(soft.y);
-          unsigned k0 = min(((b0 >> (23 - JB)) - gt.base) * (REP * 16) + lane_a, zero_a);
-          unsigned k1 = min(((b1 >> (23 - JB)) - gt.base) * (REP * 16) + lane_a, zero_a);
+          unsigned r0 = (b0 >> (23 - JB)) - gt.base, r1 = (b1 >> (23 - JB)) - gt.base;
           float2 um = make_float2(__uint_as_float(and_or(b0, lowmask, one_bits)),
                                   __uint_as_float(and_or(b1, lowmask, one_bits)));
           bu[p] = __fadd2_rn(um, make_float2(-1.0f, -1.0f));
-          bc[2 * p] = lds128(k0);
-          bc[2 * p + 1] = lds128(k1);
+          if (PRED) {
+            bc[2 * p] = lds128_if(r0 * (REP * 16) + lane_a, r0, gt.last);
+            bc[2 * p + 1] = lds128_if(r1 * (REP * 16) + lane_a, r1, gt.last);
+          } else {
+            bc[2 * p] = lds128(min(r0 * (REP * 16) + lane_a, zero_a));
+            bc[2 * p + 1] = lds128(min(r1 * (REP * 16) + lane_a, zero_a));
+          }
         }
         float2 fx = make_float2(0.0f, 0.0f), fy = fx, fz = fx;
 #pragma unroll
@@ -1099,7 +1112,8 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps, bool QORD = true>
+template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps, bool QORD = true,
+          bool PRED = true>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev, unsigned long long* ctr) {
@@ -1120,7 +1134,7 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
       if (lane == 0) u = atomicAdd(ctr, 1ull);
       int64_t t = tb + (int64_t)__shfl_sync(0xffffffffu, u, 0);
       if (t >= t_end) break;
-      grav_tile<JB, REP, NB, QORD>(a, s_tab, gt, s_src[wid], t, lane);
+      grav_tile<JB, REP, NB, QORD, PRED>(a, s_tab, gt, s_src[wid], t, lane);
       __syncwarp();
     }
     return;
@@ -1134,10 +1148,11 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
   __syncthreads();
   int64_t t = t0 + wid;
   if (t < t_end)
-    grav_tile<JB, REP, NB, QORD>(a, s_tab, gt, s_src[wid], t, lane);
+    grav_tile<JB, REP, NB, QORD, PRED>(a, s_tab, gt, s_src[wid], t, lane);
 }
 
-template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps, bool QORD = true>
+template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps, bool QORD = true,
+          bool PRED = true>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                int64_t tcap, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err,
@@ -1152,7 +1167,7 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS, QORD>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS, QORD, PRED>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
@@ -1166,7 +1181,7 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
     grid = grid < cap ? grid : cap;
     HB_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
   }
-  k_gravity<JB, REP, NB, MINB, WARPS, QORD><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin, ctr);
+  k_gravity<JB, REP, NB, MINB, WARPS, QORD, PRED><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin, ctr);
   return HB_OK;
 }
 
@@ -1186,14 +1201,15 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
   // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
   // gone.)
   static int qord = -1;
-  if (qord < 0) {  // HB_GRAV_QORD: 1 = targets in spatial quarters (bank-group spread), 0 = tile order
+  if (qord < 0) {  // HB_GRAV_QORD (A/B): 0 tile order, 1 spatial quarters, 2 quarters + predicated gathers
     const char* e = getenv("HB_GRAV_QORD");
-    qord = e ? atoi(e) != 0 : 1;
+    qord = e ? atoi(e) : 2;
   }
   int rc = gt.jbits == 4
                ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
-               : (qord ? launch_gravity_kind<5, 8, 8, 2, 16, true>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
-                       : launch_gravity_kind<5, 8, 8, 2, 16, false>(d, table, gt, tcap, ntd, t_begin, st, err, ctr));
+               : (qord == 2 ? launch_gravity_kind<5, 8, 8, 2, 16, true, true>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
+                  : qord == 1 ? launch_gravity_kind<5, 8, 8, 2, 16, true, false>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
+                              : launch_gravity_kind<5, 8, 8, 2, 16, false, false>(d, table, gt, tcap, ntd, t_begin, st, err, ctr));
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;
