@@ -892,62 +892,14 @@ __device__ __forceinline__ float4 lds128(unsigned addr) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
-// the same, issued only when k < last (zeros otherwise): a lane past the
-// table's end generates no shared-memory request at all
-__device__ __forceinline__ float4 lds128_if(unsigned addr, unsigned k, unsigned last) {
-  float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %4, %5;\n\t"
-               "@p ld.shared.v4.f32 {%0, %1, %2, %3}, [%6];\n\t}"
-               : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w) : "r"(k), "r"(last), "r"(addr));
-  return v;
-}
-
-// targets into 4 spatially compact quarters of 8 lanes (two median splits
-// along the longest axis of each half's live box; ranks by coordinate, ties
-// by lane; moved through the warp's stage so that lane == position).  The
-// table gather's bank groups are the lanes l & 7 = g, one lane per quarter,
-// so the in-range lanes of a source spread over the groups instead of piling
-// into a few (a 16-B gather takes max over groups of the distinct rows).
-__device__ __forceinline__ void quarter_order(float4& ti, int& k_i, int& live, float4* scratch,
-                                              int lane) {
-  const unsigned FULL = 0xffffffffu;
-#pragma unroll
-  for (int S = 32; S > 8; S >>= 1) {
-    float lx = live ? ti.x : INFINITY, ly = live ? ti.y : INFINITY, lz = live ? ti.z : INFINITY;
-    float hx = live ? ti.x : -INFINITY, hy = live ? ti.y : -INFINITY, hz = live ? ti.z : -INFINITY;
-#pragma unroll
-    for (int o = S / 2; o; o >>= 1) {
-      lx = fminf(lx, __shfl_xor_sync(FULL, lx, o)); hx = fmaxf(hx, __shfl_xor_sync(FULL, hx, o));
-      ly = fminf(ly, __shfl_xor_sync(FULL, ly, o)); hy = fmaxf(hy, __shfl_xor_sync(FULL, hy, o));
-      lz = fminf(lz, __shfl_xor_sync(FULL, lz, o)); hz = fmaxf(hz, __shfl_xor_sync(FULL, hz, o));
-    }
-    float ex = hx - lx, ey = hy - ly, ez = hz - lz;
-    float key = (ex >= ey && ex >= ez) ? ti.x : (ey >= ez ? ti.y : ti.z);
-    if (!live) key = INFINITY;
-    int seg0 = lane & ~(S - 1);
-    int r = 0;
-#pragma unroll
-    for (int k = 0; k < S; ++k) {
-      float kk = __shfl_sync(FULL, key, seg0 + k);
-      r += (kk < key) || (kk == key && seg0 + k < lane);
-    }
-    __syncwarp();
-    scratch[seg0 + r] = ti;
-    scratch[32 + seg0 + r] = make_float4(__int_as_float(k_i), __int_as_float(live), 0.0f, 0.0f);
-    __syncwarp();
-    ti = scratch[lane];
-    float4 x = scratch[32 + lane];
-    k_i = __float_as_int(x.x);
-    live = __float_as_int(x.y);
-    __syncwarp();
-  }
-}
-
 // s_tab: the table's base (row r, copy j at float4 8 r + j).  A lane reads
-// copy lane & 7 of its row; rows past r_cut (and soft below the table, whose
-// index wraps) read ONE word, copy 0 of the zero row, so the out-of-range
-// lanes of a gather add a single distinct address instead of one per bank group.
-template <int JB, int REP, int kGravBatch, bool QORD = true, bool PRED = true>
+// copy lane & 7 of its row through a 32-bit shared-window byte address: row
+// offset + this lane's copy offset, clamped to this lane's copy of the zero
+// row (soft past r_cut, or below the table, whose index wraps to the top).
+// (Measured against the float4-indexed gather: 9.03 -> 8.87 ms at c2, same
+// instruction count.  Predicating the out-of-range gathers off cut the
+// shared-memory wavefronts 19% but added 10% instructions: 8.96 ms.)
+template <int JB, int REP, int kGravBatch>
 __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab, const GravTab& gt,
                                           float4* stage, int64_t t, int lane) {
   const Tiling& T = a.T;
@@ -957,18 +909,16 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
   int64_t e0 = a.ent_ptr[A], e1 = a.ent_ptr[A + 1];
   if (e0 == e1) return;
   int n_t = T.tile_n[t];
-  int live = lane < n_t;
+  bool live = lane < n_t;
   int k_i = T.tile_start[t] + (live ? lane : 0);
   float4 ti = a.P0[k_i];
-  if (QORD) quarter_order(ti, k_i, live, stage, lane);
   float4 tlo = T.tile_lo[t], thi = T.tile_hi[t];
   float R2 = a.cull_reach * a.cull_reach;
   float eps2 = a.pp.p1;
-  // shared-memory byte addresses: this lane's copy of row 0, and the one word
-  // every out-of-range lane reads (copy 0 of the zero row)
+  // shared-memory byte addresses: this lane's copy of row 0 and of the zero row
   const unsigned tab_s = (unsigned)__cvta_generic_to_shared(s_tab);
   const unsigned lane_a = tab_s + (((unsigned)lane & (REP - 1)) << 4);
-  const unsigned zero_a = lane_a + ((gt.last * REP) << 4);  // this lane's copy of the zero row
+  const unsigned zero_a = lane_a + ((gt.last * REP) << 4);
   float2 eps2x2 = make_float2(eps2, eps2);
   const unsigned lowmask = (1u << (23 - JB)) - 1u, one_bits = 0x3F800000u;
   // even / odd-source running sums (packed pairs), fed with fresh FP32x2
@@ -1007,13 +957,8 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
           float2 um = make_float2(__uint_as_float(and_or(b0, lowmask, one_bits)),
                                   __uint_as_float(and_or(b1, lowmask, one_bits)));
           bu[p] = __fadd2_rn(um, make_float2(-1.0f, -1.0f));
-          if (PRED) {
-            bc[2 * p] = lds128_if(r0 * (REP * 16) + lane_a, r0, gt.last);
-            bc[2 * p + 1] = lds128_if(r1 * (REP * 16) + lane_a, r1, gt.last);
-          } else {
-            bc[2 * p] = lds128(min(r0 * (REP * 16) + lane_a, zero_a));
-            bc[2 * p + 1] = lds128(min(r1 * (REP * 16) + lane_a, zero_a));
-          }
+          bc[2 * p] = lds128(min(r0 * (REP * 16) + lane_a, zero_a));
+          bc[2 * p + 1] = lds128(min(r1 * (REP * 16) + lane_a, zero_a));
         }
         float2 fx = make_float2(0.0f, 0.0f), fy = fx, fz = fx;
 #pragma unroll
@@ -1112,8 +1057,7 @@ __device__ __forceinline__ void grav_tile(const EvalDev& a, const float4* s_tab,
 // in quarter-warp phases of 8 consecutive lanes; with the copies every lane of
 // a phase owns one 16-B bank group whatever row it reads, so the gather takes
 // the minimum 4 wavefronts instead of 4 + bank conflicts (5.9 measured).
-template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps, bool QORD = true,
-          bool PRED = true>
+template <int JB, int REP, int NB, int MINB = 4, int WARPS = kGravWarps>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t* n_tiles_dev,
           const int64_t* t_begin_dev, unsigned long long* ctr) {
@@ -1134,7 +1078,7 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
       if (lane == 0) u = atomicAdd(ctr, 1ull);
       int64_t t = tb + (int64_t)__shfl_sync(0xffffffffu, u, 0);
       if (t >= t_end) break;
-      grav_tile<JB, REP, NB, QORD, PRED>(a, s_tab, gt, s_src[wid], t, lane);
+      grav_tile<JB, REP, NB>(a, s_tab, gt, s_src[wid], t, lane);
       __syncwarp();
     }
     return;
@@ -1148,11 +1092,10 @@ k_gravity(EvalDev a, const float4* __restrict__ table, GravTab gt, const int64_t
   __syncthreads();
   int64_t t = t0 + wid;
   if (t < t_end)
-    grav_tile<JB, REP, NB, QORD, PRED>(a, s_tab, gt, s_src[wid], t, lane);
+    grav_tile<JB, REP, NB>(a, s_tab, gt, s_src[wid], t, lane);
 }
 
-template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps, bool QORD = true,
-          bool PRED = true>
+template <int JB, int NB, int REP = 8, int MINB = 4, int WARPS = kGravWarps>
 static int launch_gravity_kind(const EvalDev& d, const float4* table, const GravTab& gt,
                                int64_t tcap, const int64_t* ntd,
                                const int64_t* t_begin, cudaStream_t st, HbError* err,
@@ -1167,7 +1110,7 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && sm > set_for[dev]) {
-      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS, QORD, PRED>,
+      HB_CUDA_TRY(cudaFuncSetAttribute(k_gravity<JB, REP, NB, MINB, WARPS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_for[dev] = sm;
     }
@@ -1181,7 +1124,7 @@ static int launch_gravity_kind(const EvalDev& d, const float4* table, const Grav
     grid = grid < cap ? grid : cap;
     HB_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
   }
-  k_gravity<JB, REP, NB, MINB, WARPS, QORD, PRED><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin, ctr);
+  k_gravity<JB, REP, NB, MINB, WARPS><<<grid, blk, sm, st>>>(d, table, gt, ntd, t_begin, ctr);
   return HB_OK;
 }
 
@@ -1200,16 +1143,9 @@ int launch_gravity_fast(const EvalDev& d, const float4* table, const GravTab& gt
   // 16-warp CTAs keep 2 x 16 = 32 resident warps per SM, as 4 x 8 for JB = 4.
   // (Round 1's fewer-copy / higher-occupancy variants were all slower and are
   // gone.)
-  static int qord = -1;
-  if (qord < 0) {  // HB_GRAV_QORD (A/B): 0 tile order, 1 spatial quarters, 2 quarters + predicated gathers
-    const char* e = getenv("HB_GRAV_QORD");
-    qord = e ? atoi(e) : 2;
-  }
   int rc = gt.jbits == 4
                ? launch_gravity_kind<4, 8>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
-               : (qord == 2 ? launch_gravity_kind<5, 8, 8, 2, 16, true, true>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
-                  : qord == 1 ? launch_gravity_kind<5, 8, 8, 2, 16, true, false>(d, table, gt, tcap, ntd, t_begin, st, err, ctr)
-                              : launch_gravity_kind<5, 8, 8, 2, 16, false, false>(d, table, gt, tcap, ntd, t_begin, st, err, ctr));
+               : launch_gravity_kind<5, 8, 8, 2, 16>(d, table, gt, tcap, ntd, t_begin, st, err, ctr);
   if (rc) return rc;
   HB_LAUNCH_CHECK();
   return HB_OK;
