@@ -52,7 +52,10 @@ __global__ void k_bin_stencil(int64_t nbins, ListGeom g, int32_t* src, int32_t* 
   int64_t flat;
   int cd;
   bool ok = cell(o, flat, cd);
-  for (int o2 = 0; o2 < o && ok; ++o2) {
+  // duplicates (the same cell and shift reached twice) need an axis with
+  // fewer than 3 bins; otherwise the 27 offsets are distinct
+  bool dup_possible = g.nb[0] < 3 || g.nb[1] < 3 || g.nb[2] < 3;
+  for (int o2 = 0; o2 < o && ok && dup_possible; ++o2) {
     int64_t f2;
     int c2;
     if (cell(o2, f2, c2) && f2 == flat && c2 == cd) ok = false;
