@@ -183,7 +183,8 @@ __device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, fl
 }
 
 // ---------------------------------------------------------------- pass A
-__global__ void __launch_bounds__(kSphWarps * 32, 6)
+template <int MINB = 6>
+__global__ void __launch_bounds__(kSphWarps * 32, MINB)
 k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   __shared__ float4 s_stage[kSphWarps][kStageA][1];
   __shared__ int2 s_meta[kSphWarps][kStageA];
@@ -280,7 +281,8 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
 // 3.32 vs 2.83 ms at c2: staging and flush count outweigh the two MUFU.)
 // Two pairs per walk iteration at 4 CTAs / SM (127 registers, no spills).
 constexpr int kStageB = 192;
-__global__ void __launch_bounds__(kSphWarps * 32, 4)
+template <int MINB = 4>
+__global__ void __launch_bounds__(kSphWarps * 32, MINB)
 k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   __shared__ float4 s_stage[kSphWarps][kStageB][3];
   __shared__ int2 s_meta[kSphWarps][kStageB];
@@ -655,8 +657,18 @@ int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   a.skip_leaf = s.skip_leaf;
   a.skip_tiles = s.skip_tiles;
   unsigned grid = grid_for(s.T->n_tiles_cap, kSphWarps);
-  if (pass == 0) k_sph_density<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-  else if (pass == 1) k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  static int occ = -1;
+  if (occ < 0) {  // HB_SPH_OCC (A/B): 1 = pass A 7 CTAs / SM, pass B 5 CTAs / SM (register caps)
+    const char* e = getenv("HB_SPH_OCC");
+    occ = e ? atoi(e) : 0;
+  }
+  if (pass == 0) {
+    if (occ) k_sph_density<7><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+    else k_sph_density<><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  } else if (pass == 1) {
+    if (occ) k_sph_force<5><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+    else k_sph_force<><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  }
   else k_sph_grad<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   HB_LAUNCH_CHECK();
   return HB_OK;
