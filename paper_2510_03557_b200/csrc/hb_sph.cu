@@ -183,12 +183,14 @@ __device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, fl
 }
 
 // ---------------------------------------------------------------- pass A
-template <int MINB = 6>
+// 7 CTAs / SM (the shared-memory limit; 73 registers, small spills): 1.413 ->
+// 1.342 ms at c2, 89.6 -> 84.9 ms at c4 against 6 CTAs at 80 registers
+template <int STG = kStageA, int MINB = 7>
 __global__ void __launch_bounds__(kSphWarps * 32, MINB)
 k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
-  __shared__ float4 s_stage[kSphWarps][kStageA][1];
-  __shared__ int2 s_meta[kSphWarps][kStageA];
-  __shared__ unsigned s_mask[kSphWarps][kStageA / 32][32];
+  __shared__ float4 s_stage[kSphWarps][STG][1];
+  __shared__ int2 s_meta[kSphWarps][STG];
+  __shared__ unsigned s_mask[kSphWarps][STG / 32][32];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = (int64_t)blockIdx.x * kSphWarps + wid;
   if (t >= *n_tiles_dev) return;
@@ -263,7 +265,7 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
   };
   // cull radius from the tile's largest h (emit_tile_box: tile_lo.w), not this
   // lane's: every lane culls sources for the whole tile
-  sph_sweep<1, false, kStageA>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
+  sph_sweep<1, false, STG>(a, A, e0, e1, tlo, thi, tlo.w, a.reach * 1.0001f, stage, meta,
                                cnt, consume);
   if (live) {
     float norm3 = h > 0.0f ? kSigma * hinv * hinv * hinv : 0.0f;
@@ -281,8 +283,8 @@ k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
 // 3.32 vs 2.83 ms at c2: staging and flush count outweigh the two MUFU.)
 // Two pairs per walk iteration at 4 CTAs / SM (127 registers, no spills).
 constexpr int kStageB = 192;
-template <int MINB = 4>
-__global__ void __launch_bounds__(kSphWarps * 32, MINB)
+// (5 CTAs / SM at 96 registers spills and measured 2.41 -> 2.62 ms at c2)
+__global__ void __launch_bounds__(kSphWarps * 32, 4)
 k_sph_force(SphDev a, const int64_t* n_tiles_dev) {
   __shared__ float4 s_stage[kSphWarps][kStageB][3];
   __shared__ int2 s_meta[kSphWarps][kStageB];
@@ -658,17 +660,13 @@ int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   a.skip_tiles = s.skip_tiles;
   unsigned grid = grid_for(s.T->n_tiles_cap, kSphWarps);
   static int occ = -1;
-  if (occ < 0) {  // HB_SPH_OCC (A/B): 1 = pass A 7 CTAs / SM, pass B 5 CTAs / SM (register caps)
+  if (occ < 0) {  // HB_SPH_OCC (A/B): 1 = pass A with 224-source stages at 8 CTAs / SM
     const char* e = getenv("HB_SPH_OCC");
     occ = e ? atoi(e) : 0;
   }
-  if (pass == 0) {
-    if (occ) k_sph_density<7><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-    else k_sph_density<><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-  } else if (pass == 1) {
-    if (occ) k_sph_force<5><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-    else k_sph_force<><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-  }
+  if (pass == 0 && occ) k_sph_density<224, 8><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  else if (pass == 0) k_sph_density<><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  else if (pass == 1) k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   else k_sph_grad<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   HB_LAUNCH_CHECK();
   return HB_OK;
