@@ -183,8 +183,9 @@ __device__ __forceinline__ unsigned build_masks(float4 (*stage)[NP], int cnt, fl
 }
 
 // ---------------------------------------------------------------- pass A
-// 7 CTAs / SM (the shared-memory limit; 73 registers, small spills): 1.413 ->
-// 1.342 ms at c2, 89.6 -> 84.9 ms at c4 against 6 CTAs at 80 registers
+// 7 CTAs / SM (the shared-memory limit; 72 registers, small spills): 1.413 ->
+// 1.342 ms at c2, 89.6 -> 84.9 ms at c4 against 6 CTAs at 80 registers (8 CTAs
+// with 224-source stages at 64 registers spill: 1.49 ms, 94.0 ms)
 template <int STG = kStageA, int MINB = 7>
 __global__ void __launch_bounds__(kSphWarps * 32, MINB)
 k_sph_density(SphDev a, const int64_t* n_tiles_dev) {
@@ -659,13 +660,7 @@ int launch_sph(int pass, const SphArgs& s, cudaStream_t st, HbError* err) {
   a.skip_leaf = s.skip_leaf;
   a.skip_tiles = s.skip_tiles;
   unsigned grid = grid_for(s.T->n_tiles_cap, kSphWarps);
-  static int occ = -1;
-  if (occ < 0) {  // HB_SPH_OCC (A/B): 1 = pass A with 224-source stages at 8 CTAs / SM
-    const char* e = getenv("HB_SPH_OCC");
-    occ = e ? atoi(e) : 0;
-  }
-  if (pass == 0 && occ) k_sph_density<224, 8><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
-  else if (pass == 0) k_sph_density<><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
+  if (pass == 0) k_sph_density<><<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   else if (pass == 1) k_sph_force<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   else k_sph_grad<<<grid, kSphWarps * 32, 0, st>>>(a, s.n_tiles_dev);
   HB_LAUNCH_CHECK();
